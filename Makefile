@@ -1,0 +1,26 @@
+# Builds: gen (input generators), oracle (CPU test oracle), spchol (the CUDA product library).
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+PKG := paper_2409_14009_b200
+CSRC := $(PKG)/csrc
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -Iinclude -I$(CSRC)
+
+.PHONY: all gen oracle spchol clean
+all: gen oracle spchol
+
+gen: gen/libgen.so
+gen/libgen.so: gen/gen.c
+	gcc -O2 -shared -fPIC -o $@ $<
+
+oracle: oracle/liboracle.so
+oracle/liboracle.so: oracle/oracle.c
+	gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC -o $@ $< -lm
+
+SPCHOL_SRC := $(wildcard $(CSRC)/*.cu) $(wildcard $(CSRC)/*.cpp)
+SPCHOL_HDR := $(wildcard $(CSRC)/*.h) $(wildcard $(CSRC)/*.cuh) include/spchol.h
+spchol: $(PKG)/libspchol.so
+$(PKG)/libspchol.so: $(SPCHOL_SRC) $(SPCHOL_HDR)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SPCHOL_SRC) -lcudart
+
+clean:
+	rm -f gen/libgen.so oracle/liboracle.so $(PKG)/libspchol.so

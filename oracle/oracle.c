@@ -1,0 +1,592 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of what the product path computes
+ * (SURVEY.md §8(c) steps O1-O10).  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code with
+ * paper_2409_14009_b200/ (no headers, helpers or tables); the only common module is gen/
+ * (input generators).
+ *
+ * Compiled with -O2 -ffp-contract=off (no FMA contraction), IEEE FP64, round-to-nearest.
+ *
+ * Steps and the passages they follow (P:n = /root/reference/PAPER.md line n):
+ *   O1 permute            C = P A P^T                                  (perm is an input)
+ *   O2 symbolic           row-merge: struct(L_j) = {j} u {i>j: C_ij!=0} u U_{c: parent(c)=j} struct(L_c)\{c}
+ *                         parent(j) = min(struct(L_j)\{j})
+ *   O3 postorder          DFS from roots ascending, children ascending, number on exit
+ *   O4 column counts      cc_j = |struct(L_j)|, nnz(L) = sum cc_j, F = sum cc_j^2
+ *   O5 supernodes         fundamental [LNP93] (reading R1): j+1 joins j iff
+ *                         parent(j)=j+1, cc_j = cc_{j+1}+1 and j+1 has exactly one child.
+ *                         rule=1 gives the "maximal" partition of Fig. 1 (no child condition).
+ *   O6 greedy merge       pairs (J, p(J)), minimum new fill first, stop before cumulative growth
+ *                         exceeds cap * nnz(L)  (readings R3-R6)
+ *   O7 final permutation  postorder of the merged supernodal tree (reading R6)
+ *   O8 relind             relind(J,P)[q] = (m_P - 1) - position of rows(J)[q] in rows(P),
+ *                         for the rows of J that are >= f_P ("distance from the bottom")
+ *   O9 numeric            scalar left-looking column Cholesky of C_f = P_f A P_f^T on its exact
+ *                         structure (A = L L^T); the unique Cholesky factor.
+ *   O10 solve             L y = P_f b, L^T z = y, x = P_f^T z  ("triangular factors are used
+ *                         to compute the solution")
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  int64_t n;
+  /* O3 / fundamental / merge (all in O3 numbering) */
+  int32_t* post;      /* post[new3] = old (user-permuted numbering) */
+  int32_t* parent3;   /* exact etree in O3 numbering */
+  int32_t* cc3;       /* column counts in O3 numbering */
+  int64_t nnzL;
+  double flops;       /* sum cc^2 */
+  int32_t nfund;
+  int32_t* ffirst;    /* [nfund+1] fundamental partition, O3 numbering */
+  int32_t* fparent;   /* fundamental supernodal parent (-1 = root) */
+  int32_t* fgroup;    /* fundamental supernode -> merged group id (fundamental index of its top) */
+  int64_t added;      /* storage added by merging */
+  int32_t nmerges;
+  int32_t* merge_child; int32_t* merge_parent; int64_t* merge_cost;  /* merge log */
+  /* final (O7) numbering */
+  int32_t* perm_final; /* perm_final[orig] = final */
+  int32_t* o7;         /* o7[o3] = final */
+  int32_t nsuper;
+  int32_t* sfirst;     /* [nsuper+1] */
+  int32_t* sparent;    /* merged supernodal parent, -1 = root */
+  int64_t* rows_ptr;   /* [nsuper+1] */
+  int32_t* rows;       /* rows(J), final numbering, ascending */
+  int64_t* rel_ptr;    /* [nsuper+1] index into rel_list */
+  int32_t* rel_anc;    /* per (J,P) pair: P */
+  int32_t* rel_q0;     /* per pair: first q in rows(J) with rows(J)[q] >= f_P */
+  int64_t* rel_off;    /* per pair: offset into relind */
+  int64_t npairs;
+  int32_t* relind;
+  int32_t* parent_final; /* exact etree in final numbering */
+  int32_t* cc_final;
+  /* exact structure of L in final numbering (only when requested) */
+  int64_t* Lp; int32_t* Li; double* Lx;
+  /* permuted input C_f (for numeric) */
+  int64_t* Cp; int32_t* Ci; double* Cx;
+  int numeric_done;
+} orc_t;
+
+/* ---------------- helpers ---------------- */
+static int cmp_i32(const void* a, const void* b) {
+  int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  return (x > y) - (x < y);
+}
+
+/* O1: C = P A P^T in lower CSC (rows ascending).  perm[old] = new. */
+static void permute_lower(int64_t n, const int64_t* Ap, const int32_t* Ai, const double* Ax,
+                          const int32_t* perm, int64_t** Cp_out, int32_t** Ci_out, double** Cx_out) {
+  int64_t nnz = Ap[n];
+  int64_t* Cp = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+  int32_t* Ci = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nnz ? nnz : 1));
+  double* Cx = Ax ? (double*)malloc(sizeof(double) * (size_t)(nnz ? nnz : 1)) : NULL;
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t p = Ap[j]; p < Ap[j + 1]; ++p) {
+      int32_t a = perm[Ai[p]], b = perm[j];
+      int32_t col = a < b ? a : b;
+      Cp[col + 1]++;
+    }
+  for (int64_t j = 0; j < n; ++j) Cp[j + 1] += Cp[j];
+  int64_t* next = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+  memcpy(next, Cp, sizeof(int64_t) * (size_t)n);
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t p = Ap[j]; p < Ap[j + 1]; ++p) {
+      int32_t a = perm[Ai[p]], b = perm[j];
+      int32_t col = a < b ? a : b, row = a < b ? b : a;
+      int64_t q = next[col]++;
+      Ci[q] = row;
+      if (Cx) Cx[q] = Ax[p];
+    }
+  free(next);
+  /* sort rows within each column (insertion sort; columns are short) */
+  for (int64_t j = 0; j < n; ++j) {
+    for (int64_t p = Cp[j] + 1; p < Cp[j + 1]; ++p) {
+      int32_t r = Ci[p]; double v = Cx ? Cx[p] : 0.0; int64_t q = p - 1;
+      while (q >= Cp[j] && Ci[q] > r) { Ci[q + 1] = Ci[q]; if (Cx) Cx[q + 1] = Cx[q]; --q; }
+      Ci[q + 1] = r; if (Cx) Cx[q + 1] = v;
+    }
+  }
+  *Cp_out = Cp; *Ci_out = Ci; if (Cx_out) *Cx_out = Cx; else free(Cx);
+}
+
+/*
+ * O2: symbolic factorization by row-merge.  Computes parent and cc for every column.
+ * keep[j] != 0 (or keep == NULL && keep_all) retains struct(L_j) sorted in (*Sp, *Si).
+ * Structures of columns that are not kept are freed as soon as their parent consumed them.
+ */
+static int rowmerge(int64_t n, const int64_t* Cp, const int32_t* Ci, int32_t* parent, int32_t* cc,
+                    const char* keep, int keep_all, int64_t** Sp_out, int32_t** Si_out) {
+  int32_t** st = (int32_t**)calloc((size_t)n + 1, sizeof(int32_t*));
+  int32_t* len = (int32_t*)calloc((size_t)n + 1, sizeof(int32_t));
+  int32_t* mark = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  int32_t* buf = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  /* children lists: head/next over columns */
+  int32_t* chead = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  int32_t* cnext = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  int32_t* ctail = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  if (!st || !len || !mark || !buf || !chead || !cnext || !ctail) return -1;
+  for (int64_t j = 0; j < n; ++j) { mark[j] = -1; chead[j] = -1; ctail[j] = -1; cnext[j] = -1; }
+  for (int64_t j = 0; j < n; ++j) {
+    int32_t cnt = 0;
+    buf[cnt++] = (int32_t)j; mark[j] = (int32_t)j;
+    for (int64_t p = Cp[j]; p < Cp[j + 1]; ++p) {
+      int32_t i = Ci[p];
+      if (i > j && mark[i] != j) { mark[i] = (int32_t)j; buf[cnt++] = i; }
+    }
+    for (int32_t c = chead[j]; c != -1; c = cnext[c]) {
+      for (int32_t q = 0; q < len[c]; ++q) {
+        int32_t i = st[c][q];
+        if (i != c && mark[i] != j) { mark[i] = (int32_t)j; buf[cnt++] = i; }
+      }
+      if (!(keep_all || (keep && keep[c]))) { free(st[c]); st[c] = NULL; }
+    }
+    int32_t par = -1;
+    for (int32_t q = 1; q < cnt; ++q) if (par == -1 || buf[q] < par) par = buf[q];
+    parent[j] = par; cc[j] = cnt;
+    st[j] = (int32_t*)malloc(sizeof(int32_t) * (size_t)cnt);
+    memcpy(st[j], buf, sizeof(int32_t) * (size_t)cnt);
+    qsort(st[j], (size_t)cnt, sizeof(int32_t), cmp_i32);
+    len[j] = cnt;
+    if (par != -1) {  /* append j to parent's child list (ascending) */
+      if (ctail[par] == -1) chead[par] = (int32_t)j; else cnext[ctail[par]] = (int32_t)j;
+      ctail[par] = (int32_t)j;
+    }
+  }
+  int64_t* Sp = NULL; int32_t* Si = NULL;
+  if (Sp_out) {
+    Sp = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+    for (int64_t j = 0; j < n; ++j) Sp[j + 1] = Sp[j] + ((keep_all || (keep && keep[j])) ? len[j] : 0);
+    Si = (int32_t*)malloc(sizeof(int32_t) * (size_t)(Sp[n] ? Sp[n] : 1));
+    for (int64_t j = 0; j < n; ++j)
+      if (keep_all || (keep && keep[j])) memcpy(Si + Sp[j], st[j], sizeof(int32_t) * (size_t)len[j]);
+    *Sp_out = Sp; *Si_out = Si;
+  }
+  for (int64_t j = 0; j < n; ++j) free(st[j]);
+  free(st); free(len); free(mark); free(buf); free(chead); free(cnext); free(ctail);
+  return 0;
+}
+
+/* O3: postorder; post[k] = node numbered k. */
+static void postorder(int64_t n, const int32_t* parent, int32_t* post) {
+  int32_t* head = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  int32_t* next = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  int32_t* stack = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  for (int64_t j = 0; j < n; ++j) head[j] = -1;
+  /* children ascending: insert in descending order at the head */
+  for (int64_t j = n - 1; j >= 0; --j)
+    if (parent[j] != -1) { next[j] = head[parent[j]]; head[parent[j]] = (int32_t)j; }
+  int64_t k = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    if (parent[r] != -1) continue;
+    int64_t top = 0; stack[top++] = (int32_t)r;
+    while (top > 0) {
+      int32_t v = stack[top - 1];
+      int32_t c = head[v];
+      if (c == -1) { post[k++] = v; --top; }
+      else { head[v] = next[c]; stack[top++] = c; }
+    }
+  }
+  free(head); free(next); free(stack);
+}
+
+/* ---------------- lazy min-heap of (cost, id) for O6 ---------------- */
+typedef struct { int64_t cost; int32_t id; } hent;
+typedef struct { hent* a; int64_t n, cap; } heap_t;
+static int hless(hent x, hent y) { return x.cost < y.cost || (x.cost == y.cost && x.id < y.id); }
+static void hpush(heap_t* h, hent e) {
+  if (h->n == h->cap) { h->cap = h->cap ? 2 * h->cap : 1024; h->a = (hent*)realloc(h->a, sizeof(hent) * (size_t)h->cap); }
+  int64_t i = h->n++;
+  h->a[i] = e;
+  while (i > 0) { int64_t p = (i - 1) / 2; if (!hless(h->a[i], h->a[p])) break; hent t = h->a[i]; h->a[i] = h->a[p]; h->a[p] = t; i = p; }
+}
+static hent hpop(heap_t* h) {
+  hent top = h->a[0];
+  h->a[0] = h->a[--h->n];
+  int64_t i = 0;
+  for (;;) {
+    int64_t l = 2 * i + 1, r = l + 1, m = i;
+    if (l < h->n && hless(h->a[l], h->a[m])) m = l;
+    if (r < h->n && hless(h->a[r], h->a[m])) m = r;
+    if (m == i) break;
+    hent t = h->a[i]; h->a[i] = h->a[m]; h->a[m] = t; i = m;
+  }
+  return top;
+}
+static int32_t uf_find(int32_t* uf, int32_t x) {
+  int32_t r = x;
+  while (uf[r] != r) r = uf[r];
+  while (uf[x] != r) { int32_t nx = uf[x]; uf[x] = r; x = nx; }
+  return r;
+}
+
+/* ---------------- public API ---------------- */
+void orc_free(orc_t* o);
+
+/*
+ * Symbolic phase O1-O8.  rule: 0 fundamental, 1 maximal.  cap < 0 disables merging.
+ * keep_L: also build the exact structure of L in final numbering (needed by orc_numeric).
+ * values may be NULL (then orc_numeric is unavailable).
+ */
+orc_t* orc_symbolic(int64_t n, const int64_t* Ap, const int32_t* Ai, const double* Ax,
+                    const int32_t* perm, double cap, int rule, int keep_L) {
+  orc_t* o = (orc_t*)calloc(1, sizeof(orc_t));
+  o->n = n;
+  int32_t* ident = NULL;
+  if (!perm) { ident = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1)); for (int64_t i = 0; i < n; ++i) ident[i] = (int32_t)i; perm = ident; }
+  /* O1 */
+  int64_t *Cp; int32_t* Ci;
+  permute_lower(n, Ap, Ai, NULL, perm, &Cp, &Ci, NULL);
+  /* O2 on C */
+  int32_t* parent = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  int32_t* cc = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  rowmerge(n, Cp, Ci, parent, cc, NULL, 0, NULL, NULL);
+  /* O3 */
+  o->post = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  postorder(n, parent, o->post);
+  int32_t* ipost = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  for (int64_t k = 0; k < n; ++k) ipost[o->post[k]] = (int32_t)k;
+  o->parent3 = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  o->cc3 = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  for (int64_t j = 0; j < n; ++j) {
+    o->parent3[ipost[j]] = parent[j] == -1 ? -1 : ipost[parent[j]];
+    o->cc3[ipost[j]] = cc[j];
+  }
+  /* O4 */
+  o->nnzL = 0; o->flops = 0.0;
+  for (int64_t j = 0; j < n; ++j) { o->nnzL += o->cc3[j]; o->flops += (double)o->cc3[j] * (double)o->cc3[j]; }
+  /* O5 in O3 numbering */
+  int32_t* nchild = (int32_t*)calloc((size_t)n + 1, sizeof(int32_t));
+  for (int64_t j = 0; j < n; ++j) if (o->parent3[j] != -1) nchild[o->parent3[j]]++;
+  o->ffirst = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  int32_t* fsn = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));  /* column -> fundamental */
+  int32_t nf = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    int join = j > 0 && o->parent3[j - 1] == j && o->cc3[j - 1] == o->cc3[j] + 1 && (rule == 1 || nchild[j] == 1);
+    if (!join) o->ffirst[nf++] = (int32_t)j;
+    fsn[j] = nf - 1;
+  }
+  o->ffirst[nf] = (int32_t)n;
+  o->nfund = nf;
+  o->fparent = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+  for (int32_t f = 0; f < nf; ++f) {
+    int32_t last = o->ffirst[f + 1] - 1;
+    o->fparent[f] = o->parent3[last] == -1 ? -1 : fsn[o->parent3[last]];
+  }
+  /* rows of the fundamental heads: second row-merge on C3 = Q C Q^T keeping only head columns */
+  int64_t *C3p; int32_t* C3i;
+  {
+    int32_t* q = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    for (int64_t i = 0; i < n; ++i) q[i] = ipost[i];
+    permute_lower(n, Cp, Ci, NULL, q, &C3p, &C3i, NULL);
+    free(q);
+  }
+  char* keep = (char*)calloc((size_t)n + 1, 1);
+  for (int32_t f = 0; f < nf; ++f) keep[o->ffirst[f]] = 1;
+  int32_t* par2 = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  int32_t* cc2 = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  int64_t* Hp; int32_t* Hi;
+  rowmerge(n, C3p, C3i, par2, cc2, keep, 0, &Hp, &Hi);
+  for (int64_t j = 0; j < n; ++j)
+    if (par2[j] != o->parent3[j] || cc2[j] != o->cc3[j]) { /* self-check: relabelling must commute */
+      orc_free(o); o = NULL; goto done_early;
+    }
+  /* O6 greedy merge over the fundamental supernodal tree */
+  {
+    int64_t* k = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nf ? nf : 1));
+    int64_t* m = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nf ? nf : 1));
+    int32_t* uf = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    char* alive = (char*)malloc((size_t)(nf ? nf : 1));
+    for (int32_t f = 0; f < nf; ++f) {
+      k[f] = o->ffirst[f + 1] - o->ffirst[f];
+      m[f] = o->cc3[o->ffirst[f]];
+      uf[f] = f; alive[f] = 1;
+    }
+    o->merge_child = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    o->merge_parent = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    o->merge_cost = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nf ? nf : 1));
+    heap_t h = {0};
+    double budget = cap * (double)o->nnzL;
+    if (cap >= 0) {
+      for (int32_t f = 0; f < nf; ++f)
+        if (o->fparent[f] != -1) {
+          int32_t P = o->fparent[f];
+          hent e = {k[f] * (k[f] + m[P] - m[f]), f};
+          hpush(&h, e);
+        }
+    }
+    int64_t added = 0;
+    while (h.n > 0) {
+      hent e = hpop(&h);
+      int32_t J = e.id;
+      if (!alive[J]) continue;
+      int32_t P = uf_find(uf, o->fparent[J]);
+      int64_t cost = k[J] * (k[J] + m[P] - m[J]);
+      if (cost != e.cost) { hent e2 = {cost, J}; hpush(&h, e2); continue; }
+      if ((double)(added + cost) > budget) break;   /* never exceed the cap */
+      o->merge_child[o->nmerges] = J; o->merge_parent[o->nmerges] = P; o->merge_cost[o->nmerges] = cost; o->nmerges++;
+      added += cost;
+      m[P] = k[J] + m[P];
+      k[P] = k[J] + k[P];
+      alive[J] = 0; uf[J] = P;
+    }
+    free(h.a);
+    o->added = added;
+    o->fgroup = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    for (int32_t f = 0; f < nf; ++f) o->fgroup[f] = uf_find(uf, f);
+    free(k); free(m); free(uf); free(alive);
+  }
+  /* O7 final permutation: postorder of the merged tree */
+  {
+    /* group ids are the fundamental indices of alive tops */
+    int32_t* gparent = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    int32_t* gmin = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    for (int32_t f = 0; f < nf; ++f) { gparent[f] = -2; gmin[f] = INT32_MAX; }
+    for (int32_t f = 0; f < nf; ++f) {
+      int32_t g = o->fgroup[f];
+      if (o->ffirst[f] < gmin[g]) gmin[g] = o->ffirst[f];
+      if (g == f) gparent[g] = o->fparent[f] == -1 ? -1 : o->fgroup[o->fparent[f]];
+    }
+    /* groups sorted by smallest O3 column: order children/roots by gmin */
+    int32_t ng = 0;
+    int32_t* gl = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    for (int32_t f = 0; f < nf; ++f) if (o->fgroup[f] == f) gl[ng++] = f;
+    /* sort gl by gmin (simple: gmin values are distinct column indices) */
+    int32_t* bycol = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    for (int64_t j = 0; j < n; ++j) bycol[j] = -1;
+    for (int32_t a = 0; a < ng; ++a) bycol[gmin[gl[a]]] = gl[a];
+    ng = 0;
+    for (int64_t j = 0; j < n; ++j) if (bycol[j] != -1) gl[ng++] = bycol[j];
+    free(bycol);
+    /* children lists in gmin-ascending order */
+    int32_t* head = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    int32_t* nxt = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    for (int32_t f = 0; f < nf; ++f) head[f] = -1;
+    for (int32_t a = ng - 1; a >= 0; --a) {
+      int32_t g = gl[a];
+      if (gparent[g] >= 0) { nxt[g] = head[gparent[g]]; head[gparent[g]] = g; }
+    }
+    /* member columns of each group, ascending */
+    int64_t* gcnt = (int64_t*)calloc((size_t)nf + 1, sizeof(int64_t));
+    for (int64_t j = 0; j < n; ++j) gcnt[o->fgroup[fsn[j]] + 1]++;
+    for (int32_t f = 0; f < nf; ++f) gcnt[f + 1] += gcnt[f];
+    int32_t* gcols = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    int64_t* gpos = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nf + 1));
+    memcpy(gpos, gcnt, sizeof(int64_t) * (size_t)(nf + 1));
+    for (int64_t j = 0; j < n; ++j) gcols[gpos[o->fgroup[fsn[j]]]++] = (int32_t)j;  /* ascending j */
+    free(gpos);
+    o->o7 = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    o->sfirst = (int32_t*)malloc(sizeof(int32_t) * (size_t)(ng + 1));
+    int32_t* gsuper = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    int32_t* stack = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    int32_t* hd = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    memcpy(hd, head, sizeof(int32_t) * (size_t)(nf ? nf : 1));
+    int32_t counter = 0, ns = 0;
+    for (int32_t a = 0; a < ng; ++a) {
+      int32_t r = gl[a];
+      if (gparent[r] != -1) continue;
+      int32_t top = 0; stack[top++] = r;
+      while (top > 0) {
+        int32_t v = stack[top - 1];
+        int32_t c = hd[v];
+        if (c == -1) {
+          --top;
+          gsuper[v] = ns; o->sfirst[ns++] = counter;
+          for (int64_t p = gcnt[v]; p < gcnt[v + 1]; ++p) o->o7[gcols[p]] = counter++;
+        } else { hd[v] = nxt[c]; stack[top++] = c; }
+      }
+    }
+    o->sfirst[ns] = counter;
+    o->nsuper = ns;
+    o->sparent = (int32_t*)malloc(sizeof(int32_t) * (size_t)(ns ? ns : 1));
+    for (int32_t a = 0; a < ng; ++a) {
+      int32_t g = gl[a];
+      o->sparent[gsuper[g]] = gparent[g] == -1 ? -1 : gsuper[gparent[g]];
+    }
+    /* rows(J) = cols(J) u rows(top fundamental member) in final numbering */
+    o->rows_ptr = (int64_t*)calloc((size_t)ns + 1, sizeof(int64_t));
+    int32_t* gof = (int32_t*)malloc(sizeof(int32_t) * (size_t)(ns ? ns : 1)); /* super -> group id */
+    for (int32_t a = 0; a < ng; ++a) gof[gsuper[gl[a]]] = gl[a];
+    for (int32_t s = 0; s < ns; ++s) {
+      int32_t g = gof[s];
+      int64_t kg = gcnt[g + 1] - gcnt[g];
+      int64_t mtop = Hp[o->ffirst[g] + 1] - Hp[o->ffirst[g]];
+      int64_t ktop = o->ffirst[g + 1] - o->ffirst[g];
+      o->rows_ptr[s + 1] = o->rows_ptr[s] + (kg - ktop) + mtop;
+    }
+    o->rows = (int32_t*)malloc(sizeof(int32_t) * (size_t)(o->rows_ptr[ns] ? o->rows_ptr[ns] : 1));
+    for (int32_t s = 0; s < ns; ++s) {
+      int32_t g = gof[s];
+      int64_t w = o->rows_ptr[s];
+      for (int64_t p = gcnt[g]; p < gcnt[g + 1]; ++p) {
+        int32_t c = gcols[p];
+        if (fsn[c] != g) o->rows[w++] = o->o7[c];
+      }
+      for (int64_t p = Hp[o->ffirst[g]]; p < Hp[o->ffirst[g] + 1]; ++p) o->rows[w++] = o->o7[Hi[p]];
+      qsort(o->rows + o->rows_ptr[s], (size_t)(w - o->rows_ptr[s]), sizeof(int32_t), cmp_i32);
+    }
+    free(gof); free(stack); free(hd); free(head); free(nxt); free(gcnt); free(gcols); free(gsuper);
+    free(gparent); free(gmin); free(gl);
+  }
+  /* final permutation and exact etree / cc in final numbering */
+  o->perm_final = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  for (int64_t i = 0; i < n; ++i) o->perm_final[i] = o->o7[ipost[perm[i]]];
+  o->parent_final = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  o->cc_final = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  for (int64_t j = 0; j < n; ++j) {
+    o->parent_final[o->o7[j]] = o->parent3[j] == -1 ? -1 : o->o7[o->parent3[j]];
+    o->cc_final[o->o7[j]] = o->cc3[j];
+  }
+  /* O8 relind */
+  {
+    int32_t ns = o->nsuper;
+    int32_t* snode = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    for (int32_t s = 0; s < ns; ++s) for (int32_t c = o->sfirst[s]; c < o->sfirst[s + 1]; ++c) snode[c] = s;
+    o->rel_ptr = (int64_t*)calloc((size_t)ns + 1, sizeof(int64_t));
+    /* count pairs and relind length */
+    int64_t np = 0, nr = 0;
+    for (int32_t J = 0; J < ns; ++J) {
+      int64_t k = o->sfirst[J + 1] - o->sfirst[J];
+      int64_t m = o->rows_ptr[J + 1] - o->rows_ptr[J];
+      int32_t last = -1;
+      for (int64_t q = k; q < m; ++q) {
+        int32_t P = snode[o->rows[o->rows_ptr[J] + q]];
+        if (P != last) { np++; nr += m - q; last = P; }
+      }
+      o->rel_ptr[J + 1] = np;
+    }
+    o->npairs = np;
+    o->rel_anc = (int32_t*)malloc(sizeof(int32_t) * (size_t)(np ? np : 1));
+    o->rel_q0 = (int32_t*)malloc(sizeof(int32_t) * (size_t)(np ? np : 1));
+    o->rel_off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(np + 1));
+    o->relind = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nr ? nr : 1));
+    int32_t* indmap = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    int64_t pi = 0, ri = 0;
+    for (int32_t J = 0; J < ns; ++J) {
+      int64_t k = o->sfirst[J + 1] - o->sfirst[J];
+      int64_t m = o->rows_ptr[J + 1] - o->rows_ptr[J];
+      const int32_t* rJ = o->rows + o->rows_ptr[J];
+      int32_t last = -1;
+      for (int64_t q = k; q < m; ++q) {
+        int32_t P = snode[rJ[q]];
+        if (P == last) continue;
+        last = P;
+        int64_t mP = o->rows_ptr[P + 1] - o->rows_ptr[P];
+        const int32_t* rP = o->rows + o->rows_ptr[P];
+        for (int64_t x = 0; x < mP; ++x) indmap[rP[x]] = (int32_t)(mP - 1 - x);   /* indmap */
+        o->rel_anc[pi] = P; o->rel_q0[pi] = (int32_t)q; o->rel_off[pi] = ri;
+        for (int64_t qq = q; qq < m; ++qq) o->relind[ri++] = indmap[rJ[qq]];
+        ++pi;
+      }
+    }
+    o->rel_off[np] = ri;
+    free(indmap); free(snode);
+  }
+  if (keep_L) {
+    /* exact structure of L for C_f = P_f A P_f^T, plus the permuted values */
+    permute_lower(n, Ap, Ai, Ax, o->perm_final, &o->Cp, &o->Ci, Ax ? &o->Cx : NULL);
+    int32_t* p4 = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    int32_t* c4 = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    rowmerge(n, o->Cp, o->Ci, p4, c4, NULL, 1, &o->Lp, &o->Li);
+    for (int64_t j = 0; j < n; ++j)
+      if (p4[j] != o->parent_final[j] || c4[j] != o->cc_final[j]) { free(p4); free(c4); orc_free(o); o = NULL; goto done_early; }
+    free(p4); free(c4);
+  }
+done_early:
+  free(nchild); free(fsn); free(keep); free(par2); free(cc2); free(Hp); free(Hi);
+  free(C3p); free(C3i); free(Cp); free(Ci); free(parent); free(cc); free(ipost); free(ident);
+  return o;
+}
+
+/*
+ * O9: scalar left-looking column Cholesky on the exact structure (George-Liu row lists).
+ * Returns 0, or -3 with *fail_col = first column whose pivot is not > 0.
+ * ncols < n factors only the leading ncols columns' dependencies... (full factor when ncols = n).
+ */
+int orc_numeric(orc_t* o, int64_t* fail_col) {
+  int64_t n = o->n;
+  *fail_col = -1;
+  if (!o->Lp || !o->Cx) return -2;
+  if (!o->Lx) o->Lx = (double*)malloc(sizeof(double) * (size_t)(o->Lp[n] ? o->Lp[n] : 1));
+  double* w = (double*)calloc((size_t)n + 1, sizeof(double));
+  int32_t* head = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  int32_t* next = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  int64_t* pos = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int32_t* list = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  for (int64_t j = 0; j < n; ++j) head[j] = -1;
+  const int64_t* Lp = o->Lp; const int32_t* Li = o->Li; double* Lx = o->Lx;
+  int rc = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    /* w = C_f(:, j) (lower part) */
+    for (int64_t p = o->Cp[j]; p < o->Cp[j + 1]; ++p) w[o->Ci[p]] = o->Cx[p];
+    /* the columns k < j with L(j,k) != 0, ascending */
+    int32_t cnt = 0;
+    for (int32_t k = head[j]; k != -1; k = next[k]) list[cnt++] = k;
+    qsort(list, (size_t)cnt, sizeof(int32_t), cmp_i32);
+    head[j] = -1;
+    for (int32_t a = 0; a < cnt; ++a) {
+      int32_t k = list[a];
+      int64_t pk = pos[k];            /* Li[pk] == j */
+      double ljk = Lx[pk];
+      for (int64_t p = pk; p < Lp[k + 1]; ++p) w[Li[p]] -= Lx[p] * ljk;
+      /* move k to the list of its next row */
+      if (pk + 1 < Lp[k + 1]) { pos[k] = pk + 1; int32_t r = Li[pk + 1]; next[k] = head[r]; head[r] = k; }
+    }
+    double d = w[j];
+    if (!(d > 0.0)) { *fail_col = j; rc = -3; break; }
+    double ljj = sqrt(d);
+    Lx[Lp[j]] = ljj;  /* Li[Lp[j]] == j */
+    w[j] = 0.0;
+    for (int64_t p = Lp[j] + 1; p < Lp[j + 1]; ++p) { Lx[p] = w[Li[p]] / ljj; w[Li[p]] = 0.0; }
+    if (Lp[j] + 1 < Lp[j + 1]) { pos[j] = Lp[j] + 1; int32_t r = Li[Lp[j] + 1]; next[j] = head[r]; head[r] = (int32_t)j; }
+  }
+  free(w); free(head); free(next); free(pos); free(list);
+  o->numeric_done = rc == 0;
+  return rc;
+}
+
+/* O10: x = P_f^T L^{-T} L^{-1} P_f b */
+int orc_solve(const orc_t* o, const double* b, double* x) {
+  if (!o->numeric_done) return -7;
+  int64_t n = o->n;
+  double* y = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
+  for (int64_t i = 0; i < n; ++i) y[o->perm_final[i]] = b[i];
+  const int64_t* Lp = o->Lp; const int32_t* Li = o->Li; const double* Lx = o->Lx;
+  for (int64_t j = 0; j < n; ++j) {
+    y[j] /= Lx[Lp[j]];
+    for (int64_t p = Lp[j] + 1; p < Lp[j + 1]; ++p) y[Li[p]] -= Lx[p] * y[j];
+  }
+  for (int64_t j = n - 1; j >= 0; --j) {
+    for (int64_t p = Lp[j] + 1; p < Lp[j + 1]; ++p) y[j] -= Lx[p] * y[Li[p]];
+    y[j] /= Lx[Lp[j]];
+  }
+  for (int64_t i = 0; i < n; ++i) x[i] = y[o->perm_final[i]];
+  free(y);
+  return 0;
+}
+
+void orc_free(orc_t* o) {
+  if (!o) return;
+  free(o->post); free(o->parent3); free(o->cc3); free(o->ffirst); free(o->fparent); free(o->fgroup);
+  free(o->merge_child); free(o->merge_parent); free(o->merge_cost);
+  free(o->perm_final); free(o->o7); free(o->sfirst); free(o->sparent); free(o->rows_ptr); free(o->rows);
+  free(o->rel_ptr); free(o->rel_anc); free(o->rel_q0); free(o->rel_off); free(o->relind);
+  free(o->parent_final); free(o->cc_final); free(o->Lp); free(o->Li); free(o->Lx);
+  free(o->Cp); free(o->Ci); free(o->Cx);
+  free(o);
+}
+
+/* ---------------- accessors (for the ctypes wrapper) ---------------- */
+#define GET(name, type) type orc_get_##name(const orc_t* o) { return o->name; }
+GET(n, int64_t) GET(nnzL, int64_t) GET(flops, double) GET(nfund, int32_t) GET(added, int64_t)
+GET(nmerges, int32_t) GET(nsuper, int32_t) GET(npairs, int64_t)
+#define PTR(name, type) type* orc_ptr_##name(const orc_t* o) { return o->name; }
+PTR(post, int32_t) PTR(parent3, int32_t) PTR(cc3, int32_t) PTR(ffirst, int32_t) PTR(fparent, int32_t)
+PTR(fgroup, int32_t) PTR(merge_child, int32_t) PTR(merge_parent, int32_t) PTR(merge_cost, int64_t)
+PTR(perm_final, int32_t) PTR(o7, int32_t) PTR(sfirst, int32_t) PTR(sparent, int32_t) PTR(rows_ptr, int64_t)
+PTR(rows, int32_t) PTR(rel_ptr, int64_t) PTR(rel_anc, int32_t) PTR(rel_q0, int32_t) PTR(rel_off, int64_t)
+PTR(relind, int32_t) PTR(parent_final, int32_t) PTR(cc_final, int32_t) PTR(Lp, int64_t) PTR(Li, int32_t)
+PTR(Lx, double)
