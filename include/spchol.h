@@ -1,0 +1,202 @@
+/*
+ * spchol.h — C ABI of the B200-native right-looking supernodal sparse Cholesky (RL) library.
+ *
+ * Method: Karsavuran, Ng, Peyton, "GPU Accelerated Sparse Cholesky Factorization"
+ * (arXiv 2409.14009).  Citations "P:n" are lines of that paper's PAPER.md, "S:n" lines of
+ * SPEC.md (interfaces only), "R#" the readings listed in DESIGN.md.
+ *
+ * The problem: solve A x = b for sparse symmetric positive definite A via the
+ * Cholesky factorization A = L L^T "using a right-looking approach", the "resulting triangular
+ * factors ... used to compute the solution".
+ *
+ * Conventions for every call:
+ *   - extern "C"; no C++ exception crosses the ABI; every call returns an int status
+ *     (SPCHOL_OK = 0, negative = error) and on error sets a thread-local message readable with
+ *     spchol_last_error().
+ *   - Pointers are HOST pointers unless the name or comment says "device" (d_ prefix).
+ *   - Index widths: column pointers and every L / panel offset are int64 (nnz(L) exceeds 2^31 on
+ *     the 3-dof config); row indices and permutations are int32 (n < 2^31).
+ *   - One handle must not be used from two threads at once.  Different handles are independent.
+ */
+#ifndef SPCHOL_H_
+#define SPCHOL_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct spchol_handle spchol_handle;
+
+enum {
+  SPCHOL_OK = 0,
+  SPCHOL_ERR_DIMENSION = -1,   /* n < 0, or array lengths inconsistent with n             */
+  SPCHOL_ERR_VALIDATION = -2,  /* input violates the CSC contract, perm not a bijection   */
+  SPCHOL_ERR_NOT_SPD = -3,     /* a pivot was <= 0 or NaN                  */
+  SPCHOL_ERR_DEVICE_OOM = -4,  /* device allocation failed (panels do not fit)     */
+  SPCHOL_ERR_CUDA = -5,        /* any other CUDA runtime error                            */
+  SPCHOL_ERR_NCCL = -6,        /* multi-GPU exchange failed                               */
+  SPCHOL_ERR_STATE = -7        /* call out of order (solve before a successful factor)    */
+};
+
+typedef struct {
+  double merge_cap;     /* supernode merging stops before the cumulative added storage exceeds
+                           merge_cap * nnz(L) (reading R4).  Default 0.25.
+                           A negative value disables merging (fundamental partition). */
+  int32_t device;       /* CUDA device ordinal used by this handle. Default 0.  A negative value
+                           makes a host-only handle: analyze runs the symbolic phase and the
+                           launch plan but allocates nothing on a device; factor/solve return
+                           SPCHOL_ERR_STATE (used to check the symbolic phase without a GPU). */
+  int32_t block;        /* column block width of the blocked cdiv (POTRF/TRSM) for large supernodes;
+                           0 = library default (64).  Must be a multiple of 8 in [8, 64]. */
+  int32_t small_max_k;  /* supernodes with k <= small_max_k and a panel that fits shared memory
+                           are factored by the fused one-CTA-per-supernode kernel; 0 = default,
+                           -1 = never. */
+  int32_t use_graph;    /* 1 = capture the factor's launch sequence in a CUDA graph (default 1). */
+} spchol_options;
+
+/* Fill *opt with the defaults above. */
+void spchol_default_options(spchol_options* opt);
+
+/*
+ * spchol_analyze — symbolic analysis (integer only, host) + device setup.
+ *
+ * Input A: n x n, lower triangle in CSC, 0-based. colptr[n+1] (int64, colptr[0]=0,
+ * non-decreasing), rowidx[colptr[n]] (int32): within each column rows strictly increasing, first
+ * entry of column j is the diagonal j (always stored), all rows in [j, n).  values[colptr[n]]
+ * (FP64) may be NULL (then spchol_set_values must be called before factor).  A is taken as
+ * lower + lower^T - diag.
+ * perm: old -> new fill-reducing ordering (e.g. nested dissection), a bijection of
+ * [0,n); NULL = identity.
+ *
+ * Steps: permute -> elimination tree -> postorder ->
+ * column counts -> fundamental supernodes [LNP93] -> greedy child-parent merging at
+ * merge_cap -> final permutation P_f (postorder of the merged supernodal tree) ->
+ * rows(J) -> relative indices relind(J,P) via indmap -> level sets of the
+ * supernodal tree, panel layout in one device arena, launch plan.  A's values (if given) are
+ * uploaded to the device.
+ *
+ * Ownership: analyze deep-copies everything it needs; the caller may free its arrays on return.
+ * The handle owns all host and device memory; spchol_destroy frees it.
+ * Errors: DIMENSION (n < 0), VALIDATION (contract violations above; perm not a bijection),
+ * DEVICE_OOM, CUDA.  On error *out is set to NULL.
+ */
+int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* rowidx, const double* values,
+                   const int32_t* perm, const spchol_options* opt, spchol_handle** out);
+
+/* Replace A's values (same pattern as analyze; host array of colptr[n] doubles, copied to the
+ * device on the handle's stream, synchronously w.r.t. the host buffer). */
+int spchol_set_values(spchol_handle* h, const double* values);
+
+/* Same, from a device array (d_values, colptr[n] doubles), enqueued on the handle's stream. */
+int spchol_set_values_device(spchol_handle* h, const double* d_values);
+
+/* CUDA stream (cudaStream_t; NULL = the handle's own non-blocking stream, the default) on which
+ * factor/solve enqueue their work.  Events recorded by the caller on the same stream bracket exactly that work. */
+int spchol_set_stream(spchol_handle* h, void* stream);
+
+/*
+ * spchol_factor_async — enqueue the numeric RL factorization of
+ * C_f = P_f A P_f^T on the handle's stream and return without synchronizing:
+ *   a1 panel init: panels := 0, A's entries scattered into their supernode panels;
+ *   per level of the supernodal elimination tree (leaves first), for every supernode J in it:
+ *   a3/a4 cdiv(J): POTRF of the k_J x k_J diagonal block, TRSM of the t_J x k_J rest;
+ *   a5/a6 U_J = L_{R,J} L_{R,J}^T (DSYRK) assembled into the ancestor panels through
+ *   relind, fused in one kernel (no U workspace).
+ * A failing pivot is recorded on the device (a7); read it with spchol_factor_status.
+ */
+int spchol_factor_async(spchol_handle* h);
+
+/*
+ * spchol_factor_status — synchronize the handle's stream; *fail_col = first failing column in
+ * the final numbering (-1 if none), *fail_col_orig = the same column in the caller's original
+ * numbering (-1 if none).  Returns SPCHOL_OK or SPCHOL_ERR_NOT_SPD (reading R8).
+ * Either pointer may be NULL.
+ */
+int spchol_factor_status(spchol_handle* h, int64_t* fail_col, int64_t* fail_col_orig);
+
+/* spchol_factor = spchol_factor_async + spchol_factor_status. */
+int spchol_factor(spchol_handle* h, int64_t* fail_col, int64_t* fail_col_orig);
+
+/*
+ * spchol_solve — x = A^{-1} b with the computed factor: y = P_f b; L y' = y (forward, supernodes
+ * leaves first); L^T z = y' (backward, root first); x = P_f^T z.  b, x: host arrays,
+ * column-major n x nrhs with leading dimension ld >= n; b and x may alias.
+ * Errors: STATE before a successful factor, DIMENSION on nrhs < 1 or ld < n.
+ */
+int spchol_solve(spchol_handle* h, const double* b, double* x, int32_t nrhs, int64_t ld);
+
+/* Same with device arrays, enqueued on the handle's stream (no synchronization). */
+int spchol_solve_device(spchol_handle* h, const double* d_b, double* d_x, int32_t nrhs, int64_t ld);
+
+/* ---------------- introspection / parity exports ---------------- */
+enum {
+  SPCHOL_Q_N = 0,            /* n                                                         */
+  SPCHOL_Q_NNZ_A = 1,        /* stored entries of A's lower triangle                       */
+  SPCHOL_Q_NNZ_L = 2,        /* nnz(L) of the exact factor, diagonal included              */
+  SPCHOL_Q_NFUND = 3,        /* fundamental supernodes                                     */
+  SPCHOL_Q_NSUPER = 4,       /* supernodes after merging                                   */
+  SPCHOL_Q_ADDED = 5,        /* stored entries added by merging                            */
+  SPCHOL_Q_NLEVELS = 6,      /* levels of the merged supernodal tree                       */
+  SPCHOL_Q_ROWS_LEN = 7,     /* sum_J m_J (length of the rows array)                       */
+  SPCHOL_Q_NPAIRS = 8,       /* (J, ancestor P) pairs with a relind vector                 */
+  SPCHOL_Q_RELIND_LEN = 9,   /* total relind entries                                       */
+  SPCHOL_Q_PANEL_DOUBLES = 10, /* doubles in the device panel arena (incl. ld padding)     */
+  SPCHOL_Q_NMERGES = 11,     /* merges applied                                             */
+  SPCHOL_Q_FLOPS_EXACT = 12, /* sum_j cc_j^2 (the metric's flop count)                     */
+  SPCHOL_Q_FLOPS_EXEC = 13,  /* flops of the supernodal algorithm incl. padding             */
+  SPCHOL_Q_LAUNCHES = 14,    /* kernels launched by one factor                              */
+  SPCHOL_Q_UPDATE_ENTRIES = 15 /* sum_J t_J (t_J+1)/2 scattered update entries              */
+};
+int spchol_query(const spchol_handle* h, int key, int64_t* value);
+
+/*
+ * Integer symbolic arrays (the bit-exact parity contract).  Any pointer may be NULL (skipped).
+ * Sizes: post[n] (O3 postorder: post[k] = the user-permuted index numbered k), parent3[n] and
+ * cc3[n] (etree / column counts in postorder numbering), ffirst[NFUND+1] (fundamental
+ * partition, postorder numbering), fgroup[NFUND] (fundamental -> merged group = fundamental
+ * index of the group's top), perm_final[n] (P_f, old -> final), sfirst[NSUPER+1], sparent[NSUPER],
+ * rows_ptr[NSUPER+1], rows[ROWS_LEN] (final numbering, ascending), rel_ptr[NSUPER+1] (pairs of J),
+ * rel_anc[NPAIRS], rel_q0[NPAIRS] (first row index q in rows(J) with rows(J)[q] >= f_P),
+ * rel_off[NPAIRS+1], relind[RELIND_LEN], parent_final[n], cc_final[n], level[NSUPER].
+ */
+int spchol_export_symbolic(const spchol_handle* h, int32_t* post, int32_t* parent3, int32_t* cc3,
+                           int32_t* ffirst, int32_t* fgroup, int32_t* perm_final, int32_t* sfirst,
+                           int32_t* sparent, int64_t* rows_ptr, int32_t* rows, int64_t* rel_ptr,
+                           int32_t* rel_anc, int32_t* rel_q0, int64_t* rel_off, int32_t* relind,
+                           int32_t* parent_final, int32_t* cc_final, int32_t* level);
+
+/*
+ * Copy the device panels back.  panel_off[NSUPER+1] (doubles; panel J occupies
+ * [panel_off[J], panel_off[J+1]), column-major with leading dimension ld[J] >= m_J),
+ * ld[NSUPER], panels[PANEL_DOUBLES].  After factor, panel J column c (0 <= c < k_J), row q
+ * (c <= q < m_J) holds L(rows(J)[q], sfirst[J] + c); entries inside the panel but outside the
+ * exact pattern of L ("padding") are exactly +-0.0.  Synchronizes the stream.
+ */
+int spchol_export_panels(const spchol_handle* h, int64_t* panel_off, int32_t* ld, double* panels);
+
+/* Copy panel J (panel_off[J+1]-panel_off[J] doubles, layout as above) to out.  Synchronizes. */
+int spchol_export_panel(const spchol_handle* h, int32_t J, double* out);
+
+/* diag[j] = L(j,j) for every final column j (n doubles; log det A = 2 sum log diag).
+ * Synchronizes the stream. */
+int spchol_export_diagonal(spchol_handle* h, double* diag);
+
+/* Kernel timing (CUDA events bracketing every launch of each kernel class on the handle's
+ * stream while enabled; disabled by default and incompatible with graph replay, which is
+ * bypassed while enabled).  kind: 0 = fused small-supernode kernel, 1 = POTRF, 2 = TRSM,
+ * 3 = in-panel update GEMM, 4 = SYRK/GEMM + relind scatter (U_J), 5 = panel init.
+ * Returns launches, summed milliseconds, algorithmic flops and bytes of that class since the last
+ * reset.  spchol_kernel_stats synchronizes the stream. */
+int spchol_enable_kernel_timing(spchol_handle* h, int enable);
+int spchol_kernel_stats(spchol_handle* h, int kind, int64_t* launches, double* ms, double* flops,
+                        double* bytes);
+
+void spchol_destroy(spchol_handle* h);
+const char* spchol_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPCHOL_H_ */

@@ -1,0 +1,58 @@
+// sm_100a device kernels of the numeric RL factorization (arXiv 2409.14009, §II.A "RL").
+// P:n = PAPER.md line n.  All arithmetic is FP64 ("D" BLAS).
+//
+//   potrf_kernel        a3: cdiv POTRF of one <=64-column diagonal block in shared memory, plus its
+//                       triangular inverse (used by TRSM-as-GEMM)               ("DPOTRF")
+//   gemm_kernel<MODE>   FP64 DMMA (mma.sync m8n8k4) 64x64 tile, cp.async 3-stage smem pipeline
+//     MODE_TRSM         a4: L_{R,b} = A_{R,b} L_bb^{-T}                          ("DTRSM")
+//     MODE_LOCAL        right-looking update of the supernode's own trailing columns
+//     MODE_SCATTER      a5+a6: U_J = L_{R,J} L_{R,J}^T ("DSYRK") with the relind assembly
+//                        fused into the epilogue: FP64 RED into ancestors
+//   init_scatter        a1: A's entries into the zeroed panel arena
+//   solve kernels       forward / backward supernodal triangular solves
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace spchol {
+
+// Panel J: column-major m x k rectangle at panels + off, leading dimension ld (even, >= m).
+struct SnInfo {
+  long long off;
+  int ld, m, k, ucol;  // ucol: first U-column descriptor of J (see MODE_SCATTER)
+};
+// A GEMM tile task; meaning of the fields per mode is documented in gemm_kernel.
+struct GTask {
+  int sn, r0, s0, c0, nb, slot;
+};
+struct PTask {
+  int sn, c0, nb, slot;
+};
+
+enum { MODE_LOCAL = 0, MODE_TRSM = 1, MODE_SCATTER = 2 };
+
+constexpr int TILE = 64;           // CTA tile edge (rows and columns)
+constexpr int BK = 32;             // K chunk per pipeline stage
+constexpr int STAGES = 3;          // cp.async pipeline depth
+constexpr int LDS = TILE + 8;      // smem column stride (doubles): 8 mod 16 -> conflict-free DMMA fragments
+constexpr int GEMM_THREADS = 128;  // 4 warps, 2x2, warp tile 32x32
+constexpr int GEMM_SMEM = 2 * STAGES * BK * LDS * (int)sizeof(double);
+constexpr int NBMAX = 64;          // cdiv block width
+constexpr int POTRF_THREADS = 256;
+constexpr int POTRF_SMEM = 2 * NBMAX * (NBMAX + 1) * (int)sizeof(double);
+
+void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels,
+                 const double* linv, const long long* ucol_base, const long long* ucol_map,
+                 const int* posmap, cudaStream_t st);
+void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels,
+                  double* linv, unsigned long long* fail, cudaStream_t st);
+void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st);
+void launch_solve_fwd(const int* sns, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
+                      const int* rows, const double* panels, double* y, cudaStream_t st);
+void launch_solve_bwd(const int* sns, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
+                      const int* rows, const double* panels, double* y, cudaStream_t st);
+void launch_permute(const int* perm, const double* in, double* out, long long n, int inverse, cudaStream_t st);
+void launch_gather(const double* src, const long long* idx, double* out, long long n, cudaStream_t st);
+cudaError_t kernels_init_attributes();
+
+}  // namespace spchol

@@ -1,0 +1,103 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle — run on a B200 (-m gpu)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+import paper_2409_14009_b200 as sp
+from helpers import backward_error, logdet_from_diag, lower_panel_mask, panel_index_of_pattern
+from test_oracle_pins import grid_logdet
+
+pytestmark = pytest.mark.gpu
+
+SYM_KEYS = ["post", "parent3", "cc3", "ffirst", "fgroup", "perm_final", "sfirst", "sparent", "rows_ptr", "rows",
+            "rel_ptr", "rel_anc", "rel_q0", "rel_off", "relind", "parent_final", "cc_final"]
+TOL_L = 1e-10      # north_star: max|L_gpu - L_oracle| / max|L| <= 1e-10
+TOL_BERR = 1e-12   # north_star: ||Ax-b|| / (||A|| ||x||) <= 1e-12
+
+
+def run_parity(prob, **opts):
+    o = oracle.Oracle.from_problem(prob)
+    s_or = o.symbolic()
+    assert o.factor() == -1
+    Lp, Li, Lx = o.L_csc()
+    with sp.Solver.from_problem(prob, **opts) as h:
+        s_gpu = h.spchol_export_symbolic()
+        for k in SYM_KEYS:                                   # bit-exact symbolic
+            assert np.array_equal(s_gpu[k], s_or[k]), k
+        assert h.spchol_factor() == (-1, -1)
+        off, ld, pan = h.spchol_export_panels()
+        idx = panel_index_of_pattern(s_gpu, off, ld, Lp, Li)
+        err = np.abs(pan[idx] - Lx).max() / np.abs(Lx).max()
+        assert err <= TOL_L, err
+        mask = lower_panel_mask(s_gpu, off, ld, len(pan))
+        mask[idx] = False                                    # padding = lower panel part outside the pattern
+        assert np.all(pan[mask] == 0.0), "padding entries must stay exactly 0"
+        xstar, b = gen.rhs(prob)
+        x = h.spchol_solve(b)
+        assert backward_error(prob, x, b) <= TOL_BERR
+        diag = h.spchol_export_diagonal()
+        assert np.array_equal(diag, pan[off[:-1][np.repeat(np.arange(len(ld)), np.diff(s_gpu["sfirst"]))]
+                                         + (np.arange(prob.n) - np.repeat(s_gpu["sfirst"][:-1], np.diff(s_gpu["sfirst"])))
+                                         * (np.repeat(ld, np.diff(s_gpu["sfirst"])).astype(np.int64) + 1)])
+    return err
+
+
+@pytest.mark.parametrize("name", ["C1", "T1", "T2", "T3", "S2", "S3", "S4", "S5"])
+def test_parity_configs(name):
+    run_parity(gen.make(name))
+
+
+@pytest.mark.parametrize("block", [8, 16, 24, 40])
+def test_parity_block_sizes(block):
+    """cdiv block widths that leave ragged block columns (k not a multiple of the block)."""
+    run_parity(gen.make("S5"), block=block)
+    run_parity(gen.make("T3"), block=block)
+
+
+@pytest.mark.parametrize("trial", range(0, 40))
+def test_parity_random_corpus(trial):
+    run_parity(gen.random_spd(trial))
+
+
+def test_parity_no_graph_and_refactor():
+    p = gen.make("S4")
+    with sp.Solver.from_problem(p, use_graph=0) as h:
+        h.spchol_factor()
+        d1 = h.spchol_export_diagonal()
+        h.spchol_factor()            # refactor with the same values: identical up to RED ordering
+        d2 = h.spchol_export_diagonal()
+        assert np.abs(d1 - d2).max() <= 1e-12 * np.abs(d1).max()
+        ref = grid_logdet(27, (20, 20, 20), 1)
+        assert abs(logdet_from_diag(d1) - ref) <= 1e-10 * abs(ref)
+
+
+@pytest.mark.parametrize("name", ["T3", "S4"])
+def test_not_spd_first_failing_column(name):
+    p = gen.make(name)
+    with sp.Solver.from_problem(p, device=-1) as h0:
+        pf = h0.spchol_export_symbolic()["perm_final"]
+    for j0 in (0, 5, p.n // 3, p.n - 1):
+        i0 = int(np.where(pf == j0)[0][0])
+        vals = p.values.copy()
+        vals[p.colptr[i0]] = -1.0
+        q = gen.Problem(p.name, p.n, p.colptr, p.rowidx, vals, p.perm)
+        assert oracle.Oracle.from_problem(q).factor() == j0
+        with sp.Solver.from_problem(q) as h:
+            with pytest.raises(sp.NotSPDError) as ei:
+                h.spchol_factor()
+            assert ei.value.fail_col == j0 and ei.value.fail_col_orig == i0
+            with pytest.raises(sp.SpcholError):
+                h.spchol_solve(np.ones(p.n))
+
+
+def test_edge_cases():
+    # n = 1; diagonal A; dense A; forest (block diagonal); arrow
+    for D in (np.array([[9.0]]), np.diag(np.arange(1.0, 30.0)),
+              np.eye(70) * 80 + np.tril(np.full((70, 70), 1.0), -1),
+              np.kron(np.eye(3), np.eye(20) * 4 + np.diag(np.full(19, -1.0), -1))):
+        run_parity(gen.from_dense_lower(D))
+    n = 50
+    D = np.eye(n) * 60
+    D[n - 1, :n - 1] = 1.0
+    run_parity(gen.from_dense_lower(D))
