@@ -1,0 +1,297 @@
+#!/usr/bin/env python
+"""Benchmark: numeric RL supernodal Cholesky factorization (arXiv 2409.14009) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+A "step" is one numeric factorization (panel init, per-level POTRF,
+TRSM, SYRK/GEMM + relind scatter) of the config's matrix, with A's values already resident in HBM.
+Metric (BASELINE.json): numeric factor time and FP64 GFLOP/s = F_exact / factor time, where
+F_exact = sum_j cc_j^2 over the exact factor (padding flops excluded), and % of FP64 peak.
+
+N > 1 (torchrun): the distributed factorization is not built yet, so every rank factors its own
+replica of the matrix on its GPU ("replicas only"); value = total flops of
+all ranks / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gen  # noqa: E402
+
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+# bounded CPU samples: leading principal block of the ND-ordered matrix (whole ND subtrees)
+CPU_SAMPLE_COLS = {"C1": 900, "C2": 400000, "C3": 30000, "C4": 60000, "C5": 30000}
+REF_STEP_COLS = {"C1": 900, "C2": 200000, "C3": 20000, "C4": 30000, "C5": 15000}
+
+
+def fp64_peak():
+    """Measured FP64 DMMA peak (tools/fp64_peak.cu on this pool's B200, profiles/fp64_peak.json)."""
+    with open(FP64_PEAK_FILE) as f:
+        d = json.load(f)
+    return d
+
+
+class Clocks:
+    """nvidia-smi clock/throttle sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.samples = []
+        if self.p is None:
+            return
+        time.sleep(0.25)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def summary(self):
+        if not getattr(self, "samples", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        loaded = [x for x in sm if x > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (as it stands) on the host cores, a bounded sample per step."""
+    import oracle
+    world, rank, _ = dist_setup(args)
+    if rank != 0:
+        return
+    prob = gen.make(args.config)
+    ns = min(prob.n, REF_STEP_COLS.get(args.config, 20000))
+    sub = gen.leading_submatrix(prob, ns)
+    o = oracle.Oracle.from_problem(sub)
+    for _ in range(args.warmup):
+        o.factor()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        fc = o.factor()
+        times.append(time.perf_counter() - t0)
+        assert fc == -1
+    t = sum(times) / len(times)
+    gflops = o.flops / t / 1e9
+    sample = f"leading {ns}x{ns} principal block of {args.config}'s ND-ordered matrix (F_exact {o.flops:.4g} flop)"
+    line = {
+        "impl": "reference", "metric": "numeric factor FP64 GFLOP/s (F_exact / factor time)", "value": gflops,
+        "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": gen.CONFIGS[args.config]["desc"], "sample": sample},
+        "cpu_baseline": {"value": gflops, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": gflops, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, seconds_hint=True):
+    import oracle
+    prob = gen.make(args.config)
+    ns = min(prob.n, CPU_SAMPLE_COLS.get(args.config, 30000))
+    sub = gen.leading_submatrix(prob, ns)
+    o = oracle.Oracle.from_problem(sub)
+    t0 = time.perf_counter()
+    fc = o.factor()
+    t = time.perf_counter() - t0
+    assert fc == -1
+    return {"value": o.flops / t / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
+            "sample": f"leading {ns}x{ns} principal block of {args.config}'s ND-ordered matrix "
+                      f"(F_exact {o.flops:.4g} flop, {t:.1f} s single-threaded)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(gen.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import paper_2409_14009_b200 as sp
+
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    prob = gen.make(args.config)
+    t0 = time.perf_counter()
+    h = sp.Solver.from_problem(prob, device=dev)
+    analyze_s = time.perf_counter() - t0
+    stream = torch.cuda.Stream()
+    h.spchol_set_stream(stream.cuda_stream)
+    F = float(h.query("FLOPS_EXACT"))
+    Fexec = float(h.query("FLOPS_EXEC"))
+    launches_per_step = h.query("LAUNCHES")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up (graph capture happens on the first factor)
+    for _ in range(args.warmup):
+        h.spchol_factor()
+    # ---- timed region: K factorizations, device-resident values; inputs (13.5 GB panels on C4)
+    # are far larger than the 126 MB L2, so no explicit flush is needed between steps.
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with Clocks(dev) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            h.spchol_factor_async()
+        ev1.record(stream)
+        barrier()
+    fc, _ = h.spchol_factor_status()
+    assert fc == -1
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    value = world * F / (ms / 1e3) / 1e9
+    peak = fp64_peak()
+
+    # ---- roofline of the dominant kernel (SYRK/GEMM + relind scatter), CUDA events per launch
+    h.spchol_enable_kernel_timing(True)
+    barrier()
+    for _ in range(args.steps):
+        h.spchol_factor_async()
+    barrier()
+    stats = {k: h.spchol_kernel_stats(k) for k in sp.KERNEL_KINDS}
+    h.spchol_enable_kernel_timing(False)
+    dom = max(stats, key=lambda k: stats[k]["ms"])
+    sd = stats[dom]
+    achieved = sd["flops"] / (sd["ms"] / 1e3) / 1e12 if sd["ms"] > 0 else 0.0
+    traffic = None
+    if os.path.exists(TRAFFIC_FILE):
+        with open(TRAFFIC_FILE) as f:
+            tr = json.load(f)
+        if tr.get("config") == args.config and tr.get("kernel") == dom:
+            traffic = tr.get("traffic_bytes_per_launch")
+    step_ms_timed = sum(v["ms"] for v in stats.values()) / args.steps
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak["dmma_tflops_burst"], "unit": "TFLOP/s",
+                "frac": achieved / peak["dmma_tflops_burst"], "traffic": traffic, "kernel": dom,
+                "kernel_share_of_step": sd["ms"] / args.steps / step_ms_timed if step_ms_timed else None,
+                "launches_per_step": sd["launches"] // args.steps,
+                "peak_source": "measured FP64 DMMA m8n8k4 microbenchmark on this pool's B200 "
+                               "(profiles/fp64_peak.json; MEASURED_PEAKS.json has no FP64 entry)",
+                "per_kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in stats.items()},
+                "per_kernel_tflops": {k: (v["flops"] / (v["ms"] / 1e3) / 1e12 if v["ms"] > 0 and v["flops"] > 0 else None)
+                                      for k, v in stats.items()}}
+
+    # ---- end to end through the public API with host buffers (pinned): H2D of A's values and b,
+    # factor, solve, D2H of x — every step.
+    e2e = None
+    if not args.no_e2e:
+        vals_h = torch.from_numpy(prob.values).pin_memory()
+        xs, b = gen.rhs(prob)
+        b_h = torch.from_numpy(b).pin_memory()
+        x_h = torch.empty_like(b_h).pin_memory()
+        L = sp.lib()
+        import ctypes
+        vp = ctypes.c_void_p
+        def e2e_step():
+            assert L.spchol_set_values(h._h, vp(vals_h.data_ptr())) == 0
+            assert L.spchol_factor(h._h, None, None) == 0
+            assert L.spchol_solve(h._h, vp(b_h.data_ptr()), vp(x_h.data_ptr()), 1, prob.n) == 0
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        barrier()
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
+        berr = gen.backward_error(prob, x_h.numpy(), b)   # verification only, not timed
+        e2e = {"value": world * F / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * (prob.nnz + prob.n),
+               "d2h_bytes_per_step": 8 * prob.n + 8, "seconds_per_step": e2e_s, "includes": "set_values(H2D) + factor + solve(H2D b, D2H x)",
+               "backward_error": berr}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(args)
+    line = {
+        "metric": "numeric factor FP64 GFLOP/s (F_exact / factor time)",
+        "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": gen.CONFIGS[args.config]["desc"], "config_id": args.config, "n": prob.n,
+                   "nnz_A_lower": prob.nnz, "nnz_L": h.query("NNZ_L"), "flops_exact": F, "flops_executed": Fexec,
+                   "supernodes": h.query("NSUPER"), "levels": h.query("NLEVELS"),
+                   "panel_GB": h.query("PANEL_DOUBLES") * 8 / 1e9, "analyze_s": analyze_s,
+                   "l2": "no flush needed: panels (GB) >> 126 MB L2",
+                   "parallelism": "replicas" if world > 1 else "1 GPU"},
+        "factor_s": ms / 1e3,
+        "pct_fp64_peak": 100.0 * (F / (ms / 1e3) / 1e12) / peak["dmma_tflops_burst"],
+        "clocks": clk.summary(),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

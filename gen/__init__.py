@@ -192,3 +192,41 @@ def to_dense(prob: Problem):
             A[i, j] = prob.values[p]
             A[j, i] = prob.values[p]
     return A
+
+
+def leading_submatrix(prob: Problem, ns: int) -> Problem:
+    """The leading ns x ns principal submatrix of P A P^T (P = prob.perm), in that order, identity perm.
+
+    Used as the bounded CPU-baseline sample: in nested-dissection order the leading block is a
+    union of whole ND subtrees, so its factor is exactly the leading block of the full factor.
+    """
+    inv = np.argsort(prob.perm)
+    newidx = np.full(prob.n, -1, np.int64)
+    newidx[inv[:ns]] = np.arange(ns)
+    colid = np.repeat(np.arange(prob.n), np.diff(prob.colptr))
+    r, c = newidx[prob.rowidx], newidx[colid]
+    keep = (r >= 0) & (c >= 0)
+    r, c, v = r[keep], c[keep], prob.values[keep]
+    lo, hi = np.minimum(r, c), np.maximum(r, c)
+    order = np.lexsort((hi, lo))
+    lo, hi, v = lo[order], hi[order], v[order]
+    colptr = np.zeros(ns + 1, np.int64)
+    np.add.at(colptr, lo + 1, 1)
+    return Problem(f"{prob.name}[:{ns}]", ns, np.cumsum(colptr), hi.astype(np.int32), v.astype(np.float64),
+                   np.arange(ns, dtype=np.int32), prob.grid, prob.dof, prob.kind)
+
+
+def inf_norm(prob: Problem) -> float:
+    """||A||_inf of the symmetric A stored as its lower triangle."""
+    rowsum = np.zeros(prob.n)
+    cols = np.repeat(np.arange(prob.n), np.diff(prob.colptr))
+    np.add.at(rowsum, prob.rowidx, np.abs(prob.values))
+    off = prob.rowidx != cols
+    np.add.at(rowsum, cols[off], np.abs(prob.values[off]))
+    return float(rowsum.max())
+
+
+def backward_error(prob: Problem, x, b) -> float:
+    """Normwise backward error ||A x - b||_inf / (||A||_inf ||x||_inf) (verification only)."""
+    r = symv(prob, x=x) - b
+    return float(np.abs(r).max() / (inf_norm(prob) * np.abs(x).max()))

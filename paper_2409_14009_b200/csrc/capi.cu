@@ -60,6 +60,7 @@ struct spchol_handle {
   Symbolic S;
   spchol_options opt{};
   int nb = NBMAX;
+  static constexpr int OUTER = 4;   // outer block = OUTER inner blocks
   cudaStream_t stream = nullptr, own_stream = nullptr;
   // host plan
   std::vector<SnInfo> sn;
@@ -105,7 +106,7 @@ extern "C" const char* spchol_last_error(void) { return g_err.c_str(); }
 // ------------------------------------------------------------------------------------- plan
 static void build_plan(spchol_handle* h) {
   const Symbolic& S = h->S;
-  const int ns = S.nsuper, NB = h->nb;
+  const int ns = S.nsuper, NB = h->nb, OUTER = spchol_handle::OUTER;
   h->sn.resize(ns);
   h->panel_off.assign(ns + 1, 0);
   for (int J = 0; J < ns; ++J) {
@@ -138,17 +139,22 @@ static void build_plan(spchol_handle* h) {
       const SnInfo& I = h->sn[h->level_sns[x]];
       maxblk = std::max(maxblk, (I.k + NB - 1) / NB);
     }
+    // two-level blocked right-looking cdiv: inner blocks of NB columns (POTRF + TRSM + update of
+    // the rest of the outer block column, K = NB), outer blocks of W = OUTER*NB columns whose
+    // trailing update (K = W) is the bulk of the in-panel work.
+    const int W = OUTER * NB;
     for (int s = 0; s < maxblk; ++s) {
       long long p0 = (long long)h->ptasks.size(), t0 = (long long)h->gtasks.size();
-      double fp = 0, ft = 0, fl = 0, bp = 0, bt = 0, bl = 0;
+      double fp = 0, ft = 0, fl = 0, bp = 0, bt = 0, bl = 0, fo = 0, bo = 0;
       int slot = 0;
-      std::vector<GTask> local;
+      std::vector<GTask> local, outer;
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
         const int J = h->level_sns[x];
         const SnInfo& I = h->sn[J];
         const int c0 = s * NB;
         if (c0 >= I.k) continue;
         const int nb = std::min(NB, I.k - c0), c1 = c0 + nb;
+        const int C0 = (c0 / W) * W, C1 = std::min(C0 + W, I.k);   // enclosing outer block
         h->ptasks.push_back(PTask{J, c0, nb, slot});
         fp += (double)nb * nb * nb / 3.0;
         bp += 16.0 * nb * nb;
@@ -156,10 +162,17 @@ static void build_plan(spchol_handle* h) {
         for (int r0 = c1 & ~1; r0 < I.m; r0 += TILE) h->gtasks.push_back(GTask{J, r0, c1, c0, nb, slot});
         ft += (double)(I.m - c1) * nb * nb;
         bt += 16.0 * (double)(I.m - c1) * nb;
+        // inner update: columns [c1, C1) of this outer block, K = nb
         for (int r0 = c1; r0 < I.m; r0 += TILE)
-          for (int s0 = c1; s0 < I.k && s0 <= r0; s0 += TILE) local.push_back(GTask{J, r0, s0, c0, nb, 0});
-        for (int c = c1; c < I.k; ++c) { fl += 2.0 * nb * (double)(I.m - c); bl += 16.0 * (double)(I.m - c); }
-        bl += 8.0 * (double)(I.m - c1) * nb;
+          for (int s0 = c1; s0 < C1 && s0 <= r0; s0 += TILE) local.push_back(GTask{J, r0, s0, c0, nb, C1});
+        for (int c = c1; c < C1; ++c) { fl += 2.0 * nb * (double)(I.m - c); bl += 16.0 * (double)(I.m - c); }
+        // outer update after the last inner block of the outer block: columns [C1, k), K = C1 - C0
+        if (c1 == C1 && C1 < I.k) {
+          for (int r0 = C1; r0 < I.m; r0 += TILE)
+            for (int s0 = C1; s0 < I.k && s0 <= r0; s0 += TILE) outer.push_back(GTask{J, r0, s0, C0, C1 - C0, I.k});
+          for (int c = C1; c < I.k; ++c) { fo += 2.0 * (C1 - C0) * (double)(I.m - c); bo += 16.0 * (double)(I.m - c); }
+          bo += 8.0 * (double)(I.m - C1) * (C1 - C0);
+        }
         ++slot;
       }
       h->max_slots = std::max(h->max_slots, slot);
@@ -169,6 +182,9 @@ static void build_plan(spchol_handle* h) {
       long long l0 = (long long)h->gtasks.size();
       h->gtasks.insert(h->gtasks.end(), local.begin(), local.end());
       push(K_LOCAL, l0, (long long)h->gtasks.size(), fl, bl);
+      long long o0 = (long long)h->gtasks.size();
+      h->gtasks.insert(h->gtasks.end(), outer.begin(), outer.end());
+      push(K_LOCAL, o0, (long long)h->gtasks.size(), fo, bo);
     }
     long long s0g = (long long)h->gtasks.size();
     double fs = 0, bs = 0;

@@ -26,7 +26,8 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 // A and B are row blocks of column-major matrices (so both operands stream contiguous columns).
 //   MODE_LOCAL   (right-looking update inside supernode J after its block column [c0, c0+nb)):
 //                A = panel rows [r0, r0+64), B = panel rows [s0, s0+64), columns [c0, c0+nb), K = nb;
-//                panel(row r0+i, col s0+j) -= C(i,j) for r0+i >= s0+j, r0+i < m, s0+j < k.
+//                panel(row r0+i, col s0+j) -= C(i,j) for r0+i >= s0+j, r0+i < m, s0+j < slot
+//                (slot = exclusive column bound of the updated block).
 //   MODE_TRSM    A = panel rows [r0, r0+64) x cols [c0, c0+nb), B = L_bb^{-1} (workspace slot), K = nb;
 //                panel(r0+i, c0+j) = C(i,j) for r0+i >= s0 (= c0+nb; r0 is rounded down to even)
 //                (in place: the CTA owns these rows).
@@ -116,103 +117,210 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_kernel(const GTask* __restr
     }
   }
   cp_async_wait<0>();
-  // ---- epilogue
+  // ---- epilogue: stage the 64x64 tile through shared memory (column-major, stride LDC), then
+  // each warp streams whole 64-row columns: 16-byte vector RMW / stores (LOCAL, TRSM) or runs of
+  // consecutive RED (SCATTER, relind runs are long: consecutive U rows land in consecutive
+  // ancestor rows).  All destination loads of a thread are issued before its stores.
+  constexpr int LDC = TILE + 4;   // 68 doubles: conflict-free fragment writes and v2 reads
+  __syncthreads();
+  double* sC = smem;
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      const int col = wn * 32 + j * 8 + 2 * t + v;
-      if (MODE == MODE_LOCAL) {
-        const int gc = T.s0 + col;
-        if (gc >= S.k) continue;
-        double* dcol = panels + S.off + (long long)gc * S.ld;
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int gr = T.r0 + wm * 32 + i * 8 + g;
-          if (gr < S.m && gr >= gc) dcol[gr] -= acc[i][j][v];
-        }
-      } else if (MODE == MODE_TRSM) {
-        if (col >= T.nb) continue;
-        double* dcol = panels + S.off + (long long)(T.c0 + col) * S.ld;
+      for (int v = 0; v < 2; ++v)
+        sC[(wn * 32 + j * 8 + 2 * t + v) * LDC + wm * 32 + i * 8 + g] = acc[i][j][v];
+  __syncthreads();
+  const int pr = 2 * lane;                 // row pair inside the tile
+  constexpr int NIT = TILE / (GEMM_THREADS / 32);   // columns per warp (16)
+  if (MODE == MODE_LOCAL) {
+    const int gr = T.r0 + pr;
+    double2 dv[NIT];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int gr = T.r0 + wm * 32 + i * 8 + g;
-          if (gr < S.m && gr >= T.s0) dcol[gr] = acc[i][j][v];
-        }
+    for (int it = 0; it < NIT; ++it) {
+      const int gc = T.s0 + warp + 4 * it;
+      const bool ok = gc < T.slot && gr + 1 >= gc && gr < S.m;
+      dv[it] = ok ? *reinterpret_cast<const double2*>(panels + S.off + (long long)gc * S.ld + gr) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int col = warp + 4 * it, gc = T.s0 + col;
+      if (!(gc < T.slot && gr + 1 >= gc && gr < S.m)) continue;
+      const double2 c2 = *reinterpret_cast<const double2*>(sC + col * LDC + pr);
+      double* d = panels + S.off + (long long)gc * S.ld + gr;
+      const bool v0 = gr >= gc, v1 = gr + 1 < S.m;
+      if (v0 && v1) {
+        *reinterpret_cast<double2*>(d) = make_double2(dv[it].x - c2.x, dv[it].y - c2.y);
       } else {
-        const int uc = T.s0 + col - S.k;
-        if (uc < 0 || T.s0 + col >= S.m) continue;
-        const long long cb = ucol_base[S.ucol + uc];
-        const long long mb = ucol_map[S.ucol + uc];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int gr = T.r0 + wm * 32 + i * 8 + g;
-          if (gr < S.m && gr - S.k >= uc) atomicAdd(panels + cb + posmap[mb + gr], -acc[i][j][v]);
-        }
+        if (v0) d[0] = dv[it].x - c2.x;
+        if (v1) d[1] = dv[it].y - c2.y;
       }
     }
+  } else if (MODE == MODE_TRSM) {
+    const int gr = T.r0 + pr;
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int col = warp + 4 * it;
+      if (col >= T.nb || gr + 1 < T.s0 || gr >= S.m) continue;
+      const double2 c2 = *reinterpret_cast<const double2*>(sC + col * LDC + pr);
+      double* d = panels + S.off + (long long)(T.c0 + col) * S.ld + gr;
+      const bool v0 = gr >= T.s0, v1 = gr + 1 < S.m;
+      if (v0 && v1) *reinterpret_cast<double2*>(d) = c2;
+      else {
+        if (v0) d[0] = c2.x;
+        if (v1) d[1] = c2.y;
+      }
+    }
+  } else {
+#pragma unroll 4
+    for (int it = 0; it < NIT; ++it) {
+      const int col = warp + 4 * it;
+      const int uc = T.s0 + col - S.k;
+      if (uc < 0 || T.s0 + col >= S.m) continue;
+      const long long cb = ucol_base[S.ucol + uc];
+      const long long mb = ucol_map[S.ucol + uc];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = lane + 32 * h, gr = T.r0 + row;   // lanes cover 32 consecutive rows
+        if (gr < S.m && gr - S.k >= uc) atomicAdd(panels + cb + posmap[mb + gr], -sC[col * LDC + row]);
+      }
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------------------------
-// potrf_kernel: one CTA factors the nb x nb diagonal block [c0, c0+nb) of supernode J in shared
-// memory (unblocked right-looking Cholesky), writes L_bb back (lower part only: the strict upper
-// triangle of the panel is padding and stays 0), and writes X = L_bb^{-1} (column-major, ld 64,
-// zero-padded) to its workspace slot for the TRSM.  A pivot that is not > 0 (incl. NaN) records
-// its global column (final numbering) with atomicMin (a7).
+// potrf_kernel: one CTA (256 threads) factors the nb x nb (nb <= 64) diagonal block [c0, c0+nb) of
+// supernode J ("DPOTRF") and forms X = L_bb^{-1} for TRSM-as-GEMM.
+// The 64x64 lower triangle is cut into 4x4 register blocks; thread t < 136 owns block (bi, bj),
+// bi >= bj.  Cholesky, right-looking, step j: the owners of column j publish it (double-buffered
+// shared vector, ONE barrier per step), every thread scales its rows/columns by 1/sqrt(pivot) and
+// applies the rank-1 update to its block.  Inverse, step s (forward substitution on I): the owners
+// of row s of X scale it by 1/L_ss and publish it; rows r > s subtract L(r,s) X(s,:).
+// The strict upper triangle of the panel is padding and is never written.  X is written to the
+// task's workspace slot, column-major, ld 64, zero padded.  A pivot that is not > 0 (incl. NaN)
+// records its global column (final numbering) with atomicMin (a7).
 // ----------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(POTRF_THREADS) potrf_kernel(const PTask* __restrict__ tasks,
                                                               const SnInfo* __restrict__ sn,
                                                               const int* __restrict__ sfirst, double* panels,
                                                               double* linv, unsigned long long* fail) {
-  extern __shared__ double psm[];
-  double(*D)[NBMAX + 1] = reinterpret_cast<double(*)[NBMAX + 1]>(psm);                         // D[col][row]
-  double(*X)[NBMAX + 1] = reinterpret_cast<double(*)[NBMAX + 1]>(psm + NBMAX * (NBMAX + 1));   // X[col][row]
-  __shared__ int bad;
+  __shared__ double vbuf[2][NBMAX];            // published column of L / row of X
+  __shared__ double Ls[NBMAX][NBMAX + 1];      // Ls[row][col] = L(row, col) after the Cholesky
+  __shared__ double invd[NBMAX];
   const PTask T = tasks[blockIdx.x];
   const SnInfo S = sn[T.sn];
   const int nb = T.nb, tid = threadIdx.x;
+  // block coordinates: t -> (bi, bj), bi >= bj, row-major over the lower block triangle
+  const bool owner = tid < 136;
+  int bi = 0, bj = owner ? tid : 0;
+  while (bj > bi) { bj -= bi + 1; ++bi; }
+  const int r0 = 4 * bi, q0 = 4 * bj;
   double* P = panels + S.off + (long long)T.c0 * S.ld + T.c0;
-  for (int idx = tid; idx < nb * nb; idx += POTRF_THREADS) {
-    const int c = idx / nb, r = idx % nb;
-    D[c][r] = r >= c ? P[(long long)c * S.ld + r] : 0.0;
-    X[c][r] = r == c ? 1.0 : 0.0;
-  }
-  if (tid == 0) bad = -1;
-  __syncthreads();
-  for (int j = 0; j < nb; ++j) {
-    const double d = D[j][j];
-    if (tid == 0 && !(d > 0.0) && bad < 0) bad = j;
-    const double l = sqrt(d);
-    __syncthreads();
-    for (int r = j + tid; r < nb; r += POTRF_THREADS) D[j][r] = r == j ? l : D[j][r] / l;
-    __syncthreads();
-    const int mm = nb - j - 1;
-    for (int idx = tid; idx < mm * mm; idx += POTRF_THREADS) {
-      const int c = j + 1 + idx / mm, r = j + 1 + idx % mm;
-      if (r >= c) D[c][r] -= D[j][r] * D[j][c];
+  double a[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + i, c = q0 + q;
+      a[i][q] = (owner && r < nb && c < nb && r >= c) ? P[(long long)c * S.ld + r] : 0.0;
     }
-    __syncthreads();
+  int bad = -1;
+  for (int jb = 0; jb < (nb + 3) / 4; ++jb) {
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = 4 * jb + jj;
+      if (j >= nb) break;
+      double* col = vbuf[j & 1];
+      if (owner && bj == jb) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) col[r0 + i] = a[i][jj];
+      }
+      __syncthreads();
+      const double d = col[j];
+      const double l = sqrt(d), rl = 1.0 / l;
+      if (bad < 0 && !(d > 0.0)) bad = j;
+      double lr[4], lc[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        lr[i] = col[r0 + i] * rl;
+        lc[i] = col[q0 + i] * rl;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (r0 + i >= q0 + q && q0 + q > j) a[i][q] -= lr[i] * lc[q];
+      if (bj == jb) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = r0 + i;
+          if (r > j) a[i][jj] = lr[i];
+          else if (r == j) a[i][jj] = l;
+        }
+      }
+      if (tid == 0) invd[j] = rl;
+    }
   }
   if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[T.sn] + T.c0 + bad));
-  for (int idx = tid; idx < nb * nb; idx += POTRF_THREADS) {
-    const int c = idx / nb, r = idx % nb;
-    if (r >= c) P[(long long)c * S.ld + r] = D[c][r];
-  }
-  // X = L^{-1}: forward substitution on the identity, row q finalised then eliminated below
-  for (int q = 0; q < nb; ++q) {
-    for (int c = tid; c <= q; c += POTRF_THREADS) X[c][q] /= D[q][q];
-    __syncthreads();
-    const int rr = nb - q - 1;
-    for (int idx = tid; idx < rr * (q + 1); idx += POTRF_THREADS) {
-      const int c = idx / rr, r = q + 1 + idx % rr;
-      X[c][r] -= D[q][r] * X[c][q];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + i, c = q0 + q;
+      if (owner) Ls[r][c] = a[i][q];
+      if (owner && r < nb && c < nb && r >= c) P[(long long)c * S.ld + r] = a[i][q];
     }
-    __syncthreads();
+  // inverse: x = identity restricted to the block, forward substitution over pivot rows s
+  double x[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[i][q] = (owner && r0 + i == q0 + q && r0 + i < nb) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int sb = 0; sb < (nb + 3) / 4; ++sb) {
+#pragma unroll
+    for (int ss = 0; ss < 4; ++ss) {
+      const int s = 4 * sb + ss;
+      if (s >= nb) break;
+      double* row = vbuf[s & 1];
+      if (owner && bi == sb) {
+        const double is = invd[s];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          x[ss][q] *= is;
+          row[q0 + q] = x[ss][q];
+        }
+      }
+      __syncthreads();
+      if (owner && r0 + 3 > s) {
+        double xs[4], lrs[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xs[q] = row[q0 + q];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) lrs[i] = Ls[r0 + i][s];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (r0 + i > s && q0 + q <= s) x[i][q] -= lrs[i] * xs[q];
+      }
+    }
   }
   double* W = linv + (long long)T.slot * (NBMAX * NBMAX);
-  for (int idx = tid; idx < NBMAX * NBMAX; idx += POTRF_THREADS) {
-    const int c = idx / NBMAX, r = idx % NBMAX;
-    W[idx] = (c < nb && r < nb) ? X[c][r] : 0.0;
+  // the whole 64x64 slot is written: owners write their lower blocks, the rest writes zeros
+  for (int e = tid; e < NBMAX * NBMAX; e += POTRF_THREADS) {
+    const int c = e / NBMAX, r = e % NBMAX;
+    if (r < c || r >= nb || c >= nb) W[e] = 0.0;
+  }
+  if (owner) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = r0 + i, c = q0 + q;
+        if (r >= c && r < nb && c < nb) W[c * NBMAX + r] = x[i][q];
+      }
   }
 }
 
@@ -291,7 +399,6 @@ cudaError_t kernels_init_attributes() {
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
-  if ((e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM))) return e;
   return cudaSuccess;
 }
 
@@ -309,7 +416,7 @@ void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, dou
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels, double* linv,
                   unsigned long long* fail, cudaStream_t st) {
   if (ntasks <= 0) return;
-  potrf_kernel<<<ntasks, POTRF_THREADS, POTRF_SMEM, st>>>(tasks, sn, sfirst, panels, linv, fail);
+  potrf_kernel<<<ntasks, POTRF_THREADS, 0, st>>>(tasks, sn, sfirst, panels, linv, fail);
 }
 
 void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st) {

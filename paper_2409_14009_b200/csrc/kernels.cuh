@@ -39,7 +39,6 @@ constexpr int GEMM_THREADS = 128;  // 4 warps, 2x2, warp tile 32x32
 constexpr int GEMM_SMEM = 2 * STAGES * BK * LDS * (int)sizeof(double);
 constexpr int NBMAX = 64;          // cdiv block width
 constexpr int POTRF_THREADS = 256;
-constexpr int POTRF_SMEM = 2 * NBMAX * (NBMAX + 1) * (int)sizeof(double);
 
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels,
                  const double* linv, const long long* ucol_base, const long long* ucol_map,

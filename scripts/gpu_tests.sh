@@ -1,3 +1,1 @@
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -30
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q ${PYARGS} 2>&1 | tail -40

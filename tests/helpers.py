@@ -40,19 +40,8 @@ def lower_panel_mask(sym, off, ld, total):
     return mask
 
 
-def inf_norm(prob):
-    rowsum = np.zeros(prob.n)
-    cols = np.repeat(np.arange(prob.n), np.diff(prob.colptr))
-    np.add.at(rowsum, prob.rowidx, np.abs(prob.values))
-    off = prob.rowidx != cols
-    np.add.at(rowsum, cols[off], np.abs(prob.values[off]))
-    return rowsum.max()
-
-
-def backward_error(prob, x, b):
-    """||A x - b||_inf / (||A||_inf ||x||_inf)  (north_star's normwise backward error)."""
-    r = gen.symv(prob, x=x) - b
-    return np.abs(r).max() / (inf_norm(prob) * np.abs(x).max())
+inf_norm = gen.inf_norm
+backward_error = gen.backward_error
 
 
 def logdet_from_diag(diag):
