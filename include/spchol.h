@@ -193,6 +193,12 @@ int spchol_enable_kernel_timing(spchol_handle* h, int enable);
 int spchol_kernel_stats(spchol_handle* h, int kind, int64_t* launches, double* ms, double* flops,
                         double* bytes);
 
+/* Per-launch trace of the timed launches since the last spchol_kernel_stats/enable call (timing
+ * must be enabled): for launch i < min(cap, *count): kinds[i] (as above), levels[i] (level of the
+ * supernodal tree, -1 for the init), ntasks[i] (CTAs), ms[i].  Diagnostics only. */
+int spchol_kernel_trace(spchol_handle* h, int64_t cap, int64_t* count, int32_t* kinds, int32_t* levels,
+                        int32_t* ntasks, double* ms);
+
 void spchol_destroy(spchol_handle* h);
 const char* spchol_last_error(void);
 

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspchol.so")
+LIB_PATH = os.environ.get("SPCHOL_LIB") or os.path.join(_HERE, "libspchol.so")
 _LIB = None
 
 SPCHOL_OK = 0
@@ -36,7 +36,7 @@ EXPORTS = [
     "spchol_set_stream", "spchol_factor_async", "spchol_factor_status", "spchol_factor",
     "spchol_solve", "spchol_solve_device", "spchol_query", "spchol_export_symbolic",
     "spchol_export_panels", "spchol_export_panel", "spchol_export_diagonal", "spchol_enable_kernel_timing", "spchol_kernel_stats",
-    "spchol_destroy", "spchol_last_error",
+    "spchol_kernel_trace", "spchol_destroy", "spchol_last_error",
 ]
 
 
@@ -85,6 +85,7 @@ def lib():
         L.spchol_enable_kernel_timing.argtypes = [vp, ctypes.c_int]
         L.spchol_kernel_stats.argtypes = [vp, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(dbl),
                                           ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
+        L.spchol_kernel_trace.argtypes = [vp, i64, ctypes.POINTER(i64), vp, vp, vp, vp]
         L.spchol_destroy.argtypes = [vp]
         L.spchol_destroy.restype = None
         L.spchol_last_error.argtypes = []
@@ -244,6 +245,15 @@ class Solver:
         _check(self._L.spchol_kernel_stats(self._h, k, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl),
                                            ctypes.byref(by)))
         return dict(launches=int(n.value), ms=ms.value, flops=fl.value, bytes=by.value)
+
+    def spchol_kernel_trace(self, cap=100000):
+        cnt = ctypes.c_int64()
+        kinds, levels = np.empty(cap, np.int32), np.empty(cap, np.int32)
+        ntasks, ms = np.empty(cap, np.int32), np.empty(cap, np.float64)
+        _check(self._L.spchol_kernel_trace(self._h, cap, ctypes.byref(cnt), _vp(kinds), _vp(levels), _vp(ntasks),
+                                           _vp(ms)))
+        c = min(cap, int(cnt.value))
+        return dict(kinds=kinds[:c], levels=levels[:c], ntasks=ntasks[:c], ms=ms[:c])
 
     # ---- convenience (still only marshalling)
     factor = spchol_factor

@@ -11,6 +11,7 @@
 //   ucol     per U_J column c: (panel offset of that column inside its ancestor, posmap base)
 //   tasks    per launch: batched tile tasks of every supernode of one level (level-set schedule)
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -35,11 +36,16 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 enum LaunchKind { K_SMALL = 0, K_POTRF = 1, K_TRSM = 2, K_LOCAL = 3, K_SCATTER = 4, K_INIT = 5, K_NKINDS = 6 };
+enum OpType { OP_LAUNCH = 0, OP_RECORD = 1, OP_WAIT = 2 };
+// One step of the factor's launch plan.  OP_LAUNCH: a batched kernel (kind, tasks [off, off+n)) on
+// stream `stream` (0 = critical path: cdiv chain + relind scatter, 1 = trailing updates);
+// OP_RECORD / OP_WAIT: event `ev` recorded on / awaited by `stream` (lookahead fork/join).
 struct Launch {
   int kind;
   long long off;   // first task
   int n;           // tasks
   double flops, bytes;
+  int op = OP_LAUNCH, stream = 0, ev = -1;
 };
 template <class T>
 cudaError_t dalloc(T** p, size_t count) {
@@ -72,6 +78,9 @@ struct spchol_handle {
   std::vector<long long> panel_off;
   double flops_exec = 0, update_entries = 0;
   int max_slots = 0;
+  int nevents = 0;
+  bool no_lookahead = false;     // SPCHOL_NO_LOOKAHEAD=1 (diagnostics)
+  std::vector<int> plan_level;   // level of each plan entry (diagnostics)
   // device
   double *d_panels = nullptr, *d_avals = nullptr, *d_linv = nullptr, *d_y = nullptr, *d_y2 = nullptr;
   long long *d_diag_idx = nullptr, *d_amap = nullptr, *d_ucol_base = nullptr, *d_ucol_map = nullptr, *d_rows_ptr = nullptr;
@@ -81,6 +90,11 @@ struct spchol_handle {
   PTask* d_ptasks = nullptr;
   unsigned long long* d_fail = nullptr;
   bool values_set = false, factored = false;
+  cudaStream_t side_stream = nullptr;           // stream 1 of the plan (trailing updates, low priority)
+  cudaStream_t crit_stream = nullptr;           // stream 0 of the plan (cdiv chain, high priority)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int prio_lo = 0, prio_hi = 0;
+  std::vector<cudaEvent_t> plan_events;
   // graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -130,10 +144,11 @@ static void build_plan(spchol_handle* h) {
     for (int J = 0; J < ns; ++J) h->level_sns[nx[S.level[J]]++] = J;
   }
   auto push = [&](int kind, long long off, long long end, double fl, double by) {
-    if (end > off) h->plan.push_back(Launch{kind, off, (int)(end - off), fl, by});
+    if (end > off) h->plan.push_back(Launch{kind, off, (int)(end - off), fl, by, OP_LAUNCH, 0, -1});
   };
   h->max_slots = 0;
   for (int l = 0; l < S.nlevels; ++l) {
+    const size_t plan_before = h->plan.size();
     int maxblk = 0;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
       const SnInfo& I = h->sn[h->level_sns[x]];
@@ -141,13 +156,18 @@ static void build_plan(spchol_handle* h) {
     }
     // two-level blocked right-looking cdiv: inner blocks of NB columns (POTRF + TRSM + update of
     // the rest of the outer block column, K = NB), outer blocks of W = OUTER*NB columns whose
-    // trailing update (K = W) is the bulk of the in-panel work.
+    // trailing update (K = W) is the bulk of the in-panel work.  Lookahead: the outer update of
+    // block S is split into NEXT (the columns of outer block S+1, on the critical stream 0) and
+    // REST (all later columns, on stream 1), so the cdiv chain of block S+1 (latency-bound POTRF
+    // and TRSM launches with few CTAs) overlaps REST(S).  Ordering: REST(S) after the cdiv of
+    // block S (event), NEXT(S+1) after REST(S) (same entries), REST(S+1) after REST(S) (stream 1).
     const int W = OUTER * NB;
+    int pending_rest_ev = -1;      // event recorded after the latest REST launch on stream 1
     for (int s = 0; s < maxblk; ++s) {
       long long p0 = (long long)h->ptasks.size(), t0 = (long long)h->gtasks.size();
-      double fp = 0, ft = 0, fl = 0, bp = 0, bt = 0, bl = 0, fo = 0, bo = 0;
+      double fp = 0, ft = 0, fl = 0, bp = 0, bt = 0, bl = 0, fn = 0, bn = 0, fr = 0, br = 0;
       int slot = 0;
-      std::vector<GTask> local, outer;
+      std::vector<GTask> local, nxt, rest;
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
         const int J = h->level_sns[x];
         const SnInfo& I = h->sn[J];
@@ -166,12 +186,15 @@ static void build_plan(spchol_handle* h) {
         for (int r0 = c1; r0 < I.m; r0 += TILE)
           for (int s0 = c1; s0 < C1 && s0 <= r0; s0 += TILE) local.push_back(GTask{J, r0, s0, c0, nb, C1});
         for (int c = c1; c < C1; ++c) { fl += 2.0 * nb * (double)(I.m - c); bl += 16.0 * (double)(I.m - c); }
-        // outer update after the last inner block of the outer block: columns [C1, k), K = C1 - C0
+        // outer update after the last inner block of the outer block, K = C1 - C0
         if (c1 == C1 && C1 < I.k) {
+          const int C2 = std::min(C1 + W, I.k);
           for (int r0 = C1; r0 < I.m; r0 += TILE)
-            for (int s0 = C1; s0 < I.k && s0 <= r0; s0 += TILE) outer.push_back(GTask{J, r0, s0, C0, C1 - C0, I.k});
-          for (int c = C1; c < I.k; ++c) { fo += 2.0 * (C1 - C0) * (double)(I.m - c); bo += 16.0 * (double)(I.m - c); }
-          bo += 8.0 * (double)(I.m - C1) * (C1 - C0);
+            for (int s0 = C1; s0 < C2 && s0 <= r0; s0 += TILE) nxt.push_back(GTask{J, r0, s0, C0, C1 - C0, C2});
+          for (int c = C1; c < C2; ++c) { fn += 2.0 * (C1 - C0) * (double)(I.m - c); bn += 16.0 * (double)(I.m - c); }
+          for (int r0 = C2; r0 < I.m; r0 += TILE)
+            for (int s0 = C2; s0 < I.k && s0 <= r0; s0 += TILE) rest.push_back(GTask{J, r0, s0, C0, C1 - C0, I.k});
+          for (int c = C2; c < I.k; ++c) { fr += 2.0 * (C1 - C0) * (double)(I.m - c); br += 16.0 * (double)(I.m - c); }
         }
         ++slot;
       }
@@ -182,10 +205,32 @@ static void build_plan(spchol_handle* h) {
       long long l0 = (long long)h->gtasks.size();
       h->gtasks.insert(h->gtasks.end(), local.begin(), local.end());
       push(K_LOCAL, l0, (long long)h->gtasks.size(), fl, bl);
-      long long o0 = (long long)h->gtasks.size();
-      h->gtasks.insert(h->gtasks.end(), outer.begin(), outer.end());
-      push(K_LOCAL, o0, (long long)h->gtasks.size(), fo, bo);
+      if (!rest.empty() && h->no_lookahead) {   // diagnostics: NEXT and REST as one launch, serial
+        nxt.insert(nxt.end(), rest.begin(), rest.end());
+        fn += fr; bn += br;
+        rest.clear();
+      }
+      if (!rest.empty()) {            // fork REST(S) onto stream 1 after the cdiv of block S
+        const int ev = h->nevents++;
+        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 0, ev});
+        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 1, ev});
+        long long r0g = (long long)h->gtasks.size();
+        h->gtasks.insert(h->gtasks.end(), rest.begin(), rest.end());
+        if ((long long)h->gtasks.size() > r0g)
+          h->plan.push_back(Launch{K_LOCAL, r0g, (int)((long long)h->gtasks.size() - r0g), fr, br, OP_LAUNCH, 1, -1});
+      }
+      if (!nxt.empty()) {
+        if (pending_rest_ev >= 0) h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 0, pending_rest_ev});
+        long long n0 = (long long)h->gtasks.size();
+        h->gtasks.insert(h->gtasks.end(), nxt.begin(), nxt.end());
+        push(K_LOCAL, n0, (long long)h->gtasks.size(), fn, bn);
+      }
+      if (!rest.empty()) {
+        pending_rest_ev = h->nevents++;
+        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 1, pending_rest_ev});
+      }
     }
+    if (pending_rest_ev >= 0) h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 0, pending_rest_ev});  // join
     long long s0g = (long long)h->gtasks.size();
     double fs = 0, bs = 0;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
@@ -200,6 +245,8 @@ static void build_plan(spchol_handle* h) {
       bs += 8.0 * (double)t * I.k + 16.0 * 0.5 * t * (t + 1.0);
     }
     push(K_SCATTER, s0g, (long long)h->gtasks.size(), fs, bs);
+    h->plan_level.resize(h->plan.size(), l);
+    (void)plan_before;
   }
 }
 
@@ -236,6 +283,18 @@ static int setup_device(spchol_handle* h) {
   CK(kernels_init_attributes());
   CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
   h->stream = h->own_stream;
+  {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));   // numerically lower = higher priority
+    h->prio_lo = lo;
+    h->prio_hi = hi;
+    CK(cudaStreamCreateWithPriority(&h->side_stream, cudaStreamNonBlocking, lo));
+    CK(cudaStreamCreateWithPriority(&h->crit_stream, cudaStreamNonBlocking, hi));
+    CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  }
+  h->plan_events.resize(h->nevents);
+  for (auto& e : h->plan_events) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(dalloc(&h->d_panels, (size_t)h->panel_doubles));
   CK(dalloc(&h->d_avals, (size_t)S.nnzA));
   CK(upload(&h->d_amap, amap));
@@ -265,6 +324,11 @@ static void free_device(spchol_handle* h) {
                   h->d_gtasks, h->d_ptasks, h->d_fail};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->plan_events) if (e) cudaEventDestroy(e);
+  if (h->side_stream) cudaStreamDestroy(h->side_stream);
+  if (h->crit_stream) cudaStreamDestroy(h->crit_stream);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
 }
 
@@ -281,6 +345,7 @@ extern "C" int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* r
   std::string err;
   int rc = analyze_symbolic(n, colptr, rowidx, perm, h->opt.merge_cap, h->S, err);
   if (rc != SPCHOL_OK) { delete h; return fail(rc, err); }
+  if (const char* e = getenv("SPCHOL_NO_LOOKAHEAD")) h->no_lookahead = atoi(e) != 0;
   build_plan(h);
   if (h->opt.device < 0) { *out = h; return SPCHOL_OK; }   // host-only analysis (no device state)
   rc = setup_device(h);
@@ -344,24 +409,49 @@ static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
   CK(cudaMemsetAsync(h->d_panels, 0, sizeof(double) * (size_t)std::max(1LL, h->panel_doubles), st));
   launch_init(h->d_avals, h->d_amap, S.nnzA, h->d_panels, st);
   tstop(ti);
+  // The plan's stream 0 (critical path) runs on a high-priority internal stream so its few-CTA
+  // cdiv launches are scheduled ahead of the trailing-update CTAs of stream 1 (low priority).
+  // Both fork from st and join back into it (required under graph capture).  With kernel
+  // timing enabled everything runs serialized on st.
+  const bool multi = !h->timing;
+  cudaStream_t s0 = multi ? h->crit_stream : st;
+  cudaStream_t s1 = multi ? h->side_stream : st;
+  if (multi) {
+    CK(cudaEventRecord(h->ev_fork, st));
+    CK(cudaStreamWaitEvent(s0, h->ev_fork, 0));
+  }
   for (size_t i = 0; i < h->plan.size(); ++i) {
     const Launch& L = h->plan[i];
+    cudaStream_t ls = L.stream == 1 ? s1 : s0;
+    if (L.op == OP_RECORD) {
+      if (multi) CK(cudaEventRecord(h->plan_events[L.ev], ls));
+      continue;
+    }
+    if (L.op == OP_WAIT) {
+      if (multi) CK(cudaStreamWaitEvent(ls, h->plan_events[L.ev], 0));
+      continue;
+    }
     ti = tstart((int)i);
+    const int prio = multi ? (L.stream == 1 ? h->prio_lo : h->prio_hi) : 0;
     switch (L.kind) {
       case K_POTRF:
-        launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, st);
+        launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio);
         break;
       case K_TRSM:
-        launch_gemm(MODE_TRSM, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, st);
+        launch_gemm(MODE_TRSM, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
         break;
       case K_LOCAL:
-        launch_gemm(MODE_LOCAL, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, st);
+        launch_gemm(MODE_LOCAL, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
         break;
       case K_SCATTER:
-        launch_gemm(MODE_SCATTER, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, st);
+        launch_gemm(MODE_SCATTER, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
         break;
     }
     tstop(ti);
+  }
+  if (multi) {
+    CK(cudaEventRecord(h->ev_join, s0));
+    CK(cudaStreamWaitEvent(st, h->ev_join, 0));
   }
   CK(cudaGetLastError());
   return SPCHOL_OK;
@@ -383,7 +473,7 @@ extern "C" int spchol_factor_async(spchol_handle* h) {
       if (rc != SPCHOL_OK) { if (g) cudaGraphDestroy(g); return rc; }
       if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
       h->graph = g;
-      CK(cudaGraphInstantiate(&h->gexec, g, 0));
+      CK(cudaGraphInstantiateWithFlags(&h->gexec, g, cudaGraphInstantiateFlagUseNodePriority));  // honour per-node priorities
     }
     CK(cudaGraphLaunch(h->gexec, h->stream));
     return SPCHOL_OK;
@@ -476,7 +566,12 @@ extern "C" int spchol_query(const spchol_handle* h, int key, int64_t* value) {
     case SPCHOL_Q_NMERGES: *value = S.nmerges; break;
     case SPCHOL_Q_FLOPS_EXACT: *value = (int64_t)S.flops_exact; break;
     case SPCHOL_Q_FLOPS_EXEC: *value = (int64_t)h->flops_exec; break;
-    case SPCHOL_Q_LAUNCHES: *value = (int64_t)h->plan.size() + 1; break;
+    case SPCHOL_Q_LAUNCHES: {
+      int64_t nl = 1;
+      for (const Launch& L : h->plan) nl += L.op == OP_LAUNCH;
+      *value = nl;
+      break;
+    }
     case SPCHOL_Q_UPDATE_ENTRIES: *value = (int64_t)h->update_entries; break;
     default: return fail(SPCHOL_ERR_VALIDATION, "unknown query key");
   }
@@ -544,6 +639,28 @@ extern "C" int spchol_export_diagonal(spchol_handle* h, double* diag) {
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(diag, h->d_y, sizeof(double) * (size_t)S.n, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  return SPCHOL_OK;
+}
+
+extern "C" int spchol_kernel_trace(spchol_handle* h, int64_t cap, int64_t* count, int32_t* kinds, int32_t* levels,
+                                   int32_t* ntasks, double* ms) {
+  if (!h || !count) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
+  if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
+  CK(cudaSetDevice(h->opt.device));
+  CK(cudaStreamSynchronize(h->stream));
+  int64_t c = 0;
+  for (auto& pr : h->pending) {
+    if (c < cap) {
+      float t = 0;
+      cudaEventElapsedTime(&t, h->ev_pool[pr.second], h->ev_pool[pr.second + 1]);
+      if (kinds) kinds[c] = pr.first < 0 ? K_INIT : h->plan[pr.first].kind;
+      if (levels) levels[c] = pr.first < 0 ? -1 : h->plan_level[pr.first];
+      if (ntasks) ntasks[c] = pr.first < 0 ? 0 : h->plan[pr.first].n;
+      if (ms) ms[c] = t;
+    }
+    ++c;
+  }
+  *count = c;
   return SPCHOL_OK;
 }
 

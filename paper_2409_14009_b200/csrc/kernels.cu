@@ -39,7 +39,7 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 //                one level may hit the same ancestor entry).
 // ----------------------------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(GEMM_THREADS) gemm_kernel(const GTask* __restrict__ tasks,
+__global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const GTask* __restrict__ tasks,
                                                             const SnInfo* __restrict__ sn, double* panels,
                                                             const double* __restrict__ linv,
                                                             const long long* __restrict__ ucol_base,
@@ -190,137 +190,183 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_kernel(const GTask* __restr
 }
 
 // ----------------------------------------------------------------------------------------------
-// potrf_kernel: one CTA (256 threads) factors the nb x nb (nb <= 64) diagonal block [c0, c0+nb) of
-// supernode J ("DPOTRF") and forms X = L_bb^{-1} for TRSM-as-GEMM.
-// The 64x64 lower triangle is cut into 4x4 register blocks; thread t < 136 owns block (bi, bj),
-// bi >= bj.  Cholesky, right-looking, step j: the owners of column j publish it (double-buffered
-// shared vector, ONE barrier per step), every thread scales its rows/columns by 1/sqrt(pivot) and
-// applies the rank-1 update to its block.  Inverse, step s (forward substitution on I): the owners
-// of row s of X scale it by 1/L_ss and publish it; rows r > s subtract L(r,s) X(s,:).
-// The strict upper triangle of the panel is padding and is never written.  X is written to the
-// task's workspace slot, column-major, ld 64, zero padded.  A pivot that is not > 0 (incl. NaN)
-// records its global column (final numbering) with atomicMin (a7).
+// potrf_kernel: one CTA (4 warps) factors the nb x nb (nb <= 64) diagonal block [c0, c0+nb) of
+// supernode J ("DPOTRF") and forms X = L_bb^{-1} for TRSM-as-GEMM.  A block with nb < 64 is
+// padded with the identity (chol/inverse of blockdiag(A, I) = blockdiag(L, I)).
+// 2x2 blocking of the 64x64 block into 32x32 pieces keeps the dependent chain short:
+//   warp 0: L11 = chol(A11), X11 = L11^{-1}         (register rows + shuffles, no barriers)
+//   all:    L21 = A21 X11^T;  A22 -= L21 L21^T
+//   warp 0: L22 = chol(A22), X22 = L22^{-1}
+//   all:    T = L21 X11;  X21 = -X22 T
+// The strict upper triangle of the panel is padding and is never written.  X goes to the task's
+// workspace slot, column-major, ld 64, zero padded.  A pivot that is not > 0 (incl. NaN) records
+// its global column (final numbering) with atomicMin (a7).
 // ----------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(POTRF_THREADS) potrf_kernel(const PTask* __restrict__ tasks,
-                                                              const SnInfo* __restrict__ sn,
-                                                              const int* __restrict__ sfirst, double* panels,
-                                                              double* linv, unsigned long long* fail) {
-  __shared__ double vbuf[2][NBMAX];            // published column of L / row of X
-  __shared__ double Ls[NBMAX][NBMAX + 1];      // Ls[row][col] = L(row, col) after the Cholesky
-  __shared__ double invd[NBMAX];
+constexpr int PLD = NBMAX + 1;   // shared-memory column stride (doubles) of the 64x64 blocks
+
+// Cholesky of the 32x32 block at (b, b) of D (D[col][row]) by one warp: lane r owns row r.  The
+// step loop stays rolled (small code): the registers rotate so the current column is always a[0].
+__device__ __noinline__ void chol32_warp(double* D, int b, int lane, int* bad, double* rdiag) {
+  double a[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = c <= lane ? D[(b + c) * PLD + b + lane] : 0.0;
+#pragma unroll 1
+  for (int j = 0; j < 32; ++j) {
+    const double d = __shfl_sync(0xffffffffu, a[0], j);
+    const double rl = rsqrt(d), l = d * rl;
+    if (*bad < 0 && !(d > 0.0)) *bad = b + j;
+    const double lrj = lane > j ? a[0] * rl : (lane == j ? l : 0.0);
+    if (lane >= j) D[(b + j) * PLD + b + lane] = lrj;
+    if (lane == j) rdiag[b + j] = rl;
+#pragma unroll
+    for (int c = 1; c < 32; ++c) {
+      const double lc = __shfl_sync(0xffffffffu, lrj, (j + c) & 31);
+      if (j + c <= lane) a[c] -= lrj * lc;
+    }
+#pragma unroll
+    for (int c = 0; c < 31; ++c) a[c] = a[c + 1];
+    a[31] = 0.0;
+  }
+}
+
+// X_bb = L_bb^{-1} for the 32x32 block at (b, b) by one warp: lane c solves L x = e_c, column
+// oriented (x_s final at step s, then eliminated from the rows below); registers rotate as above.
+__device__ __noinline__ void inv32_warp(const double* D, double* X, int b, int lane, const double* rdiag) {
+  double y[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) y[i] = i == lane ? 1.0 : 0.0;
+#pragma unroll 1
+  for (int s = 0; s < 32; ++s) {
+    const double xs = y[0] * rdiag[b + s];
+    X[(b + lane) * PLD + b + s] = xs;
+#pragma unroll
+    for (int i = 1; i < 32; ++i)
+      if (s + i < 32) y[i] -= D[(b + s) * PLD + b + s + i] * xs;
+#pragma unroll
+    for (int i = 0; i < 31; ++i) y[i] = y[i + 1];
+    y[31] = 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(POTRF_THREADS, 4) potrf_kernel(const PTask* __restrict__ tasks,
+                                                                 const SnInfo* __restrict__ sn,
+                                                                 const int* __restrict__ sfirst, double* panels,
+                                                                 double* linv, unsigned long long* fail) {
+  extern __shared__ double psm[];
+  double* D = psm;                      // D[col * PLD + row]: A, then L (lower); upper-right 32x32 holds T
+  double* X = psm + NBMAX * PLD;        // X[col * PLD + row] = (L^{-1})(row, col)
+  __shared__ double rdiag[NBMAX];
   const PTask T = tasks[blockIdx.x];
   const SnInfo S = sn[T.sn];
-  const int nb = T.nb, tid = threadIdx.x;
-  // block coordinates: t -> (bi, bj), bi >= bj, row-major over the lower block triangle
-  const bool owner = tid < 136;
-  int bi = 0, bj = owner ? tid : 0;
-  while (bj > bi) { bj -= bi + 1; ++bi; }
-  const int r0 = 4 * bi, q0 = 4 * bj;
+  const int nb = T.nb, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* P = panels + S.off + (long long)T.c0 * S.ld + T.c0;
-  double a[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = r0 + i, c = q0 + q;
-      a[i][q] = (owner && r < nb && c < nb && r >= c) ? P[(long long)c * S.ld + r] : 0.0;
-    }
-  int bad = -1;
-  for (int jb = 0; jb < (nb + 3) / 4; ++jb) {
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const int j = 4 * jb + jj;
-      if (j >= nb) break;
-      double* col = vbuf[j & 1];
-      if (owner && bj == jb) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) col[r0 + i] = a[i][jj];
-      }
-      __syncthreads();
-      const double d = col[j];
-      const double l = sqrt(d), rl = 1.0 / l;
-      if (bad < 0 && !(d > 0.0)) bad = j;
-      double lr[4], lc[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        lr[i] = col[r0 + i] * rl;
-        lc[i] = col[q0 + i] * rl;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (r0 + i >= q0 + q && q0 + q > j) a[i][q] -= lr[i] * lc[q];
-      if (bj == jb) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = r0 + i;
-          if (r > j) a[i][jj] = lr[i];
-          else if (r == j) a[i][jj] = l;
-        }
-      }
-      if (tid == 0) invd[j] = rl;
-    }
-  }
-  if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[T.sn] + T.c0 + bad));
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = r0 + i, c = q0 + q;
-      if (owner) Ls[r][c] = a[i][q];
-      if (owner && r < nb && c < nb && r >= c) P[(long long)c * S.ld + r] = a[i][q];
-    }
-  // inverse: x = identity restricted to the block, forward substitution over pivot rows s
-  double x[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) x[i][q] = (owner && r0 + i == q0 + q && r0 + i < nb) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int sb = 0; sb < (nb + 3) / 4; ++sb) {
-#pragma unroll
-    for (int ss = 0; ss < 4; ++ss) {
-      const int s = 4 * sb + ss;
-      if (s >= nb) break;
-      double* row = vbuf[s & 1];
-      if (owner && bi == sb) {
-        const double is = invd[s];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          x[ss][q] *= is;
-          row[q0 + q] = x[ss][q];
-        }
-      }
-      __syncthreads();
-      if (owner && r0 + 3 > s) {
-        double xs[4], lrs[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) xs[q] = row[q0 + q];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) lrs[i] = Ls[r0 + i][s];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (r0 + i > s && q0 + q <= s) x[i][q] -= lrs[i] * xs[q];
-      }
-    }
-  }
-  double* W = linv + (long long)T.slot * (NBMAX * NBMAX);
-  // the whole 64x64 slot is written: owners write their lower blocks, the rest writes zeros
   for (int e = tid; e < NBMAX * NBMAX; e += POTRF_THREADS) {
-    const int c = e / NBMAX, r = e % NBMAX;
-    if (r < c || r >= nb || c >= nb) W[e] = 0.0;
+    const int c = e >> 6, r = e & 63;
+    double v = 0.0;
+    if (r >= c) v = (r < nb) ? (c < nb ? P[(long long)c * S.ld + r] : 0.0) : (r == c ? 1.0 : 0.0);
+    D[c * PLD + r] = v;
+    X[c * PLD + r] = 0.0;
   }
-  if (owner) {
+  int bad = -1;
+  __syncthreads();
+  if (warp == 0) {
+    chol32_warp(D, 0, lane, &bad, rdiag);
+    __syncwarp();
+    inv32_warp(D, X, 0, lane, rdiag);
+  }
+  __syncthreads();
+  // L21 = A21 X11^T: thread -> row i = 32 + (tid & 31), columns c = cg + 4m (cg = warp)
+  {
+    const int i = 32 + lane;
+    double arow[32];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int p = 0; p < 32; ++p) arow[p] = D[p * PLD + i];
+    double out[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = r0 + i, c = q0 + q;
-        if (r >= c && r < nb && c < nb) W[c * NBMAX + r] = x[i][q];
-      }
+    for (int m = 0; m < 8; ++m) {   // (out[] needs static indices)
+      const int c = warp + 4 * m;
+      double s = 0.0;
+#pragma unroll
+      for (int p = 0; p < 32; ++p)
+        if (p <= c) s += arow[p] * X[p * PLD + c];      // X11(c, p)
+      out[m] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 8; ++m) D[(warp + 4 * m) * PLD + i] = out[m];
+  }
+  __syncthreads();
+  // A22 -= L21 L21^T (lower): thread -> row i = 32 + lane, columns j = 32 + warp + 4m <= i
+  {
+    const int i = 32 + lane;
+    double lrow[32];
+#pragma unroll
+    for (int p = 0; p < 32; ++p) lrow[p] = D[p * PLD + i];
+#pragma unroll 1
+    for (int m = 0; m < 8; ++m) {
+      const int j = 32 + warp + 4 * m;
+      if (j > i) continue;
+      double s = 0.0;
+#pragma unroll
+      for (int p = 0; p < 32; ++p) s += lrow[p] * D[p * PLD + j];
+      D[j * PLD + i] -= s;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    chol32_warp(D, 32, lane, &bad, rdiag);
+    __syncwarp();
+    inv32_warp(D, X, 32, lane, rdiag);
+  }
+  __syncthreads();
+  // T = L21 X11 (32x32), stored in D's upper-right block: T(q, c) at D[(32 + c) * PLD + q]
+  {
+    const int q = lane;
+    double lrow[32];
+#pragma unroll
+    for (int p = 0; p < 32; ++p) lrow[p] = D[p * PLD + 32 + q];
+#pragma unroll 1
+    for (int m = 0; m < 8; ++m) {
+      const int c = warp + 4 * m;
+      double s = 0.0;
+#pragma unroll
+      for (int p = 0; p < 32; ++p)
+        if (p >= c) s += lrow[p] * X[c * PLD + p];       // X11(p, c)
+      D[(32 + c) * PLD + q] = s;
+    }
+  }
+  __syncthreads();
+  // X21 = -X22 T: X(32 + i, c) = -sum_{q <= i} X22(i, q) T(q, c)
+  {
+    const int i = lane;
+    double xrow[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) xrow[q] = q <= i ? X[(32 + q) * PLD + 32 + i] : 0.0;
+#pragma unroll 1
+    for (int m = 0; m < 8; ++m) {
+      const int c = warp + 4 * m;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) s += xrow[q] * D[(32 + c) * PLD + q];
+      X[c * PLD + 32 + i] = -s;
+    }
+  }
+  // failure flag: any lane of warp 0 may hold it
+  if (warp == 0) {
+    int b2 = bad;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int ob = __shfl_xor_sync(0xffffffffu, b2, o);
+      b2 = (b2 < 0) ? ob : (ob < 0 ? b2 : min(b2, ob));
+    }
+    if (lane == 0 && b2 >= 0 && b2 < nb) atomicMin(fail, (unsigned long long)(sfirst[T.sn] + T.c0 + b2));
+  }
+  __syncthreads();
+  for (int e = tid; e < NBMAX * NBMAX; e += POTRF_THREADS) {
+    const int c = e >> 6, r = e & 63;
+    const bool valid = r >= c && r < nb && c < nb;
+    if (valid) P[(long long)c * S.ld + r] = D[c * PLD + r];
+    linv[(long long)T.slot * (NBMAX * NBMAX) + e] = valid ? X[c * PLD + r] : 0.0;
   }
 }
 
@@ -396,27 +442,46 @@ __global__ void gather_kernel(const double* __restrict__ src, const long long* _
 // ---------------------------------------------------------------------------------------------- launchers
 cudaError_t kernels_init_attributes() {
   cudaError_t e;
+  if ((e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   return cudaSuccess;
 }
 
+// Launch with an explicit scheduling priority (cudaLaunchAttributePriority is recorded into the
+// kernel node under graph capture; stream priorities alone are not).
+template <typename... KArgs, typename... Args>
+static void launch_prio(void (*kern)(KArgs...), int grid, int block, int smem, cudaStream_t st, int prio,
+                        Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = prio;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, const double* linv,
-                 const long long* ucol_base, const long long* ucol_map, const int* posmap, cudaStream_t st) {
+                 const long long* ucol_base, const long long* ucol_map, const int* posmap, cudaStream_t st, int prio) {
   if (ntasks <= 0) return;
   if (mode == MODE_LOCAL)
-    gemm_kernel<MODE_LOCAL><<<ntasks, GEMM_THREADS, GEMM_SMEM, st>>>(tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
+    launch_prio(gemm_kernel<MODE_LOCAL>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
   else if (mode == MODE_TRSM)
-    gemm_kernel<MODE_TRSM><<<ntasks, GEMM_THREADS, GEMM_SMEM, st>>>(tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
+    launch_prio(gemm_kernel<MODE_TRSM>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
   else
-    gemm_kernel<MODE_SCATTER><<<ntasks, GEMM_THREADS, GEMM_SMEM, st>>>(tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
+    launch_prio(gemm_kernel<MODE_SCATTER>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
 }
 
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels, double* linv,
-                  unsigned long long* fail, cudaStream_t st) {
+                  unsigned long long* fail, cudaStream_t st, int prio) {
   if (ntasks <= 0) return;
-  potrf_kernel<<<ntasks, POTRF_THREADS, 0, st>>>(tasks, sn, sfirst, panels, linv, fail);
+  launch_prio(potrf_kernel, ntasks, POTRF_THREADS, POTRF_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
 }
 
 void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st) {

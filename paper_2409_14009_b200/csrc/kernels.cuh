@@ -32,19 +32,29 @@ struct PTask {
 enum { MODE_LOCAL = 0, MODE_TRSM = 1, MODE_SCATTER = 2 };
 
 constexpr int TILE = 64;           // CTA tile edge (rows and columns)
-constexpr int BK = 32;             // K chunk per pipeline stage
-constexpr int STAGES = 3;          // cp.async pipeline depth
+#ifndef SPCHOL_MINB
+#define SPCHOL_MINB 4
+#endif
+#ifndef SPCHOL_BK
+#define SPCHOL_BK 8
+#endif
+#ifndef SPCHOL_STAGES
+#define SPCHOL_STAGES 4
+#endif
+constexpr int BK = SPCHOL_BK;      // K chunk per pipeline stage
+constexpr int STAGES = SPCHOL_STAGES;  // cp.async pipeline depth
 constexpr int LDS = TILE + 8;      // smem column stride (doubles): 8 mod 16 -> conflict-free DMMA fragments
 constexpr int GEMM_THREADS = 128;  // 4 warps, 2x2, warp tile 32x32
 constexpr int GEMM_SMEM = 2 * STAGES * BK * LDS * (int)sizeof(double);
 constexpr int NBMAX = 64;          // cdiv block width
-constexpr int POTRF_THREADS = 256;
+constexpr int POTRF_THREADS = 128;
+constexpr int POTRF_SMEM = 2 * NBMAX * (NBMAX + 1) * (int)sizeof(double);
 
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels,
                  const double* linv, const long long* ucol_base, const long long* ucol_map,
-                 const int* posmap, cudaStream_t st);
+                 const int* posmap, cudaStream_t st, int prio = 0);
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels,
-                  double* linv, unsigned long long* fail, cudaStream_t st);
+                  double* linv, unsigned long long* fail, cudaStream_t st, int prio = 0);
 void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st);
 void launch_solve_fwd(const int* sns, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
                       const int* rows, const double* panels, double* y, cudaStream_t st);

@@ -1,0 +1,74 @@
+"""The product's fast host analyze (C++) against the oracle's independent symbolic phase: bit-exact
+on every integer array — small configs directly, the full BASELINE configs
+against sha256 digests written by tests/golden/make_symbolic_golden.py (oracle only)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+import paper_2409_14009_b200 as sp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+KEYS = ["post", "parent3", "cc3", "ffirst", "fgroup", "perm_final", "sfirst", "sparent", "rows_ptr", "rows",
+        "rel_ptr", "rel_anc", "rel_q0", "rel_off", "relind", "parent_final", "cc_final"]
+
+
+def compare(prob, cap=0.25):
+    with sp.Solver.from_problem(prob, device=-1, merge_cap=cap) as h:
+        a = h.spchol_export_symbolic()
+        o = oracle.Oracle.from_problem(prob, cap=cap, keep_L=False)
+        b = o.symbolic()
+        for k in KEYS:
+            assert np.array_equal(a[k], b[k]), k
+        assert h.query("NNZ_L") == o.nnzL
+        assert h.query("FLOPS_EXACT") == int(o.flops)
+        assert h.query("ADDED") == o.added and h.query("NMERGES") == o.nmerges
+        return h.query("NSUPER")
+
+
+@pytest.mark.parametrize("name", ["C1", "T1", "T2", "T3", "S2", "S3", "S4", "S5"])
+def test_analyze_small_configs(name):
+    compare(gen.make(name))
+
+
+@pytest.mark.parametrize("cap", [-1.0, 0.0, 0.05, 0.25, 1.0, 10.0])
+def test_analyze_merge_caps(cap):
+    compare(gen.make("S5"), cap)
+    compare(gen.make("C1"), cap)
+
+
+@pytest.mark.parametrize("block", range(0, 10))
+def test_analyze_random_corpus(block):
+    for trial in range(block * 100, block * 100 + 100):
+        compare(gen.random_spd(1000 + trial))
+
+
+def test_analyze_grids_misc():
+    for args in [(5, 1, 1, 1, 1), (9, 2, 2, 1, 1), (27, 3, 3, 3, 3), (7, 10, 1, 1, 1), (9, 17, 13, 1, 1),
+                 (27, 6, 5, 4, 1), (7, 12, 11, 10, 1), (5, 50, 3, 1, 1)]:
+        kind, kx, ky, kz, dof = args
+        compare(gen.make_grid(kind, kx, ky, kz, dof))
+
+
+def _digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_analyze_full_configs_against_golden(name):
+    path = os.path.join(HERE, "golden", f"symbolic_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    g = json.load(open(path))
+    p = gen.make(name)
+    with sp.Solver.from_problem(p, device=-1) as h:
+        a = h.spchol_export_symbolic()
+        for k in KEYS:
+            assert str(a[k].dtype) == g["dtypes"][k], k
+            assert _digest(a[k]) == g["sha256"][k], k
+        assert h.query("NNZ_L") == g["nnz_L"] and h.query("NSUPER") == g["nsuper"]
+        assert h.query("NFUND") == g["nfund"] and h.query("ADDED") == g["added"]

@@ -1,0 +1,87 @@
+"""The C-ABI library loads on a CPU-only box, exports every symbol include/spchol.h declares, and
+its host-side paths (validation, host-only analyze, state errors) behave as documented."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import gen
+import paper_2409_14009_b200 as sp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "spchol.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(spchol_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    L = sp.lib()
+    names = header_functions()
+    assert len(names) >= 17
+    for nm in names:
+        assert hasattr(L, nm), nm
+    assert sorted(sp.EXPORTS) == names
+
+
+def test_default_options():
+    o = sp.default_options()
+    assert o.merge_cap == 0.25 and o.device == 0 and o.use_graph == 1
+
+
+def _err(fn):
+    with pytest.raises(sp.SpcholError) as ei:
+        fn()
+    return ei.value.code
+
+
+def test_validation_errors():
+    p = gen.make("T1")
+    # non-bijective perm
+    bad = p.perm.copy()
+    bad[0] = bad[1]
+    assert _err(lambda: sp.Solver(p.n, p.colptr, p.rowidx, None, bad, device=-1)) == sp.SPCHOL_ERR_VALIDATION
+    # missing diagonal (first entry of column 0 replaced)
+    ri = p.rowidx.copy()
+    ri[p.colptr[3]] = ri[p.colptr[3] + 1] if p.colptr[4] - p.colptr[3] > 1 else 0
+    assert _err(lambda: sp.Solver(p.n, p.colptr, ri, None, p.perm, device=-1)) == sp.SPCHOL_ERR_VALIDATION
+    # rows not increasing
+    ri = p.rowidx.copy()
+    j = next(j for j in range(p.n) if p.colptr[j + 1] - p.colptr[j] >= 3)
+    ri[p.colptr[j] + 1], ri[p.colptr[j] + 2] = ri[p.colptr[j] + 2], ri[p.colptr[j] + 1]
+    assert _err(lambda: sp.Solver(p.n, p.colptr, ri, None, p.perm, device=-1)) == sp.SPCHOL_ERR_VALIDATION
+    # row out of range
+    ri = p.rowidx.copy()
+    ri[p.colptr[p.n] - 1] = p.n
+    assert _err(lambda: sp.Solver(p.n, p.colptr, ri, None, p.perm, device=-1)) == sp.SPCHOL_ERR_VALIDATION
+    # negative n
+    assert _err(lambda: sp.Solver(-1, np.zeros(1, np.int64), np.zeros(0, np.int32), device=-1)) == sp.SPCHOL_ERR_DIMENSION
+    # bad block option
+    assert _err(lambda: sp.Solver.from_problem(p, device=-1, block=12)) == sp.SPCHOL_ERR_VALIDATION
+
+
+def test_host_only_handle_state_errors():
+    p = gen.make("T2")
+    with sp.Solver.from_problem(p, device=-1) as h:
+        assert _err(h.spchol_factor) == sp.SPCHOL_ERR_STATE
+        assert _err(lambda: h.spchol_solve(np.ones(p.n))) == sp.SPCHOL_ERR_STATE
+        assert _err(lambda: h.spchol_set_values(p.values)) == sp.SPCHOL_ERR_STATE
+        assert h.query("N") == p.n and h.query("NNZ_A") == p.nnz
+        off, ld, _ = h.spchol_export_panels(values=False)
+        sym = h.spchol_export_symbolic()
+        m = np.diff(sym["rows_ptr"])
+        k = np.diff(sym["sfirst"])
+        assert np.all(ld >= m) and np.all(ld % 2 == 0)
+        assert np.array_equal(np.diff(off), ld.astype(np.int64) * k)
+        assert h.query("PANEL_DOUBLES") == off[-1]
+
+
+def test_n_zero_and_n_one():
+    with sp.Solver(0, np.zeros(1, np.int64), np.zeros(0, np.int32), device=-1) as h:
+        assert h.query("NSUPER") == 0 and h.query("NNZ_L") == 0
+    with sp.Solver(1, np.array([0, 1], np.int64), np.array([0], np.int32), device=-1) as h:
+        assert h.query("NSUPER") == 1 and h.query("NNZ_L") == 1
