@@ -46,6 +46,7 @@ struct Launch {
   int n;           // tasks
   double flops, bytes;
   int op = OP_LAUNCH, stream = 0, ev = -1;
+  int aux = 0;     // K_SMALL: dynamic shared memory (doubles)
 };
 template <class T>
 cudaError_t dalloc(T** p, size_t count) {
@@ -74,6 +75,8 @@ struct spchol_handle {
   std::vector<GTask> gtasks;
   std::vector<PTask> ptasks;
   std::vector<int> level_sns, level_off;
+  std::vector<int> small_sns;           // supernodes handled by the fused small kernel, by level
+  std::vector<char> is_small;
   long long panel_doubles = 0;
   std::vector<long long> panel_off;
   double flops_exec = 0, update_entries = 0;
@@ -84,7 +87,7 @@ struct spchol_handle {
   // device
   double *d_panels = nullptr, *d_avals = nullptr, *d_linv = nullptr, *d_y = nullptr, *d_y2 = nullptr;
   long long *d_diag_idx = nullptr, *d_amap = nullptr, *d_ucol_base = nullptr, *d_ucol_map = nullptr, *d_rows_ptr = nullptr;
-  int *d_posmap = nullptr, *d_sfirst = nullptr, *d_rows = nullptr, *d_perm = nullptr, *d_level_sns = nullptr;
+  int *d_small_sns = nullptr, *d_posmap = nullptr, *d_sfirst = nullptr, *d_rows = nullptr, *d_perm = nullptr, *d_level_sns = nullptr;
   SnInfo* d_sn = nullptr;
   GTask* d_gtasks = nullptr;
   PTask* d_ptasks = nullptr;
@@ -147,10 +150,43 @@ static void build_plan(spchol_handle* h) {
     if (end > off) h->plan.push_back(Launch{kind, off, (int)(end - off), fl, by, OP_LAUNCH, 0, -1});
   };
   h->max_slots = 0;
+  // fused small-supernode path: k <= small_max_k, m <= 256, m k <= SMALL_MAXELEMS (shared memory)
+  const int kmax = h->opt.small_max_k < 0 ? 0 : (h->opt.small_max_k == 0 ? SMALL_MAXK : std::min(h->opt.small_max_k, SMALL_MAXK));
+  h->is_small.assign(ns, 0);
+  for (int J = 0; J < ns; ++J) {
+    const SnInfo& I = h->sn[J];
+    h->is_small[J] = I.k <= kmax && I.m <= SMALL_MAXM && (long long)I.m * I.k <= SMALL_MAXELEMS;
+  }
   for (int l = 0; l < S.nlevels; ++l) {
     const size_t plan_before = h->plan.size();
+    // small supernodes of this level: one launch on stream 1 (independent of the level's big ones)
+    {
+      long long s0 = (long long)h->small_sns.size();
+      int mx = 0;
+      double fsm = 0, bsm = 0;
+      for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
+        const int J = h->level_sns[x];
+        if (!h->is_small[J]) continue;
+        const SnInfo& I = h->sn[J];
+        h->small_sns.push_back(J);
+        mx = std::max(mx, I.m * I.k);
+        const double t = I.m - I.k;
+        for (int c = 0; c < I.k; ++c) fsm += (double)(I.m - c) * (double)(I.m - c);
+        bsm += 16.0 * I.m * I.k + 16.0 * 0.5 * t * (t + 1);
+      }
+      long long s1 = (long long)h->small_sns.size();
+      if (s1 > s0) {
+        const int ev = h->nevents++;
+        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 0, ev});
+        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 1, ev});
+        Launch L{K_SMALL, s0, (int)(s1 - s0), fsm, bsm, OP_LAUNCH, 1, -1};
+        L.aux = mx;
+        h->plan.push_back(L);
+      }
+    }
     int maxblk = 0;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
+      if (h->is_small[h->level_sns[x]]) continue;
       const SnInfo& I = h->sn[h->level_sns[x]];
       maxblk = std::max(maxblk, (I.k + NB - 1) / NB);
     }
@@ -170,6 +206,7 @@ static void build_plan(spchol_handle* h) {
       std::vector<GTask> local, nxt, rest;
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
         const int J = h->level_sns[x];
+        if (h->is_small[J]) continue;
         const SnInfo& I = h->sn[J];
         const int c0 = s * NB;
         if (c0 >= I.k) continue;
@@ -230,11 +267,19 @@ static void build_plan(spchol_handle* h) {
         h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 1, pending_rest_ev});
       }
     }
-    if (pending_rest_ev >= 0) h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 0, pending_rest_ev});  // join
+    bool s1_used = false;
+    for (size_t q = plan_before; q < h->plan.size(); ++q) s1_used |= h->plan[q].stream == 1;
+    if (s1_used) {  // join stream 1 (small-supernode launch and trailing updates) before the level's scatter
+      const int ev = h->nevents++;
+      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 1, ev});
+      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 0, ev});
+    }
+    (void)pending_rest_ev;
     long long s0g = (long long)h->gtasks.size();
     double fs = 0, bs = 0;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
       const int J = h->level_sns[x];
+      if (h->is_small[J]) continue;
       const SnInfo& I = h->sn[J];
       const int t = I.m - I.k;
       if (t <= 0) continue;
@@ -246,7 +291,6 @@ static void build_plan(spchol_handle* h) {
     }
     push(K_SCATTER, s0g, (long long)h->gtasks.size(), fs, bs);
     h->plan_level.resize(h->plan.size(), l);
-    (void)plan_before;
   }
 }
 
@@ -311,6 +355,7 @@ static int setup_device(spchol_handle* h) {
   CK(upload(&h->d_rows, S.rows));
   CK(upload(&h->d_perm, S.perm_final));
   CK(upload(&h->d_level_sns, h->level_sns));
+  CK(upload(&h->d_small_sns, h->small_sns));
   CK(dalloc(&h->d_y, (size_t)S.n));
   CK(dalloc(&h->d_y2, (size_t)S.n));
   return SPCHOL_OK;
@@ -319,7 +364,7 @@ static int setup_device(spchol_handle* h) {
 static void free_device(spchol_handle* h) {
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->graph) cudaGraphDestroy(h->graph);
-  void* ptrs[] = {h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
+  void* ptrs[] = {h->d_small_sns, h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
                   h->d_rows_ptr, h->d_posmap, h->d_sfirst, h->d_rows, h->d_perm, h->d_level_sns, h->d_sn,
                   h->d_gtasks, h->d_ptasks, h->d_fail};
   for (void* p : ptrs) if (p) cudaFree(p);
@@ -434,6 +479,10 @@ static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
     ti = tstart((int)i);
     const int prio = multi ? (L.stream == 1 ? h->prio_lo : h->prio_hi) : 0;
     switch (L.kind) {
+      case K_SMALL:
+        launch_small(h->d_small_sns + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_ucol_base, h->d_ucol_map,
+                     h->d_posmap, h->d_fail, L.aux, ls, prio);
+        break;
       case K_POTRF:
         launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio);
         break;

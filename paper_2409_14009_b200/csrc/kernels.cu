@@ -370,6 +370,96 @@ __global__ void __launch_bounds__(POTRF_THREADS, 4) potrf_kernel(const PTask* __
   }
 }
 
+// ----------------------------------------------------------------------------------------------
+// small_kernel: the whole RL step of one small supernode J per CTA (k_J <= 64, m_J <= 256,
+// m_J k_J <= SMALL_MAXELEMS), with the panel resident in shared memory:
+//   cdiv(J): unblocked right-looking Cholesky of the k x k block + TRSM of the rows below,
+//     thread r owns panel row r, two barriers per column;
+//   U_J = L_R L_R^T, 4x4 register blocks of the lower t x t update, K = k;
+//   assembly: each U entry is RED-added (negated) into its ancestor panel through
+//     relind (posmap), exactly as in the tiled scatter kernel.
+// Thousands of these supernodes make up the lower levels of the 2D configs.
+// ----------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restrict__ sns,
+                                                              const SnInfo* __restrict__ sn,
+                                                              const int* __restrict__ sfirst, double* panels,
+                                                              const long long* __restrict__ ucol_base,
+                                                              const long long* __restrict__ ucol_map,
+                                                              const int* __restrict__ posmap,
+                                                              unsigned long long* fail) {
+  extern __shared__ double P[];         // m x k, column-major, ld = m
+  const int J = sns[blockIdx.x];
+  const SnInfo S = sn[J];
+  const int m = S.m, k = S.k, t = m - k, tid = threadIdx.x;
+  double* G = panels + S.off;
+  for (int e = tid; e < m * k; e += SMALL_THREADS) {
+    const int c = e / m, r = e - c * m;
+    P[e] = G[(long long)c * S.ld + r];
+  }
+  __syncthreads();
+  int bad = -1;
+  const int r = tid;
+  __shared__ double colbuf[SMALL_MAXM];   // L(:, j) of the current step
+  for (int j = 0; j < k; ++j) {
+    const double d = P[j * m + j];
+    const double rl = rsqrt(d);
+    if (bad < 0 && !(d > 0.0)) bad = j;
+    const double v = (r < m && r >= j) ? (r == j ? d * rl : P[j * m + r] * rl) : 0.0;
+    if (r < m) colbuf[r] = v;
+    __syncthreads();                        // everyone has read the pivot; column j published
+    if (r < m && r >= j) P[j * m + r] = v;
+    if (r < m && r > j) {
+      const int ce = min(r, k - 1);
+      for (int c = j + 1; c <= ce; ++c) P[c * m + r] -= v * colbuf[c];
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[J] + bad));
+  for (int e = tid; e < m * k; e += SMALL_THREADS) {
+    const int c = e / m, rr = e - c * m;
+    if (rr >= c) G[(long long)c * S.ld + rr] = P[e];
+  }
+  if (t <= 0) return;
+  // U_J in 4x4 register blocks over the lower block triangle of the t x t update
+  const int nbt = (t + 3) >> 2, nblk = nbt * (nbt + 1) / 2;
+  for (int bidx = tid; bidx < nblk; bidx += SMALL_THREADS) {
+    int bi = (int)((sqrtf(8.0f * bidx + 1.0f) - 1.0f) * 0.5f);
+    while (bi * (bi + 1) / 2 > bidx) --bi;
+    while ((bi + 1) * (bi + 2) / 2 <= bidx) ++bi;
+    const int bj = bidx - bi * (bi + 1) / 2;
+    const int r0 = k + 4 * bi, c0 = k + 4 * bj;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
+    for (int p = 0; p < k; ++p) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = r0 + i < m ? P[p * m + r0 + i] : 0.0;
+        b[i] = c0 + i < m ? P[p * m + c0 + i] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] += a[i] * b[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gc = c0 + q;
+      if (gc >= m) continue;
+      const long long cb = ucol_base[S.ucol + gc - k];
+      const long long mb = ucol_map[S.ucol + gc - k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int gr = r0 + i;
+        if (gr < m && gr >= gc) atomicAdd(panels + cb + posmap[mb + gr], -acc[i][q]);
+      }
+    }
+  }
+}
+
 __global__ void init_scatter_kernel(const double* __restrict__ vals, const long long* __restrict__ amap,
                                     long long nnz, double* panels) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz; e += (long long)gridDim.x * blockDim.x)
@@ -443,6 +533,7 @@ __global__ void gather_kernel(const double* __restrict__ src, const long long* _
 cudaError_t kernels_init_attributes() {
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_MAXELEMS * (int)sizeof(double)))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
@@ -482,6 +573,14 @@ void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* s
                   unsigned long long* fail, cudaStream_t st, int prio) {
   if (ntasks <= 0) return;
   launch_prio(potrf_kernel, ntasks, POTRF_THREADS, POTRF_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
+}
+
+void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,
+                  const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,
+                  int smem_doubles, cudaStream_t st, int prio) {
+  if (count <= 0) return;
+  launch_prio(small_kernel, count, SMALL_THREADS, smem_doubles * (int)sizeof(double), st, prio, sns, sn, sfirst, panels,
+              ucol_base, ucol_map, posmap, fail);
 }
 
 void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st) {

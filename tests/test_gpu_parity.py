@@ -43,21 +43,25 @@ def run_parity(prob, **opts):
     return err
 
 
+@pytest.mark.parametrize("small", [0, -1, 16])
 @pytest.mark.parametrize("name", ["C1", "T1", "T2", "T3", "S2", "S3", "S4", "S5"])
-def test_parity_configs(name):
-    run_parity(gen.make(name))
+def test_parity_configs(name, small):
+    """small = fused small-supernode kernel cutoff (0 default, -1 never: everything tiled)."""
+    run_parity(gen.make(name), small_max_k=small)
 
 
 @pytest.mark.parametrize("block", [8, 16, 24, 40])
 def test_parity_block_sizes(block):
     """cdiv block widths that leave ragged block columns (k not a multiple of the block)."""
-    run_parity(gen.make("S5"), block=block)
-    run_parity(gen.make("T3"), block=block)
+    run_parity(gen.make("S5"), block=block, small_max_k=-1)
+    run_parity(gen.make("T3"), block=block, small_max_k=-1)
+    run_parity(gen.make("S4"), block=block)
 
 
 @pytest.mark.parametrize("trial", range(0, 40))
 def test_parity_random_corpus(trial):
     run_parity(gen.random_spd(trial))
+    run_parity(gen.random_spd(trial), small_max_k=-1)
 
 
 def test_parity_no_graph_and_refactor():
@@ -83,7 +87,7 @@ def test_not_spd_first_failing_column(name):
         vals[p.colptr[i0]] = -1.0
         q = gen.Problem(p.name, p.n, p.colptr, p.rowidx, vals, p.perm)
         assert oracle.Oracle.from_problem(q).factor() == j0
-        with sp.Solver.from_problem(q) as h:
+        with sp.Solver.from_problem(q, small_max_k=(-1 if j0 % 2 else 0)) as h:
             with pytest.raises(sp.NotSPDError) as ei:
                 h.spchol_factor()
             assert ei.value.fail_col == j0 and ei.value.fail_col_orig == i0
