@@ -81,6 +81,10 @@ struct spchol_handle {
   std::vector<long long> panel_off;
   double flops_exec = 0, update_entries = 0;
   int max_slots = 0;
+  int nslots_total = 0;
+  struct SolveStep { int level; long long p0; int np; long long t0; int nt; };
+  std::vector<SolveStep> solve_steps;   // per (level, inner block step): POTRF and TRSM task ranges
+  std::vector<int> small_level_off;     // small_sns range per level
   int nevents = 0;
   bool no_lookahead = false;     // SPCHOL_NO_LOOKAHEAD=1 (diagnostics)
   std::vector<int> plan_level;   // level of each plan entry (diagnostics)
@@ -99,8 +103,8 @@ struct spchol_handle {
   int prio_lo = 0, prio_hi = 0;
   std::vector<cudaEvent_t> plan_events;
   // graph
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t gexec = nullptr;
+  cudaGraph_t graph = nullptr, solve_graph = nullptr;
+  cudaGraphExec_t gexec = nullptr, solve_gexec = nullptr;
   // timing
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -162,6 +166,7 @@ static void build_plan(spchol_handle* h) {
     // small supernodes of this level: one launch on stream 1 (independent of the level's big ones)
     {
       long long s0 = (long long)h->small_sns.size();
+      h->small_level_off.push_back((int)s0);
       int mx = 0;
       double fsm = 0, bsm = 0;
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
@@ -202,7 +207,7 @@ static void build_plan(spchol_handle* h) {
     for (int s = 0; s < maxblk; ++s) {
       long long p0 = (long long)h->ptasks.size(), t0 = (long long)h->gtasks.size();
       double fp = 0, ft = 0, fl = 0, bp = 0, bt = 0, bl = 0, fn = 0, bn = 0, fr = 0, br = 0;
-      int slot = 0;
+      int slot = h->nslots_total;   // every diagonal block keeps its own inverse (reused by the solve)
       std::vector<GTask> local, nxt, rest;
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
         const int J = h->level_sns[x];
@@ -235,8 +240,9 @@ static void build_plan(spchol_handle* h) {
         }
         ++slot;
       }
-      h->max_slots = std::max(h->max_slots, slot);
+      h->nslots_total = slot;
       long long p1 = (long long)h->ptasks.size(), t1 = (long long)h->gtasks.size();
+      if (p1 > p0) h->solve_steps.push_back(spchol_handle::SolveStep{l, p0, (int)(p1 - p0), t0, (int)(t1 - t0)});
       push(K_POTRF, p0, p1, fp, bp);
       push(K_TRSM, t0, t1, ft, bt);
       long long l0 = (long long)h->gtasks.size();
@@ -292,6 +298,7 @@ static void build_plan(spchol_handle* h) {
     push(K_SCATTER, s0g, (long long)h->gtasks.size(), fs, bs);
     h->plan_level.resize(h->plan.size(), l);
   }
+  h->small_level_off.push_back((int)h->small_sns.size());
 }
 
 static int setup_device(spchol_handle* h) {
@@ -349,7 +356,7 @@ static int setup_device(spchol_handle* h) {
   CK(upload(&h->d_sfirst, S.sfirst));
   CK(upload(&h->d_gtasks, h->gtasks));
   CK(upload(&h->d_ptasks, h->ptasks));
-  CK(dalloc(&h->d_linv, (size_t)std::max(1, h->max_slots) * NBMAX * NBMAX));
+  CK(dalloc(&h->d_linv, (size_t)std::max(1, h->nslots_total) * NBMAX * NBMAX));
   CK(dalloc(&h->d_fail, 1));
   CK(upload(&h->d_rows_ptr, std::vector<long long>(S.rows_ptr.begin(), S.rows_ptr.end())));
   CK(upload(&h->d_rows, S.rows));
@@ -362,6 +369,8 @@ static int setup_device(spchol_handle* h) {
 }
 
 static void free_device(spchol_handle* h) {
+  if (h->solve_gexec) cudaGraphExecDestroy(h->solve_gexec);
+  if (h->solve_graph) cudaGraphDestroy(h->solve_graph);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->graph) cudaGraphDestroy(h->graph);
   void* ptrs[] = {h->d_small_sns, h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
@@ -554,17 +563,58 @@ extern "C" int spchol_factor(spchol_handle* h, int64_t* fail_col, int64_t* fail_
   return spchol_factor_status(h, fail_col, fail_col_orig);
 }
 
+// Supernodal triangular solves: y = P_f b; forward L y' = y level by level (leaves first),
+// backward L^T z = y' (root first); x = P_f^T z.  Small supernodes: one CTA each (column sweep in
+// the CTA).  Large supernodes: per inner 64-column block b, y_b := X_bb y_b with the diagonal-block
+// inverse kept from the factor, then the rows below are updated by a row-tiled block GEMV (RED into
+// y); backward in reverse with the transposed operations.
 static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaStream_t st) {
   const Symbolic& S = h->S;
   launch_permute(h->d_perm, d_b, h->d_y, S.n, 0, st);
-  for (int l = 0; l < S.nlevels; ++l)
-    launch_solve_fwd(h->d_level_sns + h->level_off[l], h->level_off[l + 1] - h->level_off[l], h->d_sn, h->d_sfirst,
-                     h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, st);
-  for (int l = S.nlevels - 1; l >= 0; --l)
-    launch_solve_bwd(h->d_level_sns + h->level_off[l], h->level_off[l + 1] - h->level_off[l], h->d_sn, h->d_sfirst,
-                     h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, st);
+  std::vector<std::pair<size_t, size_t>> lvl_steps(S.nlevels, {0, 0});
+  for (size_t q = 0; q < h->solve_steps.size(); ++q) {
+    auto& r = lvl_steps[h->solve_steps[q].level];
+    if (r.second == 0) r.first = q;
+    r.second = q + 1;
+  }
+  for (int l = 0; l < S.nlevels; ++l) {
+    launch_solve_fwd(h->d_small_sns + h->small_level_off[l], h->small_level_off[l + 1] - h->small_level_off[l], h->d_sn,
+                     h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, st);
+    for (size_t q = lvl_steps[l].first; q < lvl_steps[l].second; ++q) {
+      const auto& T = h->solve_steps[q];
+      launch_solve_diag(h->d_ptasks + T.p0, T.np, h->d_sfirst, h->d_linv, h->d_y, 0, st);
+      launch_solve_upd(h->d_gtasks + T.t0, T.nt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, 0, st);
+    }
+  }
+  for (int l = S.nlevels - 1; l >= 0; --l) {
+    for (size_t q = lvl_steps[l].second; q > lvl_steps[l].first; --q) {
+      const auto& T = h->solve_steps[q - 1];
+      launch_solve_upd(h->d_gtasks + T.t0, T.nt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, 1, st);
+      launch_solve_diag(h->d_ptasks + T.p0, T.np, h->d_sfirst, h->d_linv, h->d_y, 1, st);
+    }
+    launch_solve_bwd(h->d_small_sns + h->small_level_off[l], h->small_level_off[l + 1] - h->small_level_off[l], h->d_sn,
+                     h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, st);
+  }
   launch_permute(h->d_perm, h->d_y, d_x, S.n, 1, st);
   CK(cudaGetLastError());
+  return SPCHOL_OK;
+}
+
+// One solve of the internal buffer d_y2 in place, captured in a CUDA graph on first use.
+static int run_solve_y2(spchol_handle* h) {
+  if (!h->opt.use_graph) return enqueue_solve(h, h->d_y2, h->d_y2, h->stream);
+  if (!h->solve_gexec) {
+    cudaStream_t cs = h->own_stream;
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_solve(h, h->d_y2, h->d_y2, cs);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
+    if (rc != SPCHOL_OK) { if (g) cudaGraphDestroy(g); return rc; }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture(solve)");
+    h->solve_graph = g;
+    CK(cudaGraphInstantiateWithFlags(&h->solve_gexec, g, 0));
+  }
+  CK(cudaGraphLaunch(h->solve_gexec, h->stream));
   return SPCHOL_OK;
 }
 
@@ -573,10 +623,12 @@ extern "C" int spchol_solve_device(spchol_handle* h, const double* d_b, double* 
   if (host_only(h) || !h->factored) return fail(SPCHOL_ERR_STATE, "solve before a successful factor");
   if (nrhs < 1 || ld < h->S.n) return fail(SPCHOL_ERR_DIMENSION, "nrhs < 1 or ld < n");
   CK(cudaSetDevice(h->opt.device));
+  const size_t nbytes = sizeof(double) * (size_t)h->S.n;
   for (int r = 0; r < nrhs; ++r) {
-    int rc = enqueue_solve(h, d_b + (size_t)r * ld, h->d_y2, h->stream);
+    CK(cudaMemcpyAsync(h->d_y2, d_b + (size_t)r * ld, nbytes, cudaMemcpyDeviceToDevice, h->stream));
+    int rc = run_solve_y2(h);
     if (rc != SPCHOL_OK) return rc;
-    CK(cudaMemcpyAsync(d_x + (size_t)r * ld, h->d_y2, sizeof(double) * (size_t)h->S.n, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync(d_x + (size_t)r * ld, h->d_y2, nbytes, cudaMemcpyDeviceToDevice, h->stream));
   }
   return SPCHOL_OK;
 }
@@ -589,7 +641,7 @@ extern "C" int spchol_solve(spchol_handle* h, const double* b, double* x, int32_
   const size_t nbytes = sizeof(double) * (size_t)h->S.n;
   for (int r = 0; r < nrhs; ++r) {
     CK(cudaMemcpyAsync(h->d_y2, b + (size_t)r * ld, nbytes, cudaMemcpyHostToDevice, h->stream));
-    int rc = enqueue_solve(h, h->d_y2, h->d_y2, h->stream);
+    int rc = run_solve_y2(h);
     if (rc != SPCHOL_OK) return rc;
     CK(cudaMemcpyAsync(x + (size_t)r * ld, h->d_y2, nbytes, cudaMemcpyDeviceToHost, h->stream));
   }

@@ -516,6 +516,70 @@ __global__ void solve_bwd_kernel(const int* __restrict__ sns, const SnInfo* __re
   }
 }
 
+// Solve, large supernodes.  y_b := X y_b (forward) or X^T y_b (backward) for the 64-column block
+// [c0, c0+nb) of supernode J, X = L_bb^{-1} (kept from the factor's POTRF, column-major ld 64).
+__global__ void __launch_bounds__(64) solve_diag_kernel(const PTask* __restrict__ tasks, const int* __restrict__ sfirst,
+                                                        const double* __restrict__ linv, double* y, int transpose) {
+  __shared__ double yb[NBMAX];
+  const PTask T = tasks[blockIdx.x];
+  const int r = threadIdx.x, f = sfirst[T.sn] + T.c0;
+  const double* X = linv + (long long)T.slot * (NBMAX * NBMAX);
+  yb[r] = r < T.nb ? y[f + r] : 0.0;
+  __syncthreads();
+  double s = 0.0;
+  if (!transpose) {
+    for (int c = 0; c <= r && c < T.nb; ++c) s += X[c * NBMAX + r] * yb[c];
+  } else {
+    for (int c = r; c < T.nb; ++c) s += X[r * NBMAX + c] * yb[c];
+  }
+  if (r < T.nb) y[f + r] = s;
+}
+
+// Solve, large supernodes: rows [r0, r0+64) ∩ [s0 = c0+nb, m) of J's panel against block column
+// [c0, c0+nb).  Forward: y[rows(J)[q]] -= L(q, blk) y_b (RED: ancestors are shared by the level).
+// Backward: y_b -= L(rows, blk)^T y[rows] (partial sums per tile, RED into y_b).
+__global__ void __launch_bounds__(256) solve_upd_kernel(const GTask* __restrict__ tasks, const SnInfo* __restrict__ sn,
+                                                        const int* __restrict__ sfirst,
+                                                        const long long* __restrict__ rows_ptr,
+                                                        const int* __restrict__ rows, const double* __restrict__ panels,
+                                                        double* y, int transpose) {
+  __shared__ double vb[NBMAX];     // forward: y_b; backward: y at the tile rows
+  __shared__ double part[4][NBMAX];
+  const GTask T = tasks[blockIdx.x];
+  const SnInfo S = sn[T.sn];
+  const int tid = threadIdx.x, lane = tid & 63, grp = tid >> 6;
+  const int f = sfirst[T.sn];
+  const int* R = rows + rows_ptr[T.sn];
+  const double* L = panels + S.off + (long long)T.c0 * S.ld;
+  const int q = T.r0 + lane;
+  const bool rowok = q >= T.s0 && q < S.m;
+  if (!transpose) {
+    if (tid < NBMAX) vb[tid] = tid < T.nb ? y[f + T.c0 + tid] : 0.0;
+    __syncthreads();
+    double s = 0.0;
+    if (rowok)
+      for (int c = grp; c < T.nb; c += 4) s += L[(long long)c * S.ld + q] * vb[c];
+    part[grp][lane] = s;
+    __syncthreads();
+    if (grp == 0 && rowok) atomicAdd(y + R[q], -(part[0][lane] + part[1][lane] + part[2][lane] + part[3][lane]));
+  } else {
+    if (tid < NBMAX) vb[tid] = rowok ? y[R[q]] : 0.0;
+    __syncthreads();
+    // column c handled by group grp, lanes over rows; reduce over the 64 rows
+    for (int c = grp; c < T.nb; c += 4) {
+      double s = rowok ? L[(long long)c * S.ld + q] * vb[lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if ((lane & 31) == 0) part[grp][(c >> 2) * 2 + (lane >> 5)] = s;   // two half-sums per column
+    }
+    __syncthreads();
+    if (tid < T.nb) {
+      const int c = tid, g = c & 3, slotc = (c >> 2) * 2;
+      atomicAdd(y + f + T.c0 + c, -(part[g][slotc] + part[g][slotc + 1]));
+    }
+  }
+}
+
 __global__ void permute_kernel(const int* __restrict__ perm, const double* __restrict__ in, double* out, long long n,
                                int inverse) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -603,6 +667,14 @@ void launch_gather(const double* src, const long long* idx, double* out, long lo
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   gather_kernel<<<(int)blocks, 256, 0, st>>>(src, idx, out, n);
+}
+void launch_solve_diag(const PTask* tasks, int count, const int* sfirst, const double* linv, double* y, int transpose,
+                       cudaStream_t st) {
+  if (count > 0) solve_diag_kernel<<<count, 64, 0, st>>>(tasks, sfirst, linv, y, transpose);
+}
+void launch_solve_upd(const GTask* tasks, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
+                      const int* rows, const double* panels, double* y, int transpose, cudaStream_t st) {
+  if (count > 0) solve_upd_kernel<<<count, 256, 0, st>>>(tasks, sn, sfirst, rows_ptr, rows, panels, y, transpose);
 }
 void launch_permute(const int* perm, const double* in, double* out, long long n, int inverse, cudaStream_t st) {
   if (n <= 0) return;

@@ -67,6 +67,10 @@ void launch_solve_fwd(const int* sns, int count, const SnInfo* sn, const int* sf
                       const int* rows, const double* panels, double* y, cudaStream_t st);
 void launch_solve_bwd(const int* sns, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
                       const int* rows, const double* panels, double* y, cudaStream_t st);
+void launch_solve_diag(const PTask* tasks, int count, const int* sfirst, const double* linv, double* y, int transpose,
+                       cudaStream_t st);
+void launch_solve_upd(const GTask* tasks, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
+                      const int* rows, const double* panels, double* y, int transpose, cudaStream_t st);
 void launch_permute(const int* perm, const double* in, double* out, long long n, int inverse, cudaStream_t st);
 void launch_gather(const double* src, const long long* idx, double* out, long long n, cudaStream_t st);
 cudaError_t kernels_init_attributes();
