@@ -125,6 +125,24 @@ extern "C" void spchol_default_options(spchol_options* o) {
 extern "C" const char* spchol_last_error(void) { return g_err.c_str(); }
 
 // ------------------------------------------------------------------------------------- plan
+// Lower-triangular tile grid (row tiles starting at rbase, column tiles at cbase, step TILE; a tile
+// (r0, s0) is emitted iff r0 < rend, s0 < cend, s0 <= r0) in super-tile order: SUPER x SUPER
+// blocks of tiles, row-major inside, so the CTAs in flight share a few operand row blocks in L2
+// instead of streaming the whole panel once per row band.
+template <class F>
+static void for_tiles(int rbase, int rend, int cbase, int cend, F emit) {
+  constexpr int SUPER = 8;
+  const int nr = rend > rbase ? (rend - rbase + TILE - 1) / TILE : 0;
+  const int nc = cend > cbase ? (cend - cbase + TILE - 1) / TILE : 0;
+  for (int I = 0; I < nr; I += SUPER)
+    for (int Jb = 0; Jb < nc; Jb += SUPER)
+      for (int i = I; i < std::min(I + SUPER, nr); ++i)
+        for (int j = Jb; j < std::min(Jb + SUPER, nc); ++j) {
+          const int r0 = rbase + i * TILE, s0 = cbase + j * TILE;
+          if (s0 <= r0) emit(r0, s0);
+        }
+}
+
 static void build_plan(spchol_handle* h) {
   const Symbolic& S = h->S;
   const int ns = S.nsuper, NB = h->nb, OUTER = spchol_handle::OUTER;
@@ -225,17 +243,14 @@ static void build_plan(spchol_handle* h) {
         ft += (double)(I.m - c1) * nb * nb;
         bt += 16.0 * (double)(I.m - c1) * nb;
         // inner update: columns [c1, C1) of this outer block, K = nb
-        for (int r0 = c1; r0 < I.m; r0 += TILE)
-          for (int s0 = c1; s0 < C1 && s0 <= r0; s0 += TILE) local.push_back(GTask{J, r0, s0, c0, nb, C1});
+        for_tiles(c1, I.m, c1, C1, [&](int r0, int s0) { local.push_back(GTask{J, r0, s0, c0, nb, C1}); });
         for (int c = c1; c < C1; ++c) { fl += 2.0 * nb * (double)(I.m - c); bl += 16.0 * (double)(I.m - c); }
         // outer update after the last inner block of the outer block, K = C1 - C0
         if (c1 == C1 && C1 < I.k) {
           const int C2 = std::min(C1 + W, I.k);
-          for (int r0 = C1; r0 < I.m; r0 += TILE)
-            for (int s0 = C1; s0 < C2 && s0 <= r0; s0 += TILE) nxt.push_back(GTask{J, r0, s0, C0, C1 - C0, C2});
+          for_tiles(C1, I.m, C1, C2, [&](int r0, int s0) { nxt.push_back(GTask{J, r0, s0, C0, C1 - C0, C2}); });
           for (int c = C1; c < C2; ++c) { fn += 2.0 * (C1 - C0) * (double)(I.m - c); bn += 16.0 * (double)(I.m - c); }
-          for (int r0 = C2; r0 < I.m; r0 += TILE)
-            for (int s0 = C2; s0 < I.k && s0 <= r0; s0 += TILE) rest.push_back(GTask{J, r0, s0, C0, C1 - C0, I.k});
+          for_tiles(C2, I.m, C2, I.k, [&](int r0, int s0) { rest.push_back(GTask{J, r0, s0, C0, C1 - C0, I.k}); });
           for (int c = C2; c < I.k; ++c) { fr += 2.0 * (C1 - C0) * (double)(I.m - c); br += 16.0 * (double)(I.m - c); }
         }
         ++slot;
@@ -290,8 +305,7 @@ static void build_plan(spchol_handle* h) {
       const int t = I.m - I.k;
       if (t <= 0) continue;
       const int base = I.k & ~1;
-      for (int r0 = base; r0 < I.m; r0 += TILE)
-        for (int c0 = base; c0 <= r0; c0 += TILE) h->gtasks.push_back(GTask{J, r0, c0, 0, 0, 0});
+      for_tiles(base, I.m, base, I.m, [&](int r0, int c0) { h->gtasks.push_back(GTask{J, r0, c0, 0, 0, 0}); });
       fs += (double)I.k * t * (t + 1);
       bs += 8.0 * (double)t * I.k + 16.0 * 0.5 * t * (t + 1.0);
     }
