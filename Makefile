@@ -20,7 +20,7 @@ SPCHOL_SRC := $(wildcard $(CSRC)/*.cu) $(wildcard $(CSRC)/*.cpp)
 SPCHOL_HDR := $(wildcard $(CSRC)/*.h) $(wildcard $(CSRC)/*.cuh) include/spchol.h
 spchol: $(PKG)/libspchol.so
 $(PKG)/libspchol.so: $(SPCHOL_SRC) $(SPCHOL_HDR)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SPCHOL_SRC) -lcudart
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SPCHOL_SRC) -lcudart -ldl
 
 clean:
 	rm -f gen/libgen.so oracle/liboracle.so $(PKG)/libspchol.so

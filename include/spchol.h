@@ -54,6 +54,12 @@ typedef struct {
                            are factored by the fused one-CTA-per-supernode kernel; 0 = default,
                            -1 = never. */
   int32_t use_graph;    /* 1 = capture the factor's launch sequence in a CUDA graph (default 1). */
+  int32_t dist_rank;    /* multi-GPU: this process's rank (default 0), one process per GPU */
+  int32_t dist_world;   /* multi-GPU: number of ranks (default 1).  With dist_world > 1 the merged
+                           supernodal tree is mapped to ranks by proportional subtree-to-GPU mapping
+                           (SURVEY §8(e)): each rank factors its own subtrees (phase A), the top
+                           (separator) panels are summed over ranks with NCCL (phase B), and the
+                           top supernodes are factored (phase C).  Needs spchol_dist_attach_nccl. */
 } spchol_options;
 
 /* Fill *opt with the defaults above. */
@@ -198,6 +204,24 @@ int spchol_kernel_stats(spchol_handle* h, int kind, int64_t* launches, double* m
  * supernodal tree, -1 for the init), ntasks[i] (CTAs), ms[i].  Diagnostics only. */
 int spchol_kernel_trace(spchol_handle* h, int64_t cap, int64_t* count, int32_t* kinds, int32_t* levels,
                         int32_t* ntasks, double* ms);
+
+/* ---------------- multi-GPU (one process per GPU) ---------------- */
+/* Create an NCCL unique id (128 bytes) on one rank; the caller broadcasts it to the others. */
+int spchol_dist_nccl_unique_id(void* out128);
+/* Attach an NCCL communicator (ncclCommInitRank over dist_world ranks, this handle's dist_rank;
+ * collective: every rank must call it).  NCCL is loaded with dlopen (libnccl.so.2). */
+int spchol_dist_attach_nccl(spchol_handle* h, const void* unique_id128);
+/* owner[NSUPER]: rank owning each supernode's subtree, -1 for the top supernodes (all 0 when
+ * dist_world == 1); *top_off: first double of the contiguous top-panel region; *top_slot: first
+ * diagonal-inverse slot of the top supernodes.  Any pointer may be NULL. */
+int spchol_export_mapping(const spchol_handle* h, int32_t* owner, int64_t* top_off, int64_t* top_slot);
+/* Diagnostics (single process standing in for several ranks on one GPU, never a reported result):
+ * phase 1 = a1 init + phase A (own subtrees), 2 = phase C (top supernodes), 3 = synchronize,
+ * check the pivots and mark the handle factored with its factor complete.  The phase-B exchange is
+ * then done by the caller with spchol_dist_debug_accumulate(dst, src, which): dst region += src
+ * region, which = 0 top panels, 1 subtree panels, 2 subtree diagonal inverses. */
+int spchol_factor_phase(spchol_handle* h, int phase);
+int spchol_dist_debug_accumulate(spchol_handle* dst, const spchol_handle* src, int which);
 
 void spchol_destroy(spchol_handle* h);
 const char* spchol_last_error(void);

@@ -36,13 +36,15 @@ EXPORTS = [
     "spchol_set_stream", "spchol_factor_async", "spchol_factor_status", "spchol_factor",
     "spchol_solve", "spchol_solve_device", "spchol_query", "spchol_export_symbolic",
     "spchol_export_panels", "spchol_export_panel", "spchol_export_diagonal", "spchol_enable_kernel_timing", "spchol_kernel_stats",
-    "spchol_kernel_trace", "spchol_destroy", "spchol_last_error",
+    "spchol_kernel_trace", "spchol_dist_nccl_unique_id", "spchol_dist_attach_nccl", "spchol_export_mapping",
+    "spchol_factor_phase", "spchol_dist_debug_accumulate", "spchol_destroy", "spchol_last_error",
 ]
 
 
 class spchol_options(ctypes.Structure):
     _fields_ = [("merge_cap", ctypes.c_double), ("device", ctypes.c_int32), ("block", ctypes.c_int32),
-                ("small_max_k", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
+                ("small_max_k", ctypes.c_int32), ("use_graph", ctypes.c_int32),
+                ("dist_rank", ctypes.c_int32), ("dist_world", ctypes.c_int32)]
 
 
 class SpcholError(RuntimeError):
@@ -86,6 +88,11 @@ def lib():
         L.spchol_kernel_stats.argtypes = [vp, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(dbl),
                                           ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
         L.spchol_kernel_trace.argtypes = [vp, i64, ctypes.POINTER(i64), vp, vp, vp, vp]
+        L.spchol_dist_nccl_unique_id.argtypes = [vp]
+        L.spchol_dist_attach_nccl.argtypes = [vp, vp]
+        L.spchol_export_mapping.argtypes = [vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.spchol_factor_phase.argtypes = [vp, ctypes.c_int]
+        L.spchol_dist_debug_accumulate.argtypes = [vp, vp, ctypes.c_int]
         L.spchol_destroy.argtypes = [vp]
         L.spchol_destroy.restype = None
         L.spchol_last_error.argtypes = []
@@ -255,6 +262,26 @@ class Solver:
         c = min(cap, int(cnt.value))
         return dict(kinds=kinds[:c], levels=levels[:c], ntasks=ntasks[:c], ms=ms[:c])
 
+    # ---- multi-GPU
+    def spchol_dist_attach_nccl(self, unique_id: bytes):
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(self._L.spchol_dist_attach_nccl(self._h, buf))
+
+    def spchol_export_mapping(self):
+        owner = np.empty(self.spchol_query("NSUPER"), np.int32)
+        to, ts = ctypes.c_int64(), ctypes.c_int64()
+        _check(self._L.spchol_export_mapping(self._h, _vp(owner), ctypes.byref(to), ctypes.byref(ts)))
+        return owner, int(to.value), int(ts.value)
+
+    def spchol_factor_phase(self, phase):
+        rc = self._L.spchol_factor_phase(self._h, int(phase))
+        if rc == SPCHOL_ERR_NOT_SPD:
+            raise NotSPDError(rc, self._L.spchol_last_error().decode(), -1, -1)
+        _check(rc)
+
+    def spchol_dist_debug_accumulate(self, src, which):
+        _check(self._L.spchol_dist_debug_accumulate(self._h, src._h, int(which)))
+
     # ---- convenience (still only marshalling)
     factor = spchol_factor
     solve = spchol_solve
@@ -265,6 +292,12 @@ class Solver:
         sym = self.spchol_export_symbolic()
         off, ld, pan = self.spchol_export_panels()
         return sym, off, ld, pan
+
+
+def spchol_dist_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().spchol_dist_nccl_unique_id(buf))
+    return buf.raw
 
 
 def analyze(n, colptr, rowidx, values=None, perm=None, **options) -> Solver:

@@ -10,7 +10,10 @@
 //            = m_P - 1 - relind(J,P)[q]
 //   ucol     per U_J column c: (panel offset of that column inside its ancestor, posmap base)
 //   tasks    per launch: batched tile tasks of every supernode of one level (level-set schedule)
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -21,6 +24,9 @@
 #include "symbolic.h"
 
 using namespace spchol;
+namespace spchol {
+void proportional_map(const Symbolic& S, const std::vector<double>& work, int world, std::vector<int>& owner);
+}
 
 namespace {
 thread_local std::string g_err;
@@ -36,6 +42,48 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 enum LaunchKind { K_SMALL = 0, K_POTRF = 1, K_TRSM = 2, K_LOCAL = 3, K_SCATTER = 4, K_INIT = 5, K_NKINDS = 6 };
+}  // namespace
+
+// ------------------------------------------------------------------------------------- NCCL
+// NCCL is loaded on demand (dlopen of libnccl.so.2, normally the copy torch already loaded), so the
+// library has no link-time NCCL dependency and single-GPU use never touches it.
+namespace {
+typedef int (*nccl_getid_t)(void*);
+struct NcclUid { char internal[128]; };
+typedef int (*nccl_init_t)(void**, int, NcclUid, int);
+typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_destroy_t)(void*);
+typedef const char* (*nccl_errstr_t)(int);
+struct NcclApi {
+  void* so = nullptr;
+  nccl_getid_t getid = nullptr;
+  nccl_init_t init = nullptr;
+  nccl_allreduce_t allreduce = nullptr;
+  nccl_destroy_t destroy = nullptr;
+  nccl_errstr_t errstr = nullptr;
+};
+NcclApi g_nccl;
+constexpr int NCCL_SUM = 0, NCCL_MIN = 3, NCCL_UINT64 = 5, NCCL_FLOAT64 = 8;
+bool nccl_load(std::string& err) {
+  if (g_nccl.so) return true;
+  void* so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!so) so = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!so) { err = std::string("cannot load NCCL: ") + dlerror(); return false; }
+  g_nccl.getid = (nccl_getid_t)dlsym(so, "ncclGetUniqueId");
+  g_nccl.init = (nccl_init_t)dlsym(so, "ncclCommInitRank");
+  g_nccl.allreduce = (nccl_allreduce_t)dlsym(so, "ncclAllReduce");
+  g_nccl.destroy = (nccl_destroy_t)dlsym(so, "ncclCommDestroy");
+  g_nccl.errstr = (nccl_errstr_t)dlsym(so, "ncclGetErrorString");
+  if (!g_nccl.getid || !g_nccl.init || !g_nccl.allreduce || !g_nccl.destroy) { err = "NCCL symbols missing"; return false; }
+  g_nccl.so = so;
+  return true;
+}
+int nccl_fail(int r, const char* where) {
+  return fail(SPCHOL_ERR_NCCL, std::string(where) + ": " + (g_nccl.errstr ? g_nccl.errstr(r) : "nccl error"));
+}
+}  // namespace
+
+namespace {
 enum OpType { OP_LAUNCH = 0, OP_RECORD = 1, OP_WAIT = 2 };
 // One step of the factor's launch plan.  OP_LAUNCH: a batched kernel (kind, tasks [off, off+n)) on
 // stream `stream` (0 = critical path: cdiv chain + relind scatter, 1 = trailing updates);
@@ -80,8 +128,17 @@ struct spchol_handle {
   long long panel_doubles = 0;
   std::vector<long long> panel_off;
   double flops_exec = 0, update_entries = 0;
-  int max_slots = 0;
   int nslots_total = 0;
+  std::vector<int> slot_base;          // first inverse slot of each supernode's diagonal blocks
+  // multi-GPU: subtree-to-GPU mapping, phase A = own subtrees, B = NCCL all-reduce
+  // of the top panels, C = top supernodes
+  int rank = 0, world = 1;
+  std::vector<int> owner;              // rank owning each supernode's subtree, -1 = top
+  long long top_off = -1;              // first double of the contiguous top-panel region
+  int top_slot = -1;                   // first inverse slot of the top supernodes
+  size_t plan_all_end = 0, plan_a_end = 0;
+  void* nccl_comm = nullptr;
+  bool gathered = false;
   struct SolveStep { int level; long long p0; int np; long long t0; int nt; };
   std::vector<SolveStep> solve_steps;   // per (level, inner block step): POTRF and TRSM task ranges
   std::vector<int> small_level_off;     // small_sns range per level
@@ -120,6 +177,8 @@ extern "C" void spchol_default_options(spchol_options* o) {
   o->block = 0;
   o->small_max_k = 0;
   o->use_graph = 1;
+  o->dist_rank = 0;
+  o->dist_world = 1;
 }
 
 extern "C" const char* spchol_last_error(void) { return g_err.c_str(); }
@@ -143,53 +202,26 @@ static void for_tiles(int rbase, int rend, int cbase, int cend, F emit) {
         }
 }
 
-static void build_plan(spchol_handle* h) {
+// Appends, level by level, the launches for the supernodes J with active(J).  record_solve: also
+// record the solve's step structure (only for the whole-tree plan).
+template <class Active>
+static void append_levels(spchol_handle* h, Active active, bool record_solve) {
   const Symbolic& S = h->S;
-  const int ns = S.nsuper, NB = h->nb, OUTER = spchol_handle::OUTER;
-  h->sn.resize(ns);
-  h->panel_off.assign(ns + 1, 0);
-  for (int J = 0; J < ns; ++J) {
-    int k = S.sfirst[J + 1] - S.sfirst[J];
-    int m = (int)(S.rows_ptr[J + 1] - S.rows_ptr[J]);
-    int ld = m + (m & 1);
-    h->sn[J].off = h->panel_off[J];
-    h->sn[J].ld = ld; h->sn[J].m = m; h->sn[J].k = k; h->sn[J].ucol = -1;
-    h->panel_off[J + 1] = h->panel_off[J] + (long long)ld * k;
-    for (int c = 0; c < k; ++c) h->flops_exec += (double)(m - c) * (double)(m - c);
-    h->update_entries += 0.5 * (double)(m - k) * (double)(m - k + 1);
-  }
-  h->panel_doubles = h->panel_off[ns];
-  // levels
-  h->level_off.assign(S.nlevels + 1, 0);
-  for (int J = 0; J < ns; ++J) h->level_off[S.level[J] + 1]++;
-  for (int l = 0; l < S.nlevels; ++l) h->level_off[l + 1] += h->level_off[l];
-  h->level_sns.assign(ns, 0);
-  {
-    std::vector<int> nx(h->level_off.begin(), h->level_off.end() - 1);
-    for (int J = 0; J < ns; ++J) h->level_sns[nx[S.level[J]]++] = J;
-  }
+  const int NB = h->nb, OUTER = spchol_handle::OUTER;
   auto push = [&](int kind, long long off, long long end, double fl, double by) {
     if (end > off) h->plan.push_back(Launch{kind, off, (int)(end - off), fl, by, OP_LAUNCH, 0, -1});
   };
-  h->max_slots = 0;
-  // fused small-supernode path: k <= small_max_k, m <= 256, m k <= SMALL_MAXELEMS (shared memory)
-  const int kmax = h->opt.small_max_k < 0 ? 0 : (h->opt.small_max_k == 0 ? SMALL_MAXK : std::min(h->opt.small_max_k, SMALL_MAXK));
-  h->is_small.assign(ns, 0);
-  for (int J = 0; J < ns; ++J) {
-    const SnInfo& I = h->sn[J];
-    h->is_small[J] = I.k <= kmax && I.m <= SMALL_MAXM && (long long)I.m * I.k <= SMALL_MAXELEMS;
-  }
   for (int l = 0; l < S.nlevels; ++l) {
     const size_t plan_before = h->plan.size();
     // small supernodes of this level: one launch on stream 1 (independent of the level's big ones)
     {
       long long s0 = (long long)h->small_sns.size();
-      h->small_level_off.push_back((int)s0);
+      if (record_solve) h->small_level_off.push_back((int)s0);
       int mx = 0;
       double fsm = 0, bsm = 0;
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
         const int J = h->level_sns[x];
-        if (!h->is_small[J]) continue;
+        if (!h->is_small[J] || !active(J)) continue;
         const SnInfo& I = h->sn[J];
         h->small_sns.push_back(J);
         mx = std::max(mx, I.m * I.k);
@@ -209,7 +241,7 @@ static void build_plan(spchol_handle* h) {
     }
     int maxblk = 0;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
-      if (h->is_small[h->level_sns[x]]) continue;
+      if (h->is_small[h->level_sns[x]] || !active(h->level_sns[x])) continue;
       const SnInfo& I = h->sn[h->level_sns[x]];
       maxblk = std::max(maxblk, (I.k + NB - 1) / NB);
     }
@@ -225,14 +257,14 @@ static void build_plan(spchol_handle* h) {
     for (int s = 0; s < maxblk; ++s) {
       long long p0 = (long long)h->ptasks.size(), t0 = (long long)h->gtasks.size();
       double fp = 0, ft = 0, fl = 0, bp = 0, bt = 0, bl = 0, fn = 0, bn = 0, fr = 0, br = 0;
-      int slot = h->nslots_total;   // every diagonal block keeps its own inverse (reused by the solve)
       std::vector<GTask> local, nxt, rest;
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
         const int J = h->level_sns[x];
-        if (h->is_small[J]) continue;
+        if (h->is_small[J] || !active(J)) continue;
         const SnInfo& I = h->sn[J];
         const int c0 = s * NB;
         if (c0 >= I.k) continue;
+        const int slot = h->slot_base[J] + s;   // every diagonal block keeps its own inverse (solve)
         const int nb = std::min(NB, I.k - c0), c1 = c0 + nb;
         const int C0 = (c0 / W) * W, C1 = std::min(C0 + W, I.k);   // enclosing outer block
         h->ptasks.push_back(PTask{J, c0, nb, slot});
@@ -253,11 +285,9 @@ static void build_plan(spchol_handle* h) {
           for_tiles(C2, I.m, C2, I.k, [&](int r0, int s0) { rest.push_back(GTask{J, r0, s0, C0, C1 - C0, I.k}); });
           for (int c = C2; c < I.k; ++c) { fr += 2.0 * (C1 - C0) * (double)(I.m - c); br += 16.0 * (double)(I.m - c); }
         }
-        ++slot;
       }
-      h->nslots_total = slot;
       long long p1 = (long long)h->ptasks.size(), t1 = (long long)h->gtasks.size();
-      if (p1 > p0) h->solve_steps.push_back(spchol_handle::SolveStep{l, p0, (int)(p1 - p0), t0, (int)(t1 - t0)});
+      if (record_solve && p1 > p0) h->solve_steps.push_back(spchol_handle::SolveStep{l, p0, (int)(p1 - p0), t0, (int)(t1 - t0)});
       push(K_POTRF, p0, p1, fp, bp);
       push(K_TRSM, t0, t1, ft, bt);
       long long l0 = (long long)h->gtasks.size();
@@ -300,7 +330,7 @@ static void build_plan(spchol_handle* h) {
     double fs = 0, bs = 0;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
       const int J = h->level_sns[x];
-      if (h->is_small[J]) continue;
+      if (h->is_small[J] || !active(J)) continue;
       const SnInfo& I = h->sn[J];
       const int t = I.m - I.k;
       if (t <= 0) continue;
@@ -312,7 +342,86 @@ static void build_plan(spchol_handle* h) {
     push(K_SCATTER, s0g, (long long)h->gtasks.size(), fs, bs);
     h->plan_level.resize(h->plan.size(), l);
   }
-  h->small_level_off.push_back((int)h->small_sns.size());
+  if (record_solve) h->small_level_off.push_back((int)h->small_sns.size());
+}
+
+
+static void build_plan(spchol_handle* h) {
+  const Symbolic& S = h->S;
+  const int ns = S.nsuper, NB = h->nb;
+  h->sn.resize(ns);
+  h->panel_off.assign(ns + 1, 0);
+  std::vector<double> work(ns, 0.0);
+  for (int J = 0; J < ns; ++J) {
+    int k = S.sfirst[J + 1] - S.sfirst[J];
+    int m = (int)(S.rows_ptr[J + 1] - S.rows_ptr[J]);
+    int ld = m + (m & 1);
+    h->sn[J].ld = ld; h->sn[J].m = m; h->sn[J].k = k; h->sn[J].ucol = -1;
+    for (int c = 0; c < k; ++c) work[J] += (double)(m - c) * (double)(m - c);
+    h->flops_exec += work[J];
+    h->update_entries += 0.5 * (double)(m - k) * (double)(m - k + 1);
+  }
+  // subtree-to-GPU mapping (multi-GPU): owner[J] = rank, or -1 for the top (separator) supernodes
+  proportional_map(S, work, h->world, h->owner);
+  // panel arena: supernodes in order, except that the top supernodes (multi-GPU) come last so
+  // their panels form one contiguous region (the NCCL all-reduce of phase B)
+  {
+    long long off = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int J = 0; J < ns; ++J) {
+        const bool top = h->world > 1 && h->owner[J] < 0;
+        if (top != (pass == 1)) continue;
+        if (pass == 1 && h->top_off < 0) h->top_off = off;
+        h->sn[J].off = off;
+        off += (long long)h->sn[J].ld * h->sn[J].k;
+      }
+    h->panel_doubles = off;
+    if (h->top_off < 0) h->top_off = off;
+    for (int J = 0; J < ns; ++J) h->panel_off[J] = h->sn[J].off;
+    h->panel_off[ns] = off;
+  }
+  // levels
+  h->level_off.assign(S.nlevels + 1, 0);
+  for (int J = 0; J < ns; ++J) h->level_off[S.level[J] + 1]++;
+  for (int l = 0; l < S.nlevels; ++l) h->level_off[l + 1] += h->level_off[l];
+  h->level_sns.assign(ns, 0);
+  {
+    std::vector<int> nx(h->level_off.begin(), h->level_off.end() - 1);
+    for (int J = 0; J < ns; ++J) h->level_sns[nx[S.level[J]]++] = J;
+  }
+  // fused small-supernode path: k <= small_max_k, m <= 256, m k <= SMALL_MAXELEMS (shared memory)
+  const int kmax = h->opt.small_max_k < 0 ? 0 : (h->opt.small_max_k == 0 ? SMALL_MAXK : std::min(h->opt.small_max_k, SMALL_MAXK));
+  h->is_small.assign(ns, 0);
+  for (int J = 0; J < ns; ++J) {
+    const SnInfo& I = h->sn[J];
+    h->is_small[J] = I.k <= kmax && I.m <= SMALL_MAXM && (long long)I.m * I.k <= SMALL_MAXELEMS;
+  }
+  // persistent diagonal-block inverse slots (factor TRSM + solve): non-top supernodes first
+  h->slot_base.assign(ns, 0);
+  {
+    int slot = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int J = 0; J < ns; ++J) {
+        const bool top = h->world > 1 && h->owner[J] < 0;
+        if (top != (pass == 1) || h->is_small[J]) continue;
+        if (pass == 1 && h->top_slot < 0) h->top_slot = slot;
+        h->slot_base[J] = slot;
+        slot += (h->sn[J].k + NB - 1) / NB;
+      }
+    h->nslots_total = slot;
+    if (h->top_slot < 0) h->top_slot = slot;
+  }
+  // the whole tree (single GPU and the solve), then per-rank phase A / phase C for multi-GPU
+  append_levels(h, [](int) { return true; }, true);
+  h->plan_all_end = h->plan.size();
+  if (h->world > 1) {
+    const int me = h->rank;
+    append_levels(h, [h, me](int J) { return h->owner[J] == me; }, false);
+    h->plan_a_end = h->plan.size();
+    append_levels(h, [h](int J) { return h->owner[J] < 0; }, false);
+  } else {
+    h->plan_a_end = h->plan.size();
+  }
 }
 
 static int setup_device(spchol_handle* h) {
@@ -343,6 +452,9 @@ static int setup_device(spchol_handle* h) {
   for (long long e = 0; e < S.nnzA; ++e) {
     const int c = S.a_col[e], J = S.snode[c];
     amap[e] = h->sn[J].off + (long long)(c - S.sfirst[J]) * h->sn[J].ld + S.a_pos[e];
+    // multi-GPU: a rank initialises its own subtrees' entries; the top entries are added once
+    // (by rank 0) so that the phase-B sum over ranks counts A exactly once
+    if (h->world > 1 && !(h->owner[J] == h->rank || (h->owner[J] < 0 && h->rank == 0))) amap[e] = -1;
   }
   CK(cudaSetDevice(h->opt.device));
   CK(kernels_init_attributes());
@@ -383,6 +495,7 @@ static int setup_device(spchol_handle* h) {
 }
 
 static void free_device(spchol_handle* h) {
+  if (h->nccl_comm && g_nccl.destroy) g_nccl.destroy(h->nccl_comm);
   if (h->solve_gexec) cudaGraphExecDestroy(h->solve_gexec);
   if (h->solve_graph) cudaGraphDestroy(h->solve_graph);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
@@ -406,6 +519,12 @@ extern "C" int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* r
   *out = nullptr;
   spchol_handle* h = new spchol_handle();
   if (opt) h->opt = *opt; else spchol_default_options(&h->opt);
+  if (h->opt.dist_world < 1 || h->opt.dist_rank < 0 || h->opt.dist_rank >= h->opt.dist_world) {
+    delete h;
+    return fail(SPCHOL_ERR_VALIDATION, "need 0 <= dist_rank < dist_world");
+  }
+  h->rank = h->opt.dist_rank;
+  h->world = h->opt.dist_world;
   if (h->opt.block) {
     if (h->opt.block < 8 || h->opt.block > NBMAX || h->opt.block % 8) { delete h; return fail(SPCHOL_ERR_VALIDATION, "block must be a multiple of 8 in [8, 64]"); }
     h->nb = h->opt.block;
@@ -456,8 +575,8 @@ extern "C" int spchol_set_stream(spchol_handle* h, void* stream) {
 }
 
 // Enqueue the whole factorization on st (no host synchronization).
-static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
-  const Symbolic& S = h->S;
+// Enqueue the plan entries [begin, end) (launches, lookahead fork/join events) on st.
+static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t end) {
   auto tstart = [&](int idx) -> size_t {
     if (!h->timing) return 0;
     while (h->ev_used + 2 > h->ev_pool.size()) {
@@ -472,11 +591,6 @@ static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
     return i;
   };
   auto tstop = [&](size_t i) { if (h->timing) cudaEventRecord(h->ev_pool[i + 1], st); };
-  CK(cudaMemsetAsync(h->d_fail, 0xFF, sizeof(unsigned long long), st));
-  size_t ti = tstart(-1);
-  CK(cudaMemsetAsync(h->d_panels, 0, sizeof(double) * (size_t)std::max(1LL, h->panel_doubles), st));
-  launch_init(h->d_avals, h->d_amap, S.nnzA, h->d_panels, st);
-  tstop(ti);
   // The plan's stream 0 (critical path) runs on a high-priority internal stream so its few-CTA
   // cdiv launches are scheduled ahead of the trailing-update CTAs of stream 1 (low priority).
   // Both fork from st and join back into it (required under graph capture).  With kernel
@@ -488,7 +602,7 @@ static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
     CK(cudaEventRecord(h->ev_fork, st));
     CK(cudaStreamWaitEvent(s0, h->ev_fork, 0));
   }
-  for (size_t i = 0; i < h->plan.size(); ++i) {
+  for (size_t i = begin; i < end; ++i) {
     const Launch& L = h->plan[i];
     cudaStream_t ls = L.stream == 1 ? s1 : s0;
     if (L.op == OP_RECORD) {
@@ -499,7 +613,7 @@ static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
       if (multi) CK(cudaStreamWaitEvent(ls, h->plan_events[L.ev], 0));
       continue;
     }
-    ti = tstart((int)i);
+    size_t ti = tstart((int)i);
     const int prio = multi ? (L.stream == 1 ? h->prio_lo : h->prio_hi) : 0;
     switch (L.kind) {
       case K_SMALL:
@@ -529,13 +643,62 @@ static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
   return SPCHOL_OK;
 }
 
+// a1: fail flag reset, panels := 0, A's entries (this rank's share under multi-GPU) into the arena.
+static int enqueue_init(spchol_handle* h, cudaStream_t st) {
+  size_t ti = 0;
+  if (h->timing) {
+    while (h->ev_used + 2 > h->ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      h->ev_pool.push_back(e);
+    }
+    ti = h->ev_used;
+    h->ev_used += 2;
+    cudaEventRecord(h->ev_pool[ti], st);
+    h->pending.push_back({-1, ti});
+  }
+  CK(cudaMemsetAsync(h->d_fail, 0xFF, sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(h->d_panels, 0, sizeof(double) * (size_t)std::max(1LL, h->panel_doubles), st));
+  launch_init(h->d_avals, h->d_amap, h->S.nnzA, h->d_panels, st);
+  if (h->timing) cudaEventRecord(h->ev_pool[ti + 1], st);
+  CK(cudaGetLastError());
+  return SPCHOL_OK;
+}
+
+// Phase B (multi-GPU): sum the top-panel region over the ranks (each holds its share of A's top
+// entries plus the contributions of its own subtrees), and the failure flags (min).
+static int enqueue_exchange(spchol_handle* h, cudaStream_t st) {
+  if (!h->nccl_comm) return SPCHOL_OK;
+  const size_t cnt = (size_t)(h->panel_doubles - h->top_off);
+  if (cnt) {
+    int r = g_nccl.allreduce(h->d_panels + h->top_off, h->d_panels + h->top_off, cnt, NCCL_FLOAT64, NCCL_SUM,
+                             h->nccl_comm, st);
+    if (r) return nccl_fail(r, "ncclAllReduce(top panels)");
+  }
+  return SPCHOL_OK;
+}
+
+static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
+  int rc = enqueue_init(h, st);
+  if (rc) return rc;
+  if (h->world == 1) return enqueue_ops(h, st, 0, h->plan_all_end);
+  if (!h->nccl_comm) return fail(SPCHOL_ERR_STATE, "multi-GPU handle without an NCCL communicator (spchol_dist_attach_nccl)");
+  if ((rc = enqueue_ops(h, st, h->plan_all_end, h->plan_a_end))) return rc;
+  if ((rc = enqueue_exchange(h, st))) return rc;
+  if ((rc = enqueue_ops(h, st, h->plan_a_end, h->plan.size()))) return rc;
+  int r = g_nccl.allreduce(h->d_fail, h->d_fail, 1, NCCL_UINT64, NCCL_MIN, h->nccl_comm, st);
+  if (r) return nccl_fail(r, "ncclAllReduce(fail flag)");
+  return SPCHOL_OK;
+}
+
 extern "C" int spchol_factor_async(spchol_handle* h) {
   if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
   if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
   if (!h->values_set) return fail(SPCHOL_ERR_STATE, "values not set");
   CK(cudaSetDevice(h->opt.device));
   h->factored = false;
-  if (h->opt.use_graph && !h->timing) {
+  // multi-GPU factors are launched directly (no graph capture of the NCCL calls)
+  if (h->opt.use_graph && !h->timing && h->world == 1) {
     if (!h->gexec) {
       cudaStream_t cs = h->own_stream;
       CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
@@ -568,6 +731,7 @@ extern "C" int spchol_factor_status(spchol_handle* h, int64_t* fail_col, int64_t
     return fail(SPCHOL_ERR_NOT_SPD, "matrix is not positive definite: pivot <= 0 at final column " + std::to_string(fc));
   }
   h->factored = true;
+  h->gathered = h->world == 1;
   return SPCHOL_OK;
 }
 
@@ -614,8 +778,29 @@ static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaS
   return SPCHOL_OK;
 }
 
+// Multi-GPU: before the first solve after a factor, every rank receives the whole factor — the
+// subtree panels and their diagonal-block inverses are disjoint across ranks (zero elsewhere), so a
+// sum all-reduce assembles them; the top region is already identical on all ranks.
+static int gather_factor(spchol_handle* h) {
+  if (h->gathered) return SPCHOL_OK;
+  if (!h->nccl_comm) return fail(SPCHOL_ERR_STATE, "multi-GPU handle without an NCCL communicator");
+  int r = 0;
+  if (h->top_off > 0 && (r = g_nccl.allreduce(h->d_panels, h->d_panels, (size_t)h->top_off, NCCL_FLOAT64, NCCL_SUM,
+                                               h->nccl_comm, h->stream)))
+    return nccl_fail(r, "ncclAllReduce(subtree panels)");
+  if (h->top_slot > 0 && (r = g_nccl.allreduce(h->d_linv, h->d_linv, (size_t)h->top_slot * NBMAX * NBMAX, NCCL_FLOAT64,
+                                                NCCL_SUM, h->nccl_comm, h->stream)))
+    return nccl_fail(r, "ncclAllReduce(subtree inverses)");
+  h->gathered = true;
+  return SPCHOL_OK;
+}
+
 // One solve of the internal buffer d_y2 in place, captured in a CUDA graph on first use.
 static int run_solve_y2(spchol_handle* h) {
+  if (!h->gathered) {
+    int rc = gather_factor(h);
+    if (rc) return rc;
+  }
   if (!h->opt.use_graph) return enqueue_solve(h, h->d_y2, h->d_y2, h->stream);
   if (!h->solve_gexec) {
     cudaStream_t cs = h->own_stream;
@@ -776,6 +961,85 @@ extern "C" int spchol_kernel_trace(spchol_handle* h, int64_t cap, int64_t* count
     ++c;
   }
   *count = c;
+  return SPCHOL_OK;
+}
+
+extern "C" int spchol_dist_nccl_unique_id(void* out128) {
+  if (!out128) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
+  std::string err;
+  if (!nccl_load(err)) return fail(SPCHOL_ERR_NCCL, err);
+  int r = g_nccl.getid(out128);
+  return r ? nccl_fail(r, "ncclGetUniqueId") : SPCHOL_OK;
+}
+
+extern "C" int spchol_dist_attach_nccl(spchol_handle* h, const void* unique_id128) {
+  if (!h || !unique_id128) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
+  if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
+  if (h->nccl_comm) return fail(SPCHOL_ERR_STATE, "communicator already attached");
+  std::string err;
+  if (!nccl_load(err)) return fail(SPCHOL_ERR_NCCL, err);
+  CK(cudaSetDevice(h->opt.device));
+  NcclUid id;
+  std::memcpy(id.internal, unique_id128, 128);
+  void* comm = nullptr;
+  int r = g_nccl.init(&comm, h->world, id, h->rank);
+  if (r) return nccl_fail(r, "ncclCommInitRank");
+  h->nccl_comm = comm;
+  return SPCHOL_OK;
+}
+
+extern "C" int spchol_export_mapping(const spchol_handle* h, int32_t* owner, int64_t* top_off, int64_t* top_slot) {
+  if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
+  if (owner) for (int J = 0; J < h->S.nsuper; ++J) owner[J] = h->world > 1 ? h->owner[J] : 0;
+  if (top_off) *top_off = h->top_off;
+  if (top_slot) *top_slot = h->top_slot;
+  return SPCHOL_OK;
+}
+
+extern "C" int spchol_factor_phase(spchol_handle* h, int phase) {
+  if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
+  if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
+  if (!h->values_set) return fail(SPCHOL_ERR_STATE, "values not set");
+  CK(cudaSetDevice(h->opt.device));
+  int rc = SPCHOL_OK;
+  switch (phase) {
+    case 1:
+      h->factored = false;
+      rc = enqueue_init(h, h->stream);
+      if (!rc) rc = enqueue_ops(h, h->stream, h->world == 1 ? 0 : h->plan_all_end, h->world == 1 ? h->plan_all_end : h->plan_a_end);
+      break;
+    case 2:
+      if (h->world > 1) rc = enqueue_ops(h, h->stream, h->plan_a_end, h->plan.size());
+      break;
+    case 3:
+      rc = spchol_factor_status(h, nullptr, nullptr);
+      if (!rc) h->gathered = true;
+      break;
+    default:
+      return fail(SPCHOL_ERR_VALIDATION, "phase must be 1, 2 or 3");
+  }
+  return rc;
+}
+
+extern "C" int spchol_dist_debug_accumulate(spchol_handle* dst, const spchol_handle* src, int which) {
+  if (!dst || !src) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
+  if (host_only(dst) || host_only(src)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
+  if (dst->panel_doubles != src->panel_doubles || dst->top_off != src->top_off || dst->top_slot != src->top_slot)
+    return fail(SPCHOL_ERR_VALIDATION, "handles of different problems");
+  CK(cudaSetDevice(dst->opt.device));
+  CK(cudaStreamSynchronize(src->stream));
+  double* d;
+  const double* sp;
+  long long cnt;
+  switch (which) {
+    case 0: d = dst->d_panels + dst->top_off; sp = src->d_panels + src->top_off; cnt = dst->panel_doubles - dst->top_off; break;
+    case 1: d = dst->d_panels; sp = src->d_panels; cnt = dst->top_off; break;
+    case 2: d = dst->d_linv; sp = src->d_linv; cnt = (long long)dst->top_slot * NBMAX * NBMAX; break;
+    default: return fail(SPCHOL_ERR_VALIDATION, "which must be 0, 1 or 2");
+  }
+  launch_axpy(sp, d, cnt, dst->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(dst->stream));
   return SPCHOL_OK;
 }
 

@@ -462,8 +462,10 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
 
 __global__ void init_scatter_kernel(const double* __restrict__ vals, const long long* __restrict__ amap,
                                     long long nnz, double* panels) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz; e += (long long)gridDim.x * blockDim.x)
-    panels[amap[e]] = vals[e];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz; e += (long long)gridDim.x * blockDim.x) {
+    const long long d = amap[e];
+    if (d >= 0) panels[d] = vals[e];     // d < 0: entry initialised by another rank (multi-GPU)
+  }
 }
 
 // Forward solve for the supernodes of one level: y_J := L_JJ^{-1} y_J, then y_R -= L_RJ y_J.
@@ -661,6 +663,16 @@ void launch_solve_fwd(const int* sns, int count, const SnInfo* sn, const int* sf
 void launch_solve_bwd(const int* sns, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
                       const int* rows, const double* panels, double* y, cudaStream_t st) {
   if (count > 0) solve_bwd_kernel<<<count, 256, 0, st>>>(sns, sn, sfirst, rows_ptr, rows, panels, y);
+}
+__global__ void axpy_kernel(const double* __restrict__ x, double* y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] += x[i];
+}
+void launch_axpy(const double* x, double* y, long long n, cudaStream_t st) {
+  if (n <= 0) return;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  axpy_kernel<<<(int)blocks, 256, 0, st>>>(x, y, n);
 }
 void launch_gather(const double* src, const long long* idx, double* out, long long n, cudaStream_t st) {
   if (n <= 0) return;

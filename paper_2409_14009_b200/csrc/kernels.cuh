@@ -72,6 +72,7 @@ void launch_solve_diag(const PTask* tasks, int count, const int* sfirst, const d
 void launch_solve_upd(const GTask* tasks, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
                       const int* rows, const double* panels, double* y, int transpose, cudaStream_t st);
 void launch_permute(const int* perm, const double* in, double* out, long long n, int inverse, cudaStream_t st);
+void launch_axpy(const double* x, double* y, long long n, cudaStream_t st);
 void launch_gather(const double* src, const long long* idx, double* out, long long n, cudaStream_t st);
 cudaError_t kernels_init_attributes();
 

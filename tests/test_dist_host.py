@@ -1,0 +1,93 @@
+"""Multi-GPU host-side logic on CPU: two gloo processes build host-only handles for ranks 0 and 1
+and check that the subtree-to-GPU mapping is identical on both ranks, partitions the
+supernodes into whole subtrees plus a top that is closed under ancestors, and lays the top panels
+out as one contiguous region (the phase-B all-reduce)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import gen
+import paper_2409_14009_b200 as sp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, name, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        p = gen.make(name)
+        with sp.Solver.from_problem(p, device=-1, dist_world=world, dist_rank=rank) as h:
+            owner, top_off, top_slot = h.spchol_export_mapping()
+            sym = h.spchol_export_symbolic()
+            off, ld, _ = h.spchol_export_panels(values=False)
+        t = torch.from_numpy(owner.astype(np.int64))
+        got = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(got, t)
+        for g in got:
+            assert torch.equal(g, t), "ranks disagree on the mapping"
+        sparent = sym["sparent"]
+        ns = len(sparent)
+        # whole subtrees: a local supernode's parent is local to the same rank or top
+        for J in range(ns):
+            P = sparent[J]
+            if P >= 0 and owner[P] >= 0:
+                assert owner[J] == owner[P]
+            if owner[J] < 0 and P >= 0:
+                assert owner[P] < 0, "top is closed under ancestors"
+        assert set(np.unique(owner[owner >= 0]).tolist()) <= set(range(world))
+        # top panels contiguous at the end of the arena
+        k = np.diff(sym["sfirst"])
+        sizes = ld.astype(np.int64) * k
+        top = owner < 0
+        assert off[-1] - top_off == sizes[top].sum()
+        if top.any():
+            assert off[:-1][top].min() == top_off
+        if (~top).any():
+            assert (off[:-1][~top] + sizes[~top]).max() <= top_off
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok", int(top.sum()), [int((owner == r).sum()) for r in range(world)]))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, f"error: {e!r}", 0, []))
+
+
+@pytest.mark.parametrize("name,world", [("S4", 2), ("C1", 2), ("S5", 2), ("S2", 3)])
+def test_mapping_two_process_gloo(name, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    for r in res:
+        assert r[1] == "ok", r
+    # every rank owns at least one subtree
+    assert all(c > 0 for c in res[0][3])
+
+
+def test_mapping_single_process_properties():
+    p = gen.make("C1")
+    for W in (2, 4, 8):
+        with sp.Solver.from_problem(p, device=-1, dist_world=W, dist_rank=W - 1) as h:
+            owner, top_off, top_slot = h.spchol_export_mapping()
+            assert (owner < 0).any() and all((owner == r).any() for r in range(W))
+    with sp.Solver.from_problem(p, device=-1) as h:
+        owner, top_off, _ = h.spchol_export_mapping()
+        assert (owner == 0).all() and top_off == h.query("PANEL_DOUBLES")
+    with pytest.raises(sp.SpcholError):
+        sp.Solver.from_problem(p, device=-1, dist_world=2, dist_rank=2)

@@ -105,3 +105,36 @@ def test_edge_cases():
     D = np.eye(n) * 60
     D[n - 1, :n - 1] = 1.0
     run_parity(gen.from_dense_lower(D))
+
+
+@pytest.mark.parametrize("name,world", [("S4", 2), ("S5", 3), ("C1", 2), ("S2", 4), ("T3", 2)])
+def test_distributed_dataflow_single_gpu(name, world):
+    """The multi-GPU data flow (phase A per rank, phase-B sum of the top panels, phase C, gather)
+    played by `world` handles on one GPU through the diagnostics API; NCCL is replaced by the
+    accumulate call.  The assembled factor must match the oracle like the single-GPU one."""
+    prob = gen.make(name)
+    o = oracle.Oracle.from_problem(prob)
+    assert o.factor() == -1
+    Lp, Li, Lx = o.L_csc()
+    hs = [sp.Solver.from_problem(prob, dist_world=world, dist_rank=r) for r in range(world)]
+    try:
+        for h in hs:
+            h.spchol_factor_phase(1)
+        for h in hs[1:]:
+            hs[0].spchol_dist_debug_accumulate(h, 0)      # phase B: top panels summed
+        hs[0].spchol_factor_phase(2)                       # phase C
+        for h in hs[1:]:
+            hs[0].spchol_dist_debug_accumulate(h, 1)      # gather subtree panels
+            hs[0].spchol_dist_debug_accumulate(h, 2)      # and their diagonal inverses
+        hs[0].spchol_factor_phase(3)
+        s_gpu = hs[0].spchol_export_symbolic()
+        off, ld, pan = hs[0].spchol_export_panels()
+        idx = panel_index_of_pattern(s_gpu, off, ld, Lp, Li)
+        err = np.abs(pan[idx] - Lx).max() / np.abs(Lx).max()
+        assert err <= TOL_L, err
+        xs, b = gen.rhs(prob)
+        x = hs[0].spchol_solve(b)
+        assert backward_error(prob, x, b) <= TOL_BERR
+    finally:
+        for h in hs:
+            h.close()
