@@ -144,6 +144,7 @@ struct spchol_handle {
   std::vector<int> small_level_off;     // small_sns range per level
   int nevents = 0;
   bool no_lookahead = false;     // SPCHOL_NO_LOOKAHEAD=1 (diagnostics)
+  int max_level = -1;            // SPCHOL_MAX_LEVEL=l: factor only levels <= l (diagnostics)
   std::vector<int> plan_level;   // level of each plan entry (diagnostics)
   // device
   double *d_panels = nullptr, *d_avals = nullptr, *d_linv = nullptr, *d_y = nullptr, *d_y2 = nullptr;
@@ -211,7 +212,8 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve) {
   auto push = [&](int kind, long long off, long long end, double fl, double by) {
     if (end > off) h->plan.push_back(Launch{kind, off, (int)(end - off), fl, by, OP_LAUNCH, 0, -1});
   };
-  for (int l = 0; l < S.nlevels; ++l) {
+  const int lmax = h->max_level >= 0 ? std::min(S.nlevels, h->max_level + 1) : S.nlevels;
+  for (int l = 0; l < lmax; ++l) {
     const size_t plan_before = h->plan.size();
     // small supernodes of this level: one launch on stream 1 (independent of the level's big ones)
     {
@@ -533,6 +535,7 @@ extern "C" int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* r
   int rc = analyze_symbolic(n, colptr, rowidx, perm, h->opt.merge_cap, h->S, err);
   if (rc != SPCHOL_OK) { delete h; return fail(rc, err); }
   if (const char* e = getenv("SPCHOL_NO_LOOKAHEAD")) h->no_lookahead = atoi(e) != 0;
+  if (const char* e = getenv("SPCHOL_MAX_LEVEL")) h->max_level = atoi(e);
   build_plan(h);
   if (h->opt.device < 0) { *out = h; return SPCHOL_OK; }   // host-only analysis (no device state)
   rc = setup_device(h);

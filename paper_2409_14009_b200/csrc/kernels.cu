@@ -74,19 +74,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const G
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const int nchunks = (K + BK - 1) / BK;
+  // Each thread owns NP 16-byte pieces (two rows of one K column) of each operand per chunk; the
+  // source pointers and zero-fill sizes are fixed, only the K tail needs a per-chunk check.
+  constexpr int NP = (BK * TILE / 2) / GEMM_THREADS;
+  const double* srcA[NP];
+  const double* srcB[NP];
+  int byA[NP], byB[NP], kkp[NP], dofs[NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const int p = tid + i * GEMM_THREADS;
+    const int kk = p >> 5, rp = (p & 31) * 2;
+    const int ra = max(0, min(2, arows - rp)), rb = max(0, min(2, brows - rp));
+    byA[i] = ra * 8;
+    byB[i] = rb * 8;
+    srcA[i] = ra ? A + (long long)kk * lda + rp : A;
+    srcB[i] = rb ? B + (long long)kk * ldb + rp : B;
+    kkp[i] = kk;
+    dofs[i] = kk * LDS + rp;
+  }
+  const long long stepA = (long long)BK * lda, stepB = (long long)BK * ldb;
   auto load_chunk = [&](int chunk, int stage) {
     const int kc = chunk * BK;
     double* dA = sA + stage * BK * LDS;
     double* dB = sB + stage * BK * LDS;
 #pragma unroll
-    for (int i = 0; i < (BK * TILE / 2) / GEMM_THREADS; ++i) {
-      const int p = tid + i * GEMM_THREADS;
-      const int kk = p >> 5, rp = (p & 31) * 2;
-      const bool kval = (kc + kk) < K;
-      const int ra = kval ? max(0, min(2, arows - rp)) : 0;
-      const int rb = kval ? max(0, min(2, brows - rp)) : 0;
-      cp_async16(dA + kk * LDS + rp, ra ? A + (long long)(kc + kk) * lda + rp : A, ra * 8);
-      cp_async16(dB + kk * LDS + rp, rb ? B + (long long)(kc + kk) * ldb + rp : B, rb * 8);
+    for (int i = 0; i < NP; ++i) {
+      const bool kval = kc + kkp[i] < K;
+      cp_async16(dA + dofs[i], kval && byA[i] ? srcA[i] + chunk * stepA : A, kval ? byA[i] : 0);
+      cp_async16(dB + dofs[i], kval && byB[i] ? srcB[i] + chunk * stepB : B, kval ? byB[i] : 0);
     }
   };
 #pragma unroll
@@ -460,6 +475,138 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
   }
 }
 
+// ----------------------------------------------------------------------------------------------
+// potrf4_kernel: the same contract as potrf_kernel with a flatter dependency chain: 160 threads,
+// thread t < 136 owns one 4x4 register tile (bi, bj), bi >= bj, of the 64x64 lower triangle.
+// Cholesky, right-looking, step j: the owners of column j publish it (double-buffered shared
+// vector, ONE barrier per step), every thread scales its rows/columns by rsqrt(pivot) and applies
+// the rank-1 update to its tile.  Inverse, step s (forward substitution on I): the owners of row s
+// of X scale it by 1/L_ss and publish it; rows r > s subtract L(r,s) X(s,:).  160 threads x <= 96
+// registers fit the slot of one retiring GEMM CTA (lookahead co-scheduling).
+// ----------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(POTRF4_THREADS) potrf4_kernel(const PTask* __restrict__ tasks,
+                                                              const SnInfo* __restrict__ sn,
+                                                              const int* __restrict__ sfirst, double* panels,
+                                                              double* linv, unsigned long long* fail) {
+  __shared__ double vbuf[2][NBMAX];            // published column of L / row of X
+  __shared__ double Ls[NBMAX][NBMAX + 1];      // Ls[row][col] = L(row, col) after the Cholesky
+  __shared__ double invd[NBMAX];
+  const PTask T = tasks[blockIdx.x];
+  const SnInfo S = sn[T.sn];
+  const int nb = T.nb, tid = threadIdx.x;
+  // block coordinates: t -> (bi, bj), bi >= bj, row-major over the lower block triangle
+  const bool owner = tid < 136;
+  int bi = 0, bj = owner ? tid : 0;
+  while (bj > bi) { bj -= bi + 1; ++bi; }
+  const int r0 = 4 * bi, q0 = 4 * bj;
+  double* P = panels + S.off + (long long)T.c0 * S.ld + T.c0;
+  double a[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + i, c = q0 + q;
+      a[i][q] = (owner && r < nb && c < nb && r >= c) ? P[(long long)c * S.ld + r] : 0.0;
+    }
+  int bad = -1;
+  for (int jb = 0; jb < (nb + 3) / 4; ++jb) {
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = 4 * jb + jj;
+      if (j >= nb) break;
+      double* col = vbuf[j & 1];
+      if (owner && bj == jb) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) col[r0 + i] = a[i][jj];
+      }
+      __syncthreads();
+      const double d = col[j];
+      const double rl = rsqrt(d), l = d * rl;
+      if (bad < 0 && !(d > 0.0)) bad = j;
+      double lr[4], lc[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        lr[i] = col[r0 + i] * rl;
+        lc[i] = col[q0 + i] * rl;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (r0 + i >= q0 + q && q0 + q > j) a[i][q] -= lr[i] * lc[q];
+      if (bj == jb) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = r0 + i;
+          if (r > j) a[i][jj] = lr[i];
+          else if (r == j) a[i][jj] = l;
+        }
+      }
+      if (tid == 0) invd[j] = rl;
+    }
+  }
+  if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[T.sn] + T.c0 + bad));
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + i, c = q0 + q;
+      if (owner) Ls[r][c] = a[i][q];
+      if (owner && r < nb && c < nb && r >= c) P[(long long)c * S.ld + r] = a[i][q];
+    }
+  // inverse: x = identity restricted to the block, forward substitution over pivot rows s
+  double x[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[i][q] = (owner && r0 + i == q0 + q && r0 + i < nb) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int sb = 0; sb < (nb + 3) / 4; ++sb) {
+#pragma unroll
+    for (int ss = 0; ss < 4; ++ss) {
+      const int s = 4 * sb + ss;
+      if (s >= nb) break;
+      double* row = vbuf[s & 1];
+      if (owner && bi == sb) {
+        const double is = invd[s];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          x[ss][q] *= is;
+          row[q0 + q] = x[ss][q];
+        }
+      }
+      __syncthreads();
+      if (owner && r0 + 3 > s) {
+        double xs[4], lrs[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xs[q] = row[q0 + q];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) lrs[i] = Ls[r0 + i][s];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (r0 + i > s && q0 + q <= s) x[i][q] -= lrs[i] * xs[q];
+      }
+    }
+  }
+  double* W = linv + (long long)T.slot * (NBMAX * NBMAX);
+  // the whole 64x64 slot is written: owners write their lower blocks, the rest writes zeros
+  for (int e = tid; e < NBMAX * NBMAX; e += POTRF4_THREADS) {
+    const int c = e / NBMAX, r = e % NBMAX;
+    if (r < c || r >= nb || c >= nb) W[e] = 0.0;
+  }
+  if (owner) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = r0 + i, c = q0 + q;
+        if (r >= c && r < nb && c < nb) W[c * NBMAX + r] = x[i][q];
+      }
+  }
+}
+
 __global__ void init_scatter_kernel(const double* __restrict__ vals, const long long* __restrict__ amap,
                                     long long nnz, double* panels) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz; e += (long long)gridDim.x * blockDim.x) {
@@ -638,7 +785,11 @@ void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, dou
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels, double* linv,
                   unsigned long long* fail, cudaStream_t st, int prio) {
   if (ntasks <= 0) return;
+#if SPCHOL_POTRF4
+  launch_prio(potrf4_kernel, ntasks, POTRF4_THREADS, 0, st, prio, tasks, sn, sfirst, panels, linv, fail);
+#else
   launch_prio(potrf_kernel, ntasks, POTRF_THREADS, POTRF_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
+#endif
 }
 
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,

@@ -48,6 +48,10 @@ constexpr int GEMM_THREADS = 128;  // 4 warps, 2x2, warp tile 32x32
 constexpr int GEMM_SMEM = 2 * STAGES * BK * LDS * (int)sizeof(double);
 constexpr int NBMAX = 64;          // cdiv block width
 constexpr int POTRF_THREADS = 128;
+constexpr int POTRF4_THREADS = 160;
+#ifndef SPCHOL_POTRF4
+#define SPCHOL_POTRF4 1
+#endif
 constexpr int POTRF_SMEM = 2 * NBMAX * (NBMAX + 1) * (int)sizeof(double);
 
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels,
