@@ -95,6 +95,7 @@ struct Launch {
   double flops, bytes;
   int op = OP_LAUNCH, stream = 0, ev = -1;
   int aux = 0;     // K_SMALL: dynamic shared memory (doubles)
+  int aux2 = 0;    // K_SMALL: largest m in the launch
 };
 template <class T>
 cudaError_t dalloc(T** p, size_t count) {
@@ -219,7 +220,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve) {
     {
       long long s0 = (long long)h->small_sns.size();
       if (record_solve) h->small_level_off.push_back((int)s0);
-      int mx = 0;
+      int mx = 0, mxm = 0;
       double fsm = 0, bsm = 0;
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
         const int J = h->level_sns[x];
@@ -227,6 +228,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve) {
         const SnInfo& I = h->sn[J];
         h->small_sns.push_back(J);
         mx = std::max(mx, I.m * I.k);
+        mxm = std::max(mxm, I.m);
         const double t = I.m - I.k;
         for (int c = 0; c < I.k; ++c) fsm += (double)(I.m - c) * (double)(I.m - c);
         bsm += 16.0 * I.m * I.k + 16.0 * 0.5 * t * (t + 1);
@@ -238,6 +240,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve) {
         h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 1, ev});
         Launch L{K_SMALL, s0, (int)(s1 - s0), fsm, bsm, OP_LAUNCH, 1, -1};
         L.aux = mx;
+        L.aux2 = mxm;
         h->plan.push_back(L);
       }
     }
@@ -621,7 +624,7 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
     switch (L.kind) {
       case K_SMALL:
         launch_small(h->d_small_sns + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_ucol_base, h->d_ucol_map,
-                     h->d_posmap, h->d_fail, L.aux, ls, prio);
+                     h->d_posmap, h->d_fail, L.aux, L.aux2, ls, prio);
         break;
       case K_POTRF:
         launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio);

@@ -1,4 +1,5 @@
 // sm_100a kernels; see kernels.cuh for the map to the paper.
+#include <algorithm>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
   const SnInfo S = sn[J];
   const int m = S.m, k = S.k, t = m - k, tid = threadIdx.x;
   double* G = panels + S.off;
-  for (int e = tid; e < m * k; e += SMALL_THREADS) {
+  for (int e = tid; e < m * k; e += blockDim.x) {
     const int c = e / m, r = e - c * m;
     P[e] = G[(long long)c * S.ld + r];
   }
@@ -430,14 +431,14 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
     __syncthreads();
   }
   if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[J] + bad));
-  for (int e = tid; e < m * k; e += SMALL_THREADS) {
+  for (int e = tid; e < m * k; e += blockDim.x) {
     const int c = e / m, rr = e - c * m;
     if (rr >= c) G[(long long)c * S.ld + rr] = P[e];
   }
   if (t <= 0) return;
   // U_J in 4x4 register blocks over the lower block triangle of the t x t update
   const int nbt = (t + 3) >> 2, nblk = nbt * (nbt + 1) / 2;
-  for (int bidx = tid; bidx < nblk; bidx += SMALL_THREADS) {
+  for (int bidx = tid; bidx < nblk; bidx += blockDim.x) {
     int bi = (int)((sqrtf(8.0f * bidx + 1.0f) - 1.0f) * 0.5f);
     while (bi * (bi + 1) / 2 > bidx) --bi;
     while ((bi + 1) * (bi + 2) / 2 <= bidx) ++bi;
@@ -484,17 +485,28 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
 // of X scale it by 1/L_ss and publish it; rows r > s subtract L(r,s) X(s,:).  160 threads x <= 96
 // registers fit the slot of one retiring GEMM CTA (lookahead co-scheduling).
 // ----------------------------------------------------------------------------------------------
+// 1/sqrt(d) to full FP64 precision: hardware approximation (MUFU.RSQ64H) + two Newton steps;
+// shorter dependent chain than rsqrt(double) (which also handles special cases).  d <= 0 or NaN
+// gives NaN/inf, which the caller flags as a failed pivot.
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double hd = 0.5 * d;
+  y = y * fma(-hd * y, y, 1.5);
+  y = y * fma(-hd * y, y, 1.5);
+  return y;
+}
+
 __global__ void __launch_bounds__(POTRF4_THREADS) potrf4_kernel(const PTask* __restrict__ tasks,
-                                                              const SnInfo* __restrict__ sn,
-                                                              const int* __restrict__ sfirst, double* panels,
-                                                              double* linv, unsigned long long* fail) {
+                                                                const SnInfo* __restrict__ sn,
+                                                                const int* __restrict__ sfirst, double* panels,
+                                                                double* linv, unsigned long long* fail) {
   __shared__ double vbuf[2][NBMAX];            // published column of L / row of X
   __shared__ double Ls[NBMAX][NBMAX + 1];      // Ls[row][col] = L(row, col) after the Cholesky
   __shared__ double invd[NBMAX];
   const PTask T = tasks[blockIdx.x];
   const SnInfo S = sn[T.sn];
   const int nb = T.nb, tid = threadIdx.x;
-  // block coordinates: t -> (bi, bj), bi >= bj, row-major over the lower block triangle
   const bool owner = tid < 136;
   int bi = 0, bj = owner ? tid : 0;
   while (bj > bi) { bj -= bi + 1; ++bi; }
@@ -508,6 +520,8 @@ __global__ void __launch_bounds__(POTRF4_THREADS) potrf4_kernel(const PTask* __r
       const int r = r0 + i, c = q0 + q;
       a[i][q] = (owner && r < nb && c < nb && r >= c) ? P[(long long)c * S.ld + r] : 0.0;
     }
+  // Entries above the diagonal inside diagonal tiles are never read back; masking is done by zeroing
+  // the column multipliers of finished columns (a - x*0 == a exactly), so the updates run unguarded.
   int bad = -1;
   for (int jb = 0; jb < (nb + 3) / 4; ++jb) {
 #pragma unroll
@@ -521,26 +535,21 @@ __global__ void __launch_bounds__(POTRF4_THREADS) potrf4_kernel(const PTask* __r
       }
       __syncthreads();
       const double d = col[j];
-      const double rl = rsqrt(d), l = d * rl;
+      const double rl = rsqrt_nr(d), l = d * rl;
       if (bad < 0 && !(d > 0.0)) bad = j;
       double lr[4], lc[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         lr[i] = col[r0 + i] * rl;
-        lc[i] = col[q0 + i] * rl;
+        lc[i] = q0 + i > j ? col[q0 + i] * rl : 0.0;
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (r0 + i >= q0 + q && q0 + q > j) a[i][q] -= lr[i] * lc[q];
+        for (int q = 0; q < 4; ++q) a[i][q] = fma(-lr[i], lc[q], a[i][q]);
       if (bj == jb) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = r0 + i;
-          if (r > j) a[i][jj] = lr[i];
-          else if (r == j) a[i][jj] = l;
-        }
+        for (int i = 0; i < 4; ++i) a[i][jj] = r0 + i == j ? l : lr[i];
       }
       if (tid == 0) invd[j] = rl;
     }
@@ -551,10 +560,10 @@ __global__ void __launch_bounds__(POTRF4_THREADS) potrf4_kernel(const PTask* __r
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int r = r0 + i, c = q0 + q;
-      if (owner) Ls[r][c] = a[i][q];
+      if (owner) Ls[r][c] = r >= c ? a[i][q] : 0.0;
       if (owner && r < nb && c < nb && r >= c) P[(long long)c * S.ld + r] = a[i][q];
     }
-  // inverse: x = identity restricted to the block, forward substitution over pivot rows s
+  // inverse: x = identity on the block, forward substitution over pivot rows s
   double x[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -576,22 +585,18 @@ __global__ void __launch_bounds__(POTRF4_THREADS) potrf4_kernel(const PTask* __r
         }
       }
       __syncthreads();
-      if (owner && r0 + 3 > s) {
-        double xs[4], lrs[4];
+      double xs[4], lrs[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) xs[q] = row[q0 + q];
+      for (int q = 0; q < 4; ++q) xs[q] = q0 + q <= s ? row[q0 + q] : 0.0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) lrs[i] = Ls[r0 + i][s];
+      for (int i = 0; i < 4; ++i) lrs[i] = r0 + i > s ? Ls[r0 + i][s] : 0.0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (r0 + i > s && q0 + q <= s) x[i][q] -= lrs[i] * xs[q];
-      }
+        for (int q = 0; q < 4; ++q) x[i][q] = fma(-lrs[i], xs[q], x[i][q]);
     }
   }
   double* W = linv + (long long)T.slot * (NBMAX * NBMAX);
-  // the whole 64x64 slot is written: owners write their lower blocks, the rest writes zeros
   for (int e = tid; e < NBMAX * NBMAX; e += POTRF4_THREADS) {
     const int c = e / NBMAX, r = e % NBMAX;
     if (r < c || r >= nb || c >= nb) W[e] = 0.0;
@@ -794,9 +799,11 @@ void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* s
 
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,
                   const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,
-                  int smem_doubles, cudaStream_t st, int prio) {
+                  int smem_doubles, int maxm, cudaStream_t st, int prio) {
   if (count <= 0) return;
-  launch_prio(small_kernel, count, SMALL_THREADS, smem_doubles * (int)sizeof(double), st, prio, sns, sn, sfirst, panels,
+  // one thread per panel row: blockDim = the launch's largest m rounded up to a warp (<= 256)
+  const int threads = std::min(SMALL_THREADS, std::max(32, (maxm + 31) / 32 * 32));
+  launch_prio(small_kernel, count, threads, smem_doubles * (int)sizeof(double), st, prio, sns, sn, sfirst, panels,
               ucol_base, ucol_map, posmap, fail);
 }
 

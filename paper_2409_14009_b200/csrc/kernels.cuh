@@ -65,7 +65,7 @@ constexpr int SMALL_MAXM = SMALL_THREADS;
 constexpr int SMALL_MAXELEMS = 12288;   // m*k doubles in shared memory (96 KB)
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,
                   const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,
-                  int smem_doubles, cudaStream_t st, int prio = 0);
+                  int smem_doubles, int maxm, cudaStream_t st, int prio = 0);
 void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st);
 void launch_solve_fwd(const int* sns, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
                       const int* rows, const double* panels, double* y, cudaStream_t st);
