@@ -2,6 +2,8 @@
 #include <algorithm>
 #include <cstdio>
 
+#include <cuda.h>
+
 #include "kernels.cuh"
 
 namespace spchol {
@@ -39,6 +41,83 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 //                rows(P) = m_P-1-relind(J,P)); FP64 RED of -U (concurrent supernodes of
 //                one level may hit the same ancestor entry).
 // ----------------------------------------------------------------------------------------------
+// Shared epilogue of the tile kernels: stage the 64x64 tile through shared memory (column-major,
+// stride LDC), then each warp streams whole 64-row columns: 16-byte vector RMW / stores (LOCAL,
+// TRSM) or runs of consecutive RED (SCATTER, relind runs are long: consecutive U rows land in
+// consecutive ancestor rows).  All destination loads of a thread are issued before its stores.
+template <int MODE>
+__device__ __forceinline__ void gemm_epilogue(const GTask& T, const SnInfo& S, double* panels, double* smem,
+                                              const double (&acc)[4][4][2], const long long* __restrict__ ucol_base,
+                                              const long long* __restrict__ ucol_map, const int* __restrict__ posmap) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+  constexpr int LDC = TILE + 4;   // 68 doubles: conflict-free fragment writes and v2 reads
+  double* sC = smem;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+        sC[(wn * 32 + j * 8 + 2 * t + v) * LDC + wm * 32 + i * 8 + g] = acc[i][j][v];
+  __syncthreads();
+  const int pr = 2 * lane;                 // row pair inside the tile
+  constexpr int NIT = TILE / (GEMM_THREADS / 32);   // columns per warp (16)
+  if (MODE == MODE_LOCAL) {
+    const int gr = T.r0 + pr;
+    double2 dv[NIT];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int gc = T.s0 + warp + 4 * it;
+      const bool ok = gc < T.slot && gr + 1 >= gc && gr < S.m;
+      dv[it] = ok ? *reinterpret_cast<const double2*>(panels + S.off + (long long)gc * S.ld + gr) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int col = warp + 4 * it, gc = T.s0 + col;
+      if (!(gc < T.slot && gr + 1 >= gc && gr < S.m)) continue;
+      const double2 c2 = *reinterpret_cast<const double2*>(sC + col * LDC + pr);
+      double* d = panels + S.off + (long long)gc * S.ld + gr;
+      const bool v0 = gr >= gc, v1 = gr + 1 < S.m;
+      if (v0 && v1) {
+        *reinterpret_cast<double2*>(d) = make_double2(dv[it].x - c2.x, dv[it].y - c2.y);
+      } else {
+        if (v0) d[0] = dv[it].x - c2.x;
+        if (v1) d[1] = dv[it].y - c2.y;
+      }
+    }
+  } else if (MODE == MODE_TRSM) {
+    const int gr = T.r0 + pr;
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int col = warp + 4 * it;
+      if (col >= T.nb || gr + 1 < T.s0 || gr >= S.m) continue;
+      const double2 c2 = *reinterpret_cast<const double2*>(sC + col * LDC + pr);
+      double* d = panels + S.off + (long long)(T.c0 + col) * S.ld + gr;
+      const bool v0 = gr >= T.s0, v1 = gr + 1 < S.m;
+      if (v0 && v1) *reinterpret_cast<double2*>(d) = c2;
+      else {
+        if (v0) d[0] = c2.x;
+        if (v1) d[1] = c2.y;
+      }
+    }
+  } else {
+#pragma unroll 4
+    for (int it = 0; it < NIT; ++it) {
+      const int col = warp + 4 * it;
+      const int uc = T.s0 + col - S.k;
+      if (uc < 0 || T.s0 + col >= S.m) continue;
+      const long long cb = ucol_base[S.ucol + uc];
+      const long long mb = ucol_map[S.ucol + uc];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = lane + 32 * h, gr = T.r0 + row;   // lanes cover 32 consecutive rows
+        if (gr < S.m && gr - S.k >= uc) atomicAdd(panels + cb + posmap[mb + gr], -sC[col * LDC + row]);
+      }
+    }
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const GTask* __restrict__ tasks,
                                                             const SnInfo* __restrict__ sn, double* panels,
@@ -133,76 +212,144 @@ __global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const G
     }
   }
   cp_async_wait<0>();
-  // ---- epilogue: stage the 64x64 tile through shared memory (column-major, stride LDC), then
-  // each warp streams whole 64-row columns: 16-byte vector RMW / stores (LOCAL, TRSM) or runs of
-  // consecutive RED (SCATTER, relind runs are long: consecutive U rows land in consecutive
-  // ancestor rows).  All destination loads of a thread are issued before its stores.
-  constexpr int LDC = TILE + 4;   // 68 doubles: conflict-free fragment writes and v2 reads
   __syncthreads();
-  double* sC = smem;
+  gemm_epilogue<MODE>(T, S, panels, smem, acc, ucol_base, ucol_map, posmap);
+}
+
+// ----------------------------------------------------------------------------------------------
+// gemm_tma_kernel<MODE>: same tile contract and epilogues as gemm_kernel, with the operands moved by
+// the Tensor Memory Accelerator: per stage, thread 0 issues 2 x 4 boxes of 16 rows x BK columns
+// (cp.async.bulk.tensor, SWIZZLE_128B, out-of-bounds rows/columns zero-filled — ragged tiles and K
+// tails need no masking) and the CTA's warps consume them through full/empty mbarriers, no CTA-wide
+// barrier in the K loop.  128B swizzle: element (row rw of a 16-row box, column kk) sits at
+// kk*128 + (((rw>>1) ^ (kk&7))*16) + (rw&1)*8 bytes.  Lane (g, t) of k-step ks takes K index
+// kk = 2ks + (t>>1) + 4(t&1) (any K permutation is valid when A and B share it); with it the 32
+// lanes' fragment loads hit 32 distinct banks in 2 wavefronts.
+// ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"((unsigned long long)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int TBK = TMA_BOX_COLS;                       // K columns per stage (multiple of 8 = swizzle atom)
+constexpr int TSTAGES = SPCHOL_TSTAGES;
+constexpr int TSTAGE_DOUBLES = 2 * TILE * TBK;          // A and B boxes of one stage
+constexpr int TMA_SMEM = (TSTAGES * TSTAGE_DOUBLES > TILE * (TILE + 4) ? TSTAGES * TSTAGE_DOUBLES : TILE * (TILE + 4)) *
+                             (int)sizeof(double) + 1024;
+
+template <int MODE>
+__global__ void __launch_bounds__(GEMM_THREADS, 4) gemm_tma_kernel(const GTask* __restrict__ tasks,
+                                                                   const SnInfo* __restrict__ sn, double* panels,
+                                                                   const CUtensorMap* __restrict__ tmaps,
+                                                                   const CUtensorMap* __restrict__ tmap_linv,
+                                                                   const long long* __restrict__ ucol_base,
+                                                                   const long long* __restrict__ ucol_map,
+                                                                   const int* __restrict__ posmap) {
+  extern __shared__ unsigned char tsm_raw[];
+  // 1024-byte aligned (128B swizzle atom) stage buffers; offsetting the shared pointer (rather than
+  // casting through an integer) keeps the shared address space, so fragment loads stay LDS
+  const unsigned sbase = smem_u32(tsm_raw);
+  double* smem = reinterpret_cast<double*>(tsm_raw + (((sbase + 1023u) & ~1023u) - sbase));
+  __shared__ __align__(8) unsigned long long full[TSTAGES];
+  __shared__ int done[TSTAGES];            // warps finished with the stage's current chunk
+  const GTask T = tasks[blockIdx.x];
+  const SnInfo S = sn[T.sn];
+  const CUtensorMap* mapA = tmaps + T.sn;
+  const CUtensorMap* mapB = MODE == MODE_TRSM ? tmap_linv : mapA;
+  int arow, brow, acol, bcol, K;
+  if (MODE == MODE_LOCAL) { arow = T.r0; brow = T.s0; acol = bcol = T.c0; K = T.nb; }
+  else if (MODE == MODE_TRSM) { arow = T.r0; brow = 0; acol = T.c0; bcol = T.slot * NBMAX; K = T.nb; }
+  else { arow = T.r0; brow = T.s0; acol = bcol = 0; K = S.k; }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+  const int nchunks = (K + TBK - 1) / TBK;
+  if (tid == 0) {
+    for (int s = 0; s < TSTAGES; ++s) { mbar_init(&full[s], 1); done[s] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int chunk, int stage) {
+    double* dA = smem + stage * TSTAGE_DOUBLES;
+    double* dB = dA + TILE * TBK;
+    mbar_expect_tx(&full[stage], TSTAGE_DOUBLES * (unsigned)sizeof(double));
+#pragma unroll
+    for (int q = 0; q < TILE / 16; ++q) {
+      tma_load_2d(dA + q * 16 * TBK, mapA, arow + 16 * q, acol + chunk * TBK, &full[stage]);
+      tma_load_2d(dB + q * 16 * TBK, mapB, brow + 16 * q, bcol + chunk * TBK, &full[stage]);
+    }
+  };
+  if (tid == 0)
+    for (int s = 0; s < TSTAGES && s < nchunks; ++s) issue(s, s);
+  double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // fragment offsets (doubles) inside a stage, per subtile i and k-step ks (swizzled)
+  constexpr int KS = TBK / 4;
+  int offA[4][KS], offB[4][KS];
 #pragma unroll
-      for (int v = 0; v < 2; ++v)
-        sC[(wn * 32 + j * 8 + 2 * t + v) * LDC + wm * 32 + i * 8 + g] = acc[i][j][v];
-  __syncthreads();
-  const int pr = 2 * lane;                 // row pair inside the tile
-  constexpr int NIT = TILE / (GEMM_THREADS / 32);   // columns per warp (16)
-  if (MODE == MODE_LOCAL) {
-    const int gr = T.r0 + pr;
-    double2 dv[NIT];
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-      const int gc = T.s0 + warp + 4 * it;
-      const bool ok = gc < T.slot && gr + 1 >= gc && gr < S.m;
-      dv[it] = ok ? *reinterpret_cast<const double2*>(panels + S.off + (long long)gc * S.ld + gr) : make_double2(0.0, 0.0);
+    for (int ks = 0; ks < KS; ++ks) {
+      const int kk = 8 * (ks >> 1) + 2 * (ks & 1) + (t >> 1) + 4 * (t & 1);
+      const int ra = wm * 32 + i * 8 + g, rb = wn * 32 + i * 8 + g;
+      offA[i][ks] = (ra >> 4) * 16 * TBK + kk * 16 + ((((ra & 15) >> 1) ^ (kk & 7)) << 1) + (ra & 1);
+      offB[i][ks] = TILE * TBK + (rb >> 4) * 16 * TBK + kk * 16 + ((((rb & 15) >> 1) ^ (kk & 7)) << 1) + (rb & 1);
     }
+  for (int c = 0; c < nchunks; ++c) {
+    const int stage = c % TSTAGES;
+    const unsigned parity = (c / TSTAGES) & 1;
+    mbar_wait(&full[stage], parity);
+    const double* st = smem + stage * TSTAGE_DOUBLES;
+    // K tail inside the panel (e.g. a 40-column block): TMA reads real columns there, mask them
+    const int kleft = K - c * TBK;
 #pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-      const int col = warp + 4 * it, gc = T.s0 + col;
-      if (!(gc < T.slot && gr + 1 >= gc && gr < S.m)) continue;
-      const double2 c2 = *reinterpret_cast<const double2*>(sC + col * LDC + pr);
-      double* d = panels + S.off + (long long)gc * S.ld + gr;
-      const bool v0 = gr >= gc, v1 = gr + 1 < S.m;
-      if (v0 && v1) {
-        *reinterpret_cast<double2*>(d) = make_double2(dv[it].x - c2.x, dv[it].y - c2.y);
-      } else {
-        if (v0) d[0] = dv[it].x - c2.x;
-        if (v1) d[1] = dv[it].y - c2.y;
+    for (int ks = 0; ks < KS; ++ks) {
+      double a[4], b[4];
+      const bool kval = kleft >= TBK || 8 * (ks >> 1) + 2 * (ks & 1) + (t >> 1) + 4 * (t & 1) < kleft;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = kval ? st[offA[i][ks]] : 0.0;
+        b[i] = kval ? st[offB[i][ks]] : 0.0;
       }
-    }
-  } else if (MODE == MODE_TRSM) {
-    const int gr = T.r0 + pr;
 #pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-      const int col = warp + 4 * it;
-      if (col >= T.nb || gr + 1 < T.s0 || gr >= S.m) continue;
-      const double2 c2 = *reinterpret_cast<const double2*>(sC + col * LDC + pr);
-      double* d = panels + S.off + (long long)(T.c0 + col) * S.ld + gr;
-      const bool v0 = gr >= T.s0, v1 = gr + 1 < S.m;
-      if (v0 && v1) *reinterpret_cast<double2*>(d) = c2;
-      else {
-        if (v0) d[0] = c2.x;
-        if (v1) d[1] = c2.y;
-      }
-    }
-  } else {
-#pragma unroll 4
-    for (int it = 0; it < NIT; ++it) {
-      const int col = warp + 4 * it;
-      const int uc = T.s0 + col - S.k;
-      if (uc < 0 || T.s0 + col >= S.m) continue;
-      const long long cb = ucol_base[S.ucol + uc];
-      const long long mb = ucol_map[S.ucol + uc];
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int row = lane + 32 * h, gr = T.r0 + row;   // lanes cover 32 consecutive rows
-        if (gr < S.m && gr - S.k >= uc) atomicAdd(panels + cb + posmap[mb + gr], -sC[col * LDC + row]);
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+    }
+    // the last warp to finish this stage refills it with chunk c + TSTAGES (nobody waits)
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&done[stage], 1) == GEMM_THREADS / 32 - 1) {
+        done[stage] = 0;
+        if (c + TSTAGES < nchunks) issue(c + TSTAGES, stage);
       }
     }
   }
+  __syncthreads();
+  gemm_epilogue<MODE>(T, S, panels, smem, acc, ucol_base, ucol_map, posmap);
 }
 
 // ----------------------------------------------------------------------------------------------
@@ -753,6 +900,9 @@ cudaError_t kernels_init_attributes() {
   if ((e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_MAXELEMS * (int)sizeof(double)))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(gemm_tma_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(gemm_tma_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(gemm_tma_kernel<MODE_SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   return cudaSuccess;
@@ -774,6 +924,20 @@ static void launch_prio(void (*kern)(KArgs...), int grid, int block, int smem, c
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+void launch_gemm_tma(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, const void* tmaps,
+                     const void* tmap_linv, const long long* ucol_base, const long long* ucol_map, const int* posmap,
+                     cudaStream_t st, int prio) {
+  if (ntasks <= 0) return;
+  const CUtensorMap* tm = (const CUtensorMap*)tmaps;
+  const CUtensorMap* tl = (const CUtensorMap*)tmap_linv;
+  if (mode == MODE_LOCAL)
+    launch_prio(gemm_tma_kernel<MODE_LOCAL>, ntasks, GEMM_THREADS, TMA_SMEM, st, prio, tasks, sn, panels, tm, tl, ucol_base, ucol_map, posmap);
+  else if (mode == MODE_TRSM)
+    launch_prio(gemm_tma_kernel<MODE_TRSM>, ntasks, GEMM_THREADS, TMA_SMEM, st, prio, tasks, sn, panels, tm, tl, ucol_base, ucol_map, posmap);
+  else
+    launch_prio(gemm_tma_kernel<MODE_SCATTER>, ntasks, GEMM_THREADS, TMA_SMEM, st, prio, tasks, sn, panels, tm, tl, ucol_base, ucol_map, posmap);
 }
 
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, const double* linv,

@@ -57,6 +57,19 @@ constexpr int POTRF_SMEM = 2 * NBMAX * (NBMAX + 1) * (int)sizeof(double);
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels,
                  const double* linv, const long long* ucol_base, const long long* ucol_map,
                  const int* posmap, cudaStream_t st, int prio = 0);
+#ifndef SPCHOL_TBK
+#define SPCHOL_TBK 16
+#endif
+#ifndef SPCHOL_TSTAGES
+#define SPCHOL_TSTAGES 3
+#endif
+constexpr int TMA_BOX_ROWS = 16;           // 16 doubles = one 128-byte swizzle row
+constexpr int TMA_BOX_COLS = SPCHOL_TBK;   // K columns per TMA stage (the host encodes this box)
+// TMA variant: tmaps = device array of CUtensorMap (one per supernode panel, rows x columns, box
+// 16 x 8, SWIZZLE_128B), tmap_linv = CUtensorMap over the diagonal-inverse slots (64 x 64*slots).
+void launch_gemm_tma(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, const void* tmaps,
+                     const void* tmap_linv, const long long* ucol_base, const long long* ucol_map, const int* posmap,
+                     cudaStream_t st, int prio = 0);
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels,
                   double* linv, unsigned long long* fail, cudaStream_t st, int prio = 0);
 constexpr int SMALL_THREADS = 256;

@@ -138,3 +138,11 @@ def test_distributed_dataflow_single_gpu(name, world):
     finally:
         for h in hs:
             h.close()
+
+
+@pytest.mark.parametrize("name", ["S3", "S4", "S5", "T2"])
+def test_parity_tma_tiles(name, monkeypatch):
+    """The TMA + mbarrier variant of the tile kernels (SPCHOL_TMA=1): same parity bar."""
+    monkeypatch.setenv("SPCHOL_TMA", "1")
+    run_parity(gen.make(name), small_max_k=-1)
+    run_parity(gen.make(name), block=40, small_max_k=-1)
