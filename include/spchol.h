@@ -60,6 +60,10 @@ typedef struct {
                            (SURVEY §8(e)): each rank factors its own subtrees (phase A), the top
                            (separator) panels are summed over ranks with NCCL (phase B), and the
                            top supernodes are factored (phase C).  Needs spchol_dist_attach_nccl. */
+  int32_t subtree_streams; /* single GPU: independent subtrees (proportional mapping onto this many
+                           virtual ranks) are factored concurrently on their own stream pairs, the
+                           top supernodes after they join.  0 = default (4), 1 = one level-set
+                           schedule for the whole tree. */
 } spchol_options;
 
 /* Fill *opt with the defaults above. */

@@ -44,7 +44,8 @@ EXPORTS = [
 class spchol_options(ctypes.Structure):
     _fields_ = [("merge_cap", ctypes.c_double), ("device", ctypes.c_int32), ("block", ctypes.c_int32),
                 ("small_max_k", ctypes.c_int32), ("use_graph", ctypes.c_int32),
-                ("dist_rank", ctypes.c_int32), ("dist_world", ctypes.c_int32)]
+                ("dist_rank", ctypes.c_int32), ("dist_world", ctypes.c_int32),
+                ("subtree_streams", ctypes.c_int32)]
 
 
 class SpcholError(RuntimeError):

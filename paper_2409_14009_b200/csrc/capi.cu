@@ -140,7 +140,8 @@ struct spchol_handle {
   std::vector<int> owner;              // rank owning each supernode's subtree, -1 = top
   long long top_off = -1;              // first double of the contiguous top-panel region
   int top_slot = -1;                   // first inverse slot of the top supernodes
-  size_t plan_all_end = 0, plan_a_end = 0;
+  size_t plan_all_end = 0, plan_a_end = 0, plan_factor_begin = 0;
+  int nvr = 1;                         // single-GPU subtree concurrency (virtual ranks)
   void* nccl_comm = nullptr;
   bool gathered = false;
   struct SolveStep { int level; long long p0; int np; long long t0; int nt; };
@@ -162,8 +163,9 @@ struct spchol_handle {
   PTask* d_ptasks = nullptr;
   unsigned long long* d_fail = nullptr;
   bool values_set = false, factored = false;
-  cudaStream_t side_stream = nullptr;           // stream 1 of the plan (trailing updates, low priority)
-  cudaStream_t crit_stream = nullptr;           // stream 0 of the plan (cdiv chain, high priority)
+  std::vector<cudaStream_t> pstreams;           // plan streams: even = cdiv chain (high priority),
+                                                // odd = trailing updates (low priority)
+  std::vector<cudaEvent_t> join_events;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int prio_lo = 0, prio_hi = 0;
   std::vector<cudaEvent_t> plan_events;
@@ -187,6 +189,7 @@ extern "C" void spchol_default_options(spchol_options* o) {
   o->use_graph = 1;
   o->dist_rank = 0;
   o->dist_world = 1;
+  o->subtree_streams = 0;
 }
 
 extern "C" const char* spchol_last_error(void) { return g_err.c_str(); }
@@ -213,38 +216,48 @@ static void for_tiles(int rbase, int rend, int cbase, int cend, F emit) {
 // Appends, level by level, the launches for the supernodes J with active(J).  record_solve: also
 // record the solve's step structure (only for the whole-tree plan).
 template <class Active>
-static void append_levels(spchol_handle* h, Active active, bool record_solve) {
+static void append_levels(spchol_handle* h, Active active, bool record_solve, int SB = 0) {
   const Symbolic& S = h->S;
   const int NB = h->nb, OUTER = spchol_handle::OUTER;
   auto push = [&](int kind, long long off, long long end, double fl, double by) {
-    if (end > off) h->plan.push_back(Launch{kind, off, (int)(end - off), fl, by, OP_LAUNCH, 0, -1});
+    if (end > off) h->plan.push_back(Launch{kind, off, (int)(end - off), fl, by, OP_LAUNCH, SB, -1});
   };
   const int lmax = h->max_level >= 0 ? std::min(S.nlevels, h->max_level + 1) : S.nlevels;
   for (int l = 0; l < lmax; ++l) {
     const size_t plan_before = h->plan.size();
-    // small supernodes of this level: one launch on stream 1 (independent of the level's big ones)
+    // small supernodes of this level: launches on stream 1 (independent of the level's big ones),
+    // bucketed by panel size so that each launch's shared memory (sized by its largest panel)
+    // lets as many CTAs as possible be resident
     {
-      long long s0 = (long long)h->small_sns.size();
-      if (record_solve) h->small_level_off.push_back((int)s0);
-      int mx = 0, mxm = 0;
-      double fsm = 0, bsm = 0;
-      for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
-        const int J = h->level_sns[x];
-        if (!h->is_small[J] || !active(J)) continue;
-        const SnInfo& I = h->sn[J];
-        h->small_sns.push_back(J);
-        mx = std::max(mx, I.m * I.k);
-        mxm = std::max(mxm, I.m);
-        const double t = I.m - I.k;
-        for (int c = 0; c < I.k; ++c) fsm += (double)(I.m - c) * (double)(I.m - c);
-        bsm += 16.0 * I.m * I.k + 16.0 * 0.5 * t * (t + 1);
-      }
-      long long s1 = (long long)h->small_sns.size();
-      if (s1 > s0) {
-        const int ev = h->nevents++;
-        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 0, ev});
-        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 1, ev});
-        Launch L{K_SMALL, s0, (int)(s1 - s0), fsm, bsm, OP_LAUNCH, 1, -1};
+      if (record_solve) h->small_level_off.push_back((int)h->small_sns.size());
+      static const int bucket_max[] = {256, 1024, 4096, SMALL_MAXELEMS};
+      bool forked = false;
+      for (int bk = 0; bk < 4; ++bk) {
+        long long s0 = (long long)h->small_sns.size();
+        int mx = 0, mxm = 0;
+        double fsm = 0, bsm = 0;
+        for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
+          const int J = h->level_sns[x];
+          if (!h->is_small[J] || !active(J)) continue;
+          const SnInfo& I = h->sn[J];
+          const int mk = I.m * I.k;
+          if (mk > bucket_max[bk] || (bk > 0 && mk <= bucket_max[bk - 1])) continue;
+          h->small_sns.push_back(J);
+          mx = std::max(mx, mk);
+          mxm = std::max(mxm, I.m);
+          const double t = I.m - I.k;
+          for (int c = 0; c < I.k; ++c) fsm += (double)(I.m - c) * (double)(I.m - c);
+          bsm += 16.0 * I.m * I.k + 16.0 * 0.5 * t * (t + 1);
+        }
+        long long s1 = (long long)h->small_sns.size();
+        if (s1 == s0) continue;
+        if (!forked) {
+          const int ev = h->nevents++;
+          h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, SB, ev});
+          h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SB + 1, ev});
+          forked = true;
+        }
+        Launch L{K_SMALL, s0, (int)(s1 - s0), fsm, bsm, OP_LAUNCH, SB + 1, -1};
         L.aux = mx;
         L.aux2 = mxm;
         h->plan.push_back(L);
@@ -311,30 +324,30 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve) {
       }
       if (!rest.empty()) {            // fork REST(S) onto stream 1 after the cdiv of block S
         const int ev = h->nevents++;
-        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 0, ev});
-        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 1, ev});
+        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, SB, ev});
+        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SB + 1, ev});
         long long r0g = (long long)h->gtasks.size();
         h->gtasks.insert(h->gtasks.end(), rest.begin(), rest.end());
         if ((long long)h->gtasks.size() > r0g)
-          h->plan.push_back(Launch{K_LOCAL, r0g, (int)((long long)h->gtasks.size() - r0g), fr, br, OP_LAUNCH, 1, -1});
+          h->plan.push_back(Launch{K_LOCAL, r0g, (int)((long long)h->gtasks.size() - r0g), fr, br, OP_LAUNCH, SB + 1, -1});
       }
       if (!nxt.empty()) {
-        if (pending_rest_ev >= 0) h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 0, pending_rest_ev});
+        if (pending_rest_ev >= 0) h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SB, pending_rest_ev});
         long long n0 = (long long)h->gtasks.size();
         h->gtasks.insert(h->gtasks.end(), nxt.begin(), nxt.end());
         push(K_LOCAL, n0, (long long)h->gtasks.size(), fn, bn);
       }
       if (!rest.empty()) {
         pending_rest_ev = h->nevents++;
-        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 1, pending_rest_ev});
+        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, SB + 1, pending_rest_ev});
       }
     }
     bool s1_used = false;
-    for (size_t q = plan_before; q < h->plan.size(); ++q) s1_used |= h->plan[q].stream == 1;
+    for (size_t q = plan_before; q < h->plan.size(); ++q) s1_used |= h->plan[q].stream == SB + 1;
     if (s1_used) {  // join stream 1 (small-supernode launch and trailing updates) before the level's scatter
       const int ev = h->nevents++;
-      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 1, ev});
-      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 0, ev});
+      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, SB + 1, ev});
+      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SB, ev});
     }
     (void)pending_rest_ev;
     long long s0g = (long long)h->gtasks.size();
@@ -422,9 +435,27 @@ static void build_plan(spchol_handle* h) {
     h->nslots_total = slot;
     if (h->top_slot < 0) h->top_slot = slot;
   }
-  // the whole tree (single GPU and the solve), then per-rank phase A / phase C for multi-GPU
+  // the whole tree (the solve's structure; the single-GPU factor when nvr == 1), then per-rank
+  // phase A / phase C for multi-GPU
   append_levels(h, [](int) { return true; }, true);
   h->plan_all_end = h->plan.size();
+  h->plan_factor_begin = 0;
+  if (h->world == 1 && h->nvr > 1) {
+    // single GPU, subtree concurrency: proportional map onto nvr virtual ranks; each virtual rank's
+    // subtrees run on their own (critical, trailing) stream pair, the top supernodes after all of
+    // them have joined stream 0
+    std::vector<int> vown;
+    proportional_map(S, work, h->nvr, vown);
+    h->plan_factor_begin = h->plan.size();
+    for (int v = 0; v < h->nvr; ++v) append_levels(h, [&vown, v](int J) { return vown[J] == v; }, false, 2 * v);
+    for (int v = 1; v < h->nvr; ++v) {
+      const int ev = h->nevents++;
+      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 2 * v, ev});
+      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 0, ev});
+    }
+    append_levels(h, [&vown](int J) { return vown[J] < 0; }, false, 0);
+    h->plan_all_end = h->plan.size();
+  }
   if (h->world > 1) {
     const int me = h->rank;
     append_levels(h, [h, me](int J) { return h->owner[J] == me; }, false);
@@ -476,8 +507,14 @@ static int setup_device(spchol_handle* h) {
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));   // numerically lower = higher priority
     h->prio_lo = lo;
     h->prio_hi = hi;
-    CK(cudaStreamCreateWithPriority(&h->side_stream, cudaStreamNonBlocking, lo));
-    CK(cudaStreamCreateWithPriority(&h->crit_stream, cudaStreamNonBlocking, hi));
+    int nstreams = 2;
+    for (const Launch& L : h->plan) nstreams = std::max(nstreams, L.stream + 1);
+    h->pstreams.assign(nstreams, nullptr);
+    h->join_events.assign(nstreams, nullptr);
+    for (int i = 0; i < nstreams; ++i) {
+      CK(cudaStreamCreateWithPriority(&h->pstreams[i], cudaStreamNonBlocking, (i & 1) ? lo : hi));
+      CK(cudaEventCreateWithFlags(&h->join_events[i], cudaEventDisableTiming));
+    }
     CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   }
@@ -550,8 +587,8 @@ static void free_device(spchol_handle* h) {
   for (void* p : ptrs) if (p) cudaFree(p);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : h->plan_events) if (e) cudaEventDestroy(e);
-  if (h->side_stream) cudaStreamDestroy(h->side_stream);
-  if (h->crit_stream) cudaStreamDestroy(h->crit_stream);
+  for (cudaStream_t x : h->pstreams) if (x) cudaStreamDestroy(x);
+  for (cudaEvent_t e : h->join_events) if (e) cudaEventDestroy(e);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
@@ -569,6 +606,7 @@ extern "C" int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* r
   }
   h->rank = h->opt.dist_rank;
   h->world = h->opt.dist_world;
+  h->nvr = h->opt.subtree_streams == 0 ? 4 : std::max(1, std::min(16, (int)h->opt.subtree_streams));
   if (h->opt.block) {
     if (h->opt.block < 8 || h->opt.block > NBMAX || h->opt.block % 8) { delete h; return fail(SPCHOL_ERR_VALIDATION, "block must be a multiple of 8 in [8, 64]"); }
     h->nb = h->opt.block;
@@ -642,15 +680,17 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
   // Both fork from st and join back into it (required under graph capture).  With kernel
   // timing enabled everything runs serialized on st.
   const bool multi = !h->timing;
-  cudaStream_t s0 = multi ? h->crit_stream : st;
-  cudaStream_t s1 = multi ? h->side_stream : st;
+  std::vector<char> used(h->pstreams.size(), 0);
+  for (size_t i = begin; i < end; ++i) used[h->plan[i].stream] = 1;
+  used[0] = 1;
   if (multi) {
     CK(cudaEventRecord(h->ev_fork, st));
-    CK(cudaStreamWaitEvent(s0, h->ev_fork, 0));
+    for (size_t q = 0; q < used.size(); ++q)
+      if (used[q]) CK(cudaStreamWaitEvent(h->pstreams[q], h->ev_fork, 0));
   }
   for (size_t i = begin; i < end; ++i) {
     const Launch& L = h->plan[i];
-    cudaStream_t ls = L.stream == 1 ? s1 : s0;
+    cudaStream_t ls = multi ? h->pstreams[L.stream] : st;
     if (L.op == OP_RECORD) {
       if (multi) CK(cudaEventRecord(h->plan_events[L.ev], ls));
       continue;
@@ -660,7 +700,7 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
       continue;
     }
     size_t ti = tstart((int)i);
-    const int prio = multi ? (L.stream == 1 ? h->prio_lo : h->prio_hi) : 0;
+    const int prio = multi ? ((L.stream & 1) ? h->prio_lo : h->prio_hi) : 0;
     switch (L.kind) {
       case K_SMALL:
         launch_small(h->d_small_sns + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_ucol_base, h->d_ucol_map,
@@ -690,9 +730,12 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
     }
     tstop(ti);
   }
-  if (multi) {
-    CK(cudaEventRecord(h->ev_join, s0));
-    CK(cudaStreamWaitEvent(st, h->ev_join, 0));
+  if (multi) {   // join every stream the range used back into st (required under capture)
+    for (size_t q = 0; q < used.size(); ++q)
+      if (used[q]) {
+        CK(cudaEventRecord(h->join_events[q], h->pstreams[q]));
+        CK(cudaStreamWaitEvent(st, h->join_events[q], 0));
+      }
   }
   CK(cudaGetLastError());
   return SPCHOL_OK;
@@ -736,7 +779,7 @@ static int enqueue_exchange(spchol_handle* h, cudaStream_t st) {
 static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
   int rc = enqueue_init(h, st);
   if (rc) return rc;
-  if (h->world == 1) return enqueue_ops(h, st, 0, h->plan_all_end);
+  if (h->world == 1) return enqueue_ops(h, st, h->plan_factor_begin, h->plan_all_end);
   if (!h->nccl_comm) return fail(SPCHOL_ERR_STATE, "multi-GPU handle without an NCCL communicator (spchol_dist_attach_nccl)");
   if ((rc = enqueue_ops(h, st, h->plan_all_end, h->plan_a_end))) return rc;
   if ((rc = enqueue_exchange(h, st))) return rc;
@@ -1061,7 +1104,7 @@ extern "C" int spchol_factor_phase(spchol_handle* h, int phase) {
     case 1:
       h->factored = false;
       rc = enqueue_init(h, h->stream);
-      if (!rc) rc = enqueue_ops(h, h->stream, h->world == 1 ? 0 : h->plan_all_end, h->world == 1 ? h->plan_all_end : h->plan_a_end);
+      if (!rc) rc = enqueue_ops(h, h->stream, h->world == 1 ? h->plan_factor_begin : h->plan_all_end, h->world == 1 ? h->plan_all_end : h->plan_a_end);
       break;
     case 2:
       if (h->world > 1) rc = enqueue_ops(h, h->stream, h->plan_a_end, h->plan.size());

@@ -583,44 +583,39 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
     if (rr >= c) G[(long long)c * S.ld + rr] = P[e];
   }
   if (t <= 0) return;
-  // U_J in 4x4 register blocks over the lower block triangle of the t x t update
-  const int nbt = (t + 3) >> 2, nblk = nbt * (nbt + 1) / 2;
-  for (int bidx = tid; bidx < nblk; bidx += blockDim.x) {
-    int bi = (int)((sqrtf(8.0f * bidx + 1.0f) - 1.0f) * 0.5f);
-    while (bi * (bi + 1) / 2 > bidx) --bi;
-    while ((bi + 1) * (bi + 2) / 2 <= bidx) ++bi;
-    const int bj = bidx - bi * (bi + 1) / 2;
-    const int r0 = k + 4 * bi, c0 = k + 4 * bj;
-    double acc[4][4];
+  // U_J = L_R L_R^T: a work item is (8-column block cb, row r >= 8 cb); consecutive threads take
+  // consecutive rows of the same column block, so each RED instruction of a warp covers a run of
+  // consecutive U rows of one column = a run of consecutive ancestor rows (coalesced).
+  const int ncb = (t + 7) >> 3;
+  int item = tid, cb = 0, rows_in_cb = t;
+  for (;;) {
+    while (cb < ncb && item >= rows_in_cb) { item -= rows_in_cb; ++cb; rows_in_cb = t - 8 * cb; }
+    if (cb >= ncb) break;
+    const int r = 8 * cb + item;             // U row (panel row k + r)
+    const int c0 = 8 * cb;
+    double acc[8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
     for (int p = 0; p < k; ++p) {
-      double a[4], b[4];
+      const double lr = P[p * m + k + r];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        a[i] = r0 + i < m ? P[p * m + r0 + i] : 0.0;
-        b[i] = c0 + i < m ? P[p * m + c0 + i] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[i][q] += a[i] * b[q];
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int gc = c0 + q;
-      if (gc >= m) continue;
-      const long long cb = ucol_base[S.ucol + gc - k];
-      const long long mb = ucol_map[S.ucol + gc - k];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int gr = r0 + i;
-        if (gr < m && gr >= gc) atomicAdd(panels + cb + posmap[mb + gr], -acc[i][q]);
+      for (int q = 0; q < 8; ++q) {
+        const int c = c0 + q;
+        const double lc = c < t ? P[p * m + k + c] : 0.0;
+        acc[q] += lr * lc;
       }
     }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = c0 + q;
+      if (c >= t || r < c) continue;
+      const long long cbase = ucol_base[S.ucol + c];
+      const long long mbase = ucol_map[S.ucol + c];
+      atomicAdd(panels + cbase + posmap[mbase + k + r], -acc[q]);
+    }
+    item += blockDim.x;
   }
+
 }
 
 // ----------------------------------------------------------------------------------------------

@@ -10,9 +10,10 @@ ap.add_argument("--config", default="C4")
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--block", type=int, default=0)
 ap.add_argument("--nograph", action="store_true")
+ap.add_argument("--vr", type=int, default=0)
 a = ap.parse_args()
 p = gen.make(a.config)
-h = sp.Solver.from_problem(p, block=a.block, use_graph=0 if a.nograph else 1)
+h = sp.Solver.from_problem(p, block=a.block, use_graph=0 if a.nograph else 1, subtree_streams=a.vr)
 F = h.query("FLOPS_EXACT")
 for _ in range(2):
     h.spchol_factor()
@@ -41,7 +42,7 @@ h.spchol_enable_kernel_timing(True)
 for _ in range(a.steps):
     h.spchol_factor_async()
 st = {k: h.spchol_kernel_stats(k) for k in sp.KERNEL_KINDS}
-out = {"lib": os.environ.get("SPCHOL_LIB", "default"), "nograph": a.nograph, "nola": os.environ.get("SPCHOL_NO_LOOKAHEAD"), "config": a.config, "ms": ms, "tflops": F / ms / 1e9,
+out = {"lib": os.environ.get("SPCHOL_LIB", "default"), "nograph": a.nograph, "nola": os.environ.get("SPCHOL_NO_LOOKAHEAD"), "vr": a.vr, "config": a.config, "ms": ms, "tflops": F / ms / 1e9,
        "kernels": {k: {"ms": round(v["ms"] / a.steps, 2), "tf": round(v["flops"] / v["ms"] / 1e9, 2) if v["ms"] else 0}
                    for k, v in st.items() if v["launches"]}}
 print(json.dumps(out), flush=True)

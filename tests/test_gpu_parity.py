@@ -50,6 +50,14 @@ def test_parity_configs(name, small):
     run_parity(gen.make(name), small_max_k=small)
 
 
+@pytest.mark.parametrize("vr", [1, 2, 3, 8])
+@pytest.mark.parametrize("name", ["C1", "S2", "S4", "S5"])
+def test_parity_subtree_streams(name, vr):
+    """Single-GPU subtree concurrency (independent subtrees on their own stream pairs)."""
+    run_parity(gen.make(name), subtree_streams=vr)
+    run_parity(gen.make(name), subtree_streams=vr, small_max_k=-1, use_graph=0)
+
+
 @pytest.mark.parametrize("block", [8, 16, 24, 40])
 def test_parity_block_sizes(block):
     """cdiv block widths that leave ragged block columns (k not a multiple of the block)."""
