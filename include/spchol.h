@@ -179,14 +179,16 @@ int spchol_export_symbolic(const spchol_handle* h, int32_t* post, int32_t* paren
 
 /*
  * Copy the device panels back.  panel_off[NSUPER+1] (doubles; panel J occupies
- * [panel_off[J], panel_off[J+1]), column-major with leading dimension ld[J] >= m_J),
+ * [panel_off[J], panel_off[J] + ld[J] k_J), column-major with leading dimension ld[J] >= m_J; under
+ * multi-GPU the top panels are stored last, so offsets need not increase with J; panel_off[NSUPER]
+ * = PANEL_DOUBLES),
  * ld[NSUPER], panels[PANEL_DOUBLES].  After factor, panel J column c (0 <= c < k_J), row q
  * (c <= q < m_J) holds L(rows(J)[q], sfirst[J] + c); entries inside the panel but outside the
  * exact pattern of L ("padding") are exactly +-0.0.  Synchronizes the stream.
  */
 int spchol_export_panels(const spchol_handle* h, int64_t* panel_off, int32_t* ld, double* panels);
 
-/* Copy panel J (panel_off[J+1]-panel_off[J] doubles, layout as above) to out.  Synchronizes. */
+/* Copy panel J (ld[J] k_J doubles, layout as above) to out.  Synchronizes. */
 int spchol_export_panel(const spchol_handle* h, int32_t J, double* out);
 
 /* diag[j] = L(j,j) for every final column j (n doubles; log det A = 2 sum log diag).
@@ -216,14 +218,17 @@ int spchol_dist_nccl_unique_id(void* out128);
  * collective: every rank must call it).  NCCL is loaded with dlopen (libnccl.so.2). */
 int spchol_dist_attach_nccl(spchol_handle* h, const void* unique_id128);
 /* owner[NSUPER]: rank owning each supernode's subtree, -1 for the top supernodes (all 0 when
- * dist_world == 1); *top_off: first double of the contiguous top-panel region; *top_slot: first
- * diagonal-inverse slot of the top supernodes.  Any pointer may be NULL. */
-int spchol_export_mapping(const spchol_handle* h, int32_t* owner, int64_t* top_off, int64_t* top_slot);
+ * dist_world == 1); top_owner[NSUPER]: the rank that factors each top supernode (-1 otherwise);
+ * *top_off: first double of the contiguous top-panel region; *top_slot: first diagonal-inverse
+ * slot of the top supernodes.  Any pointer may be NULL. */
+int spchol_export_mapping(const spchol_handle* h, int32_t* owner, int32_t* top_owner, int64_t* top_off,
+                          int64_t* top_slot);
 /* Diagnostics (single process standing in for several ranks on one GPU, never a reported result):
- * phase 1 = a1 init + phase A (own subtrees), 2 = phase C (top supernodes), 3 = synchronize,
- * check the pivots and mark the handle factored with its factor complete.  The phase-B exchange is
- * then done by the caller with spchol_dist_debug_accumulate(dst, src, which): dst region += src
- * region, which = 0 top panels, 1 subtree panels, 2 subtree diagonal inverses. */
+ * phase 1 = a1 init + phase A (own subtrees); 1000 + l = this rank's owned top supernodes of top
+ * level l; 3 = synchronize, check the pivots and mark the handle factored with its factor
+ * complete.  The exchanges are done by the caller with spchol_dist_debug_accumulate(dst, src,
+ * which): which = 16 + J: dst's panel of top supernode J += src's, src's copy zeroed (the per-level
+ * fan-in); 1: whole panel arena, 2: all diagonal inverses (the final gather); 0: top region. */
 int spchol_factor_phase(spchol_handle* h, int phase);
 int spchol_dist_debug_accumulate(spchol_handle* dst, const spchol_handle* src, int which);
 

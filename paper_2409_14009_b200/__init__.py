@@ -91,7 +91,7 @@ def lib():
         L.spchol_kernel_trace.argtypes = [vp, i64, ctypes.POINTER(i64), vp, vp, vp, vp]
         L.spchol_dist_nccl_unique_id.argtypes = [vp]
         L.spchol_dist_attach_nccl.argtypes = [vp, vp]
-        L.spchol_export_mapping.argtypes = [vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.spchol_export_mapping.argtypes = [vp, vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.spchol_factor_phase.argtypes = [vp, ctypes.c_int]
         L.spchol_dist_debug_accumulate.argtypes = [vp, vp, ctypes.c_int]
         L.spchol_destroy.argtypes = [vp]
@@ -235,7 +235,8 @@ class Solver:
 
     def spchol_export_panel(self, J):
         off, ld, _ = self.spchol_export_panels(values=False)
-        out = np.empty(int(off[J + 1] - off[J]), np.float64)
+        k = np.diff(self.spchol_export_symbolic()["sfirst"])[J]
+        out = np.empty(int(ld[J]) * int(k), np.float64)
         _check(self._L.spchol_export_panel(self._h, int(J), _vp(out)))
         return out.reshape(-1, int(ld[J])).T if out.size else out.reshape(0, 0)
 
@@ -268,10 +269,13 @@ class Solver:
         buf = ctypes.create_string_buffer(bytes(unique_id), 128)
         _check(self._L.spchol_dist_attach_nccl(self._h, buf))
 
-    def spchol_export_mapping(self):
+    def spchol_export_mapping(self, with_top_owner=False):
         owner = np.empty(self.spchol_query("NSUPER"), np.int32)
+        towner = np.empty(self.spchol_query("NSUPER"), np.int32)
         to, ts = ctypes.c_int64(), ctypes.c_int64()
-        _check(self._L.spchol_export_mapping(self._h, _vp(owner), ctypes.byref(to), ctypes.byref(ts)))
+        _check(self._L.spchol_export_mapping(self._h, _vp(owner), _vp(towner), ctypes.byref(to), ctypes.byref(ts)))
+        if with_top_owner:
+            return owner, towner, int(to.value), int(ts.value)
         return owner, int(to.value), int(ts.value)
 
     def spchol_factor_phase(self, phase):

@@ -28,7 +28,11 @@
 
 using namespace spchol;
 namespace spchol {
-void proportional_map(const Symbolic& S, const std::vector<double>& work, int world, std::vector<int>& owner);
+void proportional_map(const Symbolic& S, const std::vector<double>& work, int world, std::vector<int>& owner,
+                      std::vector<int>* top_lo = nullptr, std::vector<int>* top_hi = nullptr);
+void assign_top_owners(const std::vector<double>& work, const std::vector<int>& owner, const std::vector<int>& lo,
+                       const std::vector<int>& hi, const std::vector<int>& level, int world,
+                       std::vector<int>& top_owner);
 }
 
 namespace {
@@ -55,6 +59,8 @@ typedef int (*nccl_getid_t)(void*);
 struct NcclUid { char internal[128]; };
 typedef int (*nccl_init_t)(void**, int, NcclUid, int);
 typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_reduce_t)(const void*, void*, size_t, int, int, int, void*, cudaStream_t);
+typedef int (*nccl_group_t)();
 typedef int (*nccl_destroy_t)(void*);
 typedef const char* (*nccl_errstr_t)(int);
 struct NcclApi {
@@ -62,6 +68,8 @@ struct NcclApi {
   nccl_getid_t getid = nullptr;
   nccl_init_t init = nullptr;
   nccl_allreduce_t allreduce = nullptr;
+  nccl_reduce_t reduce = nullptr;
+  nccl_group_t group_start = nullptr, group_end = nullptr;
   nccl_destroy_t destroy = nullptr;
   nccl_errstr_t errstr = nullptr;
 };
@@ -75,9 +83,13 @@ bool nccl_load(std::string& err) {
   g_nccl.getid = (nccl_getid_t)dlsym(so, "ncclGetUniqueId");
   g_nccl.init = (nccl_init_t)dlsym(so, "ncclCommInitRank");
   g_nccl.allreduce = (nccl_allreduce_t)dlsym(so, "ncclAllReduce");
+  g_nccl.reduce = (nccl_reduce_t)dlsym(so, "ncclReduce");
+  g_nccl.group_start = (nccl_group_t)dlsym(so, "ncclGroupStart");
+  g_nccl.group_end = (nccl_group_t)dlsym(so, "ncclGroupEnd");
   g_nccl.destroy = (nccl_destroy_t)dlsym(so, "ncclCommDestroy");
   g_nccl.errstr = (nccl_errstr_t)dlsym(so, "ncclGetErrorString");
-  if (!g_nccl.getid || !g_nccl.init || !g_nccl.allreduce || !g_nccl.destroy) { err = "NCCL symbols missing"; return false; }
+  if (!g_nccl.getid || !g_nccl.init || !g_nccl.allreduce || !g_nccl.reduce || !g_nccl.group_start ||
+      !g_nccl.group_end || !g_nccl.destroy) { err = "NCCL symbols missing"; return false; }
   g_nccl.so = so;
   return true;
 }
@@ -87,10 +99,12 @@ int nccl_fail(int r, const char* where) {
 }  // namespace
 
 namespace {
-enum OpType { OP_LAUNCH = 0, OP_RECORD = 1, OP_WAIT = 2 };
+enum OpType { OP_LAUNCH = 0, OP_RECORD = 1, OP_WAIT = 2, OP_TOP_LEVEL = 3 };
 // One step of the factor's launch plan.  OP_LAUNCH: a batched kernel (kind, tasks [off, off+n)) on
 // stream `stream` (0 = critical path: cdiv chain + relind scatter, 1 = trailing updates);
 // OP_RECORD / OP_WAIT: event `ev` recorded on / awaited by `stream` (lookahead fork/join).
+// OP_TOP_LEVEL (multi-GPU phase C): start of top level `aux` — the panels of that level's top
+// supernodes are reduced (NCCL, sum) onto their owner ranks, the other ranks zero their copies.
 struct Launch {
   int kind;
   long long off;   // first task
@@ -138,6 +152,8 @@ struct spchol_handle {
   // of the top panels, C = top supernodes
   int rank = 0, world = 1;
   std::vector<int> owner;              // rank owning each supernode's subtree, -1 = top
+  std::vector<int> top_owner;          // rank factoring each top supernode (fan-in), -1 otherwise
+  std::vector<std::vector<int>> top_by_level;
   long long top_off = -1;              // first double of the contiguous top-panel region
   int top_slot = -1;                   // first inverse slot of the top supernodes
   size_t plan_all_end = 0, plan_a_end = 0, plan_factor_begin = 0;
@@ -216,7 +232,7 @@ static void for_tiles(int rbase, int rend, int cbase, int cend, F emit) {
 // Appends, level by level, the launches for the supernodes J with active(J).  record_solve: also
 // record the solve's step structure (only for the whole-tree plan).
 template <class Active>
-static void append_levels(spchol_handle* h, Active active, bool record_solve, int SB = 0) {
+static void append_levels(spchol_handle* h, Active active, bool record_solve, int SB = 0, bool top_markers = false) {
   const Symbolic& S = h->S;
   const int NB = h->nb, OUTER = spchol_handle::OUTER;
   auto push = [&](int kind, long long off, long long end, double fl, double by) {
@@ -224,6 +240,11 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
   };
   const int lmax = h->max_level >= 0 ? std::min(S.nlevels, h->max_level + 1) : S.nlevels;
   for (int l = 0; l < lmax; ++l) {
+    if (top_markers && !h->top_by_level[l].empty()) {
+      Launch M{0, 0, 0, 0, 0, OP_TOP_LEVEL, SB, -1};
+      M.aux = l;
+      h->plan.push_back(M);
+    }
     const size_t plan_before = h->plan.size();
     // small supernodes of this level: launches on stream 1 (independent of the level's big ones),
     // bucketed by panel size so that each launch's shared memory (sized by its largest panel)
@@ -386,7 +407,14 @@ static void build_plan(spchol_handle* h) {
     h->update_entries += 0.5 * (double)(m - k) * (double)(m - k + 1);
   }
   // subtree-to-GPU mapping (multi-GPU): owner[J] = rank, or -1 for the top (separator) supernodes
-  proportional_map(S, work, h->world, h->owner);
+  {
+    std::vector<int> lo, hi;
+    proportional_map(S, work, h->world, h->owner, &lo, &hi);
+    assign_top_owners(work, h->owner, lo, hi, S.level, h->world, h->top_owner);
+    h->top_by_level.assign(S.nlevels, {});
+    if (h->world > 1)
+      for (int J = 0; J < ns; ++J) if (h->owner[J] < 0) h->top_by_level[S.level[J]].push_back(J);
+  }
   // panel arena: supernodes in order, except that the top supernodes (multi-GPU) come last so
   // their panels form one contiguous region (the NCCL all-reduce of phase B)
   {
@@ -460,7 +488,7 @@ static void build_plan(spchol_handle* h) {
     const int me = h->rank;
     append_levels(h, [h, me](int J) { return h->owner[J] == me; }, false);
     h->plan_a_end = h->plan.size();
-    append_levels(h, [h](int J) { return h->owner[J] < 0; }, false);
+    append_levels(h, [h, me](int J) { return h->owner[J] < 0 && h->top_owner[J] == me; }, false, 0, true);
   } else {
     h->plan_a_end = h->plan.size();
   }
@@ -659,6 +687,30 @@ extern "C" int spchol_set_stream(spchol_handle* h, void* stream) {
 }
 
 // Enqueue the whole factorization on st (no host synchronization).
+// Multi-GPU phase C, start of top level l: every top supernode P of the level has partial panels
+// on all ranks (A's entries on rank 0, contributions of each rank's subtrees and of the top
+// supernodes it factored); they are summed onto P's owner (one NCCL group of reduces), and the
+// other ranks zero their copies so that a final sum all-reduce assembles the factor exactly once.
+// Without a communicator (diagnostics) nothing is exchanged here.
+static int enqueue_top_reduce(spchol_handle* h, cudaStream_t st, int l) {
+  if (!h->nccl_comm) return SPCHOL_OK;
+  int r = g_nccl.group_start();
+  if (r) return nccl_fail(r, "ncclGroupStart");
+  for (int P : h->top_by_level[l]) {
+    const SnInfo& I = h->sn[P];
+    const size_t cnt = (size_t)I.ld * I.k;
+    r = g_nccl.reduce(h->d_panels + I.off, h->d_panels + I.off, cnt, NCCL_FLOAT64, NCCL_SUM, h->top_owner[P],
+                      h->nccl_comm, st);
+    if (r) { g_nccl.group_end(); return nccl_fail(r, "ncclReduce(top panel)"); }
+  }
+  r = g_nccl.group_end();
+  if (r) return nccl_fail(r, "ncclGroupEnd");
+  for (int P : h->top_by_level[l])
+    if (h->top_owner[P] != h->rank)
+      CK(cudaMemsetAsync(h->d_panels + h->sn[P].off, 0, sizeof(double) * (size_t)h->sn[P].ld * h->sn[P].k, st));
+  return SPCHOL_OK;
+}
+
 // Enqueue the plan entries [begin, end) (launches, lookahead fork/join events) on st.
 static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t end) {
   auto tstart = [&](int idx) -> size_t {
@@ -697,6 +749,11 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
     }
     if (L.op == OP_WAIT) {
       if (multi) CK(cudaStreamWaitEvent(ls, h->plan_events[L.ev], 0));
+      continue;
+    }
+    if (L.op == OP_TOP_LEVEL) {
+      int rc = enqueue_top_reduce(h, ls, L.aux);
+      if (rc) return rc;
       continue;
     }
     size_t ti = tstart((int)i);
@@ -763,27 +820,18 @@ static int enqueue_init(spchol_handle* h, cudaStream_t st) {
   return SPCHOL_OK;
 }
 
-// Phase B (multi-GPU): sum the top-panel region over the ranks (each holds its share of A's top
-// entries plus the contributions of its own subtrees), and the failure flags (min).
-static int enqueue_exchange(spchol_handle* h, cudaStream_t st) {
-  if (!h->nccl_comm) return SPCHOL_OK;
-  const size_t cnt = (size_t)(h->panel_doubles - h->top_off);
-  if (cnt) {
-    int r = g_nccl.allreduce(h->d_panels + h->top_off, h->d_panels + h->top_off, cnt, NCCL_FLOAT64, NCCL_SUM,
-                             h->nccl_comm, st);
-    if (r) return nccl_fail(r, "ncclAllReduce(top panels)");
-  }
-  return SPCHOL_OK;
-}
-
 static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
   int rc = enqueue_init(h, st);
   if (rc) return rc;
   if (h->world == 1) return enqueue_ops(h, st, h->plan_factor_begin, h->plan_all_end);
   if (!h->nccl_comm) return fail(SPCHOL_ERR_STATE, "multi-GPU handle without an NCCL communicator (spchol_dist_attach_nccl)");
-  if ((rc = enqueue_ops(h, st, h->plan_all_end, h->plan_a_end))) return rc;
-  if ((rc = enqueue_exchange(h, st))) return rc;
-  if ((rc = enqueue_ops(h, st, h->plan_a_end, h->plan.size()))) return rc;
+  // top diagonal-inverse slots are written by their owners only; zero them so the solve's gather
+  // (a sum over ranks) sees each exactly once
+  if (h->nslots_total > h->top_slot)
+    CK(cudaMemsetAsync(h->d_linv + (size_t)h->top_slot * NBMAX * NBMAX, 0,
+                       sizeof(double) * (size_t)(h->nslots_total - h->top_slot) * NBMAX * NBMAX, st));
+  if ((rc = enqueue_ops(h, st, h->plan_all_end, h->plan_a_end))) return rc;   // phase A: own subtrees
+  if ((rc = enqueue_ops(h, st, h->plan_a_end, h->plan.size()))) return rc;    // phase C: owned tops, per-level reduces
   int r = g_nccl.allreduce(h->d_fail, h->d_fail, 1, NCCL_UINT64, NCCL_MIN, h->nccl_comm, st);
   if (r) return nccl_fail(r, "ncclAllReduce(fail flag)");
   return SPCHOL_OK;
@@ -876,19 +924,19 @@ static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaS
   return SPCHOL_OK;
 }
 
-// Multi-GPU: before the first solve after a factor, every rank receives the whole factor — the
-// subtree panels and their diagonal-block inverses are disjoint across ranks (zero elsewhere), so a
-// sum all-reduce assembles them; the top region is already identical on all ranks.
+// Multi-GPU: before the first solve after a factor, every rank receives the whole factor — each
+// panel and diagonal-block inverse is non-zero on exactly one rank (subtrees on their rank, top
+// supernodes on their owner), so a sum all-reduce assembles them.
 static int gather_factor(spchol_handle* h) {
   if (h->gathered) return SPCHOL_OK;
   if (!h->nccl_comm) return fail(SPCHOL_ERR_STATE, "multi-GPU handle without an NCCL communicator");
   int r = 0;
-  if (h->top_off > 0 && (r = g_nccl.allreduce(h->d_panels, h->d_panels, (size_t)h->top_off, NCCL_FLOAT64, NCCL_SUM,
-                                               h->nccl_comm, h->stream)))
-    return nccl_fail(r, "ncclAllReduce(subtree panels)");
-  if (h->top_slot > 0 && (r = g_nccl.allreduce(h->d_linv, h->d_linv, (size_t)h->top_slot * NBMAX * NBMAX, NCCL_FLOAT64,
-                                                NCCL_SUM, h->nccl_comm, h->stream)))
-    return nccl_fail(r, "ncclAllReduce(subtree inverses)");
+  if (h->panel_doubles > 0 && (r = g_nccl.allreduce(h->d_panels, h->d_panels, (size_t)h->panel_doubles, NCCL_FLOAT64,
+                                                    NCCL_SUM, h->nccl_comm, h->stream)))
+    return nccl_fail(r, "ncclAllReduce(panels)");
+  if (h->nslots_total > 0 && (r = g_nccl.allreduce(h->d_linv, h->d_linv, (size_t)h->nslots_total * NBMAX * NBMAX,
+                                                   NCCL_FLOAT64, NCCL_SUM, h->nccl_comm, h->stream)))
+    return nccl_fail(r, "ncclAllReduce(diagonal inverses)");
   h->gathered = true;
   return SPCHOL_OK;
 }
@@ -1017,8 +1065,8 @@ extern "C" int spchol_export_panel(const spchol_handle* h, int32_t J, double* ou
   if (J < 0 || J >= h->S.nsuper) return fail(SPCHOL_ERR_DIMENSION, "supernode index out of range");
   CK(cudaSetDevice(h->opt.device));
   CK(cudaStreamSynchronize(h->stream));
-  const size_t cnt = (size_t)(h->panel_off[J + 1] - h->panel_off[J]);
-  if (cnt) CK(cudaMemcpy(out, h->d_panels + h->panel_off[J], sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+  const size_t cnt = (size_t)h->sn[J].ld * h->sn[J].k;   // panels need not be in supernode order
+  if (cnt) CK(cudaMemcpy(out, h->d_panels + h->sn[J].off, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
   return SPCHOL_OK;
 }
 
@@ -1086,9 +1134,11 @@ extern "C" int spchol_dist_attach_nccl(spchol_handle* h, const void* unique_id12
   return SPCHOL_OK;
 }
 
-extern "C" int spchol_export_mapping(const spchol_handle* h, int32_t* owner, int64_t* top_off, int64_t* top_slot) {
+extern "C" int spchol_export_mapping(const spchol_handle* h, int32_t* owner, int32_t* top_owner, int64_t* top_off,
+                                     int64_t* top_slot) {
   if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
   if (owner) for (int J = 0; J < h->S.nsuper; ++J) owner[J] = h->world > 1 ? h->owner[J] : 0;
+  if (top_owner) for (int J = 0; J < h->S.nsuper; ++J) top_owner[J] = h->world > 1 ? h->top_owner[J] : -1;
   if (top_off) *top_off = h->top_off;
   if (top_slot) *top_slot = h->top_slot;
   return SPCHOL_OK;
@@ -1104,6 +1154,9 @@ extern "C" int spchol_factor_phase(spchol_handle* h, int phase) {
     case 1:
       h->factored = false;
       rc = enqueue_init(h, h->stream);
+      if (!rc && h->world > 1 && h->nslots_total > h->top_slot)
+        CK(cudaMemsetAsync(h->d_linv + (size_t)h->top_slot * NBMAX * NBMAX, 0,
+                           sizeof(double) * (size_t)(h->nslots_total - h->top_slot) * NBMAX * NBMAX, h->stream));
       if (!rc) rc = enqueue_ops(h, h->stream, h->world == 1 ? h->plan_factor_begin : h->plan_all_end, h->world == 1 ? h->plan_all_end : h->plan_a_end);
       break;
     case 2:
@@ -1113,8 +1166,19 @@ extern "C" int spchol_factor_phase(spchol_handle* h, int phase) {
       rc = spchol_factor_status(h, nullptr, nullptr);
       if (!rc) h->gathered = true;
       break;
-    default:
-      return fail(SPCHOL_ERR_VALIDATION, "phase must be 1, 2 or 3");
+    default: {
+      // 1000 + l: this rank's owned top supernodes of level l (the ops after that level's marker)
+      if (phase < 1000 || h->world == 1) return fail(SPCHOL_ERR_VALIDATION, "phase must be 1, 2, 3 or 1000 + level");
+      const int l = phase - 1000;
+      size_t b = h->plan.size(), e = h->plan.size();
+      for (size_t i = h->plan_a_end; i < h->plan.size(); ++i)
+        if (h->plan[i].op == OP_TOP_LEVEL) {
+          if (h->plan[i].aux == l) b = i + 1;
+          else if (b < e && i > b) { e = i; break; }
+        }
+      if (b < e) rc = enqueue_ops(h, h->stream, b, e);
+      break;
+    }
   }
   return rc;
 }
@@ -1131,9 +1195,21 @@ extern "C" int spchol_dist_debug_accumulate(spchol_handle* dst, const spchol_han
   long long cnt;
   switch (which) {
     case 0: d = dst->d_panels + dst->top_off; sp = src->d_panels + src->top_off; cnt = dst->panel_doubles - dst->top_off; break;
-    case 1: d = dst->d_panels; sp = src->d_panels; cnt = dst->top_off; break;
-    case 2: d = dst->d_linv; sp = src->d_linv; cnt = (long long)dst->top_slot * NBMAX * NBMAX; break;
-    default: return fail(SPCHOL_ERR_VALIDATION, "which must be 0, 1 or 2");
+    case 1: d = dst->d_panels; sp = src->d_panels; cnt = dst->panel_doubles; break;
+    case 2: d = dst->d_linv; sp = src->d_linv; cnt = (long long)dst->nslots_total * NBMAX * NBMAX; break;
+    default:
+      if (which >= 16) {   // 16 + J: fan-in of top supernode J's panel, the source copy is zeroed
+        const int J = which - 16;
+        if (J >= dst->S.nsuper) return fail(SPCHOL_ERR_VALIDATION, "supernode out of range");
+        d = dst->d_panels + dst->sn[J].off;
+        sp = src->d_panels + src->sn[J].off;
+        cnt = (long long)dst->sn[J].ld * dst->sn[J].k;
+        launch_axpy(sp, d, cnt, dst->stream);
+        CK(cudaStreamSynchronize(dst->stream));
+        CK(cudaMemset(src->d_panels + src->sn[J].off, 0, sizeof(double) * (size_t)cnt));
+        return SPCHOL_OK;
+      }
+      return fail(SPCHOL_ERR_VALIDATION, "which must be 0, 1, 2 or 16 + supernode");
   }
   launch_axpy(sp, d, cnt, dst->stream);
   CK(cudaGetLastError());

@@ -14,9 +14,12 @@
 
 namespace spchol {
 
-void proportional_map(const Symbolic& S, const std::vector<double>& work, int world, std::vector<int>& owner) {
+void proportional_map(const Symbolic& S, const std::vector<double>& work, int world, std::vector<int>& owner,
+                      std::vector<int>* top_lo, std::vector<int>* top_hi) {
   const int ns = S.nsuper;
   owner.assign(ns, 0);
+  if (top_lo) top_lo->assign(ns, 0);
+  if (top_hi) top_hi->assign(ns, 0);
   if (world <= 1 || ns == 0) return;
   std::vector<double> sub(work);
   for (int J = 0; J < ns; ++J)
@@ -41,6 +44,8 @@ void proportional_map(const Symbolic& S, const std::vector<double>& work, int wo
     if (it.node < ns) {
       if (P == 1) { subtree_to(it.node, it.lo); continue; }
       owner[it.node] = -1;
+      if (top_lo) (*top_lo)[it.node] = it.lo;
+      if (top_hi) (*top_hi)[it.node] = it.hi;
     }
     std::vector<int> ch = kids[it.node];
     if (ch.empty()) continue;
@@ -77,6 +82,31 @@ void proportional_map(const Symbolic& S, const std::vector<double>& work, int wo
     for (int i = 0; i < nc; ++i) {
       work_list.push_back({ch[i], lo, lo + cnt[i]});
       lo += cnt[i];
+    }
+  }
+}
+
+// Owner rank of every top supernode (fan-in factorization of the top).  The top levels run one
+// after the other (each starts with the reduction of its panels), so the balance that matters is
+// per level: within a level, heaviest first, each top supernode goes to the member of its rank
+// group with the least work in that level.
+void assign_top_owners(const std::vector<double>& work, const std::vector<int>& owner, const std::vector<int>& lo,
+                       const std::vector<int>& hi, const std::vector<int>& level, int world,
+                       std::vector<int>& top_owner) {
+  const int ns = (int)owner.size();
+  top_owner.assign(ns, -1);
+  int nl = 0;
+  for (int J = 0; J < ns; ++J) nl = std::max(nl, level[J] + 1);
+  std::vector<std::vector<int>> by_level(nl);
+  for (int J = 0; J < ns; ++J) if (owner[J] < 0) by_level[level[J]].push_back(J);
+  for (auto& tops : by_level) {
+    std::stable_sort(tops.begin(), tops.end(), [&](int a, int b) { return work[a] > work[b]; });
+    std::vector<double> load(world, 0.0);
+    for (int J : tops) {
+      int best = lo[J];
+      for (int r = lo[J]; r < hi[J]; ++r) if (load[r] < load[best]) best = r;
+      top_owner[J] = best;
+      load[best] += work[J];
     }
   }
 }

@@ -36,7 +36,7 @@ def lower_panel_mask(sym, off, ld, total):
         qi = np.arange(L)
         for c in range(k):
             blk[c] = (qi >= c) & (qi < m)
-        mask[off[J]:off[J + 1]] = blk.ravel()
+        mask[off[J]:off[J] + k * L] = blk.ravel()     # panels need not be stored in supernode order
     return mask
 
 

@@ -84,8 +84,10 @@ def test_mapping_single_process_properties():
     p = gen.make("C1")
     for W in (2, 4, 8):
         with sp.Solver.from_problem(p, device=-1, dist_world=W, dist_rank=W - 1) as h:
-            owner, top_off, top_slot = h.spchol_export_mapping()
+            owner, towner, top_off, top_slot = h.spchol_export_mapping(with_top_owner=True)
             assert (owner < 0).any() and all((owner == r).any() for r in range(W))
+            # every top supernode has an owner rank; subtree supernodes have none
+            assert np.all((towner >= 0) == (owner < 0)) and towner.max() < W
     with sp.Solver.from_problem(p, device=-1) as h:
         owner, top_off, _ = h.spchol_export_mapping()
         assert (owner == 0).all() and top_off == h.query("PANEL_DOUBLES")

@@ -115,11 +115,13 @@ def test_edge_cases():
     run_parity(gen.from_dense_lower(D))
 
 
-@pytest.mark.parametrize("name,world", [("S4", 2), ("S5", 3), ("C1", 2), ("S2", 4), ("T3", 2)])
+@pytest.mark.parametrize("name,world", [("S4", 2), ("S5", 3), ("C1", 2), ("S2", 4), ("T3", 2), ("S4", 8)])
 def test_distributed_dataflow_single_gpu(name, world):
-    """The multi-GPU data flow (phase A per rank, phase-B sum of the top panels, phase C, gather)
-    played by `world` handles on one GPU through the diagnostics API; NCCL is replaced by the
-    accumulate call.  The assembled factor must match the oracle like the single-GPU one."""
+    """The multi-GPU data flow played by `world` handles on one GPU through the diagnostics API:
+    phase A per rank; then per top level, the fan-in of every top panel onto its owner (NCCL
+    reduce in production, the accumulate call here, source copies zeroed) and each rank's owned
+    top supernodes; finally the gather (sum of all arenas and inverses).  The assembled factor must
+    match the oracle like the single-GPU one."""
     prob = gen.make(name)
     o = oracle.Oracle.from_problem(prob)
     assert o.factor() == -1
@@ -128,18 +130,29 @@ def test_distributed_dataflow_single_gpu(name, world):
     try:
         for h in hs:
             h.spchol_factor_phase(1)
+        owner, towner, _, _ = hs[0].spchol_export_mapping(with_top_owner=True)
+        level = hs[0].spchol_export_symbolic()["level"]
+        assert np.all((owner >= 0) | (towner >= 0))
+        for l in sorted(set(level[owner < 0].tolist())):
+            for P in np.where((owner < 0) & (level == l))[0]:
+                dst = int(towner[P])
+                for r in range(world):
+                    if r != dst:
+                        hs[dst].spchol_dist_debug_accumulate(hs[r], 16 + int(P))
+            for h in hs:
+                h.spchol_factor_phase(1000 + l)
         for h in hs[1:]:
-            hs[0].spchol_dist_debug_accumulate(h, 0)      # phase B: top panels summed
-        hs[0].spchol_factor_phase(2)                       # phase C
-        for h in hs[1:]:
-            hs[0].spchol_dist_debug_accumulate(h, 1)      # gather subtree panels
-            hs[0].spchol_dist_debug_accumulate(h, 2)      # and their diagonal inverses
+            hs[0].spchol_dist_debug_accumulate(h, 1)      # gather panels
+            hs[0].spchol_dist_debug_accumulate(h, 2)      # and diagonal inverses
         hs[0].spchol_factor_phase(3)
         s_gpu = hs[0].spchol_export_symbolic()
         off, ld, pan = hs[0].spchol_export_panels()
         idx = panel_index_of_pattern(s_gpu, off, ld, Lp, Li)
         err = np.abs(pan[idx] - Lx).max() / np.abs(Lx).max()
         assert err <= TOL_L, err
+        mask = lower_panel_mask(s_gpu, off, ld, len(pan))
+        mask[idx] = False
+        assert np.all(pan[mask] == 0.0)
         xs, b = gen.rhs(prob)
         x = hs[0].spchol_solve(b)
         assert backward_error(prob, x, b) <= TOL_BERR
