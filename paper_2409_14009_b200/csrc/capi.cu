@@ -133,7 +133,7 @@ struct spchol_handle {
   Symbolic S;
   spchol_options opt{};
   int nb = NBMAX;
-  static constexpr int OUTER = 4;   // outer block = OUTER inner blocks
+  int outer = 4;                    // outer block = outer inner blocks (SPCHOL_OUTER, diagnostics)
   cudaStream_t stream = nullptr, own_stream = nullptr;
   // host plan
   std::vector<SnInfo> sn;
@@ -234,7 +234,7 @@ static void for_tiles(int rbase, int rend, int cbase, int cend, F emit) {
 template <class Active>
 static void append_levels(spchol_handle* h, Active active, bool record_solve, int SB = 0, bool top_markers = false) {
   const Symbolic& S = h->S;
-  const int NB = h->nb, OUTER = spchol_handle::OUTER;
+  const int NB = h->nb, OUTER = h->outer;
   auto push = [&](int kind, long long off, long long end, double fl, double by) {
     if (end > off) h->plan.push_back(Launch{kind, off, (int)(end - off), fl, by, OP_LAUNCH, SB, -1});
   };
@@ -645,6 +645,7 @@ extern "C" int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* r
   if (const char* e = getenv("SPCHOL_NO_LOOKAHEAD")) h->no_lookahead = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_MAX_LEVEL")) h->max_level = atoi(e);
   if (const char* e = getenv("SPCHOL_TMA")) h->use_tma = atoi(e) != 0;
+  if (const char* e = getenv("SPCHOL_OUTER")) h->outer = std::max(1, atoi(e));
   build_plan(h);
   if (h->opt.device < 0) { *out = h; return SPCHOL_OK; }   // host-only analysis (no device state)
   rc = setup_device(h);
