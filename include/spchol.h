@@ -64,6 +64,10 @@ typedef struct {
                            virtual ranks) are factored concurrently on their own stream pairs, the
                            top supernodes after they join.  0 = default (4), 1 = one level-set
                            schedule for the whole tree. */
+  int32_t update_mode;  /* 0 = RL (default): U_J formed in 64x64 tiles and scattered through relind
+                           (P:307).  1 = RLB: per block pair (B, B') of
+                           J's rows, L_{B',B} of B's ancestor updated directly (one relindB per
+                           block).  Same factor; RLB has more, smaller tiles on this hardware. */
 } spchol_options;
 
 /* Fill *opt with the defaults above. */
@@ -157,7 +161,8 @@ enum {
   SPCHOL_Q_FLOPS_EXACT = 12, /* sum_j cc_j^2 (the metric's flop count)                     */
   SPCHOL_Q_FLOPS_EXEC = 13,  /* flops of the supernodal algorithm incl. padding             */
   SPCHOL_Q_LAUNCHES = 14,    /* kernels launched by one factor                              */
-  SPCHOL_Q_UPDATE_ENTRIES = 15 /* sum_J t_J (t_J+1)/2 scattered update entries              */
+  SPCHOL_Q_UPDATE_ENTRIES = 15, /* sum_J t_J (t_J+1)/2 scattered update entries             */
+  SPCHOL_Q_NBLOCKS = 16       /* RLB blocks over all supernodes                   */
 };
 int spchol_query(const spchol_handle* h, int key, int64_t* value);
 
@@ -176,6 +181,15 @@ int spchol_export_symbolic(const spchol_handle* h, int32_t* post, int32_t* paren
                            int32_t* sparent, int64_t* rows_ptr, int32_t* rows, int64_t* rel_ptr,
                            int32_t* rel_anc, int32_t* rel_q0, int64_t* rel_off, int32_t* relind,
                            int32_t* parent_final, int32_t* cc_final, int32_t* level);
+
+/*
+ * RLB block structure: blk_ptr[NSUPER+1]; for each block b of supernode J
+ * (blk_ptr[J] <= b < blk_ptr[J+1]): blk_q[b] = position in rows(J) of its first row, blk_len[b]
+ * rows (consecutive global rows), blk_anc[b] = the ancestor supernode whose columns contain them,
+ * blk_relind[b] = relindB = m_P - 1 - position of the first row in rows(P).  NBLOCKS entries.
+ */
+int spchol_export_blocks(const spchol_handle* h, int64_t* blk_ptr, int32_t* blk_q, int32_t* blk_len,
+                         int32_t* blk_anc, int32_t* blk_relind);
 
 /*
  * Copy the device panels back.  panel_off[NSUPER+1] (doubles; panel J occupies
@@ -198,7 +212,8 @@ int spchol_export_diagonal(spchol_handle* h, double* diag);
 /* Kernel timing (CUDA events bracketing every launch of each kernel class on the handle's
  * stream while enabled; disabled by default and incompatible with graph replay, which is
  * bypassed while enabled).  kind: 0 = fused small-supernode kernel, 1 = POTRF, 2 = TRSM,
- * 3 = in-panel update GEMM, 4 = SYRK/GEMM + relind scatter (U_J), 5 = panel init.
+ * 3 = in-panel update GEMM, 4 = SYRK/GEMM + relind scatter (U_J), 5 = panel init, 6 = RLB
+ * block-pair updates.
  * Returns launches, summed milliseconds, algorithmic flops and bytes of that class since the last
  * reset.  spchol_kernel_stats synchronizes the stream. */
 int spchol_enable_kernel_timing(spchol_handle* h, int enable);

@@ -40,7 +40,7 @@ def lib():
         L.orc_free.argtypes = [ctypes.c_void_p]
         for nm, t in [("n", ctypes.c_int64), ("nnzL", ctypes.c_int64), ("flops", ctypes.c_double),
                       ("nfund", ctypes.c_int32), ("added", ctypes.c_int64), ("nmerges", ctypes.c_int32),
-                      ("nsuper", ctypes.c_int32), ("npairs", ctypes.c_int64)]:
+                      ("nsuper", ctypes.c_int32), ("npairs", ctypes.c_int64), ("nblocks", ctypes.c_int64)]:
             f = getattr(L, "orc_get_" + nm)
             f.restype = t
             f.argtypes = [ctypes.c_void_p]
@@ -49,7 +49,8 @@ def lib():
                       ("perm_final", _I32), ("o7", _I32), ("sfirst", _I32), ("sparent", _I32),
                       ("rows_ptr", _I64), ("rows", _I32), ("rel_ptr", _I64), ("rel_anc", _I32),
                       ("rel_q0", _I32), ("rel_off", _I64), ("relind", _I32), ("parent_final", _I32),
-                      ("cc_final", _I32), ("Lp", _I64), ("Li", _I32), ("Lx", _F64)]:
+                      ("cc_final", _I32), ("Lp", _I64), ("Li", _I32), ("Lx", _F64), ("blk_ptr", _I64),
+                      ("blk_q", _I32), ("blk_len", _I32), ("blk_anc", _I32), ("blk_relind", _I32)]:
             f = getattr(L, "orc_ptr_" + nm)
             f.restype = t
             f.argtypes = [ctypes.c_void_p]
@@ -110,6 +111,7 @@ class Oracle:
     added = property(lambda s: int(s._get("added")))
     nmerges = property(lambda s: int(s._get("nmerges")))
     npairs = property(lambda s: int(s._get("npairs")))
+    nblocks = property(lambda s: int(s._get("nblocks")))
 
     def symbolic(self):
         """All integer symbolic arrays (the bit-exact contract)."""
@@ -128,6 +130,10 @@ class Oracle:
         )
         d["rows"] = self._arr("rows", d["rows_ptr"][-1], np.int32)
         d["relind"] = self._arr("relind", d["rel_off"][-1], np.int32)
+        nbk = self.nblocks
+        d["blk_ptr"] = self._arr("blk_ptr", ns + 1, np.int64)
+        for nmk in ("blk_q", "blk_len", "blk_anc", "blk_relind"):
+            d[nmk] = self._arr(nmk, nbk, np.int32)
         nm = self.nmerges
         d["merges"] = list(zip(self._arr("merge_child", nm, np.int32).tolist(),
                                self._arr("merge_parent", nm, np.int32).tolist(),

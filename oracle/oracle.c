@@ -25,6 +25,10 @@
  *                         for the rows of J that are >= f_P ("distance from the bottom")
  *   O9 numeric            scalar left-looking column Cholesky of C_f = P_f A P_f^T on its exact
  *                         structure (A = L L^T); the unique Cholesky factor.
+ *   O8b RLB blocks        for each J, the rows below cols(J) split into maximal runs of consecutive
+ *                         global rows lying in one ancestor's column range; per block:
+ *                         first row position q in rows(J), length, ancestor P, relindB =
+ *                         m_P - 1 - position of the block's first row in rows(P)
  *   O10 solve             L y = P_f b, L^T z = y, x = P_f^T z  ("triangular factors are used
  *                         to compute the solution")
  */
@@ -62,6 +66,12 @@ typedef struct {
   int64_t* rel_off;    /* per pair: offset into relind */
   int64_t npairs;
   int32_t* relind;
+  int64_t nblocks;
+  int64_t* blk_ptr;    /* [nsuper+1] blocks of J */
+  int32_t* blk_q;      /* first row position in rows(J) */
+  int32_t* blk_len;
+  int32_t* blk_anc;
+  int32_t* blk_relind; /* relindB: m_P - 1 - position of the first row in rows(P) */
   int32_t* parent_final; /* exact etree in final numbering */
   int32_t* cc_final;
   /* exact structure of L in final numbering (only when requested) */
@@ -485,6 +495,44 @@ orc_t* orc_symbolic(int64_t n, const int64_t* Ap, const int32_t* Ai, const doubl
     o->rel_off[np] = ri;
     free(indmap); free(snode);
   }
+  /* O8b RLB blocks: maximal runs of consecutive global rows of R_J inside one ancestor */
+  {
+    int32_t ns = o->nsuper;
+    int32_t* snode = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    for (int32_t s2 = 0; s2 < ns; ++s2) for (int32_t c = o->sfirst[s2]; c < o->sfirst[s2 + 1]; ++c) snode[c] = s2;
+    o->blk_ptr = (int64_t*)calloc((size_t)ns + 1, sizeof(int64_t));
+    int64_t nb = 0;
+    for (int32_t J = 0; J < ns; ++J) {
+      int64_t k = o->sfirst[J + 1] - o->sfirst[J], m = o->rows_ptr[J + 1] - o->rows_ptr[J];
+      const int32_t* r = o->rows + o->rows_ptr[J];
+      for (int64_t q = k; q < m; ++q)
+        if (q == k || r[q] != r[q - 1] + 1 || snode[r[q]] != snode[r[q - 1]]) nb++;
+      o->blk_ptr[J + 1] = nb;
+    }
+    o->nblocks = nb;
+    o->blk_q = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nb ? nb : 1));
+    o->blk_len = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nb ? nb : 1));
+    o->blk_anc = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nb ? nb : 1));
+    o->blk_relind = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nb ? nb : 1));
+    int64_t b = 0;
+    for (int32_t J = 0; J < ns; ++J) {
+      int64_t k = o->sfirst[J + 1] - o->sfirst[J], m = o->rows_ptr[J + 1] - o->rows_ptr[J];
+      const int32_t* r = o->rows + o->rows_ptr[J];
+      for (int64_t q = k; q < m; ++q) {
+        if (q == k || r[q] != r[q - 1] + 1 || snode[r[q]] != snode[r[q - 1]]) {
+          int32_t P = snode[r[q]];
+          int64_t mP = o->rows_ptr[P + 1] - o->rows_ptr[P];
+          const int32_t* rP = o->rows + o->rows_ptr[P];
+          int64_t pos = 0;
+          while (rP[pos] != r[q]) ++pos;                 /* linear search: plain and obvious */
+          o->blk_q[b] = (int32_t)q; o->blk_len[b] = 0; o->blk_anc[b] = P; o->blk_relind[b] = (int32_t)(mP - 1 - pos);
+          ++b;
+        }
+        o->blk_len[b - 1]++;
+      }
+    }
+    free(snode);
+  }
   if (keep_L) {
     /* exact structure of L for C_f = P_f A P_f^T, plus the permuted values */
     permute_lower(n, Ap, Ai, Ax, o->perm_final, &o->Cp, &o->Ci, Ax ? &o->Cx : NULL);
@@ -574,6 +622,7 @@ void orc_free(orc_t* o) {
   free(o->merge_child); free(o->merge_parent); free(o->merge_cost);
   free(o->perm_final); free(o->o7); free(o->sfirst); free(o->sparent); free(o->rows_ptr); free(o->rows);
   free(o->rel_ptr); free(o->rel_anc); free(o->rel_q0); free(o->rel_off); free(o->relind);
+  free(o->blk_ptr); free(o->blk_q); free(o->blk_len); free(o->blk_anc); free(o->blk_relind);
   free(o->parent_final); free(o->cc_final); free(o->Lp); free(o->Li); free(o->Lx);
   free(o->Cp); free(o->Ci); free(o->Cx);
   free(o);
@@ -582,11 +631,12 @@ void orc_free(orc_t* o) {
 /* ---------------- accessors (for the ctypes wrapper) ---------------- */
 #define GET(name, type) type orc_get_##name(const orc_t* o) { return o->name; }
 GET(n, int64_t) GET(nnzL, int64_t) GET(flops, double) GET(nfund, int32_t) GET(added, int64_t)
-GET(nmerges, int32_t) GET(nsuper, int32_t) GET(npairs, int64_t)
+GET(nmerges, int32_t) GET(nsuper, int32_t) GET(npairs, int64_t) GET(nblocks, int64_t)
 #define PTR(name, type) type* orc_ptr_##name(const orc_t* o) { return o->name; }
 PTR(post, int32_t) PTR(parent3, int32_t) PTR(cc3, int32_t) PTR(ffirst, int32_t) PTR(fparent, int32_t)
 PTR(fgroup, int32_t) PTR(merge_child, int32_t) PTR(merge_parent, int32_t) PTR(merge_cost, int64_t)
 PTR(perm_final, int32_t) PTR(o7, int32_t) PTR(sfirst, int32_t) PTR(sparent, int32_t) PTR(rows_ptr, int64_t)
 PTR(rows, int32_t) PTR(rel_ptr, int64_t) PTR(rel_anc, int32_t) PTR(rel_q0, int32_t) PTR(rel_off, int64_t)
 PTR(relind, int32_t) PTR(parent_final, int32_t) PTR(cc_final, int32_t) PTR(Lp, int64_t) PTR(Li, int32_t)
-PTR(Lx, double)
+PTR(Lx, double) PTR(blk_ptr, int64_t) PTR(blk_q, int32_t) PTR(blk_len, int32_t) PTR(blk_anc, int32_t)
+PTR(blk_relind, int32_t)

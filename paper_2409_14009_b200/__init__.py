@@ -27,15 +27,15 @@ SPCHOL_ERR_STATE = -7
 
 Q = dict(N=0, NNZ_A=1, NNZ_L=2, NFUND=3, NSUPER=4, ADDED=5, NLEVELS=6, ROWS_LEN=7, NPAIRS=8,
          RELIND_LEN=9, PANEL_DOUBLES=10, NMERGES=11, FLOPS_EXACT=12, FLOPS_EXEC=13, LAUNCHES=14,
-         UPDATE_ENTRIES=15)
-KERNEL_KINDS = dict(small=0, potrf=1, trsm=2, local_update=3, syrk_scatter=4, init=5)
+         UPDATE_ENTRIES=15, NBLOCKS=16)
+KERNEL_KINDS = dict(small=0, potrf=1, trsm=2, local_update=3, syrk_scatter=4, init=5, rlb_update=6)
 
 # Every symbol include/spchol.h declares (checked by tests/test_capi_exports.py).
 EXPORTS = [
     "spchol_default_options", "spchol_analyze", "spchol_set_values", "spchol_set_values_device",
     "spchol_set_stream", "spchol_factor_async", "spchol_factor_status", "spchol_factor",
     "spchol_solve", "spchol_solve_device", "spchol_query", "spchol_export_symbolic",
-    "spchol_export_panels", "spchol_export_panel", "spchol_export_diagonal", "spchol_enable_kernel_timing", "spchol_kernel_stats",
+    "spchol_export_blocks", "spchol_export_panels", "spchol_export_panel", "spchol_export_diagonal", "spchol_enable_kernel_timing", "spchol_kernel_stats",
     "spchol_kernel_trace", "spchol_dist_nccl_unique_id", "spchol_dist_attach_nccl", "spchol_export_mapping",
     "spchol_factor_phase", "spchol_dist_debug_accumulate", "spchol_destroy", "spchol_last_error",
 ]
@@ -45,7 +45,7 @@ class spchol_options(ctypes.Structure):
     _fields_ = [("merge_cap", ctypes.c_double), ("device", ctypes.c_int32), ("block", ctypes.c_int32),
                 ("small_max_k", ctypes.c_int32), ("use_graph", ctypes.c_int32),
                 ("dist_rank", ctypes.c_int32), ("dist_world", ctypes.c_int32),
-                ("subtree_streams", ctypes.c_int32)]
+                ("subtree_streams", ctypes.c_int32), ("update_mode", ctypes.c_int32)]
 
 
 class SpcholError(RuntimeError):
@@ -83,6 +83,7 @@ def lib():
         L.spchol_query.argtypes = [vp, ctypes.c_int, ctypes.POINTER(i64)]
         L.spchol_export_symbolic.argtypes = [vp] * 19
         L.spchol_export_panels.argtypes = [vp, vp, vp, vp]
+        L.spchol_export_blocks.argtypes = [vp] * 6
         L.spchol_export_panel.argtypes = [vp, i32, vp]
         L.spchol_export_diagonal.argtypes = [vp, vp]
         L.spchol_enable_kernel_timing.argtypes = [vp, ctypes.c_int]
@@ -223,6 +224,14 @@ class Solver:
         order = ["post", "parent3", "cc3", "ffirst", "fgroup", "perm_final", "sfirst", "sparent", "rows_ptr",
                  "rows", "rel_ptr", "rel_anc", "rel_q0", "rel_off", "relind", "parent_final", "cc_final", "level"]
         _check(self._L.spchol_export_symbolic(self._h, *[_vp(d[k]) for k in order]))
+        return d
+
+    def spchol_export_blocks(self):
+        ns, nb = self.spchol_query("NSUPER"), self.spchol_query("NBLOCKS")
+        d = dict(blk_ptr=np.empty(ns + 1, np.int64), blk_q=np.empty(nb, np.int32), blk_len=np.empty(nb, np.int32),
+                 blk_anc=np.empty(nb, np.int32), blk_relind=np.empty(nb, np.int32))
+        _check(self._L.spchol_export_blocks(self._h, *[_vp(d[k]) for k in ("blk_ptr", "blk_q", "blk_len", "blk_anc",
+                                                                             "blk_relind")]))
         return d
 
     def spchol_export_panels(self, values=True):

@@ -418,6 +418,30 @@ int analyze_symbolic(int64_t n, const int64_t* colptr, const int32_t* rowidx, co
       }
     }
   }
+  // ---- RLB blocks from the relind pairs: inside a pair's tail, a block breaks where the global
+  // row is not the previous one + 1 (rows(P) positions then jump) or where the next pair starts
+  {
+    S.blk_ptr.assign(ns + 1, 0);
+    S.blk_q.clear(); S.blk_len.clear(); S.blk_anc.clear(); S.blk_relind.clear();
+    for (int32_t J = 0; J < ns; ++J) {
+      const int32_t* rJ = S.rows.data() + S.rows_ptr[J];
+      const int64_t m = S.rows_ptr[J + 1] - S.rows_ptr[J];
+      for (int64_t x = S.rel_ptr[J]; x < S.rel_ptr[J + 1]; ++x) {
+        const int64_t qend = x + 1 < S.rel_ptr[J + 1] ? S.rel_q0[x + 1] : m;   // rows of this ancestor
+        for (int64_t qq = S.rel_q0[x]; qq < qend; ++qq) {
+          const int32_t rel = S.relind[S.rel_off[x] + (qq - S.rel_q0[x])];
+          if (qq == S.rel_q0[x] || rJ[qq] != rJ[qq - 1] + 1) {
+            S.blk_q.push_back((int32_t)qq);
+            S.blk_len.push_back(0);
+            S.blk_anc.push_back(S.rel_anc[x]);
+            S.blk_relind.push_back(rel);
+          }
+          S.blk_len.back()++;
+        }
+      }
+      S.blk_ptr[J + 1] = (int64_t)S.blk_q.size();
+    }
+  }
   // ---- A entry -> (final column, position in rows(J))
   S.a_col.assign(S.nnzA, 0); S.a_pos.assign(S.nnzA, 0);
   {

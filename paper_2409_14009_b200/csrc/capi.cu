@@ -48,7 +48,7 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call);    \
   } while (0)
 
-enum LaunchKind { K_SMALL = 0, K_POTRF = 1, K_TRSM = 2, K_LOCAL = 3, K_SCATTER = 4, K_INIT = 5, K_NKINDS = 6 };
+enum LaunchKind { K_SMALL = 0, K_POTRF = 1, K_TRSM = 2, K_LOCAL = 3, K_SCATTER = 4, K_INIT = 5, K_RLB = 6, K_NKINDS = 7 };
 }  // namespace
 
 // ------------------------------------------------------------------------------------- NCCL
@@ -139,6 +139,7 @@ struct spchol_handle {
   std::vector<SnInfo> sn;
   std::vector<Launch> plan;
   std::vector<GTask> gtasks;
+  std::vector<RTask> rtasks;            // RLB block-pair tiles (update_mode 1)
   std::vector<PTask> ptasks;
   std::vector<int> level_sns, level_off;
   std::vector<int> small_sns;           // supernodes handled by the fused small kernel, by level
@@ -176,6 +177,7 @@ struct spchol_handle {
   int *d_small_sns = nullptr, *d_posmap = nullptr, *d_sfirst = nullptr, *d_rows = nullptr, *d_perm = nullptr, *d_level_sns = nullptr;
   SnInfo* d_sn = nullptr;
   GTask* d_gtasks = nullptr;
+  RTask* d_rtasks = nullptr;
   PTask* d_ptasks = nullptr;
   unsigned long long* d_fail = nullptr;
   bool values_set = false, factored = false;
@@ -206,6 +208,7 @@ extern "C" void spchol_default_options(spchol_options* o) {
   o->dist_rank = 0;
   o->dist_world = 1;
   o->subtree_streams = 0;
+  o->update_mode = 0;
 }
 
 extern "C" const char* spchol_last_error(void) { return g_err.c_str(); }
@@ -371,6 +374,49 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SB, ev});
     }
     (void)pending_rest_ev;
+    if (h->opt.update_mode == 1) {
+      // RLB: per supernode, every block pair (B above-or-equal B') updates L_{B',B} of
+      // B's ancestor directly; tiles = aligned 64-row windows intersected with the block pair
+      long long r0t = (long long)h->rtasks.size();
+      double fr2 = 0, br2 = 0;
+      for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
+        const int J = h->level_sns[x];
+        if (h->is_small[J] || !active(J)) continue;
+        const SnInfo& I = h->sn[J];
+        const int t = I.m - I.k;
+        if (t <= 0) continue;
+        const int base = I.k & ~1;
+        const int* rJ = S.rows.data() + S.rows_ptr[J];
+        for (long long b = S.blk_ptr[J]; b < S.blk_ptr[J + 1]; ++b) {
+          const int P = S.blk_anc[b], qB = S.blk_q[b], nB = S.blk_len[b];
+          const SnInfo& IP = h->sn[P];
+          long long pr = S.rel_ptr[J];     // the (J, P) relind pair
+          while (S.rel_anc[pr] != P) ++pr;
+          const long long colP = rJ[qB] - S.sfirst[P];
+          for (long long b2 = b; b2 < S.blk_ptr[J + 1]; ++b2) {
+            const int qB2 = S.blk_q[b2], nB2 = S.blk_len[b2];
+            const int posP = IP.m - 1 - S.relind[S.rel_off[pr] + (qB2 - S.rel_q0[pr])];
+            const int wr0 = base + ((qB2 - base) / TILE) * TILE, wc0 = base + ((qB - base) / TILE) * TILE;
+            for (int Ra = wr0; Ra < qB2 + nB2; Ra += TILE)
+              for (int Rb = wc0; Rb < qB + nB; Rb += TILE) {
+                const int i0 = std::max(qB2, Ra) - Ra, i1 = std::min(qB2 + nB2, Ra + TILE) - Ra;
+                const int j0 = std::max(qB, Rb) - Rb, j1 = std::min(qB + nB, Rb + TILE) - Rb;
+                const bool diag = b2 == b;
+                if (diag && Ra + i1 - 1 < Rb + j0) continue;      // entirely above the diagonal
+                RTask T{J, Ra, Rb, i0, i1, j0, j1, diag ? 1 : 0,
+                        IP.off + (colP + (Rb + j0 - qB)) * IP.ld + posP + (Ra + i0 - qB2), IP.ld, 0};
+                h->rtasks.push_back(T);
+              }
+          }
+        }
+        fr2 += (double)I.k * t * (t + 1);
+        br2 += 8.0 * (double)t * I.k + 16.0 * 0.5 * t * (t + 1.0);
+      }
+      if ((long long)h->rtasks.size() > r0t)
+        h->plan.push_back(Launch{K_RLB, r0t, (int)((long long)h->rtasks.size() - r0t), fr2, br2, OP_LAUNCH, SB, -1});
+      h->plan_level.resize(h->plan.size(), l);
+      continue;
+    }
     long long s0g = (long long)h->gtasks.size();
     double fs = 0, bs = 0;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
@@ -557,6 +603,7 @@ static int setup_device(spchol_handle* h) {
   CK(upload(&h->d_sn, h->sn));
   CK(upload(&h->d_sfirst, S.sfirst));
   CK(upload(&h->d_gtasks, h->gtasks));
+  CK(upload(&h->d_rtasks, h->rtasks));
   CK(upload(&h->d_ptasks, h->ptasks));
   CK(dalloc(&h->d_linv, (size_t)std::max(1, h->nslots_total) * NBMAX * NBMAX));
   if (h->use_tma) {
@@ -609,7 +656,7 @@ static void free_device(spchol_handle* h) {
   if (h->solve_graph) cudaGraphDestroy(h->solve_graph);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->graph) cudaGraphDestroy(h->graph);
-  void* ptrs[] = {h->d_tmaps, h->d_tmap_linv, h->d_small_sns, h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
+  void* ptrs[] = {h->d_rtasks, h->d_tmaps, h->d_tmap_linv, h->d_small_sns, h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
                   h->d_rows_ptr, h->d_posmap, h->d_sfirst, h->d_rows, h->d_perm, h->d_level_sns, h->d_sn,
                   h->d_gtasks, h->d_ptasks, h->d_fail};
   for (void* p : ptrs) if (p) cudaFree(p);
@@ -628,6 +675,7 @@ extern "C" int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* r
   *out = nullptr;
   spchol_handle* h = new spchol_handle();
   if (opt) h->opt = *opt; else spchol_default_options(&h->opt);
+  if (h->opt.update_mode < 0 || h->opt.update_mode > 1) { delete h; return fail(SPCHOL_ERR_VALIDATION, "update_mode must be 0 (RL) or 1 (RLB)"); }
   if (h->opt.dist_world < 1 || h->opt.dist_rank < 0 || h->opt.dist_rank >= h->opt.dist_world) {
     delete h;
     return fail(SPCHOL_ERR_VALIDATION, "need 0 <= dist_rank < dist_world");
@@ -760,6 +808,9 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
     size_t ti = tstart((int)i);
     const int prio = multi ? ((L.stream & 1) ? h->prio_lo : h->prio_hi) : 0;
     switch (L.kind) {
+      case K_RLB:
+        launch_rlb(h->d_rtasks + L.off, L.n, h->d_sn, h->d_panels, ls, prio);
+        break;
       case K_SMALL:
         launch_small(h->d_small_sns + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_ucol_base, h->d_ucol_map,
                      h->d_posmap, h->d_fail, L.aux, L.aux2, ls, prio);
@@ -1013,13 +1064,16 @@ extern "C" int spchol_query(const spchol_handle* h, int key, int64_t* value) {
     case SPCHOL_Q_NMERGES: *value = S.nmerges; break;
     case SPCHOL_Q_FLOPS_EXACT: *value = (int64_t)S.flops_exact; break;
     case SPCHOL_Q_FLOPS_EXEC: *value = (int64_t)h->flops_exec; break;
-    case SPCHOL_Q_LAUNCHES: {
+    case SPCHOL_Q_LAUNCHES: {   // kernels one factor launches (init + the executed plan range)
       int64_t nl = 1;
-      for (const Launch& L : h->plan) nl += L.op == OP_LAUNCH;
+      const size_t b = h->world == 1 ? h->plan_factor_begin : h->plan_all_end;
+      const size_t e = h->world == 1 ? h->plan_all_end : h->plan.size();
+      for (size_t i = b; i < e; ++i) nl += h->plan[i].op == OP_LAUNCH;
       *value = nl;
       break;
     }
     case SPCHOL_Q_UPDATE_ENTRIES: *value = (int64_t)h->update_entries; break;
+    case SPCHOL_Q_NBLOCKS: *value = (int64_t)S.blk_q.size(); break;
     default: return fail(SPCHOL_ERR_VALIDATION, "unknown query key");
   }
   return SPCHOL_OK;
@@ -1040,6 +1094,15 @@ extern "C" int spchol_export_symbolic(const spchol_handle* h, int32_t* post, int
   cp<int64_t>(rows_ptr, S.rows_ptr); cp(rows, S.rows); cp<int64_t>(rel_ptr, S.rel_ptr); cp(rel_anc, S.rel_anc);
   cp(rel_q0, S.rel_q0); cp<int64_t>(rel_off, S.rel_off); cp(relind, S.relind); cp(parent_final, S.parent_final);
   cp(cc_final, S.cc_final); cp(level, S.level);
+  return SPCHOL_OK;
+}
+
+extern "C" int spchol_export_blocks(const spchol_handle* h, int64_t* blk_ptr, int32_t* blk_q, int32_t* blk_len,
+                                    int32_t* blk_anc, int32_t* blk_relind) {
+  if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
+  const Symbolic& S = h->S;
+  cp<int64_t>(blk_ptr, S.blk_ptr); cp(blk_q, S.blk_q); cp(blk_len, S.blk_len); cp(blk_anc, S.blk_anc);
+  cp(blk_relind, S.blk_relind);
   return SPCHOL_OK;
 }
 

@@ -118,6 +118,32 @@ __device__ __forceinline__ void gemm_epilogue(const GTask& T, const SnInfo& S, d
   }
 }
 
+// RLB epilogue: the block-pair tile is written straight into the ancestor panel at
+// dst + j*ldd + i — one relindB per block, no per-row relind lookups; RED because other supernodes
+// of the level may update the same ancestor entries.
+__device__ __forceinline__ void rlb_epilogue(const RTask& R, double* panels, double* smem, const double (&acc)[4][4][2]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+  constexpr int LDC = TILE + 4;
+  double* sC = smem;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+        sC[(wn * 32 + j * 8 + 2 * t + v) * LDC + wm * 32 + i * 8 + g] = acc[i][j][v];
+  __syncthreads();
+  for (int col = R.j0 + warp; col < R.j1; col += GEMM_THREADS / 32) {
+    double* d = panels + R.dst + (long long)(col - R.j0) * R.ldd - R.i0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = lane + 32 * h;
+      if (row >= R.i0 && row < R.i1 && (!R.diag || R.ra + row >= R.rb + col)) atomicAdd(d + row, -sC[col * LDC + row]);
+    }
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const GTask* __restrict__ tasks,
                                                             const SnInfo* __restrict__ sn, double* panels,
@@ -128,7 +154,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const G
   extern __shared__ __align__(16) double smem[];
   double* sA = smem;
   double* sB = smem + STAGES * BK * LDS;
-  const GTask T = tasks[blockIdx.x];
+  GTask T;
+  RTask R;
+  if (MODE == MODE_RLB) {
+    R = reinterpret_cast<const RTask*>(tasks)[blockIdx.x];
+    T.sn = R.sn; T.r0 = R.ra; T.s0 = R.rb; T.c0 = 0; T.nb = 0; T.slot = 0;
+  } else {
+    T = tasks[blockIdx.x];
+  }
   const SnInfo S = sn[T.sn];
   const double* A;
   const double* B;
@@ -141,7 +174,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const G
     A = panels + S.off + (long long)T.c0 * S.ld + T.r0;
     B = linv + (long long)T.slot * (NBMAX * NBMAX);
     lda = S.ld; ldb = NBMAX; arows = S.m - T.r0; brows = T.nb; K = T.nb;
-  } else {
+  } else {   // MODE_SCATTER and MODE_RLB: rows of U_J, all k columns
     A = panels + S.off + T.r0;
     B = panels + S.off + T.s0;
     lda = ldb = S.ld; arows = S.m - T.r0; brows = S.m - T.s0; K = S.k;
@@ -213,7 +246,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const G
   }
   cp_async_wait<0>();
   __syncthreads();
-  gemm_epilogue<MODE>(T, S, panels, smem, acc, ucol_base, ucol_map, posmap);
+  if (MODE == MODE_RLB) rlb_epilogue(R, panels, smem, acc);
+  else gemm_epilogue<MODE>(T, S, panels, smem, acc, ucol_base, ucol_map, posmap);
 }
 
 // ----------------------------------------------------------------------------------------------
@@ -895,6 +929,7 @@ cudaError_t kernels_init_attributes() {
   if ((e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_MAXELEMS * (int)sizeof(double)))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_RLB>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_tma_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_tma_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_tma_kernel<MODE_SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM))) return e;
@@ -944,6 +979,12 @@ void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, dou
     launch_prio(gemm_kernel<MODE_TRSM>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
   else
     launch_prio(gemm_kernel<MODE_SCATTER>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
+}
+
+void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio) {
+  if (ntasks <= 0) return;
+  launch_prio(gemm_kernel<MODE_RLB>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, reinterpret_cast<const GTask*>(tasks), sn,
+              panels, (const double*)nullptr, (const long long*)nullptr, (const long long*)nullptr, (const int*)nullptr);
 }
 
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels, double* linv,

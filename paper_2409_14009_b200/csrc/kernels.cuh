@@ -28,8 +28,16 @@ struct GTask {
 struct PTask {
   int sn, c0, nb, slot;
 };
-
-enum { MODE_LOCAL = 0, MODE_TRSM = 1, MODE_SCATTER = 2 };
+// RLB tile task: the 64-row windows [ra, ra+64) x [rb, rb+64) of supernode sn's update
+// (ra, rb even: 16-byte aligned loads) restricted to one block pair: window rows [i0, i1) of block
+// B', columns [j0, j1) of block B.  Entry (i, j) goes to the ancestor panel at
+// dst + (j - j0) * ldd + (i - i0); diag (B == B'): only ra + i >= rb + j.
+struct RTask {
+  int sn, ra, rb, i0, i1, j0, j1, diag;
+  long long dst;
+  int ldd, pad;
+};
+enum { MODE_LOCAL = 0, MODE_TRSM = 1, MODE_SCATTER = 2, MODE_RLB = 3 };
 
 constexpr int TILE = 64;           // CTA tile edge (rows and columns)
 #ifndef SPCHOL_MINB
@@ -70,6 +78,7 @@ constexpr int TMA_BOX_COLS = SPCHOL_TBK;   // K columns per TMA stage (the host 
 void launch_gemm_tma(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, const void* tmaps,
                      const void* tmap_linv, const long long* ucol_base, const long long* ucol_map, const int* posmap,
                      cudaStream_t st, int prio = 0);
+void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio = 0);
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels,
                   double* linv, unsigned long long* fail, cudaStream_t st, int prio = 0);
 constexpr int SMALL_THREADS = 256;

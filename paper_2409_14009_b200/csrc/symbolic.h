@@ -27,6 +27,10 @@ struct Symbolic {
   std::vector<int64_t> rel_ptr, rel_off;
   std::vector<int32_t> rel_anc, rel_q0, relind;
   std::vector<int32_t> parent_final, cc_final;
+  // RLB blocks: per J, maximal runs of consecutive global rows of R_J inside one
+  // ancestor's column range; q = first row position in rows(J), relindB of the first row
+  std::vector<int64_t> blk_ptr;
+  std::vector<int32_t> blk_q, blk_len, blk_anc, blk_relind;
   std::vector<int32_t> level;  // height of each supernode in the merged tree (leaves = 0)
   int32_t nlevels = 0;
   // A -> final lower position: for every stored entry e of A, (final col, position in rows(J))

@@ -24,6 +24,9 @@ def compare(prob, cap=0.25):
         b = o.symbolic()
         for k in KEYS:
             assert np.array_equal(a[k], b[k]), k
+        bl = h.spchol_export_blocks()
+        for k in ("blk_ptr", "blk_q", "blk_len", "blk_anc", "blk_relind"):
+            assert np.array_equal(bl[k], b[k]), k
         assert h.query("NNZ_L") == o.nnzL
         assert h.query("FLOPS_EXACT") == int(o.flops)
         assert h.query("ADDED") == o.added and h.query("NMERGES") == o.nmerges

@@ -167,3 +167,15 @@ def test_parity_tma_tiles(name, monkeypatch):
     monkeypatch.setenv("SPCHOL_TMA", "1")
     run_parity(gen.make(name), small_max_k=-1)
     run_parity(gen.make(name), block=40, small_max_k=-1)
+
+
+@pytest.mark.parametrize("name", ["C1", "T2", "T3", "S2", "S3", "S4", "S5"])
+def test_parity_rlb(name):
+    """RLB: block-pair updates straight into the ancestor panels give the same factor."""
+    run_parity(gen.make(name), update_mode=1, small_max_k=-1)
+    run_parity(gen.make(name), update_mode=1)
+
+
+@pytest.mark.parametrize("trial", range(0, 20))
+def test_parity_rlb_random(trial):
+    run_parity(gen.random_spd(trial), update_mode=1, small_max_k=-1)

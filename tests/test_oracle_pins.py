@@ -101,6 +101,24 @@ def test_fig1_update_matrix_support():
     assert support == sorted(map(tuple, FIG1["U_J1_support"]["value"]))
 
 
+def test_fig1_rlb_blocks():
+    """RLB blocks of J1: B = {6,7} inside J3 and B' = {14} inside J6."""
+    p = fig1_problem()
+    o = oracle.Oracle.from_problem(p, cap=-1, rule=1)
+    s = o.symbolic()
+    inv = np.argsort(s["perm_final"])
+    lab = lambda c: int(inv[c]) + 1
+    blocks = {}
+    for J in range(o.nsuper):
+        cols = tuple(sorted(lab(c) for c in range(s["sfirst"][J], s["sfirst"][J + 1])))
+        rows = s["rows"][s["rows_ptr"][J]:s["rows_ptr"][J + 1]]
+        blocks[cols] = [[lab(r) for r in rows[s["blk_q"][b]:s["blk_q"][b] + s["blk_len"][b]]]
+                        for b in range(s["blk_ptr"][J], s["blk_ptr"][J + 1])]
+    assert blocks[(1, 2)] == [[6, 7], [14]]
+    assert blocks[(3, 4)] == [[8, 9], [13]]     # SPEC S:229 derived example
+    assert blocks[(12, 13, 14, 15)] == []
+
+
 def test_fig1_merge_costs_spec():
     """SPEC S:181 costs on the Fig. 1 partition: the first greedy pick is (J2,J4) at cost 2."""
     p = fig1_problem()
@@ -202,6 +220,24 @@ def check_invariants(o, s, n, cap, Lref=None):
             assert np.all(np.diff(rel) < 0)
             assert rP[len(rP) - 1 - rel].tolist() == r[q0:].tolist()
             assert r[q0] >= sf[P] and (q0 == k or r[q0 - 1] < sf[P])
+    # RLB blocks: disjoint, ordered, cover R_J; each a run of consecutive global rows
+    # inside one ancestor's columns, maximal; relindB = relind(J,P) of its first row
+    for J in range(ns):
+        k = sf[J + 1] - sf[J]
+        r = rows[rp[J]:rp[J + 1]]
+        q = k
+        for b in range(s["blk_ptr"][J], s["blk_ptr"][J + 1]):
+            assert s["blk_q"][b] == q
+            blk = r[q:q + s["blk_len"][b]]
+            assert len(blk) >= 1 and np.all(np.diff(blk) == 1)
+            P = s["blk_anc"][b]
+            assert np.all((blk >= sf[P]) & (blk < sf[P + 1]))
+            rP = rows[rp[P]:rp[P + 1]]
+            assert rP[len(rP) - 1 - s["blk_relind"][b]] == blk[0]
+            q += len(blk)
+            if q < len(r):       # maximal: the next row breaks the run or changes ancestor
+                assert r[q] != r[q - 1] + 1 or not (sf[P] <= r[q] < sf[P + 1])
+        assert q == len(r)
     # merged storage growth == sum of merge costs, never above the cap
     assert storage - o.nnzL == o.added == sum(c for _, _, c in s["merges"])
     assert o.added <= cap * o.nnzL + 1e-9
