@@ -99,6 +99,15 @@ void spchol_default_options(spchol_options* opt);
 int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* rowidx, const double* values,
                    const int32_t* perm, const spchol_options* opt, spchol_handle** out);
 
+/*
+ * Save the symbolic analysis of h to a binary file (path); spchol_load_analysis rebuilds a handle
+ * from it — launch plan and device state for opt (its merge_cap is ignored: the file's is used) —
+ * without re-running analyze.  Values must then be given with spchol_set_values.  Errors:
+ * VALIDATION (I/O failure, not an analysis file), plus those of analyze's device setup.
+ */
+int spchol_save_analysis(const spchol_handle* h, const char* path);
+int spchol_load_analysis(const char* path, const spchol_options* opt, spchol_handle** out);
+
 /* Replace A's values (same pattern as analyze; host array of colptr[n] doubles, copied to the
  * device on the handle's stream, synchronously w.r.t. the host buffer). */
 int spchol_set_values(spchol_handle* h, const double* values);

@@ -32,7 +32,7 @@ KERNEL_KINDS = dict(small=0, potrf=1, trsm=2, local_update=3, syrk_scatter=4, in
 
 # Every symbol include/spchol.h declares (checked by tests/test_capi_exports.py).
 EXPORTS = [
-    "spchol_default_options", "spchol_analyze", "spchol_set_values", "spchol_set_values_device",
+    "spchol_default_options", "spchol_analyze", "spchol_save_analysis", "spchol_load_analysis", "spchol_set_values", "spchol_set_values_device",
     "spchol_set_stream", "spchol_factor_async", "spchol_factor_status", "spchol_factor",
     "spchol_solve", "spchol_solve_device", "spchol_query", "spchol_export_symbolic",
     "spchol_export_blocks", "spchol_export_panels", "spchol_export_panel", "spchol_export_diagonal", "spchol_enable_kernel_timing", "spchol_kernel_stats",
@@ -73,6 +73,8 @@ def lib():
         L.spchol_default_options.restype = None
         L.spchol_analyze.argtypes = [i64, vp, vp, vp, vp, ctypes.POINTER(spchol_options), ctypes.POINTER(vp)]
         L.spchol_set_values.argtypes = [vp, vp]
+        L.spchol_save_analysis.argtypes = [vp, ctypes.c_char_p]
+        L.spchol_load_analysis.argtypes = [ctypes.c_char_p, ctypes.POINTER(spchol_options), ctypes.POINTER(vp)]
         L.spchol_set_values_device.argtypes = [vp, vp]
         L.spchol_set_stream.argtypes = [vp, vp]
         L.spchol_factor_async.argtypes = [vp]
@@ -130,9 +132,17 @@ class Solver:
     ``device=-1`` builds a host-only handle (symbolic analysis + launch plan, no GPU).
     """
 
-    def __init__(self, n, colptr, rowidx, values=None, perm=None, **options):
+    def __init__(self, n, colptr, rowidx, values=None, perm=None, _load=None, **options):
         L = lib()
         self._L = L
+        if _load is not None:             # spchol_load_analysis
+            self.options = default_options(**options)
+            h = ctypes.c_void_p()
+            _check(L.spchol_load_analysis(str(_load).encode(), ctypes.byref(self.options), ctypes.byref(h)))
+            self._h = h
+            self.n = self.spchol_query("N")
+            self.nnzA = self.spchol_query("NNZ_A")
+            return
         colptr = np.ascontiguousarray(colptr, np.int64)
         rowidx = np.ascontiguousarray(rowidx, np.int32)
         vals = None if values is None else np.ascontiguousarray(values, np.float64)
@@ -145,6 +155,13 @@ class Solver:
                               ctypes.byref(h))
         _check(rc)
         self._h = h
+
+    @classmethod
+    def spchol_load_analysis(cls, path, **options):
+        return cls(0, None, None, _load=path, **options)
+
+    def spchol_save_analysis(self, path):
+        _check(self._L.spchol_save_analysis(self._h, str(path).encode()))
 
     @classmethod
     def from_problem(cls, prob, with_values=True, **options):

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -164,6 +165,12 @@ struct spchol_handle {
   struct SolveStep { int level; long long p0; int np; long long t0; int nt; };
   std::vector<SolveStep> solve_steps;   // per (level, inner block step): POTRF and TRSM task ranges
   std::vector<int> small_level_off;     // small_sns range per level
+  std::vector<STask> stasks;            // level solve tasks: forward of level l at [sfwd_off[l], sfwd_off[l+1]),
+  std::vector<long long> sfwd_off, sbwd_off;   // backward at [sbwd_off[l], sbwd_off[l+1])
+  STask* d_stasks = nullptr;
+  int* d_sflags = nullptr;              // forward flags | backward flags | backward chunk counts (nslots
+                                        // each) | per-level tickets (2 * nlevels); zeroed per solve
+  bool legacy_solve = false;            // SPCHOL_SOLVE_LEGACY=1: per-block-step launches (diagnostics)
   int nevents = 0;
   bool no_lookahead = false;     // SPCHOL_NO_LOOKAHEAD=1 (diagnostics)
   int max_level = -1;            // SPCHOL_MAX_LEVEL=l: factor only levels <= l (diagnostics)
@@ -437,6 +444,57 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
 }
 
 
+// Level solve tasks (sync-free blocked triangular solve, see solve_fwd_level_kernel).  Order inside
+// a level = the ticket order: forward, triangle blocks b = 0, 1, ... interleaved over the level's
+// supernodes, then the rows below the triangles; backward, the chunks below the triangles, then the
+// triangle column blocks from the last to the first.  A task only waits for tasks before it.
+static void build_solve_tasks(spchol_handle* h) {
+  const Symbolic& S = h->S;
+  const int NB = h->nb;
+  h->stasks.clear();
+  h->sfwd_off.assign(S.nlevels + 1, 0);
+  h->sbwd_off.assign(S.nlevels + 1, 0);
+  for (int l = 0; l < S.nlevels; ++l) {
+    std::vector<int> big;
+    int maxblk = 0;
+    for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
+      const int J = h->level_sns[x];
+      if (h->is_small[J] || h->sn[J].k == 0) continue;
+      big.push_back(J);
+      maxblk = std::max(maxblk, (h->sn[J].k + NB - 1) / NB);
+    }
+    h->sfwd_off[l] = (long long)h->stasks.size();
+    for (int b = 0; b < maxblk; ++b)
+      for (int J : big) {
+        const SnInfo& I = h->sn[J];
+        if (b * NB >= I.k) continue;
+        const int nb = std::min(NB, I.k - b * NB);
+        h->stasks.push_back(STask{J, 0, b, nb, b * NB, b * NB + nb, h->slot_base[J] + b, 0});
+      }
+    for (int J : big) {
+      const SnInfo& I = h->sn[J];
+      for (int q0 = I.k; q0 < I.m; q0 += 64) h->stasks.push_back(STask{J, 1, 0, 0, q0, std::min(q0 + 64, I.m), h->slot_base[J], 0});
+    }
+    h->sbwd_off[l] = (long long)h->stasks.size();
+    for (int J : big) {
+      const SnInfo& I = h->sn[J];
+      const int nblk = (I.k + NB - 1) / NB;
+      for (int b = 0; b < nblk; ++b)
+        for (int q0 = I.k; q0 < I.m; q0 += SOLVE_RCHUNK)
+          h->stasks.push_back(STask{J, 2, b, std::min(NB, I.k - b * NB), q0, std::min(q0 + SOLVE_RCHUNK, I.m), h->slot_base[J] + b, 0});
+    }
+    for (int d = 0; d < maxblk; ++d)
+      for (int J : big) {
+        const SnInfo& I = h->sn[J];
+        const int nblk = (I.k + NB - 1) / NB, b = nblk - 1 - d;
+        if (b < 0) continue;
+        const int need = (I.m - I.k + SOLVE_RCHUNK - 1) / SOLVE_RCHUNK;
+        h->stasks.push_back(STask{J, 3, b, std::min(NB, I.k - b * NB), b * NB, b * NB + std::min(NB, I.k - b * NB), h->slot_base[J] + b, need});
+      }
+  }
+  h->sfwd_off[S.nlevels] = h->sbwd_off[S.nlevels] = (long long)h->stasks.size();
+}
+
 static void build_plan(spchol_handle* h) {
   const Symbolic& S = h->S;
   const int ns = S.nsuper, NB = h->nb;
@@ -512,6 +570,7 @@ static void build_plan(spchol_handle* h) {
   // the whole tree (the solve's structure; the single-GPU factor when nvr == 1), then per-rank
   // phase A / phase C for multi-GPU
   append_levels(h, [](int) { return true; }, true);
+  build_solve_tasks(h);
   h->plan_all_end = h->plan.size();
   h->plan_factor_begin = 0;
   if (h->world == 1 && h->nvr > 1) {
@@ -645,6 +704,8 @@ static int setup_device(spchol_handle* h) {
   CK(upload(&h->d_perm, S.perm_final));
   CK(upload(&h->d_level_sns, h->level_sns));
   CK(upload(&h->d_small_sns, h->small_sns));
+  CK(upload(&h->d_stasks, h->stasks));
+  CK(dalloc(&h->d_sflags, (size_t)3 * std::max(1, h->nslots_total) + 2 * (size_t)S.nlevels + 1));
   CK(dalloc(&h->d_y, (size_t)S.n));
   CK(dalloc(&h->d_y2, (size_t)S.n));
   return SPCHOL_OK;
@@ -656,7 +717,7 @@ static void free_device(spchol_handle* h) {
   if (h->solve_graph) cudaGraphDestroy(h->solve_graph);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->graph) cudaGraphDestroy(h->graph);
-  void* ptrs[] = {h->d_rtasks, h->d_tmaps, h->d_tmap_linv, h->d_small_sns, h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
+  void* ptrs[] = {h->d_stasks, h->d_sflags, h->d_rtasks, h->d_tmaps, h->d_tmap_linv, h->d_small_sns, h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
                   h->d_rows_ptr, h->d_posmap, h->d_sfirst, h->d_rows, h->d_perm, h->d_level_sns, h->d_sn,
                   h->d_gtasks, h->d_ptasks, h->d_fail};
   for (void* p : ptrs) if (p) cudaFree(p);
@@ -669,39 +730,121 @@ static void free_device(spchol_handle* h) {
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
 }
 
+extern "C" int spchol_set_values(spchol_handle* h, const double* values);
+
+// Everything after the symbolic phase: validation of the options, launch plan, device state.
+static int finish_handle(spchol_handle* h) {
+  if (h->opt.block) {
+    if (h->opt.block < 8 || h->opt.block > NBMAX || h->opt.block % 8) return fail(SPCHOL_ERR_VALIDATION, "block must be a multiple of 8 in [8, 64]");
+    h->nb = h->opt.block;
+  }
+  if (h->opt.update_mode < 0 || h->opt.update_mode > 1) return fail(SPCHOL_ERR_VALIDATION, "update_mode must be 0 (RL) or 1 (RLB)");
+  if (h->opt.dist_world < 1 || h->opt.dist_rank < 0 || h->opt.dist_rank >= h->opt.dist_world)
+    return fail(SPCHOL_ERR_VALIDATION, "need 0 <= dist_rank < dist_world");
+  h->rank = h->opt.dist_rank;
+  h->world = h->opt.dist_world;
+  h->nvr = h->opt.subtree_streams == 0 ? 4 : std::max(1, std::min(16, (int)h->opt.subtree_streams));
+  if (const char* e = getenv("SPCHOL_NO_LOOKAHEAD")) h->no_lookahead = atoi(e) != 0;
+  if (const char* e = getenv("SPCHOL_MAX_LEVEL")) h->max_level = atoi(e);
+  if (const char* e = getenv("SPCHOL_TMA")) h->use_tma = atoi(e) != 0;
+  if (const char* e = getenv("SPCHOL_OUTER")) h->outer = std::max(1, atoi(e));
+  if (const char* e = getenv("SPCHOL_SOLVE_LEGACY")) h->legacy_solve = atoi(e) != 0;
+  build_plan(h);
+  if (h->opt.device < 0) return SPCHOL_OK;   // host-only analysis (no device state)
+  int rc = setup_device(h);
+  if (rc != SPCHOL_OK) free_device(h);
+  return rc;
+}
+
 extern "C" int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* rowidx, const double* values,
                               const int32_t* perm, const spchol_options* opt, spchol_handle** out) {
   if (!out) return fail(SPCHOL_ERR_VALIDATION, "out is NULL");
   *out = nullptr;
   spchol_handle* h = new spchol_handle();
   if (opt) h->opt = *opt; else spchol_default_options(&h->opt);
-  if (h->opt.update_mode < 0 || h->opt.update_mode > 1) { delete h; return fail(SPCHOL_ERR_VALIDATION, "update_mode must be 0 (RL) or 1 (RLB)"); }
-  if (h->opt.dist_world < 1 || h->opt.dist_rank < 0 || h->opt.dist_rank >= h->opt.dist_world) {
-    delete h;
-    return fail(SPCHOL_ERR_VALIDATION, "need 0 <= dist_rank < dist_world");
-  }
-  h->rank = h->opt.dist_rank;
-  h->world = h->opt.dist_world;
-  h->nvr = h->opt.subtree_streams == 0 ? 4 : std::max(1, std::min(16, (int)h->opt.subtree_streams));
-  if (h->opt.block) {
-    if (h->opt.block < 8 || h->opt.block > NBMAX || h->opt.block % 8) { delete h; return fail(SPCHOL_ERR_VALIDATION, "block must be a multiple of 8 in [8, 64]"); }
-    h->nb = h->opt.block;
-  }
   std::string err;
   int rc = analyze_symbolic(n, colptr, rowidx, perm, h->opt.merge_cap, h->S, err);
   if (rc != SPCHOL_OK) { delete h; return fail(rc, err); }
-  if (const char* e = getenv("SPCHOL_NO_LOOKAHEAD")) h->no_lookahead = atoi(e) != 0;
-  if (const char* e = getenv("SPCHOL_MAX_LEVEL")) h->max_level = atoi(e);
-  if (const char* e = getenv("SPCHOL_TMA")) h->use_tma = atoi(e) != 0;
-  if (const char* e = getenv("SPCHOL_OUTER")) h->outer = std::max(1, atoi(e));
-  build_plan(h);
-  if (h->opt.device < 0) { *out = h; return SPCHOL_OK; }   // host-only analysis (no device state)
-  rc = setup_device(h);
-  if (rc != SPCHOL_OK) { free_device(h); delete h; return rc; }
-  if (values) {
+  rc = finish_handle(h);
+  if (rc != SPCHOL_OK) { delete h; return rc; }
+  if (values && h->opt.device >= 0) {
     rc = spchol_set_values(h, values);
     if (rc != SPCHOL_OK) { free_device(h); delete h; return rc; }
   }
+  *out = h;
+  return SPCHOL_OK;
+}
+
+
+// ------------------------------------------------------------------------------------- serialization
+// Binary file: magic, version, then every field of the symbolic analysis (scalars, then each array
+// as <int64 count><raw data>).  A loaded handle rebuilds the launch plan and device state from it.
+namespace {
+constexpr uint64_t SPCHOL_MAGIC = 0x4C4F484350534250ull;   // "PBSPCHOL"
+constexpr uint64_t SPCHOL_FORMAT = 1;
+template <class T>
+bool wvec(FILE* f, const std::vector<T>& v) {
+  const int64_t n = (int64_t)v.size();
+  return fwrite(&n, sizeof n, 1, f) == 1 && (n == 0 || fwrite(v.data(), sizeof(T), (size_t)n, f) == (size_t)n);
+}
+template <class T>
+bool rvec(FILE* f, std::vector<T>& v) {
+  int64_t n = 0;
+  if (fread(&n, sizeof n, 1, f) != 1 || n < 0 || n > (int64_t)1 << 40) return false;
+  v.resize((size_t)n);
+  return n == 0 || fread(v.data(), sizeof(T), (size_t)n, f) == (size_t)n;
+}
+template <class F>
+bool fields(Symbolic& S, double& cap, F&& io) {
+  return io.sc(S.n) && io.sc(S.nnzA) && io.sc(S.nnzL) && io.sc(S.flops_exact) && io.sc(S.added) && io.sc(S.nmerges) &&
+         io.sc(S.nsuper) && io.sc(S.nlevels) && io.sc(cap) && io.v(S.post) && io.v(S.parent3) && io.v(S.cc3) &&
+         io.v(S.ffirst) && io.v(S.fparent) && io.v(S.fgroup) && io.v(S.perm_final) && io.v(S.iperm_final) &&
+         io.v(S.sfirst) && io.v(S.sparent) && io.v(S.snode) && io.v(S.rows_ptr) && io.v(S.rows) && io.v(S.rel_ptr) &&
+         io.v(S.rel_off) && io.v(S.rel_anc) && io.v(S.rel_q0) && io.v(S.relind) && io.v(S.parent_final) &&
+         io.v(S.cc_final) && io.v(S.blk_ptr) && io.v(S.blk_q) && io.v(S.blk_len) && io.v(S.blk_anc) &&
+         io.v(S.blk_relind) && io.v(S.level) && io.v(S.a_col) && io.v(S.a_pos);
+}
+struct Writer {
+  FILE* f;
+  template <class T> bool sc(const T& x) { return fwrite(&x, sizeof x, 1, f) == 1; }
+  template <class T> bool v(const std::vector<T>& x) { return wvec(f, x); }
+};
+struct Reader {
+  FILE* f;
+  template <class T> bool sc(T& x) { return fread(&x, sizeof x, 1, f) == 1; }
+  template <class T> bool v(std::vector<T>& x) { return rvec(f, x); }
+};
+}  // namespace
+
+extern "C" int spchol_save_analysis(const spchol_handle* h, const char* path) {
+  if (!h || !path) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(SPCHOL_ERR_VALIDATION, std::string("cannot open ") + path);
+  double cap = h->opt.merge_cap;
+  Writer w{f};
+  bool ok = fwrite(&SPCHOL_MAGIC, 8, 1, f) == 1 && fwrite(&SPCHOL_FORMAT, 8, 1, f) == 1 &&
+            fields(const_cast<Symbolic&>(h->S), cap, w);
+  ok = (fclose(f) == 0) && ok;
+  return ok ? SPCHOL_OK : fail(SPCHOL_ERR_VALIDATION, std::string("write failed: ") + path);
+}
+
+extern "C" int spchol_load_analysis(const char* path, const spchol_options* opt, spchol_handle** out) {
+  if (!path || !out) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
+  *out = nullptr;
+  FILE* f = fopen(path, "rb");
+  if (!f) return fail(SPCHOL_ERR_VALIDATION, std::string("cannot open ") + path);
+  spchol_handle* h = new spchol_handle();
+  if (opt) h->opt = *opt; else spchol_default_options(&h->opt);
+  uint64_t magic = 0, fmt = 0;
+  double cap = 0;
+  Reader r{f};
+  bool ok = fread(&magic, 8, 1, f) == 1 && fread(&fmt, 8, 1, f) == 1 && magic == SPCHOL_MAGIC && fmt == SPCHOL_FORMAT &&
+            fields(h->S, cap, r);
+  fclose(f);
+  if (!ok) { delete h; return fail(SPCHOL_ERR_VALIDATION, std::string("not a spchol analysis file: ") + path); }
+  h->opt.merge_cap = cap;   // the analysis was built with this cap
+  int rc = finish_handle(h);
+  if (rc != SPCHOL_OK) { delete h; return rc; }
   *out = h;
   return SPCHOL_OK;
 }
@@ -941,9 +1084,9 @@ extern "C" int spchol_factor(spchol_handle* h, int64_t* fail_col, int64_t* fail_
 
 // Supernodal triangular solves: y = P_f b; forward L y' = y level by level (leaves first),
 // backward L^T z = y' (root first); x = P_f^T z.  Small supernodes: one CTA each (column sweep in
-// the CTA).  Large supernodes: per inner 64-column block b, y_b := X_bb y_b with the diagonal-block
-// inverse kept from the factor, then the rows below are updated by a row-tiled block GEMV (RED into
-// y); backward in reverse with the transposed operations.
+// the CTA).  Large supernodes: one launch per level and direction (solve_fwd/bwd_level_kernel):
+// 64-row / 64-column block tasks that wait on per-block ready flags instead of kernel boundaries;
+// the diagonal blocks are applied with the inverses kept from the factor (X_bb = L_bb^{-1}).
 static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaStream_t st) {
   const Symbolic& S = h->S;
   launch_permute(h->d_perm, d_b, h->d_y, S.n, 0, st);
@@ -953,9 +1096,20 @@ static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaS
     if (r.second == 0) r.first = q;
     r.second = q + 1;
   }
+  const size_t NS = (size_t)std::max(1, h->nslots_total);
+  int* fflag = h->d_sflags;
+  int* bflag = fflag + NS;
+  int* rcnt = bflag + NS;
+  int* tickets = rcnt + NS;
+  if (!h->legacy_solve) CK(cudaMemsetAsync(h->d_sflags, 0, sizeof(int) * (3 * NS + 2 * (size_t)S.nlevels + 1), st));
   for (int l = 0; l < S.nlevels; ++l) {
     launch_solve_fwd(h->d_small_sns + h->small_level_off[l], h->small_level_off[l + 1] - h->small_level_off[l], h->d_sn,
                      h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, st);
+    if (!h->legacy_solve) {
+      launch_solve_fwd_level(h->d_stasks + h->sfwd_off[l], (int)(h->sbwd_off[l] - h->sfwd_off[l]), tickets + 2 * l, fflag,
+                             h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, st);
+      continue;
+    }
     for (size_t q = lvl_steps[l].first; q < lvl_steps[l].second; ++q) {
       const auto& T = h->solve_steps[q];
       launch_solve_diag(h->d_ptasks + T.p0, T.np, h->d_sfirst, h->d_linv, h->d_y, 0, st);
@@ -963,10 +1117,16 @@ static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaS
     }
   }
   for (int l = S.nlevels - 1; l >= 0; --l) {
-    for (size_t q = lvl_steps[l].second; q > lvl_steps[l].first; --q) {
-      const auto& T = h->solve_steps[q - 1];
-      launch_solve_upd(h->d_gtasks + T.t0, T.nt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, 1, st);
-      launch_solve_diag(h->d_ptasks + T.p0, T.np, h->d_sfirst, h->d_linv, h->d_y, 1, st);
+    if (!h->legacy_solve) {
+      launch_solve_bwd_level(h->d_stasks + h->sbwd_off[l], (int)(h->sfwd_off[l + 1] - h->sbwd_off[l]), tickets + 2 * l + 1,
+                             bflag, rcnt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y,
+                             h->nb, st);
+    } else {
+      for (size_t q = lvl_steps[l].second; q > lvl_steps[l].first; --q) {
+        const auto& T = h->solve_steps[q - 1];
+        launch_solve_upd(h->d_gtasks + T.t0, T.nt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, 1, st);
+        launch_solve_diag(h->d_ptasks + T.p0, T.np, h->d_sfirst, h->d_linv, h->d_y, 1, st);
+      }
     }
     launch_solve_bwd(h->d_small_sns + h->small_level_off[l], h->small_level_off[l + 1] - h->small_level_off[l], h->d_sn,
                      h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, st);

@@ -910,6 +910,199 @@ __global__ void __launch_bounds__(256) solve_upd_kernel(const GTask* __restrict_
   }
 }
 
+// ------------------------------------------------------------------ sync-free level solve (large)
+// One launch per level and direction.  CTAs claim tasks in list order through an atomic ticket, so
+// every task a CTA waits for was claimed earlier by a running CTA (no deadlock whatever the
+// scheduling).  A triangle block publishes x_b in y and then its flag (release); consumers poll
+// the flag (acquire) and read x_b through L2 (__ldcg: L1 is not coherent across CTAs).
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_geq(const int* p, int v) {
+  while (ld_acquire(p) < v) __nanosleep(32);
+}
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(a), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+constexpr int XLD = NBMAX + 1;   // padded column stride of the inverse in shared memory (no bank conflicts)
+
+// Stage X = L_bb^{-1} (column-major ld NBMAX in linv) into Xs[c * XLD + r].
+__device__ __forceinline__ void stage_inverse(double* Xs, const double* X) {
+  for (int e = threadIdx.x; e < NBMAX * NBMAX; e += SOLVE_THREADS) cp_async8(Xs + (e >> 6) * XLD + (e & 63), X + e);
+}
+
+// Forward, one level: kind 0 = triangle row block b: x_b = X_b (y_b - sum_{c<b} L_bc x_c);
+// kind 1 = rows [q0, q1) below the triangle: y[rows(J)[q]] -= sum_c L_qc x_c.
+// Thread (lane = tid & 63, grp = tid >> 6): row q0 + lane, columns grp + 4j of each block.
+__global__ void __launch_bounds__(SOLVE_THREADS) solve_fwd_level_kernel(
+    const STask* __restrict__ tasks, int* ticket, int* flag, const SnInfo* __restrict__ sn,
+    const int* __restrict__ sfirst, const long long* __restrict__ rows_ptr, const int* __restrict__ rows,
+    const double* __restrict__ panels, const double* __restrict__ linv, double* y, int NB) {
+  __shared__ double Xs[NBMAX * XLD];
+  __shared__ double xs[NBMAX];
+  __shared__ double part[4][NBMAX];
+  __shared__ int s_task;
+  const int tid = threadIdx.x, lane = tid & 63, grp = tid >> 6;
+  if (tid == 0) s_task = atomicAdd(ticket, 1);
+  __syncthreads();
+  const STask T = tasks[s_task];
+  const SnInfo S = sn[T.sn];
+  const int f = sfirst[T.sn];
+  const int slot0 = T.slot - T.cb;
+  const bool tri = T.kind == 0;
+  if (tri) stage_inverse(Xs, linv + (long long)T.slot * (NBMAX * NBMAX));
+  const int q = T.q0 + lane;
+  const bool rowok = q < T.q1;
+  const double* Pq = panels + S.off + q;
+  const int ncb = tri ? T.cb : (S.k + NB - 1) / NB;
+  double acc = 0.0;
+  for (int cb = 0; cb < ncb; ++cb) {
+    const int nbc = min(NB, S.k - cb * NB);
+    const double* Lc = Pq + (long long)(cb * NB) * S.ld;
+    double lv[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int c = grp + 4 * j;
+      lv[j] = (rowok && c < nbc) ? Lc[(long long)c * S.ld] : 0.0;
+    }
+    if (tid == 0) wait_geq(flag + slot0 + cb, 1);
+    __syncthreads();
+    if (tid < NBMAX) xs[tid] = tid < nbc ? __ldcg(y + f + cb * NB + tid) : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc += lv[j] * xs[grp + 4 * j];
+  }
+  part[grp][lane] = acc;
+  __syncthreads();
+  if (tri) {
+    const int nb = T.nb, b0 = T.cb * NB;
+    if (tid < NBMAX)
+      xs[tid] = tid < nb ? __ldcg(y + f + b0 + tid) - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]) : 0.0;
+    cp_async_wait_all();
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int c = grp + 4 * j;
+      if (c <= lane && c < nb) s += Xs[c * XLD + lane] * xs[c];
+    }
+    part[grp][lane] = s;
+    __syncthreads();
+    if (tid < nb) y[f + b0 + tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(flag + T.slot, 1);
+    }
+  } else if (grp == 0 && rowok) {
+    atomicAdd(y + rows[rows_ptr[T.sn] + q], -(part[0][lane] + part[1][lane] + part[2][lane] + part[3][lane]));
+  }
+}
+
+// Backward, one level: kind 2 = y_cb -= L(q0:q1, cb)^T y[rows(J)[q0:q1]] (RED), then count;
+// kind 3 = x_cb = X_cb^T (y_cb - sum_{r>cb} L_{r,cb}^T x_r) once all kind-2 chunks of cb are in.
+// Thread (lane, grp): row lane of a 64-row chunk, columns grp + 4j; sums reduced over the lanes.
+__global__ void __launch_bounds__(SOLVE_THREADS, 2) solve_bwd_level_kernel(
+    const STask* __restrict__ tasks, int* ticket, int* flag, int* rcnt, const SnInfo* __restrict__ sn,
+    const int* __restrict__ sfirst, const long long* __restrict__ rows_ptr, const int* __restrict__ rows,
+    const double* __restrict__ panels, const double* __restrict__ linv, double* y, int NB) {
+  __shared__ double Xs[NBMAX * XLD];
+  __shared__ double xs[NBMAX];
+  __shared__ double part[4][NBMAX];
+  __shared__ double red[4][16][2];
+  __shared__ int s_task;
+  const int tid = threadIdx.x, lane = tid & 63, grp = tid >> 6;
+  if (tid == 0) s_task = atomicAdd(ticket, 1);
+  __syncthreads();
+  const STask T = tasks[s_task];
+  const SnInfo S = sn[T.sn];
+  const int f = sfirst[T.sn];
+  const int slot0 = T.slot - T.cb;
+  const bool tri = T.kind == 3;
+  const int c0 = T.cb * NB, nbc = T.nb;
+  const double* P = panels + S.off + (long long)c0 * S.ld;
+  if (tri) stage_inverse(Xs, linv + (long long)T.slot * (NBMAX * NBMAX));
+  double acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+  if (!tri) {
+    const int* R = rows + rows_ptr[T.sn];
+    for (int r = T.q0 + lane; r < T.q1; r += 64) {
+      const double yv = y[R[r]];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int c = grp + 4 * j;
+        if (c < nbc) acc[j] += P[(long long)c * S.ld + r] * yv;
+      }
+    }
+  } else {
+    const int nblk = (S.k + NB - 1) / NB;
+    for (int rb = nblk - 1; rb > T.cb; --rb) {
+      const int nbr = min(NB, S.k - rb * NB);
+      const int r = rb * NB + lane;
+      const bool ok = lane < nbr;
+      double lv[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int c = grp + 4 * j;
+        lv[j] = (ok && c < nbc) ? P[(long long)c * S.ld + r] : 0.0;
+      }
+      if (tid == 0) wait_geq(flag + slot0 + rb, 1);
+      __syncthreads();
+      if (tid < NBMAX) xs[tid] = tid < nbr ? __ldcg(y + f + rb * NB + tid) : 0.0;
+      __syncthreads();
+      const double xv = xs[lane];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] += lv[j] * xv;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    double v = acc[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0) red[grp][j][(tid >> 5) & 1] = v;
+  }
+  __syncthreads();
+  if (!tri) {
+    if (tid < nbc) atomicAdd(y + f + c0 + tid, -(red[tid & 3][tid >> 2][0] + red[tid & 3][tid >> 2][1]));
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(rcnt + T.slot, 1);
+    }
+    return;
+  }
+  if (tid == 0 && T.need > 0) wait_geq(rcnt + T.slot, T.need);
+  cp_async_wait_all();
+  __syncthreads();
+  if (tid < NBMAX)
+    xs[tid] = tid < nbc ? __ldcg(y + f + c0 + tid) - (red[tid & 3][tid >> 2][0] + red[tid & 3][tid >> 2][1]) : 0.0;
+  __syncthreads();
+  double s = 0.0;   // x_i = sum_{j >= i} X(j, i) v_j, thread i = lane, j = grp + 4jj
+#pragma unroll
+  for (int jj = 0; jj < 16; ++jj) {
+    const int j = grp + 4 * jj;
+    if (j >= lane && j < nbc) s += Xs[lane * XLD + j] * xs[j];
+  }
+  part[grp][lane] = s;
+  __syncthreads();
+  if (tid < nbc) y[f + c0 + tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    st_release(flag + T.slot, 1);
+  }
+}
+
 __global__ void permute_kernel(const int* __restrict__ perm, const double* __restrict__ in, double* out, long long n,
                                int inverse) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -1014,6 +1207,20 @@ void launch_init(const double* vals, const long long* amap, long long nnz, doubl
   init_scatter_kernel<<<(int)blocks, 256, 0, st>>>(vals, amap, nnz, panels);
 }
 
+void launch_solve_fwd_level(const STask* tasks, int ntasks, int* ticket, int* flag, const SnInfo* sn, const int* sfirst,
+                            const long long* rows_ptr, const int* rows, const double* panels, const double* linv,
+                            double* y, int NB, cudaStream_t st) {
+  if (ntasks > 0)
+    solve_fwd_level_kernel<<<ntasks, SOLVE_THREADS, 0, st>>>(tasks, ticket, flag, sn, sfirst, rows_ptr, rows, panels,
+                                                             linv, y, NB);
+}
+void launch_solve_bwd_level(const STask* tasks, int ntasks, int* ticket, int* flag, int* rcnt, const SnInfo* sn,
+                            const int* sfirst, const long long* rows_ptr, const int* rows, const double* panels,
+                            const double* linv, double* y, int NB, cudaStream_t st) {
+  if (ntasks > 0)
+    solve_bwd_level_kernel<<<ntasks, SOLVE_THREADS, 0, st>>>(tasks, ticket, flag, rcnt, sn, sfirst, rows_ptr, rows,
+                                                             panels, linv, y, NB);
+}
 void launch_solve_fwd(const int* sns, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
                       const int* rows, const double* panels, double* y, cudaStream_t st) {
   if (count > 0) solve_fwd_kernel<<<count, 256, 0, st>>>(sns, sn, sfirst, rows_ptr, rows, panels, y);

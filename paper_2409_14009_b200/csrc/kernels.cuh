@@ -37,6 +37,15 @@ struct RTask {
   long long dst;
   int ldd, pad;
 };
+// Solve task of one level (sync-free blocked triangular solve, solve_fwd_level / solve_bwd_level).
+// kind 0: forward, triangle row block cb (rows [q0, q1) = the block's columns);
+// kind 1: forward, rows [q0, q1) >= k of the panel (all column blocks; RED into the ancestors);
+// kind 2: backward, column block cb against rows [q0, q1) >= k (partial dot products, RED into y_cb);
+// kind 3: backward, triangle column block cb (waits for `need` kind-2 chunks and the blocks > cb).
+// slot = diagonal-inverse slot of block cb (slot - cb = slot of block 0 = the flag base).
+struct STask {
+  int sn, kind, cb, nb, q0, q1, slot, need;
+};
 enum { MODE_LOCAL = 0, MODE_TRSM = 1, MODE_SCATTER = 2, MODE_RLB = 3 };
 
 constexpr int TILE = 64;           // CTA tile edge (rows and columns)
@@ -97,6 +106,14 @@ void launch_solve_diag(const PTask* tasks, int count, const int* sfirst, const d
                        cudaStream_t st);
 void launch_solve_upd(const GTask* tasks, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
                       const int* rows, const double* panels, double* y, int transpose, cudaStream_t st);
+constexpr int SOLVE_THREADS = 256;
+constexpr int SOLVE_RCHUNK = 512;   // rows per backward kind-2 task
+void launch_solve_fwd_level(const STask* tasks, int ntasks, int* ticket, int* flag, const SnInfo* sn, const int* sfirst,
+                            const long long* rows_ptr, const int* rows, const double* panels, const double* linv,
+                            double* y, int NB, cudaStream_t st);
+void launch_solve_bwd_level(const STask* tasks, int ntasks, int* ticket, int* flag, int* rcnt, const SnInfo* sn,
+                            const int* sfirst, const long long* rows_ptr, const int* rows, const double* panels,
+                            const double* linv, double* y, int NB, cudaStream_t st);
 void launch_permute(const int* perm, const double* in, double* out, long long n, int inverse, cudaStream_t st);
 void launch_axpy(const double* x, double* y, long long n, cudaStream_t st);
 void launch_gather(const double* src, const long long* idx, double* out, long long n, cudaStream_t st);

@@ -85,3 +85,26 @@ def test_n_zero_and_n_one():
         assert h.query("NSUPER") == 0 and h.query("NNZ_L") == 0
     with sp.Solver(1, np.array([0, 1], np.int64), np.array([0], np.int32), device=-1) as h:
         assert h.query("NSUPER") == 1 and h.query("NNZ_L") == 1
+
+
+def test_save_load_analysis_roundtrip(tmp_path):
+    """spchol_save_analysis / spchol_load_analysis: the loaded handle carries the
+    identical symbolic analysis, plan and layout without re-running analyze."""
+    p = gen.make("S5")
+    path = tmp_path / "s5.spchol"
+    with sp.Solver.from_problem(p, device=-1, merge_cap=0.1) as h:
+        h.spchol_save_analysis(path)
+        a = h.spchol_export_symbolic()
+        ba = h.spchol_export_blocks()
+        qa = {k: h.spchol_query(k) for k in sp.Q}
+    with sp.Solver.spchol_load_analysis(path, device=-1) as g:
+        b = g.spchol_export_symbolic()
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
+        bb = g.spchol_export_blocks()
+        for k in ba:
+            assert np.array_equal(ba[k], bb[k]), k
+        assert {k: g.spchol_query(k) for k in sp.Q} == qa
+    bad = tmp_path / "bad.spchol"
+    bad.write_bytes(b"not an analysis")
+    assert _err(lambda: sp.Solver.spchol_load_analysis(bad, device=-1)) == sp.SPCHOL_ERR_VALIDATION

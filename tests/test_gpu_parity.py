@@ -179,3 +179,22 @@ def test_parity_rlb(name):
 @pytest.mark.parametrize("trial", range(0, 20))
 def test_parity_rlb_random(trial):
     run_parity(gen.random_spd(trial), update_mode=1, small_max_k=-1)
+
+
+def test_load_analysis_then_refactor(tmp_path):
+    """A handle rebuilt from a saved analysis factors new values (values-only refactorization)."""
+    p = gen.make("S4")
+    path = tmp_path / "s4.spchol"
+    with sp.Solver.from_problem(p, device=-1) as h0:
+        h0.spchol_save_analysis(path)
+    vals = p.values * 2.0                        # 2A: L scales by sqrt(2)
+    with sp.Solver.spchol_load_analysis(path) as h:
+        h.spchol_set_values(vals)
+        h.spchol_factor()
+        d2 = h.spchol_export_diagonal()
+        h.spchol_set_values(p.values)
+        h.spchol_factor()
+        d1 = h.spchol_export_diagonal()
+        assert np.abs(d2 / d1 - np.sqrt(2.0)).max() < 1e-13
+        xs, b = gen.rhs(p)
+        assert backward_error(p, h.spchol_solve(b), b) <= TOL_BERR
