@@ -168,6 +168,9 @@ struct spchol_handle {
   std::vector<STask> stasks;            // level solve tasks: forward of level l at [sfwd_off[l], sfwd_off[l+1]),
   std::vector<long long> sfwd_off, sbwd_off;   // backward at [sbwd_off[l], sbwd_off[l+1])
   STask* d_stasks = nullptr;
+  std::vector<SmallSolve> ssolve;       // small supernodes, per level by row class (m <= 64 / 128 / 256)
+  std::vector<int> ssolve_off;          // level l, class c at [ssolve_off[3l + c], ssolve_off[3l + c + 1])
+  SmallSolve* d_ssolve = nullptr;
   int* d_sflags = nullptr;              // forward flags | backward flags | backward chunk counts (nslots
                                         // each) | per-level tickets (2 * nlevels); zeroed per solve
   bool legacy_solve = false;            // SPCHOL_SOLVE_LEGACY=1: per-block-step launches (diagnostics)
@@ -493,6 +496,19 @@ static void build_solve_tasks(spchol_handle* h) {
       }
   }
   h->sfwd_off[S.nlevels] = h->sbwd_off[S.nlevels] = (long long)h->stasks.size();
+  h->ssolve.clear();
+  h->ssolve_off.assign(3 * S.nlevels + 1, 0);
+  for (int l = 0; l < S.nlevels; ++l)
+    for (int cl = 0; cl < 3; ++cl) {
+      h->ssolve_off[3 * l + cl] = (int)h->ssolve.size();
+      for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
+        const int J = h->level_sns[x];
+        const SnInfo& I = h->sn[J];
+        if (!h->is_small[J] || (I.m > 64) + (I.m > 128) != cl) continue;
+        h->ssolve.push_back(SmallSolve{I.off, S.rows_ptr[J], I.ld, I.m, I.k, S.sfirst[J]});
+      }
+    }
+  h->ssolve_off[3 * S.nlevels] = (int)h->ssolve.size();
 }
 
 static void build_plan(spchol_handle* h) {
@@ -705,6 +721,7 @@ static int setup_device(spchol_handle* h) {
   CK(upload(&h->d_level_sns, h->level_sns));
   CK(upload(&h->d_small_sns, h->small_sns));
   CK(upload(&h->d_stasks, h->stasks));
+  CK(upload(&h->d_ssolve, h->ssolve));
   CK(dalloc(&h->d_sflags, (size_t)3 * std::max(1, h->nslots_total) + 2 * (size_t)S.nlevels + 1));
   CK(dalloc(&h->d_y, (size_t)S.n));
   CK(dalloc(&h->d_y2, (size_t)S.n));
@@ -717,7 +734,7 @@ static void free_device(spchol_handle* h) {
   if (h->solve_graph) cudaGraphDestroy(h->solve_graph);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->graph) cudaGraphDestroy(h->graph);
-  void* ptrs[] = {h->d_stasks, h->d_sflags, h->d_rtasks, h->d_tmaps, h->d_tmap_linv, h->d_small_sns, h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
+  void* ptrs[] = {h->d_ssolve, h->d_stasks, h->d_sflags, h->d_rtasks, h->d_tmaps, h->d_tmap_linv, h->d_small_sns, h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
                   h->d_rows_ptr, h->d_posmap, h->d_sfirst, h->d_rows, h->d_perm, h->d_level_sns, h->d_sn,
                   h->d_gtasks, h->d_ptasks, h->d_fail};
   for (void* p : ptrs) if (p) cudaFree(p);
@@ -1103,8 +1120,9 @@ static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaS
   int* tickets = rcnt + NS;
   if (!h->legacy_solve) CK(cudaMemsetAsync(h->d_sflags, 0, sizeof(int) * (3 * NS + 2 * (size_t)S.nlevels + 1), st));
   for (int l = 0; l < S.nlevels; ++l) {
-    launch_solve_fwd(h->d_small_sns + h->small_level_off[l], h->small_level_off[l + 1] - h->small_level_off[l], h->d_sn,
-                     h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, st);
+    for (int cl = 0; cl < 3; ++cl)
+      launch_solve_small(h->d_ssolve + h->ssolve_off[3 * l + cl], h->ssolve_off[3 * l + cl + 1] - h->ssolve_off[3 * l + cl],
+                         cl, 0, h->d_rows, h->d_panels, h->d_y, st);
     if (!h->legacy_solve) {
       launch_solve_fwd_level(h->d_stasks + h->sfwd_off[l], (int)(h->sbwd_off[l] - h->sfwd_off[l]), tickets + 2 * l, fflag,
                              h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, st);
@@ -1128,8 +1146,9 @@ static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaS
         launch_solve_diag(h->d_ptasks + T.p0, T.np, h->d_sfirst, h->d_linv, h->d_y, 1, st);
       }
     }
-    launch_solve_bwd(h->d_small_sns + h->small_level_off[l], h->small_level_off[l + 1] - h->small_level_off[l], h->d_sn,
-                     h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, st);
+    for (int cl = 0; cl < 3; ++cl)
+      launch_solve_small(h->d_ssolve + h->ssolve_off[3 * l + cl], h->ssolve_off[3 * l + cl + 1] - h->ssolve_off[3 * l + cl],
+                         cl, 1, h->d_rows, h->d_panels, h->d_y, st);
   }
   launch_permute(h->d_perm, h->d_y, d_x, S.n, 1, st);
   CK(cudaGetLastError());

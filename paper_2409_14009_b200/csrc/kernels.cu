@@ -796,54 +796,144 @@ __global__ void init_scatter_kernel(const double* __restrict__ vals, const long 
   }
 }
 
-// Forward solve for the supernodes of one level: y_J := L_JJ^{-1} y_J, then y_R -= L_RJ y_J.
-__global__ void solve_fwd_kernel(const int* __restrict__ sns, const SnInfo* __restrict__ sn,
-                                 const int* __restrict__ sfirst, const long long* __restrict__ rows_ptr,
-                                 const int* __restrict__ rows, const double* __restrict__ panels, double* y) {
-  const int J = sns[blockIdx.x];
-  const SnInfo S = sn[J];
-  const int f = sfirst[J];
-  const double* P = panels + S.off;
-  for (int c = 0; c < S.k; ++c) {
-    if (threadIdx.x == 0) y[f + c] /= P[(long long)c * S.ld + c];
-    __syncthreads();
-    const double xc = y[f + c];
-    for (int r = c + 1 + threadIdx.x; r < S.k; r += blockDim.x) y[f + r] -= P[(long long)c * S.ld + r] * xc;
-    __syncthreads();
-  }
-  const int* R = rows + rows_ptr[J];
-  for (int r = S.k + threadIdx.x; r < S.m; r += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < S.k; ++c) s += P[(long long)c * S.ld + r] * y[f + c];
-    atomicAdd(y + R[r], -s);
+// Small supernodes (m <= SMALL_MAXM = 256, k <= 64): one warp per supernode, 8 per CTA, described by
+// one packed SmallSolve record.  Lane owns rows r = lane + 32 i (i < ROWS, m <= 32 ROWS) in
+// registers; x_c travels by shuffle, so the column chain has no barrier and no division
+// (reciprocals of the diagonal are formed up front).  Columns go in chunks of CH whose loads are
+// issued one chunk ahead (double buffer).
+constexpr int SW_WARPS = 8;
+
+template <int ROWS, int CH>
+__device__ __forceinline__ void sw_load_cols(double (&Lb)[CH][ROWS], const double* P, int ld, int m, int k, int c0,
+                                             int lane) {
+#pragma unroll
+  for (int j = 0; j < CH; ++j)
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) {
+      const int r = lane + 32 * i, c = c0 + j;
+      Lb[j][i] = (c < k && r > c && r < m) ? P[(long long)c * ld + r] : 0.0;
+    }
+}
+
+template <int ROWS, int CH>
+__device__ __forceinline__ void sw_fwd_cols(const double (&Lb)[CH][ROWS], double (&v)[ROWS], double dinv0, double dinv1,
+                                            int k, int c0, int lane) {
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int c = c0 + j;
+    if (c >= k) break;
+    const bool lo = c < 32;
+    const double yc = __shfl_sync(0xffffffffu, lo ? v[0] : v[ROWS > 1 ? 1 : 0], c & 31);
+    const double xc = yc * __shfl_sync(0xffffffffu, lo ? dinv0 : dinv1, c & 31);
+    if (lane == (c & 31)) { if (lo) v[0] = xc; else v[ROWS > 1 ? 1 : 0] = xc; }
+#pragma unroll
+    for (int i = 0; i < ROWS; ++i) v[i] -= Lb[j][i] * xc;
   }
 }
 
-// Backward solve for one level (root first): y_J := L_JJ^{-T} (y_J - L_RJ^T y_R).
-__global__ void solve_bwd_kernel(const int* __restrict__ sns, const SnInfo* __restrict__ sn,
-                                 const int* __restrict__ sfirst, const long long* __restrict__ rows_ptr,
-                                 const int* __restrict__ rows, const double* __restrict__ panels, double* y) {
-  const int J = sns[blockIdx.x];
-  const SnInfo S = sn[J];
-  const int f = sfirst[J];
-  const double* P = panels + S.off;
-  const int* R = rows + rows_ptr[J];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int c = warp; c < S.k; c += nw) {
-    double s = 0.0;
-    for (int r = S.k + lane; r < S.m; r += 32) s += P[(long long)c * S.ld + r] * y[R[r]];
+// Forward: y_J := L_JJ^{-1} y_J, then y[rows(J)[r]] -= (L_RJ y_J)_r (RED: ancestors are shared).
+template <int ROWS>
+__global__ void __launch_bounds__(32 * SW_WARPS, ROWS >= 4 ? 2 : 3) solve_fwd_small_kernel(const SmallSolve* __restrict__ info, int count,
+                                                                        const int* __restrict__ rows,
+                                                                        const double* __restrict__ panels, double* y) {
+  constexpr int CH = ROWS >= 8 ? 2 : 4;
+  const int w = blockIdx.x * SW_WARPS + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= count) return;
+  const SmallSolve I = info[w];
+  const double* P = panels + I.off;
+  double La[CH][ROWS], Lb[CH][ROWS];
+  sw_load_cols<ROWS, CH>(La, P, I.ld, I.m, I.k, 0, lane);
+  const double dinv0 = lane < I.k ? 1.0 / P[(long long)lane * I.ld + lane] : 0.0;
+  const double dinv1 = lane + 32 < I.k ? 1.0 / P[(long long)(lane + 32) * I.ld + lane + 32] : 0.0;
+  double v[ROWS];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) y[f + c] -= s;
+  for (int i = 0; i < ROWS; ++i) {
+    const int r = lane + 32 * i;
+    v[i] = r < I.k ? y[I.f + r] : 0.0;
   }
-  __syncthreads();
-  for (int c = S.k - 1; c >= 0; --c) {
-    if (threadIdx.x == 0) y[f + c] /= P[(long long)c * S.ld + c];
-    __syncthreads();
-    const double xc = y[f + c];
-    for (int r = threadIdx.x; r < c; r += blockDim.x) y[f + r] -= P[(long long)r * S.ld + c] * xc;
-    __syncthreads();
+  for (int c0 = 0; c0 < I.k; c0 += 2 * CH) {
+    sw_load_cols<ROWS, CH>(Lb, P, I.ld, I.m, I.k, c0 + CH, lane);
+    sw_fwd_cols<ROWS, CH>(La, v, dinv0, dinv1, I.k, c0, lane);
+    if (c0 + CH >= I.k) break;
+    sw_load_cols<ROWS, CH>(La, P, I.ld, I.m, I.k, c0 + 2 * CH, lane);
+    sw_fwd_cols<ROWS, CH>(Lb, v, dinv0, dinv1, I.k, c0 + CH, lane);
   }
+  const int* R = rows + I.rp;
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+    const int r = lane + 32 * i;
+    if (r < I.k) y[I.f + r] = v[i];
+    else if (r < I.m) atomicAdd(y + R[r], v[i]);
+  }
+}
+
+// Backward: y_J := L_JJ^{-T} (y_J - L_RJ^T y_R).
+template <int ROWS>
+__global__ void __launch_bounds__(32 * SW_WARPS, ROWS >= 8 ? 2 : 3) solve_bwd_small_kernel(const SmallSolve* __restrict__ info, int count,
+                                                                        const int* __restrict__ rows,
+                                                                        const double* __restrict__ panels, double* y) {
+  constexpr int CH = ROWS >= 8 ? 2 : 4;
+  const int w = blockIdx.x * SW_WARPS + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= count) return;
+  const SmallSolve I = info[w];
+  const double* P = panels + I.off;
+  const int* R = rows + I.rp;
+  double yr[ROWS];   // y at the rows below the triangle (final values of the ancestors)
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+    const int r = lane + 32 * i;
+    yr[i] = (r >= I.k && r < I.m) ? y[R[r]] : 0.0;
+  }
+  // t_c = y_c - sum_{r >= k} L_rc y_r: lane c (and c + 32) keeps t_c
+  double t0 = lane < I.k ? y[I.f + lane] : 0.0, t1 = lane + 32 < I.k ? y[I.f + lane + 32] : 0.0;
+  const double dinv0 = lane < I.k ? 1.0 / P[(long long)lane * I.ld + lane] : 0.0;
+  const double dinv1 = lane + 32 < I.k ? 1.0 / P[(long long)(lane + 32) * I.ld + lane + 32] : 0.0;
+  if (I.m > I.k)
+    for (int c0 = 0; c0 < I.k; c0 += CH) {
+      double sj[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int c = c0 + j;
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < ROWS; ++i) {
+          const int r = lane + 32 * i;
+          if (c < I.k && r >= I.k && r < I.m) s += P[(long long)c * I.ld + r] * yr[i];
+        }
+        sj[j] = s;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < CH; ++j) sj[j] += __shfl_xor_sync(0xffffffffu, sj[j], o);
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int c = c0 + j;
+        if (c < I.k && lane == (c & 31)) { if (c < 32) t0 -= sj[j]; else t1 -= sj[j]; }
+      }
+    }
+  // triangle, right-looking transposed: x_c = t_c / L_cc, then t_r -= L_cr x_c for r < c
+  for (int c1 = I.k; c1 > 0; c1 -= 8) {   // columns c1-1 .. c1-8
+    double L0[8], L1[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = c1 - 1 - j;
+      L0[j] = (c >= 0 && lane < c) ? P[(long long)lane * I.ld + c] : 0.0;
+      L1[j] = (c >= 0 && lane + 32 < c) ? P[(long long)(lane + 32) * I.ld + c] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = c1 - 1 - j;
+      if (c < 0) break;
+      const bool lo = c < 32;
+      const double xc = __shfl_sync(0xffffffffu, lo ? t0 : t1, c & 31) * __shfl_sync(0xffffffffu, lo ? dinv0 : dinv1, c & 31);
+      if (lane == (c & 31)) { if (lo) t0 = xc; else t1 = xc; }
+      t0 -= L0[j] * xc;
+      t1 -= L1[j] * xc;
+    }
+  }
+  if (lane < I.k) y[I.f + lane] = t0;
+  if (lane + 32 < I.k) y[I.f + lane + 32] = t1;
 }
 
 // Solve, large supernodes.  y_b := X y_b (forward) or X^T y_b (backward) for the 64-column block
@@ -1221,13 +1311,19 @@ void launch_solve_bwd_level(const STask* tasks, int ntasks, int* ticket, int* fl
     solve_bwd_level_kernel<<<ntasks, SOLVE_THREADS, 0, st>>>(tasks, ticket, flag, rcnt, sn, sfirst, rows_ptr, rows,
                                                              panels, linv, y, NB);
 }
-void launch_solve_fwd(const int* sns, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
-                      const int* rows, const double* panels, double* y, cudaStream_t st) {
-  if (count > 0) solve_fwd_kernel<<<count, 256, 0, st>>>(sns, sn, sfirst, rows_ptr, rows, panels, y);
-}
-void launch_solve_bwd(const int* sns, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
-                      const int* rows, const double* panels, double* y, cudaStream_t st) {
-  if (count > 0) solve_bwd_kernel<<<count, 256, 0, st>>>(sns, sn, sfirst, rows_ptr, rows, panels, y);
+void launch_solve_small(const SmallSolve* info, int count, int rows_class, int backward, const int* rows,
+                        const double* panels, double* y, cudaStream_t st) {
+  if (count <= 0) return;
+  const int grid = (count + SW_WARPS - 1) / SW_WARPS, thr = 32 * SW_WARPS;
+  if (!backward) {
+    if (rows_class == 0) solve_fwd_small_kernel<2><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+    else if (rows_class == 1) solve_fwd_small_kernel<4><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+    else solve_fwd_small_kernel<8><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+  } else {
+    if (rows_class == 0) solve_bwd_small_kernel<2><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+    else if (rows_class == 1) solve_bwd_small_kernel<4><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+    else solve_bwd_small_kernel<8><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+  }
 }
 __global__ void axpy_kernel(const double* __restrict__ x, double* y, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)

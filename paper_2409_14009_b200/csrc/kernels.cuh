@@ -98,10 +98,14 @@ void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst
                   const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,
                   int smem_doubles, int maxm, cudaStream_t st, int prio = 0);
 void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st);
-void launch_solve_fwd(const int* sns, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
-                      const int* rows, const double* panels, double* y, cudaStream_t st);
-void launch_solve_bwd(const int* sns, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
-                      const int* rows, const double* panels, double* y, cudaStream_t st);
+// Small-supernode solve record (one per supernode, in level / row-class order).
+struct SmallSolve {
+  long long off, rp;   // panel offset, rows_ptr[J]
+  int ld, m, k, f;     // f = first column
+};
+// rows_class 0 / 1 / 2: m <= 64 / 128 / 256 (rows per lane 2 / 4 / 8)
+void launch_solve_small(const SmallSolve* info, int count, int rows_class, int backward, const int* rows,
+                        const double* panels, double* y, cudaStream_t st);
 void launch_solve_diag(const PTask* tasks, int count, const int* sfirst, const double* linv, double* y, int transpose,
                        cudaStream_t st);
 void launch_solve_upd(const GTask* tasks, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
