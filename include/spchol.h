@@ -68,6 +68,12 @@ typedef struct {
                            (P:307).  1 = RLB: per block pair (B, B') of
                            J's rows, L_{B',B} of B's ancestor updated directly (one relindB per
                            block).  Same factor; RLB has more, smaller tiles on this hardware. */
+  int32_t deterministic; /* 1 = bitwise run-to-run reproducible factor (reading C-7):
+                           each level's supernodes are split into column-conflict-free colour
+                           classes (greedy, ascending supernode order; R_J1 and R_J2 disjoint within
+                           a class), one launch per class, plain read-modify-write scatter instead of
+                           FP64 RED; subtree_streams is forced to 1.  Requires update_mode 0.
+                           Default 0.  (The solve's RED into shared ancestors stays unordered.) */
 } spchol_options;
 
 /* Fill *opt with the defaults above. */
@@ -213,6 +219,16 @@ int spchol_export_panels(const spchol_handle* h, int64_t* panel_off, int32_t* ld
 
 /* Copy panel J (ld[J] k_J doubles, layout as above) to out.  Synchronizes. */
 int spchol_export_panel(const spchol_handle* h, int32_t J, double* out);
+
+/*
+ * The exact factor L of C_f = P_f A P_f^T in CSC, final numbering:
+ * Lp[n+1] (int64, = prefix sums of cc_final), Li[NNZ_L] (rows ascending within each column, the
+ * diagonal first), Lx[NNZ_L] (values from the panels).  padding_nonzeros (optional) receives the
+ * number of panel entries outside the exact pattern that are not exactly +-0.0 (must be 0).
+ * Li / Lx / padding_nonzeros may be NULL.  Lp and Li work on host-only handles; Lx and
+ * padding_nonzeros need a successful factor (else STATE).  Host work O(nnz(L)); synchronizes.
+ */
+int spchol_export_factor_csc(const spchol_handle* h, int64_t* Lp, int32_t* Li, double* Lx, int64_t* padding_nonzeros);
 
 /* diag[j] = L(j,j) for every final column j (n doubles; log det A = 2 sum log diag).
  * Synchronizes the stream. */

@@ -32,7 +32,8 @@ KERNEL_KINDS = dict(small=0, potrf=1, trsm=2, local_update=3, syrk_scatter=4, in
 
 # Every symbol include/spchol.h declares (checked by tests/test_capi_exports.py).
 EXPORTS = [
-    "spchol_default_options", "spchol_analyze", "spchol_save_analysis", "spchol_load_analysis", "spchol_set_values", "spchol_set_values_device",
+    "spchol_default_options", "spchol_analyze", "spchol_save_analysis", "spchol_load_analysis",
+    "spchol_export_factor_csc", "spchol_set_values", "spchol_set_values_device",
     "spchol_set_stream", "spchol_factor_async", "spchol_factor_status", "spchol_factor",
     "spchol_solve", "spchol_solve_device", "spchol_query", "spchol_export_symbolic",
     "spchol_export_blocks", "spchol_export_panels", "spchol_export_panel", "spchol_export_diagonal", "spchol_enable_kernel_timing", "spchol_kernel_stats",
@@ -45,7 +46,8 @@ class spchol_options(ctypes.Structure):
     _fields_ = [("merge_cap", ctypes.c_double), ("device", ctypes.c_int32), ("block", ctypes.c_int32),
                 ("small_max_k", ctypes.c_int32), ("use_graph", ctypes.c_int32),
                 ("dist_rank", ctypes.c_int32), ("dist_world", ctypes.c_int32),
-                ("subtree_streams", ctypes.c_int32), ("update_mode", ctypes.c_int32)]
+                ("subtree_streams", ctypes.c_int32), ("update_mode", ctypes.c_int32),
+                ("deterministic", ctypes.c_int32)]
 
 
 class SpcholError(RuntimeError):
@@ -74,6 +76,7 @@ def lib():
         L.spchol_analyze.argtypes = [i64, vp, vp, vp, vp, ctypes.POINTER(spchol_options), ctypes.POINTER(vp)]
         L.spchol_set_values.argtypes = [vp, vp]
         L.spchol_save_analysis.argtypes = [vp, ctypes.c_char_p]
+        L.spchol_export_factor_csc.argtypes = [vp, vp, vp, vp, vp]
         L.spchol_load_analysis.argtypes = [ctypes.c_char_p, ctypes.POINTER(spchol_options), ctypes.POINTER(vp)]
         L.spchol_set_values_device.argtypes = [vp, vp]
         L.spchol_set_stream.argtypes = [vp, vp]
@@ -159,6 +162,17 @@ class Solver:
     @classmethod
     def spchol_load_analysis(cls, path, **options):
         return cls(0, None, None, _load=path, **options)
+
+    def spchol_export_factor_csc(self, values=True):
+        """(Lp int64[n+1], Li int32[nnz(L)], Lx float64[nnz(L)] or None, padding_nonzeros or None)."""
+        Lp = np.empty(self.n + 1, np.int64)
+        _check(self._L.spchol_export_factor_csc(self._h, _vp(Lp), None, None, None))
+        Li = np.empty(int(Lp[-1]), np.int32)
+        Lx = np.empty(int(Lp[-1]), np.float64) if values else None
+        npad = ctypes.c_int64(-1)
+        _check(self._L.spchol_export_factor_csc(self._h, _vp(Lp), _vp(Li), _vp(Lx) if values else None,
+                                                ctypes.byref(npad) if values else None))
+        return Lp, Li, Lx, (int(npad.value) if values else None)
 
     def spchol_save_analysis(self, path):
         _check(self._L.spchol_save_analysis(self._h, str(path).encode()))

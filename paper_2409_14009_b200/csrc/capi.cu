@@ -112,7 +112,7 @@ struct Launch {
   int n;           // tasks
   double flops, bytes;
   int op = OP_LAUNCH, stream = 0, ev = -1;
-  int aux = 0;     // K_SMALL: dynamic shared memory (doubles)
+  int aux = 0;     // K_SMALL: dynamic shared memory (doubles); K_SCATTER: 1 = plain RMW (deterministic)
   int aux2 = 0;    // K_SMALL: largest m in the launch
 };
 template <class T>
@@ -219,6 +219,7 @@ extern "C" void spchol_default_options(spchol_options* o) {
   o->dist_world = 1;
   o->subtree_streams = 0;
   o->update_mode = 0;
+  o->deterministic = 0;
 }
 
 extern "C" const char* spchol_last_error(void) { return g_err.c_str(); }
@@ -240,6 +241,36 @@ static void for_tiles(int rbase, int rend, int cbase, int cend, F emit) {
           const int r0 = rbase + i * TILE, s0 = cbase + j * TILE;
           if (s0 <= r0) emit(r0, s0);
         }
+}
+
+// Deterministic mode (reading C-7): greedy column-conflict colouring of the supernodes Js (ascending
+// order): J takes the lowest colour none of whose members shares an update column (R_J) with it.
+// Within a colour no two supernodes update one ancestor entry, so their scatter needs no RED.
+static int colour_supernodes(const spchol_handle* h, const std::vector<int>& Js, std::vector<int>& colour) {
+  const Symbolic& S = h->S;
+  static thread_local std::vector<std::vector<char>> used;   // used[c][col]
+  colour.assign(Js.size(), 0);
+  int ncol = 0;
+  for (size_t x = 0; x < Js.size(); ++x) {
+    const int J = Js[x];
+    const long long b = S.rows_ptr[J] + h->sn[J].k, e = S.rows_ptr[J + 1];
+    int c = 0;
+    for (;; ++c) {
+      if (c == (int)used.size()) used.emplace_back();
+      if (used[c].size() < (size_t)S.n) used[c].assign(S.n, 0);
+      bool clash = false;
+      for (long long q = b; q < e && !clash; ++q) clash = used[c][S.rows[q]];
+      if (!clash) break;
+    }
+    for (long long q = b; q < e; ++q) used[c][S.rows[q]] = 1;
+    colour[x] = c;
+    ncol = std::max(ncol, c + 1);
+  }
+  for (size_t x = 0; x < Js.size(); ++x) {   // reset the marks for the next level
+    const int J = Js[x];
+    for (long long q = S.rows_ptr[J] + h->sn[J].k; q < S.rows_ptr[J + 1]; ++q) used[colour[x]][S.rows[q]] = 0;
+  }
+  return std::max(ncol, 1);
 }
 
 // Appends, level by level, the launches for the supernodes J with active(J).  record_solve: also
@@ -266,13 +297,19 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       if (record_solve) h->small_level_off.push_back((int)h->small_sns.size());
       static const int bucket_max[] = {256, 1024, 4096, SMALL_MAXELEMS};
       bool forked = false;
+      std::vector<int> sm, scol;
+      for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x)
+        if (h->is_small[h->level_sns[x]] && active(h->level_sns[x])) sm.push_back(h->level_sns[x]);
+      const int nsc = h->opt.deterministic ? colour_supernodes(h, sm, scol) : 1;
+      if (!h->opt.deterministic) scol.assign(sm.size(), 0);
+      for (int col = 0; col < nsc; ++col)
       for (int bk = 0; bk < 4; ++bk) {
         long long s0 = (long long)h->small_sns.size();
         int mx = 0, mxm = 0;
         double fsm = 0, bsm = 0;
-        for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
-          const int J = h->level_sns[x];
-          if (!h->is_small[J] || !active(J)) continue;
+        for (size_t x = 0; x < sm.size(); ++x) {
+          const int J = sm[x];
+          if (scol[x] != col) continue;
           const SnInfo& I = h->sn[J];
           const int mk = I.m * I.k;
           if (mk > bucket_max[bk] || (bk > 0 && mk <= bucket_max[bk - 1])) continue;
@@ -427,20 +464,30 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       h->plan_level.resize(h->plan.size(), l);
       continue;
     }
-    long long s0g = (long long)h->gtasks.size();
-    double fs = 0, bs = 0;
+    std::vector<int> bg, bcol;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
       const int J = h->level_sns[x];
-      if (h->is_small[J] || !active(J)) continue;
-      const SnInfo& I = h->sn[J];
-      const int t = I.m - I.k;
-      if (t <= 0) continue;
-      const int base = I.k & ~1;
-      for_tiles(base, I.m, base, I.m, [&](int r0, int c0) { h->gtasks.push_back(GTask{J, r0, c0, 0, 0, 0}); });
-      fs += (double)I.k * t * (t + 1);
-      bs += 8.0 * (double)t * I.k + 16.0 * 0.5 * t * (t + 1.0);
+      if (!h->is_small[J] && active(J) && h->sn[J].m > h->sn[J].k) bg.push_back(J);
     }
-    push(K_SCATTER, s0g, (long long)h->gtasks.size(), fs, bs);
+    const int nbc = h->opt.deterministic ? colour_supernodes(h, bg, bcol) : 1;
+    if (!h->opt.deterministic) bcol.assign(bg.size(), 0);
+    for (int col = 0; col < nbc; ++col) {   // one launch per colour class (one class unless deterministic)
+      long long s0g = (long long)h->gtasks.size();
+      double fs = 0, bs = 0;
+      for (size_t x = 0; x < bg.size(); ++x) {
+        if (bcol[x] != col) continue;
+        const int J = bg[x];
+        const SnInfo& I = h->sn[J];
+        const int t = I.m - I.k;
+        const int base = I.k & ~1;
+        for_tiles(base, I.m, base, I.m, [&](int r0, int c0) { h->gtasks.push_back(GTask{J, r0, c0, 0, 0, 0}); });
+        fs += (double)I.k * t * (t + 1);
+        bs += 8.0 * (double)t * I.k + 16.0 * 0.5 * t * (t + 1.0);
+      }
+      push(K_SCATTER, s0g, (long long)h->gtasks.size(), fs, bs);
+      if (h->opt.deterministic && !h->plan.empty() && h->plan.back().kind == K_SCATTER && h->plan.back().off == s0g)
+        h->plan.back().aux = 1;
+    }
     h->plan_level.resize(h->plan.size(), l);
   }
   if (record_solve) h->small_level_off.push_back((int)h->small_sns.size());
@@ -761,6 +808,10 @@ static int finish_handle(spchol_handle* h) {
   h->rank = h->opt.dist_rank;
   h->world = h->opt.dist_world;
   h->nvr = h->opt.subtree_streams == 0 ? 4 : std::max(1, std::min(16, (int)h->opt.subtree_streams));
+  if (h->opt.deterministic) {
+    if (h->opt.update_mode != 0) return fail(SPCHOL_ERR_VALIDATION, "deterministic requires update_mode 0 (RL)");
+    h->nvr = 1;   // concurrent subtrees would update the shared top panels in an unordered way
+  }
   if (const char* e = getenv("SPCHOL_NO_LOOKAHEAD")) h->no_lookahead = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_MAX_LEVEL")) h->max_level = atoi(e);
   if (const char* e = getenv("SPCHOL_TMA")) h->use_tma = atoi(e) != 0;
@@ -973,7 +1024,7 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
         break;
       case K_SMALL:
         launch_small(h->d_small_sns + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_ucol_base, h->d_ucol_map,
-                     h->d_posmap, h->d_fail, L.aux, L.aux2, ls, prio);
+                     h->d_posmap, h->d_fail, L.aux, L.aux2, h->opt.deterministic ? 1 : 0, ls, prio);
         break;
       case K_POTRF:
         launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio);
@@ -991,7 +1042,9 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
           launch_gemm(MODE_LOCAL, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
         break;
       case K_SCATTER:
-        if (h->use_tma)
+        if (L.aux == 1)
+          launch_gemm(MODE_SCATTER_DET, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
+        else if (h->use_tma)
           launch_gemm_tma(MODE_SCATTER, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_tmaps, h->d_tmap_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
         else
           launch_gemm(MODE_SCATTER, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
@@ -1310,6 +1363,74 @@ extern "C" int spchol_export_panel(const spchol_handle* h, int32_t J, double* ou
   CK(cudaStreamSynchronize(h->stream));
   const size_t cnt = (size_t)h->sn[J].ld * h->sn[J].k;   // panels need not be in supernode order
   if (cnt) CK(cudaMemcpy(out, h->d_panels + h->sn[J].off, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+  return SPCHOL_OK;
+}
+
+// Exact factor in CSC (final numbering).  Pattern: struct(L_j) by row subtrees of the final etree
+// (row i of L = the etree paths from every k < i with C_f(i,k) != 0 up to i); values
+// from the panels, where the exact rows of column j are a subsequence of rows(snode(j)).
+extern "C" int spchol_export_factor_csc(const spchol_handle* h, int64_t* Lp, int32_t* Li, double* Lx,
+                                        int64_t* padding_nonzeros) {
+  if (!h || !Lp) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
+  if ((Lx || padding_nonzeros) && (host_only(h) || !h->factored))
+    return fail(SPCHOL_ERR_STATE, "values need a successful factor on a device handle");
+  const Symbolic& S = h->S;
+  const int64_t n = S.n;
+  Lp[0] = 0;
+  for (int64_t j = 0; j < n; ++j) Lp[j + 1] = Lp[j] + S.cc_final[j];
+  if (!Li && !Lx && !padding_nonzeros) return SPCHOL_OK;
+  // lower C_f by rows: entry e of A sits at (final row, final col)
+  std::vector<int64_t> rp(n + 1, 0);
+  std::vector<int32_t> rrow(S.a_col.size());
+  for (size_t e = 0; e < S.a_col.size(); ++e) {
+    const int c = S.a_col[e], J = S.snode[c];
+    rrow[e] = S.rows[S.rows_ptr[J] + S.a_pos[e]];
+    if (rrow[e] > c) rp[rrow[e] + 1]++;
+  }
+  for (int64_t i = 0; i < n; ++i) rp[i + 1] += rp[i];
+  std::vector<int32_t> rcol(rp[n]);
+  {
+    std::vector<int64_t> nx(rp.begin(), rp.end() - 1);
+    for (size_t e = 0; e < S.a_col.size(); ++e)
+      if (rrow[e] > S.a_col[e]) rcol[nx[rrow[e]]++] = S.a_col[e];
+  }
+  std::vector<int32_t> li(Lp[n]);
+  std::vector<int64_t> nxt(Lp, Lp + n);
+  std::vector<int32_t> mark(n, -1);
+  for (int64_t i = 0; i < n; ++i) {
+    mark[i] = (int32_t)i;
+    li[nxt[i]++] = (int32_t)i;                       // diagonal first: rows ascend within a column
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e)
+      for (int32_t j = rcol[e]; mark[j] != i; j = S.parent_final[j]) {
+        if (j < 0 || nxt[j] >= Lp[j + 1]) return fail(SPCHOL_ERR_VALIDATION, "row subtree inconsistent with cc");
+        mark[j] = (int32_t)i;
+        li[nxt[j]++] = (int32_t)i;
+      }
+  }
+  for (int64_t j = 0; j < n; ++j)
+    if (nxt[j] != Lp[j + 1]) return fail(SPCHOL_ERR_VALIDATION, "column count mismatch");
+  if (Li) std::memcpy(Li, li.data(), sizeof(int32_t) * li.size());
+  if (!Lx && !padding_nonzeros) return SPCHOL_OK;
+  int64_t npad = 0;
+  std::vector<double> panel;
+  for (int J = 0; J < S.nsuper; ++J) {
+    const SnInfo& I = h->sn[J];
+    panel.resize((size_t)I.ld * I.k);
+    int rc = spchol_export_panel(h, J, panel.data());
+    if (rc != SPCHOL_OK) return rc;
+    const int32_t* rJ = S.rows.data() + S.rows_ptr[J];
+    for (int c = 0; c < I.k; ++c) {
+      const int64_t j = S.sfirst[J] + c;
+      int q = c;
+      for (int64_t e = Lp[j]; e < Lp[j + 1]; ++e, ++q) {
+        for (; q < I.m && rJ[q] != li[e]; ++q) npad += panel[(size_t)c * I.ld + q] != 0.0;
+        if (q >= I.m) return fail(SPCHOL_ERR_VALIDATION, "exact row outside the panel");
+        if (Lx) Lx[e] = panel[(size_t)c * I.ld + q];
+      }
+      for (; q < I.m; ++q) npad += panel[(size_t)c * I.ld + q] != 0.0;
+    }
+  }
+  if (padding_nonzeros) *padding_nonzeros = npad;
   return SPCHOL_OK;
 }
 

@@ -112,7 +112,11 @@ __device__ __forceinline__ void gemm_epilogue(const GTask& T, const SnInfo& S, d
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int row = lane + 32 * h, gr = T.r0 + row;   // lanes cover 32 consecutive rows
-        if (gr < S.m && gr - S.k >= uc) atomicAdd(panels + cb + posmap[mb + gr], -sC[col * LDC + row]);
+        if (gr < S.m && gr - S.k >= uc) {
+          double* d = panels + cb + posmap[mb + gr];
+          if (MODE == MODE_SCATTER_DET) *d -= sC[col * LDC + row];
+          else atomicAdd(d, -sC[col * LDC + row]);
+        }
       }
     }
   }
@@ -583,7 +587,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
                                                               const long long* __restrict__ ucol_base,
                                                               const long long* __restrict__ ucol_map,
                                                               const int* __restrict__ posmap,
-                                                              unsigned long long* fail) {
+                                                              unsigned long long* fail, int plain) {
   extern __shared__ double P[];         // m x k, column-major, ld = m
   const int J = sns[blockIdx.x];
   const SnInfo S = sn[J];
@@ -645,7 +649,9 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
       if (c >= t || r < c) continue;
       const long long cbase = ucol_base[S.ucol + c];
       const long long mbase = ucol_map[S.ucol + c];
-      atomicAdd(panels + cbase + posmap[mbase + k + r], -acc[q]);
+      double* d = panels + cbase + posmap[mbase + k + r];
+      if (plain) *d -= acc[q];   // deterministic mode: conflict-free launch
+      else atomicAdd(d, -acc[q]);
     }
     item += blockDim.x;
   }
@@ -1218,6 +1224,7 @@ cudaError_t kernels_init_attributes() {
   if ((e = cudaFuncSetAttribute(gemm_tma_kernel<MODE_SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_SCATTER_DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   return cudaSuccess;
 }
 
@@ -1260,6 +1267,8 @@ void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, dou
     launch_prio(gemm_kernel<MODE_LOCAL>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
   else if (mode == MODE_TRSM)
     launch_prio(gemm_kernel<MODE_TRSM>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
+  else if (mode == MODE_SCATTER_DET)
+    launch_prio(gemm_kernel<MODE_SCATTER_DET>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
   else
     launch_prio(gemm_kernel<MODE_SCATTER>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
 }
@@ -1282,12 +1291,12 @@ void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* s
 
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,
                   const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,
-                  int smem_doubles, int maxm, cudaStream_t st, int prio) {
+                  int smem_doubles, int maxm, int plain, cudaStream_t st, int prio) {
   if (count <= 0) return;
   // one thread per panel row: blockDim = the launch's largest m rounded up to a warp (<= 256)
   const int threads = std::min(SMALL_THREADS, std::max(32, (maxm + 31) / 32 * 32));
   launch_prio(small_kernel, count, threads, smem_doubles * (int)sizeof(double), st, prio, sns, sn, sfirst, panels,
-              ucol_base, ucol_map, posmap, fail);
+              ucol_base, ucol_map, posmap, fail, plain);
 }
 
 void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st) {

@@ -46,7 +46,9 @@ struct RTask {
 struct STask {
   int sn, kind, cb, nb, q0, q1, slot, need;
 };
-enum { MODE_LOCAL = 0, MODE_TRSM = 1, MODE_SCATTER = 2, MODE_RLB = 3 };
+// MODE_SCATTER_DET: MODE_SCATTER with plain RMW stores (deterministic mode: the launch's supernodes are
+// column-conflict free, so no two CTAs of the launch touch one ancestor entry).
+enum { MODE_LOCAL = 0, MODE_TRSM = 1, MODE_SCATTER = 2, MODE_RLB = 3, MODE_SCATTER_DET = 4 };
 
 constexpr int TILE = 64;           // CTA tile edge (rows and columns)
 #ifndef SPCHOL_MINB
@@ -96,7 +98,7 @@ constexpr int SMALL_MAXM = SMALL_THREADS;
 constexpr int SMALL_MAXELEMS = 12288;   // m*k doubles in shared memory (96 KB)
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,
                   const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,
-                  int smem_doubles, int maxm, cudaStream_t st, int prio = 0);
+                  int smem_doubles, int maxm, int plain, cudaStream_t st, int prio = 0);
 void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st);
 // Small-supernode solve record (one per supernode, in level / row-class order).
 struct SmallSolve {

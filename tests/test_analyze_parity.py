@@ -20,7 +20,7 @@ KEYS = ["post", "parent3", "cc3", "ffirst", "fgroup", "perm_final", "sfirst", "s
 def compare(prob, cap=0.25):
     with sp.Solver.from_problem(prob, device=-1, merge_cap=cap) as h:
         a = h.spchol_export_symbolic()
-        o = oracle.Oracle.from_problem(prob, cap=cap, keep_L=False)
+        o = oracle.Oracle.from_problem(prob, cap=cap, keep_L=True)
         b = o.symbolic()
         for k in KEYS:
             assert np.array_equal(a[k], b[k]), k
@@ -30,6 +30,10 @@ def compare(prob, cap=0.25):
         assert h.query("NNZ_L") == o.nnzL
         assert h.query("FLOPS_EXACT") == int(o.flops)
         assert h.query("ADDED") == o.added and h.query("NMERGES") == o.nmerges
+        # exact pattern of L (spchol_export_factor_csc) against the oracle's row-merge structure (O2)
+        Lp, Li, _, _ = h.spchol_export_factor_csc(values=False)
+        oLp, oLi, _ = o.L_csc()
+        assert np.array_equal(Lp, oLp) and np.array_equal(Li, oLi)
         return h.query("NSUPER")
 
 

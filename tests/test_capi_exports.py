@@ -108,3 +108,13 @@ def test_save_load_analysis_roundtrip(tmp_path):
     bad = tmp_path / "bad.spchol"
     bad.write_bytes(b"not an analysis")
     assert _err(lambda: sp.Solver.spchol_load_analysis(bad, device=-1)) == sp.SPCHOL_ERR_VALIDATION
+
+
+def test_deterministic_option_plan():
+    """deterministic=1 (reading C-7): colour classes add launches; RLB is rejected."""
+    p = gen.make("S4")
+    with sp.Solver.from_problem(p, device=-1, subtree_streams=1) as h0, \
+            sp.Solver.from_problem(p, device=-1, deterministic=1) as h1:
+        assert h1.query("LAUNCHES") > h0.query("LAUNCHES")
+        assert h1.query("NSUPER") == h0.query("NSUPER")
+    assert _err(lambda: sp.Solver.from_problem(p, device=-1, deterministic=1, update_mode=1)) == sp.SPCHOL_ERR_VALIDATION

@@ -33,6 +33,9 @@ def run_parity(prob, **opts):
         mask = lower_panel_mask(s_gpu, off, ld, len(pan))
         mask[idx] = False                                    # padding = lower panel part outside the pattern
         assert np.all(pan[mask] == 0.0), "padding entries must stay exactly 0"
+        cLp, cLi, cLx, npad = h.spchol_export_factor_csc()      # the exact factor in CSC
+        assert np.array_equal(cLp, Lp) and np.array_equal(cLi, Li) and npad == 0
+        assert np.abs(cLx - Lx).max() <= TOL_L * np.abs(Lx).max()
         xstar, b = gen.rhs(prob)
         x = h.spchol_solve(b)
         assert backward_error(prob, x, b) <= TOL_BERR
@@ -198,3 +201,26 @@ def test_load_analysis_then_refactor(tmp_path):
         assert np.abs(d2 / d1 - np.sqrt(2.0)).max() < 1e-13
         xs, b = gen.rhs(p)
         assert backward_error(p, h.spchol_solve(b), b) <= TOL_BERR
+
+
+@pytest.mark.parametrize("name", ["S2", "S4", "S5", "T3"])
+def test_deterministic_bitwise_reproducible(name):
+    """deterministic=1: oracle parity, and the panels are bitwise identical across refactorizations
+    and across handles (no FP64 RED in the factor)."""
+    p = gen.make(name)
+    run_parity(p, deterministic=1)
+    run_parity(p, deterministic=1, small_max_k=-1)
+    ref = None
+    for _ in range(2):
+        with sp.Solver.from_problem(p, deterministic=1) as h:
+            for _ in range(2):
+                assert h.spchol_factor() == (-1, -1)
+                _, _, pan = h.spchol_export_panels()
+                if ref is None:
+                    ref = pan.copy()
+                assert np.array_equal(pan.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("trial", range(0, 10))
+def test_deterministic_random(trial):
+    run_parity(gen.random_spd(300 + trial), deterministic=1)
