@@ -11,9 +11,10 @@ ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--block", type=int, default=0)
 ap.add_argument("--nograph", action="store_true")
 ap.add_argument("--vr", type=int, default=0)
+ap.add_argument("--det", type=int, default=0)
 a = ap.parse_args()
 p = gen.make(a.config)
-h = sp.Solver.from_problem(p, block=a.block, use_graph=0 if a.nograph else 1, subtree_streams=a.vr)
+h = sp.Solver.from_problem(p, block=a.block, use_graph=0 if a.nograph else 1, subtree_streams=a.vr, deterministic=a.det)
 F = h.query("FLOPS_EXACT")
 for _ in range(2):
     h.spchol_factor()
