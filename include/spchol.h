@@ -177,7 +177,9 @@ enum {
   SPCHOL_Q_FLOPS_EXEC = 13,  /* flops of the supernodal algorithm incl. padding             */
   SPCHOL_Q_LAUNCHES = 14,    /* kernels launched by one factor                              */
   SPCHOL_Q_UPDATE_ENTRIES = 15, /* sum_J t_J (t_J+1)/2 scattered update entries             */
-  SPCHOL_Q_NBLOCKS = 16       /* RLB blocks over all supernodes                   */
+  SPCHOL_Q_NBLOCKS = 16,      /* RLB blocks over all supernodes                   */
+  SPCHOL_Q_NMARKERS = 17,     /* multi-GPU: exchange points (markers) of this rank's phase C     */
+  SPCHOL_Q_NTOP_DIST = 18     /* multi-GPU: top supernodes distributed over their rank group     */
 };
 int spchol_query(const spchol_handle* h, int key, int64_t* value);
 
@@ -258,19 +260,39 @@ int spchol_dist_nccl_unique_id(void* out128);
  * collective: every rank must call it).  NCCL is loaded with dlopen (libnccl.so.2). */
 int spchol_dist_attach_nccl(spchol_handle* h, const void* unique_id128);
 /* owner[NSUPER]: rank owning each supernode's subtree, -1 for the top supernodes (all 0 when
- * dist_world == 1); top_owner[NSUPER]: the rank that factors each top supernode (-1 otherwise);
+ * dist_world == 1); top_owner[NSUPER]: the rank that factors an undistributed top supernode, and
+ * the rank owning block column 0 of a distributed one (block column C of a distributed top
+ * supernode with rank group [lo, hi) belongs to lo + (C + top_owner - lo) mod (hi - lo)), -1
+ * otherwise;
  * *top_off: first double of the contiguous top-panel region; *top_slot: first diagonal-inverse
  * slot of the top supernodes.  Any pointer may be NULL. */
 int spchol_export_mapping(const spchol_handle* h, int32_t* owner, int32_t* top_owner, int64_t* top_off,
                           int64_t* top_slot);
-/* Diagnostics (single process standing in for several ranks on one GPU, never a reported result):
- * phase 1 = a1 init + phase A (own subtrees); 1000 + l = this rank's owned top supernodes of top
- * level l; 3 = synchronize, check the pivots and mark the handle factored with its factor
- * complete.  The exchanges are done by the caller with spchol_dist_debug_accumulate(dst, src,
- * which): which = 16 + J: dst's panel of top supernode J += src's, src's copy zeroed (the per-level
- * fan-in); 1: whole panel arena, 2: all diagonal inverses (the final gather); 0: top region. */
+/*
+ * Multi-GPU phase C.  Top supernodes whose work reaches a threshold are distributed
+ * over their rank group: block columns of W = 256 columns are owned cyclically; the owner of a
+ * block column runs its cdiv (POTRF, TRSM, in-block updates) and then sends it to the rest of the
+ * group (NCCL send/recv), every rank applies the trailing updates of the block columns it owns and
+ * a contiguous share of the U_J tiles (SYRK + relind scatter into its own copies of the ancestors).
+ * At the start of each top level the partial panels are summed onto the block-column owners
+ * (NCCL reduce per block column).  Smaller top supernodes are factored whole by top_owner.
+ *
+ * Diagnostics (single process standing in for several ranks on one GPU, never a reported result):
+ * phase 1 = a1 init + phase A (own subtrees); 2000 + i = segment i of phase C (the plan between
+ * exchange markers i-1 and i, i <= SPCHOL_Q_NMARKERS); 3 = synchronize, check the pivots and mark
+ * the handle factored with its factor complete.  spchol_dist_debug_comm(hs, world, i) plays
+ * marker i's exchange between the world handles hs[0..world-1] (ranks 0..world-1 of one problem on
+ * one device): a level-start reduce onto the owners (other copies zeroed) or a block-column
+ * broadcast.  spchol_dist_debug_accumulate(dst, src, which): dst += src over 1 = the whole panel
+ * arena, 2 = all diagonal inverses (the final gather), 0 = the top region, 16 + J = top supernode
+ * J's panel (src's copy zeroed). */
 int spchol_factor_phase(spchol_handle* h, int phase);
+int spchol_dist_debug_comm(spchol_handle* const* hs, int world, int marker);
 int spchol_dist_debug_accumulate(spchol_handle* dst, const spchol_handle* src, int which);
+/* Executed flops of this rank's plan: phase A (own subtrees; the whole factor when dist_world == 1)
+ * and, per level l < NLEVELS, phase C's share of that level (top_level may be NULL).  Works on
+ * host-only handles (device < 0): the work model of the multi-GPU schedule. */
+int spchol_dist_plan_flops(const spchol_handle* h, double* phase_a, double* top_level);
 
 void spchol_destroy(spchol_handle* h);
 const char* spchol_last_error(void);

@@ -27,7 +27,7 @@ SPCHOL_ERR_STATE = -7
 
 Q = dict(N=0, NNZ_A=1, NNZ_L=2, NFUND=3, NSUPER=4, ADDED=5, NLEVELS=6, ROWS_LEN=7, NPAIRS=8,
          RELIND_LEN=9, PANEL_DOUBLES=10, NMERGES=11, FLOPS_EXACT=12, FLOPS_EXEC=13, LAUNCHES=14,
-         UPDATE_ENTRIES=15, NBLOCKS=16)
+         UPDATE_ENTRIES=15, NBLOCKS=16, NMARKERS=17, NTOP_DIST=18)
 KERNEL_KINDS = dict(small=0, potrf=1, trsm=2, local_update=3, syrk_scatter=4, init=5, rlb_update=6)
 
 # Every symbol include/spchol.h declares (checked by tests/test_capi_exports.py).
@@ -38,7 +38,8 @@ EXPORTS = [
     "spchol_solve", "spchol_solve_device", "spchol_query", "spchol_export_symbolic",
     "spchol_export_blocks", "spchol_export_panels", "spchol_export_panel", "spchol_export_diagonal", "spchol_enable_kernel_timing", "spchol_kernel_stats",
     "spchol_kernel_trace", "spchol_dist_nccl_unique_id", "spchol_dist_attach_nccl", "spchol_export_mapping",
-    "spchol_factor_phase", "spchol_dist_debug_accumulate", "spchol_destroy", "spchol_last_error",
+    "spchol_factor_phase", "spchol_dist_debug_comm", "spchol_dist_debug_accumulate", "spchol_dist_plan_flops",
+    "spchol_destroy", "spchol_last_error",
 ]
 
 
@@ -100,6 +101,8 @@ def lib():
         L.spchol_export_mapping.argtypes = [vp, vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.spchol_factor_phase.argtypes = [vp, ctypes.c_int]
         L.spchol_dist_debug_accumulate.argtypes = [vp, vp, ctypes.c_int]
+        L.spchol_dist_debug_comm.argtypes = [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int]
+        L.spchol_dist_plan_flops.argtypes = [vp, ctypes.POINTER(dbl), vp]
         L.spchol_destroy.argtypes = [vp]
         L.spchol_destroy.restype = None
         L.spchol_last_error.argtypes = []
@@ -327,6 +330,13 @@ class Solver:
     def spchol_dist_debug_accumulate(self, src, which):
         _check(self._L.spchol_dist_debug_accumulate(self._h, src._h, int(which)))
 
+    def spchol_dist_plan_flops(self):
+        """(phase-A flops, per-level phase-C flops) of this rank's plan."""
+        a = ctypes.c_double()
+        lv = np.zeros(self.spchol_query("NLEVELS"), np.float64)
+        _check(self._L.spchol_dist_plan_flops(self._h, ctypes.byref(a), _vp(lv)))
+        return float(a.value), lv
+
     # ---- convenience (still only marshalling)
     factor = spchol_factor
     solve = spchol_solve
@@ -337,6 +347,12 @@ class Solver:
         sym = self.spchol_export_symbolic()
         off, ld, pan = self.spchol_export_panels()
         return sym, off, ld, pan
+
+
+def spchol_dist_debug_comm(handles, marker):
+    """Play exchange marker `marker` between the handles of ranks 0..len(handles)-1 (one GPU)."""
+    arr = (ctypes.c_void_p * len(handles))(*[h._h for h in handles])
+    _check(lib().spchol_dist_debug_comm(arr, len(handles), int(marker)))
 
 
 def spchol_dist_nccl_unique_id() -> bytes:

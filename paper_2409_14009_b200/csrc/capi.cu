@@ -61,6 +61,7 @@ struct NcclUid { char internal[128]; };
 typedef int (*nccl_init_t)(void**, int, NcclUid, int);
 typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*nccl_reduce_t)(const void*, void*, size_t, int, int, int, void*, cudaStream_t);
+typedef int (*nccl_p2p_t)(const void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*nccl_group_t)();
 typedef int (*nccl_destroy_t)(void*);
 typedef const char* (*nccl_errstr_t)(int);
@@ -70,6 +71,7 @@ struct NcclApi {
   nccl_init_t init = nullptr;
   nccl_allreduce_t allreduce = nullptr;
   nccl_reduce_t reduce = nullptr;
+  nccl_p2p_t send = nullptr, recv = nullptr;
   nccl_group_t group_start = nullptr, group_end = nullptr;
   nccl_destroy_t destroy = nullptr;
   nccl_errstr_t errstr = nullptr;
@@ -85,11 +87,13 @@ bool nccl_load(std::string& err) {
   g_nccl.init = (nccl_init_t)dlsym(so, "ncclCommInitRank");
   g_nccl.allreduce = (nccl_allreduce_t)dlsym(so, "ncclAllReduce");
   g_nccl.reduce = (nccl_reduce_t)dlsym(so, "ncclReduce");
+  g_nccl.send = (nccl_p2p_t)dlsym(so, "ncclSend");
+  g_nccl.recv = (nccl_p2p_t)dlsym(so, "ncclRecv");
   g_nccl.group_start = (nccl_group_t)dlsym(so, "ncclGroupStart");
   g_nccl.group_end = (nccl_group_t)dlsym(so, "ncclGroupEnd");
   g_nccl.destroy = (nccl_destroy_t)dlsym(so, "ncclCommDestroy");
   g_nccl.errstr = (nccl_errstr_t)dlsym(so, "ncclGetErrorString");
-  if (!g_nccl.getid || !g_nccl.init || !g_nccl.allreduce || !g_nccl.reduce || !g_nccl.group_start ||
+  if (!g_nccl.getid || !g_nccl.init || !g_nccl.allreduce || !g_nccl.reduce || !g_nccl.send || !g_nccl.recv || !g_nccl.group_start ||
       !g_nccl.group_end || !g_nccl.destroy) { err = "NCCL symbols missing"; return false; }
   g_nccl.so = so;
   return true;
@@ -100,12 +104,16 @@ int nccl_fail(int r, const char* where) {
 }  // namespace
 
 namespace {
-enum OpType { OP_LAUNCH = 0, OP_RECORD = 1, OP_WAIT = 2, OP_TOP_LEVEL = 3 };
+enum OpType { OP_LAUNCH = 0, OP_RECORD = 1, OP_WAIT = 2, OP_TOP_LEVEL = 3, OP_BCAST = 4, OP_ZERO = 5 };
 // One step of the factor's launch plan.  OP_LAUNCH: a batched kernel (kind, tasks [off, off+n)) on
 // stream `stream` (0 = critical path: cdiv chain + relind scatter, 1 = trailing updates);
 // OP_RECORD / OP_WAIT: event `ev` recorded on / awaited by `stream` (lookahead fork/join).
 // OP_TOP_LEVEL (multi-GPU phase C): start of top level `aux` — the panels of that level's top
 // supernodes are reduced (NCCL, sum) onto their owner ranks, the other ranks zero their copies.
+// OP_BCAST (multi-GPU, distributed top supernode aux, column block aux2): the finished block column
+// goes from its owner to the other ranks of the supernode's group (NCCL send/recv).  OP_ZERO: the
+// ranks of aux's group zero their copies of the block columns they do not own (after the last read).
+// OP_TOP_LEVEL and OP_BCAST are "markers": every rank's plan holds the same sequence of them.
 struct Launch {
   int kind;
   long long off;   // first task
@@ -155,6 +163,11 @@ struct spchol_handle {
   int rank = 0, world = 1;
   std::vector<int> owner;              // rank owning each supernode's subtree, -1 = top
   std::vector<int> top_owner;          // rank factoring each top supernode (fan-in), -1 otherwise
+  std::vector<int> grp_lo, grp_hi;     // rank group [lo, hi) of each top supernode
+  std::vector<char> top_dist;          // top supernode distributed over its group (block-column cyclic
+                                       // cdiv, U_J tiles split over the group)
+  double dist_min_flops = 4e9;         // SPCHOL_DIST_MINFLOPS: smallest top supernode distributed
+  std::vector<size_t> markers;         // plan positions of the phase-C markers (same sequence on all ranks)
   std::vector<std::vector<int>> top_by_level;
   long long top_off = -1;              // first double of the contiguous top-panel region
   int top_slot = -1;                   // first inverse slot of the top supernodes
@@ -243,6 +256,16 @@ static void for_tiles(int rbase, int rend, int cbase, int cend, F emit) {
         }
 }
 
+// Multi-GPU, distributed top supernode J (top_dist): outer column block C (columns [C W, (C+1) W),
+// W = outer * nb) belongs to rank grp_lo + (C + top_owner - grp_lo) mod g — cyclic over J's rank group,
+// starting at the rank the per-level LPT picked; an undistributed top supernode belongs to top_owner.
+static int blk_owner(const spchol_handle* h, int J, int C) {
+  if (!h->top_dist[J]) return h->top_owner[J];
+  const int g = h->grp_hi[J] - h->grp_lo[J];
+  return h->grp_lo[J] + (C + h->top_owner[J] - h->grp_lo[J]) % g;
+}
+static bool in_group(const spchol_handle* h, int J, int r) { return r >= h->grp_lo[J] && r < h->grp_hi[J]; }
+
 // Deterministic mode (reading C-7): greedy column-conflict colouring of the supernodes Js (ascending
 // order): J takes the lowest colour none of whose members shares an update column (R_J) with it.
 // Within a colour no two supernodes update one ancestor entry, so their scatter needs no RED.
@@ -274,7 +297,11 @@ static int colour_supernodes(const spchol_handle* h, const std::vector<int>& Js,
 }
 
 // Appends, level by level, the launches for the supernodes J with active(J).  record_solve: also
-// record the solve's step structure (only for the whole-tree plan).
+// record the solve's step structure (only for the whole-tree plan).  top_markers (multi-GPU phase
+// C of rank h->rank): a level-start marker per top level; distributed top supernodes (top_dist) take
+// part on every rank of their group — cdiv tasks of the column blocks the rank owns, one OP_BCAST
+// marker per finished column block (on every rank, so all plans hold the same marker sequence), the
+// rank's share of the U_J tiles, and an OP_ZERO of the non-owned blocks after the level's scatter.
 template <class Active>
 static void append_levels(spchol_handle* h, Active active, bool record_solve, int SB = 0, bool top_markers = false) {
   const Symbolic& S = h->S;
@@ -334,9 +361,10 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         h->plan.push_back(L);
       }
     }
+    auto dtop = [&](int J) { return top_markers && h->top_dist[J]; };
     int maxblk = 0;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
-      if (h->is_small[h->level_sns[x]] || !active(h->level_sns[x])) continue;
+      if (h->is_small[h->level_sns[x]] || !(active(h->level_sns[x]) || dtop(h->level_sns[x]))) continue;
       const SnInfo& I = h->sn[h->level_sns[x]];
       maxblk = std::max(maxblk, (I.k + NB - 1) / NB);
     }
@@ -353,32 +381,43 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       long long p0 = (long long)h->ptasks.size(), t0 = (long long)h->gtasks.size();
       double fp = 0, ft = 0, fl = 0, bp = 0, bt = 0, bl = 0, fn = 0, bn = 0, fr = 0, br = 0;
       std::vector<GTask> local, nxt, rest;
+      std::vector<std::pair<int, int>> bcast;   // (J, column block) finished at this step
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
         const int J = h->level_sns[x];
-        if (h->is_small[J] || !active(J)) continue;
+        const bool dj = dtop(J);
+        if (h->is_small[J] || !(dj || active(J))) continue;
         const SnInfo& I = h->sn[J];
         const int c0 = s * NB;
         if (c0 >= I.k) continue;
         const int slot = h->slot_base[J] + s;   // every diagonal block keeps its own inverse (solve)
         const int nb = std::min(NB, I.k - c0), c1 = c0 + nb;
         const int C0 = (c0 / W) * W, C1 = std::min(C0 + W, I.k);   // enclosing outer block
-        h->ptasks.push_back(PTask{J, c0, nb, slot});
-        fp += (double)nb * nb * nb / 3.0;
-        bp += 16.0 * nb * nb;
-        // row tiles start on an even row (16-byte aligned cp.async); rows < c1 are masked (s0 = c1)
-        for (int r0 = c1 & ~1; r0 < I.m; r0 += TILE) h->gtasks.push_back(GTask{J, r0, c1, c0, nb, slot});
-        ft += (double)(I.m - c1) * nb * nb;
-        bt += 16.0 * (double)(I.m - c1) * nb;
-        // inner update: columns [c1, C1) of this outer block, K = nb
-        for_tiles(c1, I.m, c1, C1, [&](int r0, int s0) { local.push_back(GTask{J, r0, s0, c0, nb, C1}); });
-        for (int c = c1; c < C1; ++c) { fl += 2.0 * nb * (double)(I.m - c); bl += 16.0 * (double)(I.m - c); }
-        // outer update after the last inner block of the outer block, K = C1 - C0
+        auto own = [&](int col) { return !dj || blk_owner(h, J, col / W) == h->rank; };
+        if (own(C0)) {
+          h->ptasks.push_back(PTask{J, c0, nb, slot});
+          fp += (double)nb * nb * nb / 3.0;
+          bp += 16.0 * nb * nb;
+          // row tiles start on an even row (16-byte aligned cp.async); rows < c1 are masked (s0 = c1)
+          for (int r0 = c1 & ~1; r0 < I.m; r0 += TILE) h->gtasks.push_back(GTask{J, r0, c1, c0, nb, slot});
+          ft += (double)(I.m - c1) * nb * nb;
+          bt += 16.0 * (double)(I.m - c1) * nb;
+          // inner update: columns [c1, C1) of this outer block, K = nb
+          for_tiles(c1, I.m, c1, C1, [&](int r0, int s0) { local.push_back(GTask{J, r0, s0, c0, nb, C1}); });
+          for (int c = c1; c < C1; ++c) { fl += 2.0 * nb * (double)(I.m - c); bl += 16.0 * (double)(I.m - c); }
+        }
+        if (c1 == C1 && dj) bcast.push_back({J, C0 / W});
+        // outer update after the last inner block of the outer block, K = C1 - C0 (a distributed
+        // supernode: each rank updates the tiles of the column blocks it owns; W is a multiple of
+        // TILE there, so no tile straddles two blocks)
         if (c1 == C1 && C1 < I.k) {
           const int C2 = std::min(C1 + W, I.k);
-          for_tiles(C1, I.m, C1, C2, [&](int r0, int s0) { nxt.push_back(GTask{J, r0, s0, C0, C1 - C0, C2}); });
-          for (int c = C1; c < C2; ++c) { fn += 2.0 * (C1 - C0) * (double)(I.m - c); bn += 16.0 * (double)(I.m - c); }
-          for_tiles(C2, I.m, C2, I.k, [&](int r0, int s0) { rest.push_back(GTask{J, r0, s0, C0, C1 - C0, I.k}); });
-          for (int c = C2; c < I.k; ++c) { fr += 2.0 * (C1 - C0) * (double)(I.m - c); br += 16.0 * (double)(I.m - c); }
+          if (own(C1)) {
+            for_tiles(C1, I.m, C1, C2, [&](int r0, int s0) { nxt.push_back(GTask{J, r0, s0, C0, C1 - C0, C2}); });
+            for (int c = C1; c < C2; ++c) { fn += 2.0 * (C1 - C0) * (double)(I.m - c); bn += 16.0 * (double)(I.m - c); }
+          }
+          for_tiles(C2, I.m, C2, I.k, [&](int r0, int s0) { if (own(s0)) rest.push_back(GTask{J, r0, s0, C0, C1 - C0, I.k}); });
+          for (int c = C2; c < I.k; ++c)
+            if (own(c)) { fr += 2.0 * (C1 - C0) * (double)(I.m - c); br += 16.0 * (double)(I.m - c); }
         }
       }
       long long p1 = (long long)h->ptasks.size(), t1 = (long long)h->gtasks.size();
@@ -388,6 +427,12 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       long long l0 = (long long)h->gtasks.size();
       h->gtasks.insert(h->gtasks.end(), local.begin(), local.end());
       push(K_LOCAL, l0, (long long)h->gtasks.size(), fl, bl);
+      for (const auto& jc : bcast) {   // finished block columns to the rest of their group (stream SB)
+        Launch M{0, 0, 0, 0, 0, OP_BCAST, SB, -1};
+        M.aux = jc.first;
+        M.aux2 = jc.second;
+        h->plan.push_back(M);
+      }
       if (!rest.empty() && h->no_lookahead) {   // diagnostics: NEXT and REST as one launch, serial
         nxt.insert(nxt.end(), rest.begin(), rest.end());
         fn += fr; bn += br;
@@ -467,7 +512,8 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
     std::vector<int> bg, bcol;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
       const int J = h->level_sns[x];
-      if (!h->is_small[J] && active(J) && h->sn[J].m > h->sn[J].k) bg.push_back(J);
+      if (dtop(J) && !in_group(h, J, h->rank)) continue;
+      if (!h->is_small[J] && (active(J) || dtop(J)) && h->sn[J].m > h->sn[J].k) bg.push_back(J);
     }
     const int nbc = h->opt.deterministic ? colour_supernodes(h, bg, bcol) : 1;
     if (!h->opt.deterministic) bcol.assign(bg.size(), 0);
@@ -480,14 +526,32 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         const SnInfo& I = h->sn[J];
         const int t = I.m - I.k;
         const int base = I.k & ~1;
+        const long long g0 = (long long)h->gtasks.size();
         for_tiles(base, I.m, base, I.m, [&](int r0, int c0) { h->gtasks.push_back(GTask{J, r0, c0, 0, 0, 0}); });
-        fs += (double)I.k * t * (t + 1);
-        bs += 8.0 * (double)t * I.k + 16.0 * 0.5 * t * (t + 1.0);
+        double frac = 1.0;
+        if (dtop(J)) {   // this rank's contiguous share of J's U tiles (super-tile order kept)
+          const long long nt = (long long)h->gtasks.size() - g0;
+          const int g = h->grp_hi[J] - h->grp_lo[J], i = h->rank - h->grp_lo[J];
+          const long long a = g0 + nt * i / g, b = g0 + nt * (i + 1) / g;
+          h->gtasks.erase(h->gtasks.begin() + b, h->gtasks.end());
+          h->gtasks.erase(h->gtasks.begin() + g0, h->gtasks.begin() + a);
+          frac = nt ? (double)(b - a) / (double)nt : 0.0;
+        }
+        fs += frac * (double)I.k * t * (t + 1);
+        bs += frac * (8.0 * (double)t * I.k + 16.0 * 0.5 * t * (t + 1.0));
       }
       push(K_SCATTER, s0g, (long long)h->gtasks.size(), fs, bs);
       if (h->opt.deterministic && !h->plan.empty() && h->plan.back().kind == K_SCATTER && h->plan.back().off == s0g)
         h->plan.back().aux = 1;
     }
+    if (top_markers)   // distributed supernodes of the level: the group's non-owned copies are dead now
+      for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
+        const int J = h->level_sns[x];
+        if (!dtop(J) || !in_group(h, J, h->rank)) continue;
+        Launch Z{0, 0, 0, 0, 0, OP_ZERO, SB, -1};
+        Z.aux = J;
+        h->plan.push_back(Z);
+      }
     h->plan_level.resize(h->plan.size(), l);
   }
   if (record_solve) h->small_level_off.push_back((int)h->small_sns.size());
@@ -578,6 +642,8 @@ static void build_plan(spchol_handle* h) {
     std::vector<int> lo, hi;
     proportional_map(S, work, h->world, h->owner, &lo, &hi);
     assign_top_owners(work, h->owner, lo, hi, S.level, h->world, h->top_owner);
+    h->grp_lo = lo;
+    h->grp_hi = hi;
     h->top_by_level.assign(S.nlevels, {});
     if (h->world > 1)
       for (int J = 0; J < ns; ++J) if (h->owner[J] < 0) h->top_by_level[S.level[J]].push_back(J);
@@ -615,6 +681,12 @@ static void build_plan(spchol_handle* h) {
     const SnInfo& I = h->sn[J];
     h->is_small[J] = I.k <= kmax && I.m <= SMALL_MAXM && (long long)I.m * I.k <= SMALL_MAXELEMS;
   }
+  // distributed top supernodes (multi-GPU): large enough that splitting the cdiv and U_J over the
+  // rank group beats the block-column broadcasts it costs
+  h->top_dist.assign(ns, 0);
+  if (h->world > 1 && (h->outer * NB) % TILE == 0 && h->opt.update_mode == 0)
+    for (int J = 0; J < ns; ++J)
+      h->top_dist[J] = h->owner[J] < 0 && h->grp_hi[J] - h->grp_lo[J] > 1 && !h->is_small[J] && work[J] >= h->dist_min_flops;
   // persistent diagonal-block inverse slots (factor TRSM + solve): non-top supernodes first
   h->slot_base.assign(ns, 0);
   {
@@ -657,6 +729,8 @@ static void build_plan(spchol_handle* h) {
     append_levels(h, [h, me](int J) { return h->owner[J] == me; }, false);
     h->plan_a_end = h->plan.size();
     append_levels(h, [h, me](int J) { return h->owner[J] < 0 && h->top_owner[J] == me; }, false, 0, true);
+    for (size_t i = h->plan_a_end; i < h->plan.size(); ++i)
+      if (h->plan[i].op == OP_TOP_LEVEL || h->plan[i].op == OP_BCAST) h->markers.push_back(i);
   } else {
     h->plan_a_end = h->plan.size();
   }
@@ -817,6 +891,7 @@ static int finish_handle(spchol_handle* h) {
   if (const char* e = getenv("SPCHOL_TMA")) h->use_tma = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_OUTER")) h->outer = std::max(1, atoi(e));
   if (const char* e = getenv("SPCHOL_SOLVE_LEGACY")) h->legacy_solve = atoi(e) != 0;
+  if (const char* e = getenv("SPCHOL_DIST_MINFLOPS")) h->dist_min_flops = atof(e);
   build_plan(h);
   if (h->opt.device < 0) return SPCHOL_OK;   // host-only analysis (no device state)
   int rc = setup_device(h);
@@ -956,18 +1031,65 @@ static int enqueue_top_reduce(spchol_handle* h, cudaStream_t st, int l) {
   if (!h->nccl_comm) return SPCHOL_OK;
   int r = g_nccl.group_start();
   if (r) return nccl_fail(r, "ncclGroupStart");
+  const int W = h->outer * h->nb;
   for (int P : h->top_by_level[l]) {
     const SnInfo& I = h->sn[P];
-    const size_t cnt = (size_t)I.ld * I.k;
-    r = g_nccl.reduce(h->d_panels + I.off, h->d_panels + I.off, cnt, NCCL_FLOAT64, NCCL_SUM, h->top_owner[P],
-                      h->nccl_comm, st);
-    if (r) { g_nccl.group_end(); return nccl_fail(r, "ncclReduce(top panel)"); }
+    for (int C = 0; C * W < I.k; ++C) {   // block columns onto their owners (whole panel if undistributed)
+      const int c0 = C * W, nc = h->top_dist[P] ? std::min(W, I.k - c0) : I.k;
+      double* p = h->d_panels + I.off + (size_t)c0 * I.ld;
+      r = g_nccl.reduce(p, p, (size_t)I.ld * nc, NCCL_FLOAT64, NCCL_SUM, blk_owner(h, P, C), h->nccl_comm, st);
+      if (r) { g_nccl.group_end(); return nccl_fail(r, "ncclReduce(top panel)"); }
+      if (!h->top_dist[P]) break;
+    }
   }
   r = g_nccl.group_end();
   if (r) return nccl_fail(r, "ncclGroupEnd");
-  for (int P : h->top_by_level[l])
-    if (h->top_owner[P] != h->rank)
-      CK(cudaMemsetAsync(h->d_panels + h->sn[P].off, 0, sizeof(double) * (size_t)h->sn[P].ld * h->sn[P].k, st));
+  for (int P : h->top_by_level[l]) {
+    const SnInfo& I = h->sn[P];
+    for (int C = 0; C * W < I.k; ++C) {
+      const int c0 = C * W, nc = h->top_dist[P] ? std::min(W, I.k - c0) : I.k;
+      if (blk_owner(h, P, C) != h->rank)
+        CK(cudaMemsetAsync(h->d_panels + I.off + (size_t)c0 * I.ld, 0, sizeof(double) * (size_t)I.ld * nc, st));
+      if (!h->top_dist[P]) break;
+    }
+  }
+  return SPCHOL_OK;
+}
+
+// Multi-GPU phase C, distributed top supernode J: column block C is final on its owner; it goes to
+// the other ranks of J's group (their trailing updates and U_J tiles read it).  One NCCL group of
+// sends on the owner, one receive on each other member; ranks outside the group have nothing to do.
+// Every rank issues these in the same (plan) order, so the point-to-point pairs always match.
+static int enqueue_bcast(spchol_handle* h, cudaStream_t st, int J, int C) {
+  if (!h->nccl_comm || !in_group(h, J, h->rank)) return SPCHOL_OK;
+  const int W = h->outer * h->nb, o = blk_owner(h, J, C);
+  const SnInfo& I = h->sn[J];
+  const int c0 = C * W, nc = std::min(W, I.k - c0);
+  double* p = h->d_panels + I.off + (size_t)c0 * I.ld;
+  const size_t cnt = (size_t)I.ld * nc;
+  int r = g_nccl.group_start();
+  if (r) return nccl_fail(r, "ncclGroupStart");
+  if (o == h->rank) {
+    for (int q = h->grp_lo[J]; q < h->grp_hi[J] && !r; ++q)
+      if (q != o) r = g_nccl.send(p, cnt, NCCL_FLOAT64, q, h->nccl_comm, st);
+  } else {
+    r = g_nccl.recv(p, cnt, NCCL_FLOAT64, o, h->nccl_comm, st);
+  }
+  int r2 = g_nccl.group_end();
+  if (r) return nccl_fail(r, "ncclSend/ncclRecv(block column)");
+  if (r2) return nccl_fail(r2, "ncclGroupEnd");
+  return SPCHOL_OK;
+}
+
+// After the level's scatter, a group member's copies of the blocks of J it does not own are zeroed
+// (so every factor entry is non-zero on exactly one rank: the solve's gather is a sum).
+static int enqueue_zero_nonowned(spchol_handle* h, cudaStream_t st, int J) {
+  const int W = h->outer * h->nb;
+  const SnInfo& I = h->sn[J];
+  for (int C = 0; C * W < I.k; ++C)
+    if (blk_owner(h, J, C) != h->rank)
+      CK(cudaMemsetAsync(h->d_panels + I.off + (size_t)C * W * I.ld, 0,
+                         sizeof(double) * (size_t)I.ld * std::min(W, I.k - C * W), st));
   return SPCHOL_OK;
 }
 
@@ -1013,6 +1135,16 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
     }
     if (L.op == OP_TOP_LEVEL) {
       int rc = enqueue_top_reduce(h, ls, L.aux);
+      if (rc) return rc;
+      continue;
+    }
+    if (L.op == OP_BCAST) {
+      int rc = enqueue_bcast(h, ls, L.aux, L.aux2);
+      if (rc) return rc;
+      continue;
+    }
+    if (L.op == OP_ZERO) {
+      int rc = enqueue_zero_nonowned(h, ls, L.aux);
       if (rc) return rc;
       continue;
     }
@@ -1306,6 +1438,13 @@ extern "C" int spchol_query(const spchol_handle* h, int key, int64_t* value) {
     }
     case SPCHOL_Q_UPDATE_ENTRIES: *value = (int64_t)h->update_entries; break;
     case SPCHOL_Q_NBLOCKS: *value = (int64_t)S.blk_q.size(); break;
+    case SPCHOL_Q_NMARKERS: *value = (int64_t)h->markers.size(); break;
+    case SPCHOL_Q_NTOP_DIST: {
+      int64_t c = 0;
+      for (char d : h->top_dist) c += d != 0;
+      *value = c;
+      break;
+    }
     default: return fail(SPCHOL_ERR_VALIDATION, "unknown query key");
   }
   return SPCHOL_OK;
@@ -1531,15 +1670,14 @@ extern "C" int spchol_factor_phase(spchol_handle* h, int phase) {
       if (!rc) h->gathered = true;
       break;
     default: {
-      // 1000 + l: this rank's owned top supernodes of level l (the ops after that level's marker)
-      if (phase < 1000 || h->world == 1) return fail(SPCHOL_ERR_VALIDATION, "phase must be 1, 2, 3 or 1000 + level");
-      const int l = phase - 1000;
-      size_t b = h->plan.size(), e = h->plan.size();
-      for (size_t i = h->plan_a_end; i < h->plan.size(); ++i)
-        if (h->plan[i].op == OP_TOP_LEVEL) {
-          if (h->plan[i].aux == l) b = i + 1;
-          else if (b < e && i > b) { e = i; break; }
-        }
+      // 2000 + i: segment i of phase C, the plan entries between marker i-1 and marker i (the
+      // exchange of marker i is then played by spchol_dist_debug_comm)
+      const long long nm = (long long)h->markers.size();
+      if (phase < 2000 || phase - 2000 > nm || h->world == 1)
+        return fail(SPCHOL_ERR_VALIDATION, "phase must be 1, 2, 3 or 2000 + segment (segment <= markers)");
+      const long long i = phase - 2000;
+      const size_t b = i == 0 ? h->plan_a_end : h->markers[i - 1] + 1;
+      const size_t e = i < nm ? h->markers[i] : h->plan.size();
       if (b < e) rc = enqueue_ops(h, h->stream, b, e);
       break;
     }
@@ -1578,6 +1716,74 @@ extern "C" int spchol_dist_debug_accumulate(spchol_handle* dst, const spchol_han
   launch_axpy(sp, d, cnt, dst->stream);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(dst->stream));
+  return SPCHOL_OK;
+}
+
+extern "C" int spchol_dist_debug_comm(spchol_handle* const* hs, int world, int marker) {
+  if (!hs || world < 2) return fail(SPCHOL_ERR_VALIDATION, "need world >= 2 handles");
+  for (int r = 0; r < world; ++r) {
+    if (!hs[r] || host_only(hs[r])) return fail(SPCHOL_ERR_VALIDATION, "NULL or host-only handle");
+    if (hs[r]->world != world || hs[r]->rank != r || hs[r]->opt.device != hs[0]->opt.device ||
+        hs[r]->panel_doubles != hs[0]->panel_doubles || hs[r]->markers.size() != hs[0]->markers.size())
+      return fail(SPCHOL_ERR_VALIDATION, "handles must be ranks 0..world-1 of one problem on one device");
+  }
+  const spchol_handle* h0 = hs[0];
+  if (marker < 0 || marker >= (int)h0->markers.size()) return fail(SPCHOL_ERR_VALIDATION, "marker out of range");
+  const Launch& M = h0->plan[h0->markers[marker]];
+  for (int r = 1; r < world; ++r) {
+    const Launch& Mr = hs[r]->plan[hs[r]->markers[marker]];
+    if (Mr.op != M.op || Mr.aux != M.aux || Mr.aux2 != M.aux2) return fail(SPCHOL_ERR_STATE, "marker sequences differ between ranks");
+  }
+  CK(cudaSetDevice(h0->opt.device));
+  for (int r = 0; r < world; ++r) CK(cudaStreamSynchronize(hs[r]->stream));
+  const int W = h0->outer * h0->nb;
+  auto block = [&](int r, int J, int C, long long& cnt) {
+    const SnInfo& I = hs[r]->sn[J];
+    const int c0 = h0->top_dist[J] ? C * W : 0, nc = h0->top_dist[J] ? std::min(W, I.k - c0) : I.k;
+    cnt = (long long)I.ld * nc;
+    return hs[r]->d_panels + I.off + (size_t)c0 * I.ld;
+  };
+  if (M.op == OP_TOP_LEVEL) {          // per block column: sum onto the owner, other copies zeroed
+    for (int P : h0->top_by_level[M.aux])
+      for (int C = 0; C * W < h0->sn[P].k; ++C) {
+        const int o = blk_owner(h0, P, C);
+        long long cnt = 0;
+        double* dst = block(o, P, C, cnt);
+        for (int r = 0; r < world; ++r) {
+          if (r == o) continue;
+          double* src = block(r, P, C, cnt);
+          launch_axpy(src, dst, cnt, hs[o]->stream);
+          CK(cudaStreamSynchronize(hs[o]->stream));
+          CK(cudaMemset(src, 0, sizeof(double) * (size_t)cnt));
+        }
+        if (!h0->top_dist[P]) break;
+      }
+  } else {                             // OP_BCAST: owner's block column to the rest of the group
+    const int J = M.aux, C = M.aux2, o = blk_owner(h0, J, C);
+    long long cnt = 0;
+    const double* src = block(o, J, C, cnt);
+    for (int q = h0->grp_lo[J]; q < h0->grp_hi[J]; ++q)
+      if (q != o) CK(cudaMemcpy(block(q, J, C, cnt), src, sizeof(double) * (size_t)cnt, cudaMemcpyDeviceToDevice));
+  }
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return SPCHOL_OK;
+}
+
+extern "C" int spchol_dist_plan_flops(const spchol_handle* h, double* phase_a, double* top_level) {
+  if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
+  if (phase_a) *phase_a = 0;
+  if (top_level) for (int l = 0; l < h->S.nlevels; ++l) top_level[l] = 0;
+  if (h->world == 1) {
+    if (phase_a) for (size_t i = h->plan_factor_begin; i < h->plan_all_end; ++i) if (h->plan[i].op == OP_LAUNCH) *phase_a += h->plan[i].flops;
+    return SPCHOL_OK;
+  }
+  for (size_t i = h->plan_all_end; i < h->plan.size(); ++i) {
+    const Launch& L = h->plan[i];
+    if (L.op != OP_LAUNCH) continue;
+    if (i < h->plan_a_end) { if (phase_a) *phase_a += L.flops; }
+    else if (top_level) top_level[h->plan_level[i]] += L.flops;
+  }
   return SPCHOL_OK;
 }
 

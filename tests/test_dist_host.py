@@ -93,3 +93,34 @@ def test_mapping_single_process_properties():
         assert (owner == 0).all() and top_off == h.query("PANEL_DOUBLES")
     with pytest.raises(sp.SpcholError):
         sp.Solver.from_problem(p, device=-1, dist_world=2, dist_rank=2)
+
+
+def _plan_work(p, W, r):
+    with sp.Solver.from_problem(p, device=-1, dist_world=W, dist_rank=r) as h:
+        a, lv = h.spchol_dist_plan_flops()
+        return a, lv, h.query("NMARKERS"), h.query("NTOP_DIST"), h.query("FLOPS_EXEC")
+
+
+@pytest.mark.parametrize("name,minflops,outer", [("S4", "0", None), ("S5", "0", "1"), ("C1", "0", "1"),
+                                                  ("S4", None, None), ("S2", "0", "1")])
+def test_distributed_top_plan_partitions_work(name, minflops, outer, monkeypatch):
+    """Distributed top (block-column cyclic cdiv, U_J tiles split over the group): every task of the
+    single-GPU plan runs on exactly one rank — the executed flops of all ranks' plans (phase A + phase
+    C) add up to the whole factor's — and all ranks hold the same number of exchange markers."""
+    if minflops is not None:
+        monkeypatch.setenv("SPCHOL_DIST_MINFLOPS", minflops)
+    if outer is not None:
+        monkeypatch.setenv("SPCHOL_OUTER", outer)
+    p = gen.make(name)
+    with sp.Solver.from_problem(p, device=-1) as h:
+        whole, _ = h.spchol_dist_plan_flops()
+    for W in (2, 3, 4, 8):
+        res = [_plan_work(p, W, r) for r in range(W)]
+        tot = sum(a + lv.sum() for a, lv, *_ in res)
+        assert abs(tot - whole) <= 1e-9 * whole, (W, tot, whole)
+        assert len({m for _, _, m, _, _ in res}) == 1
+        if minflops == "0" and name != "C1":     # C1's top supernodes all take the fused small path
+            assert res[0][3] > 0
+        # distributing the top never makes the critical rank path longer than the fan-in schedule
+        crit = max(a for a, *_ in res) + sum(max(r_[1][l] for r_ in res) for l in range(len(res[0][1])))
+        assert crit <= whole

@@ -118,13 +118,23 @@ def test_edge_cases():
     run_parity(gen.from_dense_lower(D))
 
 
-@pytest.mark.parametrize("name,world", [("S4", 2), ("S5", 3), ("C1", 2), ("S2", 4), ("T3", 2), ("S4", 8)])
-def test_distributed_dataflow_single_gpu(name, world):
+@pytest.mark.parametrize("name,world,minflops,outer", [
+    ("S4", 2, None, None), ("S5", 3, None, None), ("C1", 2, None, None), ("S2", 4, None, None), ("T3", 2, None, None),
+    ("S4", 8, None, None),
+    # distributed top supernodes (block-column cyclic cdiv + block-column sends + U_J tiles split)
+    ("S4", 2, "0", None), ("S4", 4, "0", "1"), ("S5", 3, "0", "1"), ("S2", 4, "0", "1"), ("T3", 2, "0", "1"),
+    ("S4", 8, "0", "1"), ("S5", 8, "0", None)])
+def test_distributed_dataflow_single_gpu(name, world, minflops, outer, monkeypatch):
     """The multi-GPU data flow played by `world` handles on one GPU through the diagnostics API:
-    phase A per rank; then per top level, the fan-in of every top panel onto its owner (NCCL
-    reduce in production, the accumulate call here, source copies zeroed) and each rank's owned
-    top supernodes; finally the gather (sum of all arenas and inverses).  The assembled factor must
-    match the oracle like the single-GPU one."""
+    phase A per rank; then phase C segment by segment, each exchange marker played between the
+    handles (spchol_dist_debug_comm: the level-start reduce of the top panels onto their block-column
+    owners, other copies zeroed; the send of a finished block column of a distributed top supernode to
+    its group); finally the gather (sum of all arenas and inverses).  The assembled factor must match
+    the oracle like the single-GPU one."""
+    if minflops is not None:
+        monkeypatch.setenv("SPCHOL_DIST_MINFLOPS", minflops)
+    if outer is not None:
+        monkeypatch.setenv("SPCHOL_OUTER", outer)
     prob = gen.make(name)
     o = oracle.Oracle.from_problem(prob)
     assert o.factor() == -1
@@ -134,16 +144,17 @@ def test_distributed_dataflow_single_gpu(name, world):
         for h in hs:
             h.spchol_factor_phase(1)
         owner, towner, _, _ = hs[0].spchol_export_mapping(with_top_owner=True)
-        level = hs[0].spchol_export_symbolic()["level"]
         assert np.all((owner >= 0) | (towner >= 0))
-        for l in sorted(set(level[owner < 0].tolist())):
-            for P in np.where((owner < 0) & (level == l))[0]:
-                dst = int(towner[P])
-                for r in range(world):
-                    if r != dst:
-                        hs[dst].spchol_dist_debug_accumulate(hs[r], 16 + int(P))
+        nm = hs[0].query("NMARKERS")
+        assert all(h.query("NMARKERS") == nm for h in hs)
+        if minflops == "0" and name in ("S2", "S4", "S5"):   # (C1's and T3's tops take the small path)
+            assert hs[0].query("NTOP_DIST") > 0
+        for i in range(nm):
             for h in hs:
-                h.spchol_factor_phase(1000 + l)
+                h.spchol_factor_phase(2000 + i)
+            sp.spchol_dist_debug_comm(hs, i)
+        for h in hs:
+            h.spchol_factor_phase(2000 + nm)
         for h in hs[1:]:
             hs[0].spchol_dist_debug_accumulate(h, 1)      # gather panels
             hs[0].spchol_dist_debug_accumulate(h, 2)      # and diagonal inverses
