@@ -794,6 +794,234 @@ __global__ void __launch_bounds__(POTRF4_THREADS) potrf4_kernel(const PTask* __r
   }
 }
 
+// ----------------------------------------------------------------------------------------------
+// potrf8_kernel (default): the same contract as potrf4_kernel, blocked so that the sequential part
+// is short.  The 64x64 block (padding rows/columns >= nb are an identity) sits in shared memory,
+// row-major, and is factored right-looking in 8-column panels:
+//   * the 8x8 diagonal block of panel p is factored by ONE thread in registers (8 dependent
+//     rsqrt steps, no barrier);
+//   * TRSM: one thread per row below it, 8-step row substitution with the reciprocal pivots;
+//   * SYRK: 4x4 register tiles of the trailing lower triangle, K = 8.  Thread 0 owns the three
+//     tiles of the next diagonal block and factors it as soon as they are updated, while the
+//     others finish the trailing update (two barriers per panel).
+// The inverse X = L^{-1} (kept for TRSM-as-GEMM and the solve) is then formed by blocked
+// doubling: the eight 8x8 diagonal blocks by substitution (one thread each), then for h = 8, 16,
+// 32: X21 = -(X22 L21) X11 for each 2h x 2h diagonal block — small parallel matrix products;
+// T = X22 L21 is parked transposed in the unused upper triangle of the L buffer.
+// ----------------------------------------------------------------------------------------------
+constexpr int P8_LD = NBMAX + 1;              // row stride (doubles) of the shared buffers
+constexpr int POTRF8_THREADS = 128;
+constexpr int POTRF8_SMEM = (2 * NBMAX * P8_LD + NBMAX) * (int)sizeof(double);
+
+// Factor the 8x8 diagonal block at (b, b) of As in registers; pivots' reciprocals into rl.
+__device__ __forceinline__ void p8_diag(double* As, double* rl, int b, int nb, int& bad) {
+  double a[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) a[i][j] = As[(b + i) * P8_LD + b + j];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double d = a[j][j];
+    if (bad < 0 && b + j < nb && !(d > 0.0)) bad = b + j;
+    const double r = rsqrt_nr(d);
+    a[j][j] = d * r;
+    rl[b + j] = r;
+#pragma unroll
+    for (int i = j + 1; i < 8; ++i) a[i][j] *= r;
+#pragma unroll
+    for (int q = j + 1; q < 8; ++q)
+#pragma unroll
+      for (int i = q; i < 8; ++i) a[i][q] = fma(-a[i][j], a[q][j], a[i][q]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) As[(b + i) * P8_LD + b + j] = a[i][j];
+}
+
+// One 4x4 tile (rows r0.., cols c0..) of the trailing update A -= L_p L_p^T, panel columns [b, b+8).
+__device__ __forceinline__ void p8_syrk_tile(double* As, int b, int r0, int c0) {
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = As[(r0 + i) * P8_LD + c0 + j];
+#pragma unroll
+  for (int q = 0; q < 8; q += 2) {
+    double2 lr[4], lc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {      // rows r0+i and c0+i, panel columns q, q+1
+      lr[i] = make_double2(As[(r0 + i) * P8_LD + b + q], As[(r0 + i) * P8_LD + b + q + 1]);
+      lc[i] = make_double2(As[(c0 + i) * P8_LD + b + q], As[(c0 + i) * P8_LD + b + q + 1]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fma(-lr[i].y, lc[j].y, fma(-lr[i].x, lc[j].x, acc[i][j]));
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (r0 + i >= c0 + j) As[(r0 + i) * P8_LD + c0 + j] = acc[i][j];   // upper part of diagonal tiles unused
+}
+
+// Doubling step of the inverse for all 2h x 2h diagonal blocks (a = 0, 2h, ...), TR x TC outputs per
+// thread (TR * TC * POTRF8_THREADS = 32 h).  Upper triangles of X are zero, so the triangular sums
+// run over whole ranges without masks.
+template <int H, int TR, int TC>
+__device__ __forceinline__ void p8_double(double* As, double* Xs, int tid) {
+  constexpr int TPR = H / TC, TPB = (H / TR) * TPR;   // threads per tile row, per block
+  const int a = (tid / TPB) * 2 * H, t = tid % TPB;
+  const int r0 = (t / TPR) * TR, c0 = (t % TPR) * TC;
+  double acc[TR][TC];
+  // T = X22 L21 (rows r0.., cols c0..), parked transposed at As(a + c, a + H + r)
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TC; ++j) acc[i][j] = 0.0;
+  for (int q = 0; q < r0 + TR; ++q) {
+    double x[TR], l[TC];
+#pragma unroll
+    for (int i = 0; i < TR; ++i) x[i] = Xs[(a + H + r0 + i) * P8_LD + a + H + q];
+#pragma unroll
+    for (int j = 0; j < TC; ++j) l[j] = As[(a + H + q) * P8_LD + a + c0 + j];
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int j = 0; j < TC; ++j) acc[i][j] = fma(x[i], l[j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TC; ++j) As[(a + c0 + j) * P8_LD + a + H + r0 + i] = acc[i][j];
+  __syncthreads();
+  // X21 = -T X11
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TC; ++j) acc[i][j] = 0.0;
+  for (int q = c0; q < H; ++q) {
+    double tt[TR], x[TC];
+#pragma unroll
+    for (int i = 0; i < TR; ++i) tt[i] = As[(a + q) * P8_LD + a + H + r0 + i];
+#pragma unroll
+    for (int j = 0; j < TC; ++j) x[j] = Xs[(a + q) * P8_LD + a + c0 + j];
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int j = 0; j < TC; ++j) acc[i][j] = fma(tt[i], x[j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TC; ++j) Xs[(a + H + r0 + i) * P8_LD + a + c0 + j] = -acc[i][j];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* __restrict__ tasks,
+                                                                const SnInfo* __restrict__ sn,
+                                                                const int* __restrict__ sfirst, double* panels,
+                                                                double* linv, unsigned long long* fail) {
+  extern __shared__ double p8_smem[];
+  double* As = p8_smem;                        // L (lower), T scratch (upper, transposed)
+  double* Xs = As + NBMAX * P8_LD;             // X = L^{-1} (lower)
+  double* rl = Xs + NBMAX * P8_LD;             // reciprocal pivots 1 / L_jj
+  const PTask T = tasks[blockIdx.x];
+  const SnInfo S = sn[T.sn];
+  const int nb = T.nb, tid = threadIdx.x;
+  double* P = panels + S.off + (long long)T.c0 * S.ld + T.c0;
+  // all loads in flight at once (8-byte cp.async into the row-major buffer), padding = identity
+  for (int e = tid; e < NBMAX * NBMAX; e += POTRF8_THREADS) {
+    const int c = e / NBMAX, r = e % NBMAX;     // consecutive threads: consecutive rows (coalesced)
+    if (r < c) continue;
+    double* d = As + r * P8_LD + c;
+    if (r < nb && c < nb) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(d);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(P + (long long)c * S.ld + r));
+    } else {
+      *d = r == c ? 1.0 : 0.0;
+    }
+  }
+  for (int e = tid; e < NBMAX * P8_LD; e += POTRF8_THREADS) Xs[e] = 0.0;
+  asm volatile("cp.async.wait_all;\n" ::);
+  __syncthreads();
+  int bad = -1;
+  if (tid == 0) p8_diag(As, rl, 0, nb, bad);
+  __syncthreads();
+  for (int p = 0; p < NBMAX / 8; ++p) {
+    const int b = 8 * p, t0 = b + 8, nt = NBMAX - t0;
+    // TRSM: rows t0 + tid of panel p
+    if (tid < nt) {
+      const int r = t0 + tid;
+      double x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = As[r * P8_LD + b + j];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+#pragma unroll
+        for (int q = 0; q < j; ++q) x[j] = fma(-x[q], As[(b + j) * P8_LD + b + q], x[j]);
+        x[j] *= rl[b + j];
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) As[r * P8_LD + b + j] = x[j];
+    }
+    __syncthreads();
+    if (nt > 0) {
+      // SYRK on 4x4 tiles of the trailing triangle; tiles 0-2 = the next diagonal block (thread 0)
+      const int n4 = nt / 4, ntiles = n4 * (n4 + 1) / 2;
+      if (tid < 32) {    // warp 0: the next diagonal block — three tiles, then thread 0 factors it
+        if (tid < 3) p8_syrk_tile(As, b, t0 + (tid ? 4 : 0), t0 + (tid == 2 ? 4 : 0));
+        __syncwarp();
+        if (tid == 0) p8_diag(As, rl, t0, nb, bad);
+      } else {           // warps 1-3: the rest of the trailing update
+        for (int t = tid - 29; t < ntiles; t += POTRF8_THREADS - 32) {
+          int ti = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);   // t = ti (ti + 1) / 2 + tj
+          while (ti * (ti + 1) / 2 > t) --ti;
+          while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+          const int tj = t - ti * (ti + 1) / 2;
+          p8_syrk_tile(As, b, t0 + 4 * ti, t0 + 4 * tj);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[T.sn] + T.c0 + bad));
+  // inverse, level 0: the eight 8x8 diagonal blocks (column-oriented substitution per block)
+  if (tid < NBMAX / 8) {
+    const int b = 8 * tid;
+    double x[8][8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      x[c][c] = rl[b + c];
+#pragma unroll
+      for (int r = c + 1; r < 8; ++r) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = c; q < r; ++q) acc = fma(As[(b + r) * P8_LD + b + q], x[q][c], acc);
+        x[r][c] = -acc * rl[b + r];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c <= r; ++c) Xs[(b + r) * P8_LD + b + c] = x[r][c];
+  }
+  __syncthreads();
+  // doubling: for every 2h block at a, X21 = -(X22 L21) X11 (h x h, rows a+h.., columns a..)
+  p8_double<8, 1, 2>(As, Xs, tid);
+  p8_double<16, 2, 2>(As, Xs, tid);
+  p8_double<32, 2, 4>(As, Xs, tid);
+  double* W = linv + (long long)T.slot * (NBMAX * NBMAX);
+  for (int e = tid; e < NBMAX * NBMAX; e += POTRF8_THREADS) {
+    const int c = e / NBMAX, r = e % NBMAX;
+    const bool in = r >= c && r < nb && c < nb;
+    if (in) P[(long long)c * S.ld + r] = As[r * P8_LD + c];
+    W[e] = in ? Xs[r * P8_LD + c] : 0.0;
+  }
+}
+
 __global__ void init_scatter_kernel(const double* __restrict__ vals, const long long* __restrict__ amap,
                                     long long nnz, double* panels) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz; e += (long long)gridDim.x * blockDim.x) {
@@ -1216,6 +1444,7 @@ __global__ void gather_kernel(const double* __restrict__ src, const long long* _
 cudaError_t kernels_init_attributes() {
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(potrf8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF8_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_MAXELEMS * (int)sizeof(double)))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_RLB>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
@@ -1282,8 +1511,10 @@ void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels, double* linv,
                   unsigned long long* fail, cudaStream_t st, int prio) {
   if (ntasks <= 0) return;
-#if SPCHOL_POTRF4
+#if SPCHOL_POTRF4 == 2
   launch_prio(potrf4_kernel, ntasks, POTRF4_THREADS, 0, st, prio, tasks, sn, sfirst, panels, linv, fail);
+#elif SPCHOL_POTRF4
+  launch_prio(potrf8_kernel, ntasks, POTRF8_THREADS, POTRF8_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
 #else
   launch_prio(potrf_kernel, ntasks, POTRF_THREADS, POTRF_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
 #endif
