@@ -122,6 +122,7 @@ struct Launch {
   int op = OP_LAUNCH, stream = 0, ev = -1;
   int aux = 0;     // K_SMALL: dynamic shared memory (doubles); K_SCATTER: 1 = plain RMW (deterministic)
   int aux2 = 0;    // K_SMALL: largest m in the launch
+  int aux3 = 0;    // K_SMALL: largest k in the launch if it runs one warp per supernode, else 0
 };
 template <class T>
 cudaError_t dalloc(T** p, size_t count) {
@@ -190,6 +191,8 @@ struct spchol_handle {
   int nevents = 0;
   bool no_lookahead = false;     // SPCHOL_NO_LOOKAHEAD=1 (diagnostics)
   int max_level = -1;            // SPCHOL_MAX_LEVEL=l: factor only levels <= l (diagnostics)
+  bool small_warp = true;        // SPCHOL_SMALL_WARP=0: CTA-per-supernode small kernel for every size
+  int small_warp_maxm = 64;      // largest m of the warp-per-supernode kernel (SPCHOL_SMALL_WARP_MAXM <= 128)
   bool use_tma = false;          // SPCHOL_TMA=1: TMA + mbarrier tile kernels (measured ~2% slower)
   void* d_tmaps = nullptr;       // CUtensorMap per supernode panel (TMA boxes 16 x 8, 128B swizzle)
   void* d_tmap_linv = nullptr;   // CUtensorMap over the diagonal-inverse slots
@@ -322,7 +325,15 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
     // lets as many CTAs as possible be resident
     {
       if (record_solve) h->small_level_off.push_back((int)h->small_sns.size());
+      // warp kernel (m <= 128): one launch per rows-per-lane class; CTA kernel (m > 128, or
+      // SPCHOL_SMALL_WARP=0): buckets by m k
       static const int bucket_max[] = {256, 1024, 4096, SMALL_MAXELEMS};
+      auto bucket = [&](const SnInfo& I) {
+        if (h->small_warp && I.m <= h->small_warp_maxm) return I.m <= 32 ? 0 : (I.m <= 64 ? 1 : 2);
+        const int mk = I.m * I.k;
+        return 3 + (mk <= 256 ? 0 : mk <= 1024 ? 1 : mk <= 4096 ? 2 : 3);
+      };
+      (void)bucket_max;
       bool forked = false;
       std::vector<int> sm, scol;
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x)
@@ -330,19 +341,20 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       const int nsc = h->opt.deterministic ? colour_supernodes(h, sm, scol) : 1;
       if (!h->opt.deterministic) scol.assign(sm.size(), 0);
       for (int col = 0; col < nsc; ++col)
-      for (int bk = 0; bk < 4; ++bk) {
+      for (int bk = 0; bk < 7; ++bk) {
         long long s0 = (long long)h->small_sns.size();
-        int mx = 0, mxm = 0;
+        int mx = 0, mxm = 0, mxk = 0;
         double fsm = 0, bsm = 0;
         for (size_t x = 0; x < sm.size(); ++x) {
           const int J = sm[x];
           if (scol[x] != col) continue;
           const SnInfo& I = h->sn[J];
           const int mk = I.m * I.k;
-          if (mk > bucket_max[bk] || (bk > 0 && mk <= bucket_max[bk - 1])) continue;
+          if (bucket(I) != bk) continue;
           h->small_sns.push_back(J);
           mx = std::max(mx, mk);
           mxm = std::max(mxm, I.m);
+          mxk = std::max(mxk, I.k);
           const double t = I.m - I.k;
           for (int c = 0; c < I.k; ++c) fsm += (double)(I.m - c) * (double)(I.m - c);
           bsm += 16.0 * I.m * I.k + 16.0 * 0.5 * t * (t + 1);
@@ -358,6 +370,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         Launch L{K_SMALL, s0, (int)(s1 - s0), fsm, bsm, OP_LAUNCH, SB + 1, -1};
         L.aux = mx;
         L.aux2 = mxm;
+        L.aux3 = bk < 3 ? mxk : 0;
         h->plan.push_back(L);
       }
     }
@@ -892,6 +905,8 @@ static int finish_handle(spchol_handle* h) {
   if (const char* e = getenv("SPCHOL_OUTER")) h->outer = std::max(1, atoi(e));
   if (const char* e = getenv("SPCHOL_SOLVE_LEGACY")) h->legacy_solve = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_DIST_MINFLOPS")) h->dist_min_flops = atof(e);
+  if (const char* e = getenv("SPCHOL_SMALL_WARP")) h->small_warp = atoi(e) != 0;
+  if (const char* e = getenv("SPCHOL_SMALL_WARP_MAXM")) h->small_warp_maxm = std::max(0, std::min(128, atoi(e)));
   build_plan(h);
   if (h->opt.device < 0) return SPCHOL_OK;   // host-only analysis (no device state)
   int rc = setup_device(h);
@@ -1156,7 +1171,7 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
         break;
       case K_SMALL:
         launch_small(h->d_small_sns + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_ucol_base, h->d_ucol_map,
-                     h->d_posmap, h->d_fail, L.aux, L.aux2, h->opt.deterministic ? 1 : 0, ls, prio);
+                     h->d_posmap, h->d_fail, L.aux, L.aux2, h->opt.deterministic ? 1 : 0, ls, prio, L.aux3);
         break;
       case K_POTRF:
         launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio);

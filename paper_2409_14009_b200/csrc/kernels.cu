@@ -659,6 +659,132 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
 }
 
 // ----------------------------------------------------------------------------------------------
+// small_warp_kernel<R>: the whole RL step of one small supernode per WARP (m_J <= 32 R, k_J <= 64),
+// for the bulk of the tiny supernodes of 2D problems (C2: 205K of its 238K supernodes have m <= 64).
+// Lane owns panel rows r = lane + 32 i (i < R).  No block barriers: the panel (column-major, ld =
+// 32 R) is staged in shared memory by 8-byte cp.async (rows >= m zero-filled), factored
+// LEFT-looking column by column (column j = A(:, j) - L(:, 0:j) L(j, 0:j)^T from shared memory,
+// the pivot broadcast by shuffle, __syncwarp between columns), written back, then U_J = L_R L_R^T
+// is formed four columns at a time and RED-scattered through relind (consecutive lanes ->
+// consecutive U rows -> mostly consecutive ancestor rows).
+// ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ double rsqrt_nr(double d);
+
+template <int R>
+__global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ sns, const SnInfo* __restrict__ sn,
+                                                        const int* __restrict__ sfirst, double* panels,
+                                                        const long long* __restrict__ ucol_base,
+                                                        const long long* __restrict__ ucol_map,
+                                                        const int* __restrict__ posmap, unsigned long long* fail,
+                                                        int plain) {
+  constexpr int LD = 32 * R + 4;        // 4 mod 16 doubles: conflict-free DMMA fragment loads
+  extern __shared__ double Pw[];        // k4 x LD, column-major (columns >= k zero), then U staging
+  const int J = sns[blockIdx.x];
+  const SnInfo S = sn[J];
+  const int m = S.m, k = S.k, t = m - k, lane = threadIdx.x, k4 = (k + 3) & ~3;
+  double* G = panels + S.off;
+  for (int c = 0; c < k4; ++c)
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = lane + 32 * i;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(Pw + c * LD + r);
+      const bool in = r < m && r >= c && c < k;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(in ? G + (long long)c * S.ld + r : G),
+                   "r"(in ? 8 : 0));
+    }
+  asm volatile("cp.async.wait_all;\n" ::);
+  __syncwarp();
+  int bad = -1;
+  for (int j = 0; j < k; ++j) {
+    double a0[R], a1[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) { a0[i] = Pw[j * LD + lane + 32 * i]; a1[i] = 0.0; }
+    int q = 0;
+    for (; q + 1 < j; q += 2) {           // two accumulator chains
+      const double l0 = Pw[q * LD + j], l1 = Pw[(q + 1) * LD + j];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        a0[i] = fma(-Pw[q * LD + lane + 32 * i], l0, a0[i]);
+        a1[i] = fma(-Pw[(q + 1) * LD + lane + 32 * i], l1, a1[i]);
+      }
+    }
+    if (q < j) {
+      const double l0 = Pw[q * LD + j];
+#pragma unroll
+      for (int i = 0; i < R; ++i) a0[i] = fma(-Pw[q * LD + lane + 32 * i], l0, a0[i]);
+    }
+    double dj = 0.0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      a0[i] += a1[i];
+      if (i == (j >> 5)) dj = a0[i];
+    }
+    const double d = __shfl_sync(0xffffffffu, dj, j & 31);
+    const double rl = rsqrt_nr(d);
+    if (bad < 0 && !(d > 0.0)) bad = j;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = lane + 32 * i;
+      if (r > j) Pw[j * LD + r] = a0[i] * rl;
+      else if (r == j) Pw[j * LD + r] = d * rl;
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[J] + bad));
+  for (int c = 0; c < k; ++c)
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = lane + 32 * i;
+      if (r < m && r >= c) G[(long long)c * S.ld + r] = Pw[c * LD + r];
+    }
+  if (t <= 0) return;
+  // U_J = L_R L_R^T on the FP64 tensor core: per 8-column block Jc, the 8x8 tiles I >= Jc (DMMA
+  // m8n8k4 over K = k4), staged in shared memory, then RED-scattered column by column with lanes
+  // over rows (runs of consecutive ancestor rows).  U row r = panel row k + r.
+  double* Ust = Pw + LD * k4;           // 8 x 32 R
+  const int g = lane >> 2, tg = lane & 3, nt8 = (t + 7) >> 3;
+  for (int Jc = 0; Jc < nt8; ++Jc) {
+    double acc[4 * R][2];
+#pragma unroll
+    for (int I = 0; I < 4 * R; ++I) acc[I][0] = acc[I][1] = 0.0;
+    const int rb = k + 8 * Jc + g;
+    for (int q = 0; q < k4; q += 4) {
+      const double b = rb < m ? Pw[(q + tg) * LD + rb] : 0.0;
+#pragma unroll
+      for (int I = 0; I < 4 * R; ++I) {
+        if (I < Jc || I >= nt8) continue;   // warp-uniform
+        const int ra = k + 8 * I + g;
+        dmma(acc[I], ra < m ? Pw[(q + tg) * LD + ra] : 0.0, b);
+      }
+    }
+#pragma unroll
+    for (int I = 0; I < 4 * R; ++I) {
+      if (I < Jc || I >= nt8) continue;
+      Ust[(2 * tg) * (32 * R) + 8 * I + g] = acc[I][0];
+      Ust[(2 * tg + 1) * (32 * R) + 8 * I + g] = acc[I][1];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c8 = 0; c8 < 8; ++c8) {
+      const int c = 8 * Jc + c8;
+      if (c >= t) break;
+      const long long cbase = ucol_base[S.ucol + c];
+      const long long mbase = ucol_map[S.ucol + c];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int r = lane + 32 * i;
+        if (r >= t || r < c) continue;
+        double* d = panels + cbase + posmap[mbase + k + r];
+        const double u = Ust[c8 * (32 * R) + r];
+        if (plain) *d -= u;               // deterministic mode: conflict-free launch
+        else atomicAdd(d, -u);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ----------------------------------------------------------------------------------------------
 // potrf4_kernel: the same contract as potrf_kernel with a flatter dependency chain: 160 threads,
 // thread t < 136 owns one 4x4 register tile (bi, bj), bi >= bj, of the 64x64 lower triangle.
 // Cholesky, right-looking, step j: the owners of column j publish it (double-buffered shared
@@ -1445,6 +1571,9 @@ cudaError_t kernels_init_attributes() {
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(potrf8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF8_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(small_warp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 1 + 4) * SMALL_MAXK + 8 * 32 * 1) * 8))) return e;
+  if ((e = cudaFuncSetAttribute(small_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 2 + 4) * SMALL_MAXK + 8 * 32 * 2) * 8))) return e;
+  if ((e = cudaFuncSetAttribute(small_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 4 + 4) * SMALL_MAXK + 8 * 32 * 4) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_MAXELEMS * (int)sizeof(double)))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_RLB>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
@@ -1522,8 +1651,16 @@ void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* s
 
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,
                   const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,
-                  int smem_doubles, int maxm, int plain, cudaStream_t st, int prio) {
+                  int smem_doubles, int maxm, int plain, cudaStream_t st, int prio, int maxk) {
   if (count <= 0) return;
+  if (maxk > 0 && maxm <= 128) {   // one warp per supernode
+    const int R = maxm <= 32 ? 1 : (maxm <= 64 ? 2 : 4);
+    const int sm = ((32 * R + 4) * ((maxk + 3) & ~3) + 8 * 32 * R) * (int)sizeof(double);
+    if (R == 1) launch_prio(small_warp_kernel<1>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);
+    else if (R == 2) launch_prio(small_warp_kernel<2>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);
+    else launch_prio(small_warp_kernel<4>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);
+    return;
+  }
   // one thread per panel row: blockDim = the launch's largest m rounded up to a warp (<= 256)
   const int threads = std::min(SMALL_THREADS, std::max(32, (maxm + 31) / 32 * 32));
   launch_prio(small_kernel, count, threads, smem_doubles * (int)sizeof(double), st, prio, sns, sn, sfirst, panels,

@@ -98,7 +98,7 @@ constexpr int SMALL_MAXM = SMALL_THREADS;
 constexpr int SMALL_MAXELEMS = 12288;   // m*k doubles in shared memory (96 KB)
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,
                   const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,
-                  int smem_doubles, int maxm, int plain, cudaStream_t st, int prio = 0);
+                  int smem_doubles, int maxm, int plain, cudaStream_t st, int prio = 0, int maxk = 0);
 void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st);
 // Small-supernode solve record (one per supernode, in level / row-class order).
 struct SmallSolve {
