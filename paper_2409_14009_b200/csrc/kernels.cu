@@ -681,9 +681,10 @@ __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ 
   extern __shared__ double Pw[];        // k4 x LD, column-major (columns >= k zero), then U staging
   const int J = sns[blockIdx.x];
   const SnInfo S = sn[J];
-  const int m = S.m, k = S.k, t = m - k, lane = threadIdx.x, k4 = (k + 3) & ~3;
+  const int m = S.m, k = S.k, t = m - k, lane = threadIdx.x, k4 = (k + 3) & ~3, k8 = (k + 7) & ~7;
+  const int g = lane >> 2, tg = lane & 3;
   double* G = panels + S.off;
-  for (int c = 0; c < k4; ++c)
+  for (int c = 0; c < k8; ++c)
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int r = lane + 32 * i;
@@ -695,39 +696,69 @@ __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ 
   asm volatile("cp.async.wait_all;\n" ::);
   __syncwarp();
   int bad = -1;
-  for (int j = 0; j < k; ++j) {
-    double a0[R], a1[R];
+  // blocked left-looking factor, 8-column blocks: (1) DMMA update of the block's columns by all
+  // previous columns (rows >= c0; columns >= k are never stored), (2) the block's 8 columns in
+  // registers, right-looking, pivots and multipliers broadcast by shuffle
+  for (int c0 = 0; c0 < k; c0 += 8) {
+    if (c0 > 0) {
+      double acc[4 * R][2];
 #pragma unroll
-    for (int i = 0; i < R; ++i) { a0[i] = Pw[j * LD + lane + 32 * i]; a1[i] = 0.0; }
-    int q = 0;
-    for (; q + 1 < j; q += 2) {           // two accumulator chains
-      const double l0 = Pw[q * LD + j], l1 = Pw[(q + 1) * LD + j];
+      for (int I = 0; I < 4 * R; ++I) {
+        acc[I][0] = Pw[(c0 + 2 * tg) * LD + 8 * I + g];
+        acc[I][1] = Pw[(c0 + 2 * tg + 1) * LD + 8 * I + g];
+      }
+      for (int q = 0; q < c0; q += 4) {
+        const double bq = Pw[(q + tg) * LD + c0 + g];
+#pragma unroll
+        for (int I = 0; I < 4 * R; ++I) {
+          if (8 * I + 8 <= c0) continue;   // warp-uniform: tiles wholly above the block
+          dmma(acc[I], -Pw[(q + tg) * LD + 8 * I + g], bq);
+        }
+      }
+#pragma unroll
+      for (int I = 0; I < 4 * R; ++I) {
+        if (8 * I + 8 <= c0) continue;
+        if (c0 + 2 * tg < k) Pw[(c0 + 2 * tg) * LD + 8 * I + g] = acc[I][0];
+        if (c0 + 2 * tg + 1 < k) Pw[(c0 + 2 * tg + 1) * LD + 8 * I + g] = acc[I][1];
+      }
+      __syncwarp();
+    }
+    double v[R][8];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) v[i][cc] = Pw[(c0 + cc) * LD + lane + 32 * i];
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const int j = c0 + cc;
+      if (j >= k) break;
+      double dj = 0.0;
+#pragma unroll
+      for (int i = 0; i < R; ++i) if (i == (j >> 5)) dj = v[i][cc];
+      const double d = __shfl_sync(0xffffffffu, dj, j & 31);
+      const double rl = rsqrt_nr(d);
+      if (bad < 0 && !(d > 0.0)) bad = j;
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        a0[i] = fma(-Pw[q * LD + lane + 32 * i], l0, a0[i]);
-        a1[i] = fma(-Pw[(q + 1) * LD + lane + 32 * i], l1, a1[i]);
+        const int r = lane + 32 * i;
+        v[i][cc] = r > j ? v[i][cc] * rl : (r == j ? d * rl : 0.0);
+      }
+#pragma unroll
+      for (int c2 = cc + 1; c2 < 8; ++c2) {
+        const int rc = c0 + c2;            // multiplier L(rc, j) lives in lane rc % 32, slot rc / 32
+        double lo = 0.0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) if (i == (rc >> 5)) lo = v[i][cc];
+        const double l = __shfl_sync(0xffffffffu, lo, rc & 31);
+#pragma unroll
+        for (int i = 0; i < R; ++i) v[i][c2] = fma(-v[i][cc], l, v[i][c2]);
       }
     }
-    if (q < j) {
-      const double l0 = Pw[q * LD + j];
 #pragma unroll
-      for (int i = 0; i < R; ++i) a0[i] = fma(-Pw[q * LD + lane + 32 * i], l0, a0[i]);
-    }
-    double dj = 0.0;
+    for (int i = 0; i < R; ++i)
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      a0[i] += a1[i];
-      if (i == (j >> 5)) dj = a0[i];
-    }
-    const double d = __shfl_sync(0xffffffffu, dj, j & 31);
-    const double rl = rsqrt_nr(d);
-    if (bad < 0 && !(d > 0.0)) bad = j;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int r = lane + 32 * i;
-      if (r > j) Pw[j * LD + r] = a0[i] * rl;
-      else if (r == j) Pw[j * LD + r] = d * rl;
-    }
+      for (int cc = 0; cc < 8; ++cc)
+        if (c0 + cc < k) Pw[(c0 + cc) * LD + lane + 32 * i] = v[i][cc];
     __syncwarp();
   }
   if (lane == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[J] + bad));
@@ -741,8 +772,8 @@ __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ 
   // U_J = L_R L_R^T on the FP64 tensor core: per 8-column block Jc, the 8x8 tiles I >= Jc (DMMA
   // m8n8k4 over K = k4), staged in shared memory, then RED-scattered column by column with lanes
   // over rows (runs of consecutive ancestor rows).  U row r = panel row k + r.
-  double* Ust = Pw + LD * k4;           // 8 x 32 R
-  const int g = lane >> 2, tg = lane & 3, nt8 = (t + 7) >> 3;
+  double* Ust = Pw + LD * k8;           // 8 x 32 R
+  const int nt8 = (t + 7) >> 3;
   for (int Jc = 0; Jc < nt8; ++Jc) {
     double acc[4 * R][2];
 #pragma unroll
@@ -1655,7 +1686,7 @@ void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst
   if (count <= 0) return;
   if (maxk > 0 && maxm <= 128) {   // one warp per supernode
     const int R = maxm <= 32 ? 1 : (maxm <= 64 ? 2 : 4);
-    const int sm = ((32 * R + 4) * ((maxk + 3) & ~3) + 8 * 32 * R) * (int)sizeof(double);
+    const int sm = ((32 * R + 4) * ((maxk + 7) & ~7) + 8 * 32 * R) * (int)sizeof(double);
     if (R == 1) launch_prio(small_warp_kernel<1>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);
     else if (R == 2) launch_prio(small_warp_kernel<2>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);
     else launch_prio(small_warp_kernel<4>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);

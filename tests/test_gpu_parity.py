@@ -235,3 +235,16 @@ def test_deterministic_bitwise_reproducible(name):
 @pytest.mark.parametrize("trial", range(0, 10))
 def test_deterministic_random(trial):
     run_parity(gen.random_spd(300 + trial), deterministic=1)
+
+
+@pytest.mark.parametrize("name", ["C1", "T2", "T3", "S2"])
+@pytest.mark.parametrize("env", [{"SPCHOL_SMALL_WARP": "0"}, {"SPCHOL_SMALL_WARP_MAXM": "128"},
+                                 {"SPCHOL_SMALL_WARP_MAXM": "32"}])
+def test_parity_small_supernode_paths(name, env, monkeypatch):
+    """Small supernodes through each fused path: the CTA-per-supernode kernel only
+    (SPCHOL_SMALL_WARP=0), the warp-per-supernode kernel up to m = 128 (4 rows per lane) and up to
+    m = 32 (1 row per lane)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    run_parity(gen.make(name))
+    run_parity(gen.make(name), deterministic=1)
