@@ -24,6 +24,17 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Programmatic dependent launch (critical-stream launches, see launch_prio): wait until every
+// prerequisite grid has completed and its memory is visible (a no-op for a grid launched without
+// the attribute).  The dependents are released implicitly as CTAs exit; releasing them at entry
+// (SPCHOL_PDL_EARLY) parks their CTAs on the SMs and measured slower.
+__device__ __forceinline__ void pdl_enter() {
+#ifdef SPCHOL_PDL_EARLY
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
 // ----------------------------------------------------------------------------------------------
 // gemm_kernel<MODE>: one 64x64 output tile per CTA, C(i,j) = sum_q A(i,q) B(j,q) over q < K, where
 // A and B are row blocks of column-major matrices (so both operands stream contiguous columns).
@@ -155,6 +166,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const G
                                                             const long long* __restrict__ ucol_base,
                                                             const long long* __restrict__ ucol_map,
                                                             const int* __restrict__ posmap) {
+  pdl_enter();
   extern __shared__ __align__(16) double smem[];
   double* sA = smem;
   double* sB = smem + STAGES * BK * LDS;
@@ -303,6 +315,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 4) gemm_tma_kernel(const GTask* 
                                                                    const long long* __restrict__ ucol_base,
                                                                    const long long* __restrict__ ucol_map,
                                                                    const int* __restrict__ posmap) {
+  pdl_enter();
   extern __shared__ unsigned char tsm_raw[];
   // 1024-byte aligned (128B swizzle atom) stage buffers; offsetting the shared pointer (rather than
   // casting through an integer) keeps the shared address space, so fragment loads stay LDS
@@ -453,6 +466,7 @@ __global__ void __launch_bounds__(POTRF_THREADS, 4) potrf_kernel(const PTask* __
                                                                  const SnInfo* __restrict__ sn,
                                                                  const int* __restrict__ sfirst, double* panels,
                                                                  double* linv, unsigned long long* fail) {
+  pdl_enter();
   extern __shared__ double psm[];
   double* D = psm;                      // D[col * PLD + row]: A, then L (lower); upper-right 32x32 holds T
   double* X = psm + NBMAX * PLD;        // X[col * PLD + row] = (L^{-1})(row, col)
@@ -588,6 +602,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
                                                               const long long* __restrict__ ucol_map,
                                                               const int* __restrict__ posmap,
                                                               unsigned long long* fail, int plain) {
+  pdl_enter();
   extern __shared__ double P[];         // m x k, column-major, ld = m
   const int J = sns[blockIdx.x];
   const SnInfo S = sn[J];
@@ -677,6 +692,7 @@ __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ 
                                                         const long long* __restrict__ ucol_map,
                                                         const int* __restrict__ posmap, unsigned long long* fail,
                                                         int plain) {
+  pdl_enter();
   constexpr int LD = 32 * R + 4;        // 4 mod 16 doubles: conflict-free DMMA fragment loads
   extern __shared__ double Pw[];        // k4 x LD, column-major (columns >= k zero), then U staging
   const int J = sns[blockIdx.x];
@@ -840,6 +856,7 @@ __global__ void __launch_bounds__(POTRF4_THREADS) potrf4_kernel(const PTask* __r
                                                                 const SnInfo* __restrict__ sn,
                                                                 const int* __restrict__ sfirst, double* panels,
                                                                 double* linv, unsigned long long* fail) {
+  pdl_enter();
   __shared__ double vbuf[2][NBMAX];            // published column of L / row of X
   __shared__ double Ls[NBMAX][NBMAX + 1];      // Ls[row][col] = L(row, col) after the Cholesky
   __shared__ double invd[NBMAX];
@@ -968,7 +985,7 @@ __global__ void __launch_bounds__(POTRF4_THREADS) potrf4_kernel(const PTask* __r
 // ----------------------------------------------------------------------------------------------
 constexpr int P8_LD = NBMAX + 1;              // row stride (doubles) of the shared buffers
 constexpr int POTRF8_THREADS = 128;
-constexpr int POTRF8_SMEM = (2 * NBMAX * P8_LD + NBMAX) * (int)sizeof(double);
+constexpr int POTRF8_SMEM = (NBMAX * P8_LD + NBMAX) * (int)sizeof(double);
 
 // Factor the 8x8 diagonal block at (b, b) of As in registers; pivots' reciprocals into rl.
 __device__ __forceinline__ void p8_diag(double* As, double* rl, int b, int nb, int& bad) {
@@ -1028,12 +1045,12 @@ __device__ __forceinline__ void p8_syrk_tile(double* As, int b, int r0, int c0) 
 // thread (TR * TC * POTRF8_THREADS = 32 h).  Upper triangles of X are zero, so the triangular sums
 // run over whole ranges without masks.
 template <int H, int TR, int TC>
-__device__ __forceinline__ void p8_double(double* As, double* Xs, int tid) {
+__device__ __forceinline__ void p8_double(double* As, int tid) {
   constexpr int TPR = H / TC, TPB = (H / TR) * TPR;   // threads per tile row, per block
   const int a = (tid / TPB) * 2 * H, t = tid % TPB;
   const int r0 = (t / TPR) * TR, c0 = (t % TPR) * TC;
   double acc[TR][TC];
-  // T = X22 L21 (rows r0.., cols c0..), parked transposed at As(a + c, a + H + r)
+  // T = X22 L21 (rows r0.., cols c0..), parked transposed at As(a + c, a + H + r) (upper part)
 #pragma unroll
   for (int i = 0; i < TR; ++i)
 #pragma unroll
@@ -1041,7 +1058,7 @@ __device__ __forceinline__ void p8_double(double* As, double* Xs, int tid) {
   for (int q = 0; q < r0 + TR; ++q) {
     double x[TR], l[TC];
 #pragma unroll
-    for (int i = 0; i < TR; ++i) x[i] = Xs[(a + H + r0 + i) * P8_LD + a + H + q];
+    for (int i = 0; i < TR; ++i) x[i] = As[(a + H + r0 + i) * P8_LD + a + H + q];
 #pragma unroll
     for (int j = 0; j < TC; ++j) l[j] = As[(a + H + q) * P8_LD + a + c0 + j];
 #pragma unroll
@@ -1054,7 +1071,7 @@ __device__ __forceinline__ void p8_double(double* As, double* Xs, int tid) {
 #pragma unroll
     for (int j = 0; j < TC; ++j) As[(a + c0 + j) * P8_LD + a + H + r0 + i] = acc[i][j];
   __syncthreads();
-  // X21 = -T X11
+  // X21 = -T X11, over L21's place
 #pragma unroll
   for (int i = 0; i < TR; ++i)
 #pragma unroll
@@ -1064,7 +1081,7 @@ __device__ __forceinline__ void p8_double(double* As, double* Xs, int tid) {
 #pragma unroll
     for (int i = 0; i < TR; ++i) tt[i] = As[(a + q) * P8_LD + a + H + r0 + i];
 #pragma unroll
-    for (int j = 0; j < TC; ++j) x[j] = Xs[(a + q) * P8_LD + a + c0 + j];
+    for (int j = 0; j < TC; ++j) x[j] = As[(a + q) * P8_LD + a + c0 + j];
 #pragma unroll
     for (int i = 0; i < TR; ++i)
 #pragma unroll
@@ -1073,7 +1090,13 @@ __device__ __forceinline__ void p8_double(double* As, double* Xs, int tid) {
 #pragma unroll
   for (int i = 0; i < TR; ++i)
 #pragma unroll
-    for (int j = 0; j < TC; ++j) Xs[(a + H + r0 + i) * P8_LD + a + c0 + j] = -acc[i][j];
+    for (int j = 0; j < TC; ++j) As[(a + H + r0 + i) * P8_LD + a + c0 + j] = -acc[i][j];
+  __syncthreads();
+  // the upper part must be zero again for the next level's unmasked triangular sums
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TC; ++j) As[(a + c0 + j) * P8_LD + a + H + r0 + i] = 0.0;
   __syncthreads();
 }
 
@@ -1081,10 +1104,10 @@ __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* 
                                                                 const SnInfo* __restrict__ sn,
                                                                 const int* __restrict__ sfirst, double* panels,
                                                                 double* linv, unsigned long long* fail) {
+  pdl_enter();
   extern __shared__ double p8_smem[];
-  double* As = p8_smem;                        // L (lower), T scratch (upper, transposed)
-  double* Xs = As + NBMAX * P8_LD;             // X = L^{-1} (lower)
-  double* rl = Xs + NBMAX * P8_LD;             // reciprocal pivots 1 / L_jj
+  double* As = p8_smem;                        // A -> L -> X = L^{-1} in place (lower); upper = 0 / T scratch
+  double* rl = As + NBMAX * P8_LD;             // reciprocal pivots 1 / L_jj
   const PTask T = tasks[blockIdx.x];
   const SnInfo S = sn[T.sn];
   const int nb = T.nb, tid = threadIdx.x;
@@ -1092,16 +1115,16 @@ __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* 
   // all loads in flight at once (8-byte cp.async into the row-major buffer), padding = identity
   for (int e = tid; e < NBMAX * NBMAX; e += POTRF8_THREADS) {
     const int c = e / NBMAX, r = e % NBMAX;     // consecutive threads: consecutive rows (coalesced)
-    if (r < c) continue;
     double* d = As + r * P8_LD + c;
-    if (r < nb && c < nb) {
+    if (r < c) {
+      *d = 0.0;
+    } else if (r < nb && c < nb) {
       const unsigned sa = (unsigned)__cvta_generic_to_shared(d);
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(P + (long long)c * S.ld + r));
     } else {
       *d = r == c ? 1.0 : 0.0;
     }
   }
-  for (int e = tid; e < NBMAX * P8_LD; e += POTRF8_THREADS) Xs[e] = 0.0;
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
   int bad = -1;
@@ -1145,6 +1168,11 @@ __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* 
     }
   }
   if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[T.sn] + T.c0 + bad));
+  for (int e = tid; e < NBMAX * NBMAX; e += POTRF8_THREADS) {   // L out before it is inverted in place
+    const int c = e / NBMAX, r = e % NBMAX;
+    if (r >= c && r < nb && c < nb) P[(long long)c * S.ld + r] = As[r * P8_LD + c];
+  }
+  __syncthreads();
   // inverse, level 0: the eight 8x8 diagonal blocks (column-oriented substitution per block)
   if (tid < NBMAX / 8) {
     const int b = 8 * tid;
@@ -1163,19 +1191,17 @@ __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* 
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int c = 0; c <= r; ++c) Xs[(b + r) * P8_LD + b + c] = x[r][c];
+      for (int c = 0; c <= r; ++c) As[(b + r) * P8_LD + b + c] = x[r][c];
   }
   __syncthreads();
   // doubling: for every 2h block at a, X21 = -(X22 L21) X11 (h x h, rows a+h.., columns a..)
-  p8_double<8, 1, 2>(As, Xs, tid);
-  p8_double<16, 2, 2>(As, Xs, tid);
-  p8_double<32, 2, 4>(As, Xs, tid);
+  p8_double<8, 1, 2>(As, tid);
+  p8_double<16, 2, 2>(As, tid);
+  p8_double<32, 2, 4>(As, tid);
   double* W = linv + (long long)T.slot * (NBMAX * NBMAX);
   for (int e = tid; e < NBMAX * NBMAX; e += POTRF8_THREADS) {
     const int c = e / NBMAX, r = e % NBMAX;
-    const bool in = r >= c && r < nb && c < nb;
-    if (in) P[(long long)c * S.ld + r] = As[r * P8_LD + c];
-    W[e] = in ? Xs[r * P8_LD + c] : 0.0;
+    W[e] = (r >= c && r < nb && c < nb) ? As[r * P8_LD + c] : 0.0;
   }
 }
 
@@ -1619,6 +1645,7 @@ cudaError_t kernels_init_attributes() {
 
 // Launch with an explicit scheduling priority (cudaLaunchAttributePriority is recorded into the
 // kernel node under graph capture; stream priorities alone are not).
+static bool g_pdl = [] { const char* e = getenv("SPCHOL_PDL"); return !e || atoi(e) != 0; }();
 template <typename... KArgs, typename... Args>
 static void launch_prio(void (*kern)(KArgs...), int grid, int block, int smem, cudaStream_t st, int prio,
                         Args... args) {
@@ -1627,11 +1654,15 @@ static void launch_prio(void (*kern)(KArgs...), int grid, int block, int smem, c
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributePriority;
   attr[0].val.priority = prio;
+  // critical-stream launches (high priority): programmatic dependent launch, so the next kernel of
+  // the cdiv chain is scheduled while this one runs and only waits for its completion (pdl_enter)
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (prio < 0 && g_pdl) ? 2 : 1;
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
