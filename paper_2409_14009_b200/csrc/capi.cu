@@ -352,7 +352,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
           const int mk = I.m * I.k;
           if (bucket(I) != bk) continue;
           h->small_sns.push_back(J);
-          mx = std::max(mx, mk);
+          mx = std::max(mx, bk < 3 ? mk : small_cta_smem(I.m, I.k));
           mxm = std::max(mxm, I.m);
           mxk = std::max(mxk, I.k);
           const double t = I.m - I.k;

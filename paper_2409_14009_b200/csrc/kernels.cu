@@ -603,39 +603,87 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
                                                               const int* __restrict__ posmap,
                                                               unsigned long long* fail, int plain) {
   pdl_enter();
-  extern __shared__ double P[];         // m x k, column-major, ld = m
+  extern __shared__ double P[];         // k4 x ldp, column-major (ldp = 4 mod 16), columns >= k zero
   const int J = sns[blockIdx.x];
   const SnInfo S = sn[J];
-  const int m = S.m, k = S.k, t = m - k, tid = threadIdx.x;
+  const int m = S.m, k = S.k, t = m - k, tid = threadIdx.x, ldp = small_ldp(m), k4 = (k + 3) & ~3;
   double* G = panels + S.off;
-  for (int e = tid; e < m * k; e += blockDim.x) {
+  for (int e = tid; e < m * k4; e += blockDim.x) {
     const int c = e / m, r = e - c * m;
-    P[e] = G[(long long)c * S.ld + r];
+    P[c * ldp + r] = c < k ? G[(long long)c * S.ld + r] : 0.0;
   }
   __syncthreads();
   int bad = -1;
   const int r = tid;
   __shared__ double colbuf[SMALL_MAXM];   // L(:, j) of the current step
   for (int j = 0; j < k; ++j) {
-    const double d = P[j * m + j];
+    const double d = P[j * ldp + j];
     const double rl = rsqrt(d);
     if (bad < 0 && !(d > 0.0)) bad = j;
-    const double v = (r < m && r >= j) ? (r == j ? d * rl : P[j * m + r] * rl) : 0.0;
+    const double v = (r < m && r >= j) ? (r == j ? d * rl : P[j * ldp + r] * rl) : 0.0;
     if (r < m) colbuf[r] = v;
     __syncthreads();                        // everyone has read the pivot; column j published
-    if (r < m && r >= j) P[j * m + r] = v;
+    if (r < m && r >= j) P[j * ldp + r] = v;
     if (r < m && r > j) {
       const int ce = min(r, k - 1);
-      for (int c = j + 1; c <= ce; ++c) P[c * m + r] -= v * colbuf[c];
+      for (int c = j + 1; c <= ce; ++c) P[c * ldp + r] -= v * colbuf[c];
     }
     __syncthreads();
   }
   if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[J] + bad));
   for (int e = tid; e < m * k; e += blockDim.x) {
     const int c = e / m, rr = e - c * m;
-    if (rr >= c) G[(long long)c * S.ld + rr] = P[e];
+    if (rr >= c) G[(long long)c * S.ld + rr] = P[c * ldp + rr];
   }
   if (t <= 0) return;
+  if (SMALL_DMMA_U) {
+    // U_J = L_R L_R^T on DMMA m8n8k4: work items of 8 U columns x 32 U rows (4 row tiles) dealt to
+    // the warps; each is staged per warp in shared memory and RED-scattered column by column with
+    // lanes over 32 consecutive U rows (runs of consecutive ancestor rows).  U row r = panel row k + r.
+    const int nw = blockDim.x >> 5, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
+    double* Ust = P + ldp * k4 + warp * 256;
+    const int nt8 = (t + 7) >> 3, nr32 = (t + 31) >> 5;
+    int item = 0;
+    for (int Jc = 0; Jc < nt8; ++Jc)
+      for (int I4 = Jc >> 2; I4 < nr32; ++I4, ++item) {
+        if (item % nw != warp) continue;
+        double acc[4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+        const int rb = k + 8 * Jc + g;
+        for (int q = 0; q < k4; q += 4) {
+          const double b = rb < m ? P[(q + tg) * ldp + rb] : 0.0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int I = 4 * I4 + i;
+            if (8 * I >= t || I < Jc) continue;   // warp-uniform
+            const int ra = k + 8 * I + g;
+            dmma(acc[i], ra < m ? P[(q + tg) * ldp + ra] : 0.0, b);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          Ust[(2 * tg) * 32 + 8 * i + g] = acc[i][0];
+          Ust[(2 * tg + 1) * 32 + 8 * i + g] = acc[i][1];
+        }
+        __syncwarp();
+        const int ur = 32 * I4 + lane;
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) {
+          const int c = 8 * Jc + c8;
+          if (c >= t) break;
+          if (ur < t && ur >= c) {
+            const long long cbase = ucol_base[S.ucol + c];
+            const long long mbase = ucol_map[S.ucol + c];
+            double* d = panels + cbase + posmap[mbase + k + ur];
+            if (plain) *d -= Ust[c8 * 32 + lane];
+            else atomicAdd(d, -Ust[c8 * 32 + lane]);
+          }
+        }
+        __syncwarp();
+      }
+    return;
+  }
   // U_J = L_R L_R^T: a work item is (8-column block cb, row r >= 8 cb); consecutive threads take
   // consecutive rows of the same column block, so each RED instruction of a warp covers a run of
   // consecutive U rows of one column = a run of consecutive ancestor rows (coalesced).
@@ -650,11 +698,11 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
     for (int p = 0; p < k; ++p) {
-      const double lr = P[p * m + k + r];
+      const double lr = P[p * ldp + k + r];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int c = c0 + q;
-        const double lc = c < t ? P[p * m + k + c] : 0.0;
+        const double lc = c < t ? P[p * ldp + k + c] : 0.0;
         acc[q] += lr * lc;
       }
     }
@@ -680,8 +728,10 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
 // 32 R) is staged in shared memory by 8-byte cp.async (rows >= m zero-filled), factored
 // LEFT-looking column by column (column j = A(:, j) - L(:, 0:j) L(j, 0:j)^T from shared memory,
 // the pivot broadcast by shuffle, __syncwarp between columns), written back, then U_J = L_R L_R^T
-// is formed four columns at a time and RED-scattered through relind (consecutive lanes ->
-// consecutive U rows -> mostly consecutive ancestor rows).
+// is formed on DMMA tiles and RED-scattered through relind (consecutive lanes -> consecutive U
+// rows -> mostly consecutive ancestor rows).  A blocked variant (8-column blocks updated by DMMA,
+// factored in registers) issued 40% fewer instructions but needed more shared memory per warp and
+// measured slower (C2 level 1: 1.81 vs 1.56 ms): the kernel is latency-bound, residency wins.
 // ----------------------------------------------------------------------------------------------
 __device__ __forceinline__ double rsqrt_nr(double d);
 
@@ -697,10 +747,9 @@ __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ 
   extern __shared__ double Pw[];        // k4 x LD, column-major (columns >= k zero), then U staging
   const int J = sns[blockIdx.x];
   const SnInfo S = sn[J];
-  const int m = S.m, k = S.k, t = m - k, lane = threadIdx.x, k4 = (k + 3) & ~3, k8 = (k + 7) & ~7;
-  const int g = lane >> 2, tg = lane & 3;
+  const int m = S.m, k = S.k, t = m - k, lane = threadIdx.x, k4 = (k + 3) & ~3;
   double* G = panels + S.off;
-  for (int c = 0; c < k8; ++c)
+  for (int c = 0; c < k4; ++c)
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int r = lane + 32 * i;
@@ -712,69 +761,39 @@ __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ 
   asm volatile("cp.async.wait_all;\n" ::);
   __syncwarp();
   int bad = -1;
-  // blocked left-looking factor, 8-column blocks: (1) DMMA update of the block's columns by all
-  // previous columns (rows >= c0; columns >= k are never stored), (2) the block's 8 columns in
-  // registers, right-looking, pivots and multipliers broadcast by shuffle
-  for (int c0 = 0; c0 < k; c0 += 8) {
-    if (c0 > 0) {
-      double acc[4 * R][2];
+  for (int j = 0; j < k; ++j) {
+    double a0[R], a1[R];
 #pragma unroll
-      for (int I = 0; I < 4 * R; ++I) {
-        acc[I][0] = Pw[(c0 + 2 * tg) * LD + 8 * I + g];
-        acc[I][1] = Pw[(c0 + 2 * tg + 1) * LD + 8 * I + g];
-      }
-      for (int q = 0; q < c0; q += 4) {
-        const double bq = Pw[(q + tg) * LD + c0 + g];
-#pragma unroll
-        for (int I = 0; I < 4 * R; ++I) {
-          if (8 * I + 8 <= c0) continue;   // warp-uniform: tiles wholly above the block
-          dmma(acc[I], -Pw[(q + tg) * LD + 8 * I + g], bq);
-        }
-      }
-#pragma unroll
-      for (int I = 0; I < 4 * R; ++I) {
-        if (8 * I + 8 <= c0) continue;
-        if (c0 + 2 * tg < k) Pw[(c0 + 2 * tg) * LD + 8 * I + g] = acc[I][0];
-        if (c0 + 2 * tg + 1 < k) Pw[(c0 + 2 * tg + 1) * LD + 8 * I + g] = acc[I][1];
-      }
-      __syncwarp();
-    }
-    double v[R][8];
-#pragma unroll
-    for (int i = 0; i < R; ++i)
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) v[i][cc] = Pw[(c0 + cc) * LD + lane + 32 * i];
-#pragma unroll
-    for (int cc = 0; cc < 8; ++cc) {
-      const int j = c0 + cc;
-      if (j >= k) break;
-      double dj = 0.0;
-#pragma unroll
-      for (int i = 0; i < R; ++i) if (i == (j >> 5)) dj = v[i][cc];
-      const double d = __shfl_sync(0xffffffffu, dj, j & 31);
-      const double rl = rsqrt_nr(d);
-      if (bad < 0 && !(d > 0.0)) bad = j;
+    for (int i = 0; i < R; ++i) { a0[i] = Pw[j * LD + lane + 32 * i]; a1[i] = 0.0; }
+    int q = 0;
+    for (; q + 1 < j; q += 2) {           // two accumulator chains
+      const double l0 = Pw[q * LD + j], l1 = Pw[(q + 1) * LD + j];
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        const int r = lane + 32 * i;
-        v[i][cc] = r > j ? v[i][cc] * rl : (r == j ? d * rl : 0.0);
-      }
-#pragma unroll
-      for (int c2 = cc + 1; c2 < 8; ++c2) {
-        const int rc = c0 + c2;            // multiplier L(rc, j) lives in lane rc % 32, slot rc / 32
-        double lo = 0.0;
-#pragma unroll
-        for (int i = 0; i < R; ++i) if (i == (rc >> 5)) lo = v[i][cc];
-        const double l = __shfl_sync(0xffffffffu, lo, rc & 31);
-#pragma unroll
-        for (int i = 0; i < R; ++i) v[i][c2] = fma(-v[i][cc], l, v[i][c2]);
+        a0[i] = fma(-Pw[q * LD + lane + 32 * i], l0, a0[i]);
+        a1[i] = fma(-Pw[(q + 1) * LD + lane + 32 * i], l1, a1[i]);
       }
     }
+    if (q < j) {
+      const double l0 = Pw[q * LD + j];
 #pragma unroll
-    for (int i = 0; i < R; ++i)
+      for (int i = 0; i < R; ++i) a0[i] = fma(-Pw[q * LD + lane + 32 * i], l0, a0[i]);
+    }
+    double dj = 0.0;
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc)
-        if (c0 + cc < k) Pw[(c0 + cc) * LD + lane + 32 * i] = v[i][cc];
+    for (int i = 0; i < R; ++i) {
+      a0[i] += a1[i];
+      if (i == (j >> 5)) dj = a0[i];
+    }
+    const double d = __shfl_sync(0xffffffffu, dj, j & 31);
+    const double rl = rsqrt_nr(d);
+    if (bad < 0 && !(d > 0.0)) bad = j;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = lane + 32 * i;
+      if (r > j) Pw[j * LD + r] = a0[i] * rl;
+      else if (r == j) Pw[j * LD + r] = d * rl;
+    }
     __syncwarp();
   }
   if (lane == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[J] + bad));
@@ -788,8 +807,8 @@ __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ 
   // U_J = L_R L_R^T on the FP64 tensor core: per 8-column block Jc, the 8x8 tiles I >= Jc (DMMA
   // m8n8k4 over K = k4), staged in shared memory, then RED-scattered column by column with lanes
   // over rows (runs of consecutive ancestor rows).  U row r = panel row k + r.
-  double* Ust = Pw + LD * k8;           // 8 x 32 R
-  const int nt8 = (t + 7) >> 3;
+  double* Ust = Pw + LD * k4;           // 8 x 32 R
+  const int g = lane >> 2, tg = lane & 3, nt8 = (t + 7) >> 3;
   for (int Jc = 0; Jc < nt8; ++Jc) {
     double acc[4 * R][2];
 #pragma unroll
@@ -1631,7 +1650,7 @@ cudaError_t kernels_init_attributes() {
   if ((e = cudaFuncSetAttribute(small_warp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 1 + 4) * SMALL_MAXK + 8 * 32 * 1) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 2 + 4) * SMALL_MAXK + 8 * 32 * 2) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 4 + 4) * SMALL_MAXK + 8 * 32 * 4) * 8))) return e;
-  if ((e = cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_MAXELEMS * (int)sizeof(double)))) return e;
+  if ((e = cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_CTA_SMEM_MAX * (int)sizeof(double)))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_RLB>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_tma_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM))) return e;
@@ -1717,7 +1736,7 @@ void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst
   if (count <= 0) return;
   if (maxk > 0 && maxm <= 128) {   // one warp per supernode
     const int R = maxm <= 32 ? 1 : (maxm <= 64 ? 2 : 4);
-    const int sm = ((32 * R + 4) * ((maxk + 7) & ~7) + 8 * 32 * R) * (int)sizeof(double);
+    const int sm = ((32 * R + 4) * ((maxk + 3) & ~3) + 8 * 32 * R) * (int)sizeof(double);
     if (R == 1) launch_prio(small_warp_kernel<1>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);
     else if (R == 2) launch_prio(small_warp_kernel<2>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);
     else launch_prio(small_warp_kernel<4>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);

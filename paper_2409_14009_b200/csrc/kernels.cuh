@@ -65,6 +65,7 @@ constexpr int STAGES = SPCHOL_STAGES;  // cp.async pipeline depth
 constexpr int LDS = TILE + 8;      // smem column stride (doubles): 8 mod 16 -> conflict-free DMMA fragments
 constexpr int GEMM_THREADS = 128;  // 4 warps, 2x2, warp tile 32x32
 constexpr int GEMM_SMEM = 2 * STAGES * BK * LDS * (int)sizeof(double);
+static_assert(GEMM_SMEM >= TILE * (TILE + 4) * (int)sizeof(double), "the epilogue stages the 64x68 tile in the pipeline's shared memory");
 constexpr int NBMAX = 64;          // cdiv block width
 constexpr int POTRF_THREADS = 128;
 constexpr int POTRF4_THREADS = 160;
@@ -96,6 +97,16 @@ constexpr int SMALL_THREADS = 256;
 constexpr int SMALL_MAXK = 64;
 constexpr int SMALL_MAXM = SMALL_THREADS;
 constexpr int SMALL_MAXELEMS = 12288;   // m*k doubles in shared memory (96 KB)
+#ifndef SMALL_DMMA_U
+#define SMALL_DMMA_U 0                    // small_kernel: U_J on DMMA tiles (measured slower: the
+#endif                                    // extra shared memory costs residency)
+// small_kernel shared memory: panel with row stride small_ldp(m) (4 mod 16 doubles: conflict-free
+// DMMA fragment loads) and k rounded up to 4 columns, then 8 x 32 doubles of U staging per warp.
+__host__ __device__ constexpr int small_ldp(int m) { return (m + 15) / 16 * 16 + 4; }
+__host__ __device__ constexpr int small_cta_smem(int m, int k) {
+  return small_ldp(m) * ((k + 3) & ~3) + (SMALL_DMMA_U ? 8 * 256 : 0);
+}
+constexpr int SMALL_CTA_SMEM_MAX = 16384;   // >= small_cta_smem(m, k) for every m <= 256, m k <= SMALL_MAXELEMS
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,
                   const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,
                   int smem_doubles, int maxm, int plain, cudaStream_t st, int prio = 0, int maxk = 0);
