@@ -190,6 +190,7 @@ struct spchol_handle {
   bool legacy_solve = false;            // SPCHOL_SOLVE_LEGACY=1: per-block-step launches (diagnostics)
   int nevents = 0;
   bool no_lookahead = false;     // SPCHOL_NO_LOOKAHEAD=1 (diagnostics)
+  bool no_next_split = false;    // SPCHOL_NO_NEXT_SPLIT=1: NEXT as one critical-stream launch (diagnostics)
   int max_level = -1;            // SPCHOL_MAX_LEVEL=l: factor only levels <= l (diagnostics)
   bool small_warp = true;        // SPCHOL_SMALL_WARP=0: CTA-per-supernode small kernel for every size
   int small_warp_maxm = 64;      // largest m of the warp-per-supernode kernel (SPCHOL_SMALL_WARP_MAXM <= 128)
@@ -389,11 +390,16 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
     // and TRSM launches with few CTAs) overlaps REST(S).  Ordering: REST(S) after the cdiv of
     // block S (event), NEXT(S+1) after REST(S) (same entries), REST(S+1) after REST(S) (stream 1).
     const int W = OUTER * NB;
+    // NEXT is split further: NEXT_a = the first inner block of outer block S+1 (all the cdiv of the
+    // next step needs) stays on stream 0; NEXT_b = its other columns runs at high priority on
+    // stream 1 ahead of REST(S), and the first in-block update of S+1 (same entries) waits for it.
     int pending_rest_ev = -1;      // event recorded after the latest REST launch on stream 1
+    int pending_nextb_ev = -1;     // event recorded after the latest NEXT_b launch
+    const bool split_next = !h->no_lookahead && !h->no_next_split;
     for (int s = 0; s < maxblk; ++s) {
       long long p0 = (long long)h->ptasks.size(), t0 = (long long)h->gtasks.size();
-      double fp = 0, ft = 0, fl = 0, bp = 0, bt = 0, bl = 0, fn = 0, bn = 0, fr = 0, br = 0;
-      std::vector<GTask> local, nxt, rest;
+      double fp = 0, ft = 0, fl = 0, bp = 0, bt = 0, bl = 0, fn = 0, bn = 0, fr = 0, br = 0, fnb = 0, bnb = 0;
+      std::vector<GTask> local, nxt, nxtb, rest;
       std::vector<std::pair<int, int>> bcast;   // (J, column block) finished at this step
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
         const int J = h->level_sns[x];
@@ -425,8 +431,11 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         if (c1 == C1 && C1 < I.k) {
           const int C2 = std::min(C1 + W, I.k);
           if (own(C1)) {
-            for_tiles(C1, I.m, C1, C2, [&](int r0, int s0) { nxt.push_back(GTask{J, r0, s0, C0, C1 - C0, C2}); });
-            for (int c = C1; c < C2; ++c) { fn += 2.0 * (C1 - C0) * (double)(I.m - c); bn += 16.0 * (double)(I.m - c); }
+            const int Ca = split_next ? std::min(C1 + NB, C2) : C2;
+            for_tiles(C1, I.m, C1, Ca, [&](int r0, int s0) { nxt.push_back(GTask{J, r0, s0, C0, C1 - C0, Ca}); });
+            for (int c = C1; c < Ca; ++c) { fn += 2.0 * (C1 - C0) * (double)(I.m - c); bn += 16.0 * (double)(I.m - c); }
+            for_tiles(Ca, I.m, Ca, C2, [&](int r0, int s0) { nxtb.push_back(GTask{J, r0, s0, C0, C1 - C0, C2}); });
+            for (int c = Ca; c < C2; ++c) { fnb += 2.0 * (C1 - C0) * (double)(I.m - c); bnb += 16.0 * (double)(I.m - c); }
           }
           for_tiles(C2, I.m, C2, I.k, [&](int r0, int s0) { if (own(s0)) rest.push_back(GTask{J, r0, s0, C0, C1 - C0, I.k}); });
           for (int c = C2; c < I.k; ++c)
@@ -439,6 +448,10 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       push(K_TRSM, t0, t1, ft, bt);
       long long l0 = (long long)h->gtasks.size();
       h->gtasks.insert(h->gtasks.end(), local.begin(), local.end());
+      if (!local.empty() && pending_nextb_ev >= 0) {   // in-block update after NEXT_b (same entries)
+        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SB, pending_nextb_ev});
+        pending_nextb_ev = -1;
+      }
       push(K_LOCAL, l0, (long long)h->gtasks.size(), fl, bl);
       for (const auto& jc : bcast) {   // finished block columns to the rest of their group (stream SB)
         Launch M{0, 0, 0, 0, 0, OP_BCAST, SB, -1};
@@ -451,10 +464,19 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         fn += fr; bn += br;
         rest.clear();
       }
-      if (!rest.empty()) {            // fork REST(S) onto stream 1 after the cdiv of block S
+      if (!rest.empty() || !nxtb.empty()) {   // fork NEXT_b(S), REST(S) onto stream 1 after the cdiv of block S
         const int ev = h->nevents++;
         h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, SB, ev});
         h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SB + 1, ev});
+        if (!nxtb.empty()) {
+          long long b0 = (long long)h->gtasks.size();
+          h->gtasks.insert(h->gtasks.end(), nxtb.begin(), nxtb.end());
+          Launch NB_{K_LOCAL, b0, (int)nxtb.size(), fnb, bnb, OP_LAUNCH, SB + 1, -1};
+          NB_.aux = 1;   // high priority although on the trailing stream
+          h->plan.push_back(NB_);
+          pending_nextb_ev = h->nevents++;
+          h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, SB + 1, pending_nextb_ev});
+        }
         long long r0g = (long long)h->gtasks.size();
         h->gtasks.insert(h->gtasks.end(), rest.begin(), rest.end());
         if ((long long)h->gtasks.size() > r0g)
@@ -466,11 +488,12 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         h->gtasks.insert(h->gtasks.end(), nxt.begin(), nxt.end());
         push(K_LOCAL, n0, (long long)h->gtasks.size(), fn, bn);
       }
-      if (!rest.empty()) {
+      if (!rest.empty() || !nxtb.empty()) {
         pending_rest_ev = h->nevents++;
         h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, SB + 1, pending_rest_ev});
       }
     }
+    (void)pending_nextb_ev;
     bool s1_used = false;
     for (size_t q = plan_before; q < h->plan.size(); ++q) s1_used |= h->plan[q].stream == SB + 1;
     if (s1_used) {  // join stream 1 (small-supernode launch and trailing updates) before the level's scatter
@@ -900,6 +923,7 @@ static int finish_handle(spchol_handle* h) {
     h->nvr = 1;   // concurrent subtrees would update the shared top panels in an unordered way
   }
   if (const char* e = getenv("SPCHOL_NO_LOOKAHEAD")) h->no_lookahead = atoi(e) != 0;
+  if (const char* e = getenv("SPCHOL_NO_NEXT_SPLIT")) h->no_next_split = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_MAX_LEVEL")) h->max_level = atoi(e);
   if (const char* e = getenv("SPCHOL_TMA")) h->use_tma = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_OUTER")) h->outer = std::max(1, atoi(e));
@@ -1164,7 +1188,8 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
       continue;
     }
     size_t ti = tstart((int)i);
-    const int prio = multi ? ((L.stream & 1) ? h->prio_lo : h->prio_hi) : 0;
+    const bool hi = !(L.stream & 1) || (L.kind == K_LOCAL && L.aux == 1);   // NEXT_b: high priority on stream 1
+    const int prio = multi ? (hi ? h->prio_hi : h->prio_lo) : 0;
     switch (L.kind) {
       case K_RLB:
         launch_rlb(h->d_rtasks + L.off, L.n, h->d_sn, h->d_panels, ls, prio);
