@@ -62,6 +62,8 @@ typedef int (*nccl_init_t)(void**, int, NcclUid, int);
 typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*nccl_reduce_t)(const void*, void*, size_t, int, int, int, void*, cudaStream_t);
 typedef int (*nccl_p2p_t)(const void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_bcast_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_split_t)(void*, int, int, void**, void*);
 typedef int (*nccl_group_t)();
 typedef int (*nccl_destroy_t)(void*);
 typedef const char* (*nccl_errstr_t)(int);
@@ -72,6 +74,8 @@ struct NcclApi {
   nccl_allreduce_t allreduce = nullptr;
   nccl_reduce_t reduce = nullptr;
   nccl_p2p_t send = nullptr, recv = nullptr;
+  nccl_bcast_t bcast = nullptr;
+  nccl_split_t split = nullptr;
   nccl_group_t group_start = nullptr, group_end = nullptr;
   nccl_destroy_t destroy = nullptr;
   nccl_errstr_t errstr = nullptr;
@@ -80,7 +84,9 @@ NcclApi g_nccl;
 constexpr int NCCL_SUM = 0, NCCL_MIN = 3, NCCL_UINT64 = 5, NCCL_FLOAT64 = 8;
 bool nccl_load(std::string& err) {
   if (g_nccl.so) return true;
-  void* so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  // SPCHOL_NCCL_LIB: another NCCL build, or the tests' single-GPU stand-in (tests/mock_nccl)
+  const char* alt = getenv("SPCHOL_NCCL_LIB");
+  void* so = dlopen(alt && *alt ? alt : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!so) so = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
   if (!so) { err = std::string("cannot load NCCL: ") + dlerror(); return false; }
   g_nccl.getid = (nccl_getid_t)dlsym(so, "ncclGetUniqueId");
@@ -88,12 +94,14 @@ bool nccl_load(std::string& err) {
   g_nccl.allreduce = (nccl_allreduce_t)dlsym(so, "ncclAllReduce");
   g_nccl.reduce = (nccl_reduce_t)dlsym(so, "ncclReduce");
   g_nccl.send = (nccl_p2p_t)dlsym(so, "ncclSend");
+  g_nccl.bcast = (nccl_bcast_t)dlsym(so, "ncclBroadcast");
+  g_nccl.split = (nccl_split_t)dlsym(so, "ncclCommSplit");
   g_nccl.recv = (nccl_p2p_t)dlsym(so, "ncclRecv");
   g_nccl.group_start = (nccl_group_t)dlsym(so, "ncclGroupStart");
   g_nccl.group_end = (nccl_group_t)dlsym(so, "ncclGroupEnd");
   g_nccl.destroy = (nccl_destroy_t)dlsym(so, "ncclCommDestroy");
   g_nccl.errstr = (nccl_errstr_t)dlsym(so, "ncclGetErrorString");
-  if (!g_nccl.getid || !g_nccl.init || !g_nccl.allreduce || !g_nccl.reduce || !g_nccl.send || !g_nccl.recv || !g_nccl.group_start ||
+  if (!g_nccl.getid || !g_nccl.init || !g_nccl.allreduce || !g_nccl.reduce || !g_nccl.send || !g_nccl.recv || !g_nccl.bcast || !g_nccl.split || !g_nccl.group_start ||
       !g_nccl.group_end || !g_nccl.destroy) { err = "NCCL symbols missing"; return false; }
   g_nccl.so = so;
   return true;
@@ -175,6 +183,8 @@ struct spchol_handle {
   size_t plan_all_end = 0, plan_a_end = 0, plan_factor_begin = 0;
   int nvr = 1;                         // single-GPU subtree concurrency (virtual ranks)
   void* nccl_comm = nullptr;
+  std::vector<std::array<int, 2>> grp_keys;   // distinct rank groups [lo, hi) of the top supernodes (hi - lo < world)
+  std::vector<void*> grp_comms;               // their NCCL communicators (ncclCommSplit; null if not a member)
   bool gathered = false;
   struct SolveStep { int level; long long p0; int np; long long t0; int nt; };
   std::vector<SolveStep> solve_steps;   // per (level, inner block step): POTRF and TRSM task ranges
@@ -269,6 +279,14 @@ static int blk_owner(const spchol_handle* h, int J, int C) {
   return h->grp_lo[J] + (C + h->top_owner[J] - h->grp_lo[J]) % g;
 }
 static bool in_group(const spchol_handle* h, int J, int r) { return r >= h->grp_lo[J] && r < h->grp_hi[J]; }
+// The NCCL communicator of top supernode J's rank group (ranks lo..hi-1 as 0..hi-lo-1): the world
+// communicator when the group is everyone, else the one ncclCommSplit made at attach time.
+static void* group_comm(const spchol_handle* h, int J) {
+  if (h->grp_hi[J] - h->grp_lo[J] == h->world) return h->nccl_comm;
+  for (size_t i = 0; i < h->grp_keys.size(); ++i)
+    if (h->grp_keys[i][0] == h->grp_lo[J] && h->grp_keys[i][1] == h->grp_hi[J]) return h->grp_comms[i];
+  return nullptr;
+}
 
 // Deterministic mode (reading C-7): greedy column-conflict colouring of the supernodes Js (ascending
 // order): J takes the lowest colour none of whose members shares an update column (R_J) with it.
@@ -800,9 +818,9 @@ static int setup_device(spchol_handle* h) {
   for (long long e = 0; e < S.nnzA; ++e) {
     const int c = S.a_col[e], J = S.snode[c];
     amap[e] = h->sn[J].off + (long long)(c - S.sfirst[J]) * h->sn[J].ld + S.a_pos[e];
-    // multi-GPU: a rank initialises its own subtrees' entries; the top entries are added once
-    // (by rank 0) so that the phase-B sum over ranks counts A exactly once
-    if (h->world > 1 && !(h->owner[J] == h->rank || (h->owner[J] < 0 && h->rank == 0))) amap[e] = -1;
+    // multi-GPU: a rank initialises its own subtrees' entries; a top supernode's entries are added
+    // once, by the first rank of its group (which takes part in its reduction)
+    if (h->world > 1 && !(h->owner[J] == h->rank || (h->owner[J] < 0 && h->rank == h->grp_lo[J]))) amap[e] = -1;
   }
   CK(cudaSetDevice(h->opt.device));
   CK(kernels_init_attributes());
@@ -886,6 +904,7 @@ static int setup_device(spchol_handle* h) {
 }
 
 static void free_device(spchol_handle* h) {
+  for (void* c : h->grp_comms) if (c && g_nccl.destroy) g_nccl.destroy(c);
   if (h->nccl_comm && g_nccl.destroy) g_nccl.destroy(h->nccl_comm);
   if (h->solve_gexec) cudaGraphExecDestroy(h->solve_gexec);
   if (h->solve_graph) cudaGraphDestroy(h->solve_graph);
@@ -1068,21 +1087,27 @@ extern "C" int spchol_set_stream(spchol_handle* h, void* stream) {
 // Without a communicator (diagnostics) nothing is exchanged here.
 static int enqueue_top_reduce(spchol_handle* h, cudaStream_t st, int l) {
   if (!h->nccl_comm) return SPCHOL_OK;
-  int r = g_nccl.group_start();
-  if (r) return nccl_fail(r, "ncclGroupStart");
   const int W = h->outer * h->nb;
   for (int P : h->top_by_level[l]) {
+    // only P's rank group holds contributions to P (its descendants live there; A's entries of P
+    // are added by the group's first rank), so the sum runs over the group's communicator; one
+    // NCCL group per supernode (one communicator per group call)
+    if (!in_group(h, P, h->rank)) continue;
+    void* comm = group_comm(h, P);
+    if (!comm) return fail(SPCHOL_ERR_STATE, "no communicator for a top rank group");
+    int r = g_nccl.group_start();
+    if (r) return nccl_fail(r, "ncclGroupStart");
     const SnInfo& I = h->sn[P];
     for (int C = 0; C * W < I.k; ++C) {   // block columns onto their owners (whole panel if undistributed)
       const int c0 = C * W, nc = h->top_dist[P] ? std::min(W, I.k - c0) : I.k;
       double* p = h->d_panels + I.off + (size_t)c0 * I.ld;
-      r = g_nccl.reduce(p, p, (size_t)I.ld * nc, NCCL_FLOAT64, NCCL_SUM, blk_owner(h, P, C), h->nccl_comm, st);
+      r = g_nccl.reduce(p, p, (size_t)I.ld * nc, NCCL_FLOAT64, NCCL_SUM, blk_owner(h, P, C) - h->grp_lo[P], comm, st);
       if (r) { g_nccl.group_end(); return nccl_fail(r, "ncclReduce(top panel)"); }
       if (!h->top_dist[P]) break;
     }
+    r = g_nccl.group_end();
+    if (r) return nccl_fail(r, "ncclGroupEnd");
   }
-  r = g_nccl.group_end();
-  if (r) return nccl_fail(r, "ncclGroupEnd");
   for (int P : h->top_by_level[l]) {
     const SnInfo& I = h->sn[P];
     for (int C = 0; C * W < I.k; ++C) {
@@ -1096,9 +1121,9 @@ static int enqueue_top_reduce(spchol_handle* h, cudaStream_t st, int l) {
 }
 
 // Multi-GPU phase C, distributed top supernode J: column block C is final on its owner; it goes to
-// the other ranks of J's group (their trailing updates and U_J tiles read it).  One NCCL group of
-// sends on the owner, one receive on each other member; ranks outside the group have nothing to do.
-// Every rank issues these in the same (plan) order, so the point-to-point pairs always match.
+// the other ranks of J's group (their trailing updates and U_J tiles read it): ncclBroadcast on the
+// group's communicator; ranks outside the group have nothing to do.  Every rank issues its NCCL
+// calls in the same (plan) order on one stream, so calls on different communicators never cross.
 static int enqueue_bcast(spchol_handle* h, cudaStream_t st, int J, int C) {
   if (!h->nccl_comm || !in_group(h, J, h->rank)) return SPCHOL_OK;
   const int W = h->outer * h->nb, o = blk_owner(h, J, C);
@@ -1106,17 +1131,12 @@ static int enqueue_bcast(spchol_handle* h, cudaStream_t st, int J, int C) {
   const int c0 = C * W, nc = std::min(W, I.k - c0);
   double* p = h->d_panels + I.off + (size_t)c0 * I.ld;
   const size_t cnt = (size_t)I.ld * nc;
-  int r = g_nccl.group_start();
-  if (r) return nccl_fail(r, "ncclGroupStart");
-  if (o == h->rank) {
-    for (int q = h->grp_lo[J]; q < h->grp_hi[J] && !r; ++q)
-      if (q != o) r = g_nccl.send(p, cnt, NCCL_FLOAT64, q, h->nccl_comm, st);
-  } else {
-    r = g_nccl.recv(p, cnt, NCCL_FLOAT64, o, h->nccl_comm, st);
-  }
-  int r2 = g_nccl.group_end();
-  if (r) return nccl_fail(r, "ncclSend/ncclRecv(block column)");
-  if (r2) return nccl_fail(r2, "ncclGroupEnd");
+  void* comm = group_comm(h, J);
+  if (!comm) return fail(SPCHOL_ERR_STATE, "no communicator for a top rank group");
+  // pipelined broadcast over the group (ring / tree / NVLS as NCCL picks): each member receives the
+  // block column once instead of the owner sending it g - 1 times
+  const int r = g_nccl.bcast(p, p, cnt, NCCL_FLOAT64, o - h->grp_lo[J], comm, st);
+  if (r) return nccl_fail(r, "ncclBroadcast(block column)");
   return SPCHOL_OK;
 }
 
@@ -1262,11 +1282,10 @@ static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
   if (rc) return rc;
   if (h->world == 1) return enqueue_ops(h, st, h->plan_factor_begin, h->plan_all_end);
   if (!h->nccl_comm) return fail(SPCHOL_ERR_STATE, "multi-GPU handle without an NCCL communicator (spchol_dist_attach_nccl)");
-  // top diagonal-inverse slots are written by their owners only; zero them so the solve's gather
-  // (a sum over ranks) sees each exactly once
-  if (h->nslots_total > h->top_slot)
-    CK(cudaMemsetAsync(h->d_linv + (size_t)h->top_slot * NBMAX * NBMAX, 0,
-                       sizeof(double) * (size_t)(h->nslots_total - h->top_slot) * NBMAX * NBMAX, st));
+  // every diagonal-inverse slot is written on one rank only (its subtree's rank, or its block
+  // column's owner); zero them all so the solve's gather (a sum over ranks) sees each exactly once
+  if (h->nslots_total > 0)
+    CK(cudaMemsetAsync(h->d_linv, 0, sizeof(double) * (size_t)h->nslots_total * NBMAX * NBMAX, st));
   if ((rc = enqueue_ops(h, st, h->plan_all_end, h->plan_a_end))) return rc;   // phase A: own subtrees
   if ((rc = enqueue_ops(h, st, h->plan_a_end, h->plan.size()))) return rc;    // phase C: owned tops, per-level reduces
   int r = g_nccl.allreduce(h->d_fail, h->d_fail, 1, NCCL_UINT64, NCCL_MIN, h->nccl_comm, st);
@@ -1674,6 +1693,20 @@ extern "C" int spchol_dist_attach_nccl(spchol_handle* h, const void* unique_id12
   int r = g_nccl.init(&comm, h->world, id, h->rank);
   if (r) return nccl_fail(r, "ncclCommInitRank");
   h->nccl_comm = comm;
+  // one communicator per distinct top rank group smaller than the world (collective: every rank
+  // calls ncclCommSplit for every group in the same order, members with colour 0, others without)
+  std::vector<std::array<int, 2>> keys;
+  for (int J = 0; J < h->S.nsuper; ++J)
+    if (h->owner[J] < 0 && h->grp_hi[J] - h->grp_lo[J] < h->world) keys.push_back({h->grp_lo[J], h->grp_hi[J]});
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  h->grp_keys = keys;
+  h->grp_comms.assign(keys.size(), nullptr);
+  for (size_t i = 0; i < keys.size(); ++i) {
+    const bool member = h->rank >= keys[i][0] && h->rank < keys[i][1];
+    r = g_nccl.split(comm, member ? 0 : -1 /* NCCL_SPLIT_NOCOLOR */, h->rank, &h->grp_comms[i], nullptr);
+    if (r) return nccl_fail(r, "ncclCommSplit(top rank group)");
+  }
   return SPCHOL_OK;
 }
 
@@ -1697,9 +1730,8 @@ extern "C" int spchol_factor_phase(spchol_handle* h, int phase) {
     case 1:
       h->factored = false;
       rc = enqueue_init(h, h->stream);
-      if (!rc && h->world > 1 && h->nslots_total > h->top_slot)
-        CK(cudaMemsetAsync(h->d_linv + (size_t)h->top_slot * NBMAX * NBMAX, 0,
-                           sizeof(double) * (size_t)(h->nslots_total - h->top_slot) * NBMAX * NBMAX, h->stream));
+      if (!rc && h->world > 1 && h->nslots_total > 0)
+        CK(cudaMemsetAsync(h->d_linv, 0, sizeof(double) * (size_t)h->nslots_total * NBMAX * NBMAX, h->stream));
       if (!rc) rc = enqueue_ops(h, h->stream, h->world == 1 ? h->plan_factor_begin : h->plan_all_end, h->world == 1 ? h->plan_all_end : h->plan_a_end);
       break;
     case 2:

@@ -248,3 +248,33 @@ def test_parity_small_supernode_paths(name, env, monkeypatch):
         monkeypatch.setenv(k, v)
     run_parity(gen.make(name))
     run_parity(gen.make(name), deterministic=1)
+
+
+@pytest.mark.parametrize("name,world,minflops,outer", [("S4", 2, "0", None), ("S4", 4, "0", "1"), ("S5", 3, "0", "1"),
+                                                       ("S2", 8, "0", "1"), ("T3", 2, None, None)])
+def test_distributed_nccl_path_mock(name, world, minflops, outer):
+    """The multi-GPU factor and solve through the library's real NCCL code path (communicator
+    splits per top rank group, level-start reduces, block-column broadcasts, final gathers), each
+    rank a thread on this GPU with NCCL replaced by a blocking single-process stand-in
+    (tests/mock_nccl): no hang (same call order on every rank), factor within the parity tolerance,
+    backward error within the bound, all ranks return the same solution."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ)
+    if minflops is not None:
+        env["SPCHOL_DIST_MINFLOPS"] = minflops
+    if outer is not None:
+        env["SPCHOL_OUTER"] = outer
+    here = os.path.dirname(os.path.abspath(__file__))
+    assert os.path.exists(os.path.join(here, "mock_nccl", "libmocknccl.so")), "build it with make"
+    p = subprocess.run([sys.executable, os.path.join(here, "mock_dist_run.py"), name, str(world)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert lines, p.stdout[-2000:] + p.stderr[-2000:]
+    r = json.loads(lines[-1])
+    assert r["ok"], r
+    assert r["lerr"] <= TOL_L and r["berr"] <= TOL_BERR and r["ranks_agree"], r
+    if minflops == "0":
+        assert r["ntop_dist"] > 0
