@@ -201,6 +201,7 @@ struct spchol_handle {
   int nevents = 0;
   bool no_lookahead = false;     // SPCHOL_NO_LOOKAHEAD=1 (diagnostics)
   bool no_next_split = false;    // SPCHOL_NO_NEXT_SPLIT=1: NEXT as one critical-stream launch (diagnostics)
+  int rest_smem = 0;             // SPCHOL_REST_SMEM: dynamic shared memory of trailing-stream updates (bytes)
   int max_level = -1;            // SPCHOL_MAX_LEVEL=l: factor only levels <= l (diagnostics)
   bool small_warp = true;        // SPCHOL_SMALL_WARP=0: CTA-per-supernode small kernel for every size
   int small_warp_maxm = 64;      // largest m of the warp-per-supernode kernel (SPCHOL_SMALL_WARP_MAXM <= 128)
@@ -943,6 +944,7 @@ static int finish_handle(spchol_handle* h) {
   }
   if (const char* e = getenv("SPCHOL_NO_LOOKAHEAD")) h->no_lookahead = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_NO_NEXT_SPLIT")) h->no_next_split = atoi(e) != 0;
+  if (const char* e = getenv("SPCHOL_REST_SMEM")) h->rest_smem = std::max(0, std::min(112 * 1024, atoi(e)));
   if (const char* e = getenv("SPCHOL_MAX_LEVEL")) h->max_level = atoi(e);
   if (const char* e = getenv("SPCHOL_TMA")) h->use_tma = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_OUTER")) h->outer = std::max(1, atoi(e));
@@ -1230,8 +1232,9 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
       case K_LOCAL:
         if (h->use_tma)
           launch_gemm_tma(MODE_LOCAL, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_tmaps, h->d_tmap_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
-        else
-          launch_gemm(MODE_LOCAL, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
+        else   // trailing-stream updates may reserve extra shared memory to cap their CTAs per SM
+          launch_gemm(MODE_LOCAL, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio,
+                      multi && !hi ? h->rest_smem : 0);
         break;
       case K_SCATTER:
         if (L.aux == 1)

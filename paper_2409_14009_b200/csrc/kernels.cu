@@ -1651,7 +1651,7 @@ cudaError_t kernels_init_attributes() {
   if ((e = cudaFuncSetAttribute(small_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 2 + 4) * SMALL_MAXK + 8 * 32 * 2) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 4 + 4) * SMALL_MAXK + 8 * 32 * 4) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_CTA_SMEM_MAX * (int)sizeof(double)))) return e;
-  if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_RLB>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_tma_kernel<MODE_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_tma_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, TMA_SMEM))) return e;
@@ -1700,10 +1700,11 @@ void launch_gemm_tma(int mode, const GTask* tasks, int ntasks, const SnInfo* sn,
 }
 
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, const double* linv,
-                 const long long* ucol_base, const long long* ucol_map, const int* posmap, cudaStream_t st, int prio) {
+                 const long long* ucol_base, const long long* ucol_map, const int* posmap, cudaStream_t st, int prio,
+                 int min_smem) {
   if (ntasks <= 0) return;
   if (mode == MODE_LOCAL)
-    launch_prio(gemm_kernel<MODE_LOCAL>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
+    launch_prio(gemm_kernel<MODE_LOCAL>, ntasks, GEMM_THREADS, std::max(GEMM_SMEM, min_smem), st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
   else if (mode == MODE_TRSM)
     launch_prio(gemm_kernel<MODE_TRSM>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
   else if (mode == MODE_SCATTER_DET)

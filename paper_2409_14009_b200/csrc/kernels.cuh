@@ -76,7 +76,7 @@ constexpr int POTRF_SMEM = 2 * NBMAX * (NBMAX + 1) * (int)sizeof(double);
 
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels,
                  const double* linv, const long long* ucol_base, const long long* ucol_map,
-                 const int* posmap, cudaStream_t st, int prio = 0);
+                 const int* posmap, cudaStream_t st, int prio = 0, int min_smem = 0);
 #ifndef SPCHOL_TBK
 #define SPCHOL_TBK 16
 #endif
