@@ -1664,7 +1664,7 @@ cudaError_t kernels_init_attributes() {
 
 // Launch with an explicit scheduling priority (cudaLaunchAttributePriority is recorded into the
 // kernel node under graph capture; stream priorities alone are not).
-static bool g_pdl = [] { const char* e = getenv("SPCHOL_PDL"); return !e || atoi(e) != 0; }();
+static bool pdl_enabled() { const char* e = getenv("SPCHOL_PDL"); return !e || atoi(e) != 0; }   // read per launch
 template <typename... KArgs, typename... Args>
 static void launch_prio(void (*kern)(KArgs...), int grid, int block, int smem, cudaStream_t st, int prio,
                         Args... args) {
@@ -1681,7 +1681,7 @@ static void launch_prio(void (*kern)(KArgs...), int grid, int block, int smem, c
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (prio < 0 && g_pdl) ? 2 : 1;
+  cfg.numAttrs = (prio < 0 && pdl_enabled()) ? 2 : 1;
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
