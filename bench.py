@@ -46,13 +46,47 @@ def fp64_peak():
 
 
 class Clocks:
-    """nvidia-smi clock/throttle sampling during the timed region (B200_PROFILING.md recipe)."""
+    """Clock / throttle-reason sampling during the timed region (B200_PROFILING.md recipe): NVML
+    (pynvml) polled every 2 ms from a thread, so even a ~50 ms timed region gets samples;
+    nvidia-smi -lms 100 when NVML is unavailable."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
         self.p = None
+        self.samples = []
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                         pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+        except Exception:  # noqa: BLE001
+            self.nvml = None
+
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append([str(sm), str(mx), ""] + ["Active" if r & b else "Not Active" for b in self.bits])
+            except Exception:  # noqa: BLE001
+                pass
+            self.stop.wait(0.002)
 
     def __enter__(self):
+        self.samples = []
+        if self.nvml is not None:
+            import threading
+            self.stop = threading.Event()
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
@@ -65,7 +99,10 @@ class Clocks:
         return self
 
     def __exit__(self, *a):
-        self.samples = []
+        if self.nvml is not None:
+            self.stop.set()
+            self.t.join(timeout=5)
+            return
         if self.p is None:
             return
         time.sleep(0.25)
@@ -81,11 +118,11 @@ class Clocks:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        reasons = sorted({self.NAMES[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
         loaded = [x for x in sm if x > 0.5 * max(sm)] if sm else []
         return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def dist_setup(args):
