@@ -595,6 +595,8 @@ __global__ void __launch_bounds__(POTRF_THREADS, 4) potrf_kernel(const PTask* __
 //     relind (posmap), exactly as in the tiled scatter kernel.
 // Thousands of these supernodes make up the lower levels of the 2D configs.
 // ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ double rsqrt_nr(double d);
+
 __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restrict__ sns,
                                                               const SnInfo* __restrict__ sn,
                                                               const int* __restrict__ sfirst, double* panels,
@@ -608,17 +610,21 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
   const SnInfo S = sn[J];
   const int m = S.m, k = S.k, t = m - k, tid = threadIdx.x, ldp = small_ldp(m), k4 = (k + 3) & ~3;
   double* G = panels + S.off;
+  // all loads in flight at once (8-byte cp.async; a plain load-store loop serialises the round trips)
   for (int e = tid; e < m * k4; e += blockDim.x) {
     const int c = e / m, r = e - c * m;
-    P[c * ldp + r] = c < k ? G[(long long)c * S.ld + r] : 0.0;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(P + c * ldp + r);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa),
+                 "l"(c < k ? G + (long long)c * S.ld + r : G), "r"(c < k ? 8 : 0));
   }
+  asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
   int bad = -1;
   const int r = tid;
   __shared__ double colbuf[SMALL_MAXM];   // L(:, j) of the current step
   for (int j = 0; j < k; ++j) {
     const double d = P[j * ldp + j];
-    const double rl = rsqrt(d);
+    const double rl = rsqrt_nr(d);
     if (bad < 0 && !(d > 0.0)) bad = j;
     const double v = (r < m && r >= j) ? (r == j ? d * rl : P[j * ldp + r] * rl) : 0.0;
     if (r < m) colbuf[r] = v;
