@@ -179,7 +179,8 @@ enum {
   SPCHOL_Q_UPDATE_ENTRIES = 15, /* sum_J t_J (t_J+1)/2 scattered update entries             */
   SPCHOL_Q_NBLOCKS = 16,      /* RLB blocks over all supernodes                   */
   SPCHOL_Q_NMARKERS = 17,     /* multi-GPU: exchange points (markers) of this rank's phase C     */
-  SPCHOL_Q_NTOP_DIST = 18     /* multi-GPU: top supernodes distributed over their rank group     */
+  SPCHOL_Q_NTOP_DIST = 18,    /* multi-GPU: top supernodes distributed over their rank group     */
+  SPCHOL_Q_DEVICE_BYTES = 19  /* device memory the handle owns (panels, inverses, plan; 0 if host-only) */
 };
 int spchol_query(const spchol_handle* h, int key, int64_t* value);
 

@@ -132,10 +132,12 @@ struct Launch {
   int aux2 = 0;    // K_SMALL: largest m in the launch
   int aux3 = 0;    // K_SMALL: largest k in the launch if it runs one warp per supernode, else 0
 };
+thread_local size_t g_dev_bytes = 0;   // device bytes allocated by the handle being set up
 template <class T>
 cudaError_t dalloc(T** p, size_t count) {
   *p = nullptr;
   if (count == 0) count = 1;
+  g_dev_bytes += count * sizeof(T);
   return cudaMalloc((void**)p, count * sizeof(T));
 }
 template <class T>
@@ -163,6 +165,7 @@ struct spchol_handle {
   std::vector<int> small_sns;           // supernodes handled by the fused small kernel, by level
   std::vector<char> is_small;
   long long panel_doubles = 0;
+  size_t device_bytes = 0;              // device memory the handle owns (SPCHOL_Q_DEVICE_BYTES)
   std::vector<long long> panel_off;
   double flops_exec = 0, update_entries = 0;
   int nslots_total = 0;
@@ -867,6 +870,7 @@ static int setup_device(spchol_handle* h) {
   }
   h->plan_events.resize(h->nevents);
   for (auto& e : h->plan_events) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  g_dev_bytes = 0;
   CK(dalloc(&h->d_panels, (size_t)h->panel_doubles));
   CK(dalloc(&h->d_avals, (size_t)S.nnzA));
   CK(upload(&h->d_amap, amap));
@@ -923,6 +927,7 @@ static int setup_device(spchol_handle* h) {
   CK(dalloc(&h->d_sflags, (size_t)3 * std::max(1, h->nslots_total) + 2 * (size_t)S.nlevels + 1));
   CK(dalloc(&h->d_y, (size_t)S.n));
   CK(dalloc(&h->d_y2, (size_t)S.n));
+  h->device_bytes = g_dev_bytes;
   return SPCHOL_OK;
 }
 
@@ -1524,6 +1529,7 @@ extern "C" int spchol_query(const spchol_handle* h, int key, int64_t* value) {
     case SPCHOL_Q_UPDATE_ENTRIES: *value = (int64_t)h->update_entries; break;
     case SPCHOL_Q_NBLOCKS: *value = (int64_t)S.blk_q.size(); break;
     case SPCHOL_Q_NMARKERS: *value = (int64_t)h->markers.size(); break;
+    case SPCHOL_Q_DEVICE_BYTES: *value = (int64_t)h->device_bytes; break;
     case SPCHOL_Q_NTOP_DIST: {
       int64_t c = 0;
       for (char d : h->top_dist) c += d != 0;

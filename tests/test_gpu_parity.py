@@ -290,3 +290,15 @@ def test_parity_schedule_options(name, env, monkeypatch):
         monkeypatch.setenv(k, v)
     run_parity(gen.make(name), small_max_k=-1)
     run_parity(gen.make(name), small_max_k=-1, block=64)
+
+
+def test_device_footprint_query():
+    """SPCHOL_Q_DEVICE_BYTES: the handle's device memory covers the panel arena, the kept diagonal
+    inverses and the plan; a host-only handle owns none."""
+    prob = gen.make("S4")
+    with sp.Solver.from_problem(prob) as h:
+        nb = h.query("DEVICE_BYTES")
+        assert nb >= 8 * h.query("PANEL_DOUBLES") + 8 * h.query("NNZ_A")
+        assert nb < 64 * (h.query("PANEL_DOUBLES") + h.query("NNZ_A")) + (64 << 20)
+    with sp.Solver.from_problem(prob, device=-1) as h:
+        assert h.query("DEVICE_BYTES") == 0
