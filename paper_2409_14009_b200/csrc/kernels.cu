@@ -741,6 +741,17 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
 // ----------------------------------------------------------------------------------------------
 __device__ __forceinline__ double rsqrt_nr(double d);
 
+// v[idx][c] with explicit selects (a loop of `if (i == idx)` is turned into an indexed load, which
+// puts the whole register array in local memory)
+template <int R>
+__device__ __forceinline__ double pick_row(const double (&v)[R][8], int idx, int c) {
+  if (R == 1) return v[0][c];
+  if (R == 2) return idx ? v[R - 1][c] : v[0][c];
+  const double lo = (idx & 1) ? v[1][c] : v[0][c];
+  const double hi = (idx & 1) ? v[R - 1][c] : v[R > 2 ? 2 : 0][c];
+  return (idx & 2) ? hi : lo;
+}
+
 template <int R>
 __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ sns, const SnInfo* __restrict__ sn,
                                                         const int* __restrict__ sfirst, double* panels,
@@ -767,39 +778,50 @@ __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ 
   asm volatile("cp.async.wait_all;\n" ::);
   __syncwarp();
   int bad = -1;
-  for (int j = 0; j < k; ++j) {
-    double a0[R], a1[R];
+  // Register-blocked left-looking factor, 8 columns at a time: the block is updated by every
+  // earlier column (per column q: R own-row loads + 8 broadcast multipliers for 8R FMAs), then
+  // factored in registers, right-looking, pivots and multipliers broadcast by shuffle.
+  for (int c0 = 0; c0 < k; c0 += 8) {
+    double v[R][8];
 #pragma unroll
-    for (int i = 0; i < R; ++i) { a0[i] = Pw[j * LD + lane + 32 * i]; a1[i] = 0.0; }
-    int q = 0;
-    for (; q + 1 < j; q += 2) {           // two accumulator chains
-      const double l0 = Pw[q * LD + j], l1 = Pw[(q + 1) * LD + j];
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) v[i][cc] = c0 + cc < k ? Pw[(c0 + cc) * LD + lane + 32 * i] : 0.0;
+    for (int q = 0; q < c0; ++q) {
+      double lr[R], mq[8];
+#pragma unroll
+      for (int i = 0; i < R; ++i) lr[i] = Pw[q * LD + lane + 32 * i];
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) mq[cc] = Pw[q * LD + min(c0 + cc, LD - 1)];
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) v[i][cc] = fma(-lr[i], mq[cc], v[i][cc]);
+    }
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {       // columns >= k (all-zero) only touch columns >= k
+      const int j = c0 + cc;
+      const double d = __shfl_sync(0xffffffffu, pick_row<R>(v, j >> 5, cc), j & 31);
+      const double rl = rsqrt_nr(d);
+      if (bad < 0 && j < k && !(d > 0.0)) bad = j;
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        a0[i] = fma(-Pw[q * LD + lane + 32 * i], l0, a0[i]);
-        a1[i] = fma(-Pw[(q + 1) * LD + lane + 32 * i], l1, a1[i]);
+        const int r = lane + 32 * i;
+        v[i][cc] = r > j ? v[i][cc] * rl : (r == j ? d * rl : 0.0);
+      }
+#pragma unroll
+      for (int c2 = cc + 1; c2 < 8; ++c2) {
+        const int rc = c0 + c2;            // multiplier L(rc, j): lane rc % 32, slot rc / 32
+        const double l = __shfl_sync(0xffffffffu, pick_row<R>(v, rc >> 5, cc), rc & 31);
+#pragma unroll
+        for (int i = 0; i < R; ++i) v[i][c2] = fma(-v[i][cc], l, v[i][c2]);
       }
     }
-    if (q < j) {
-      const double l0 = Pw[q * LD + j];
 #pragma unroll
-      for (int i = 0; i < R; ++i) a0[i] = fma(-Pw[q * LD + lane + 32 * i], l0, a0[i]);
-    }
-    double dj = 0.0;
+    for (int i = 0; i < R; ++i)
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      a0[i] += a1[i];
-      if (i == (j >> 5)) dj = a0[i];
-    }
-    const double d = __shfl_sync(0xffffffffu, dj, j & 31);
-    const double rl = rsqrt_nr(d);
-    if (bad < 0 && !(d > 0.0)) bad = j;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int r = lane + 32 * i;
-      if (r > j) Pw[j * LD + r] = a0[i] * rl;
-      else if (r == j) Pw[j * LD + r] = d * rl;
-    }
+      for (int cc = 0; cc < 8; ++cc)
+        if (c0 + cc < k) Pw[(c0 + cc) * LD + lane + 32 * i] = v[i][cc];
     __syncwarp();
   }
   if (lane == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[J] + bad));
