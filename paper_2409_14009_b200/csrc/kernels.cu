@@ -620,20 +620,40 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
   int bad = -1;
-  const int r = tid;
-  __shared__ double colbuf[SMALL_MAXM];   // L(:, j) of the current step
-  for (int j = 0; j < k; ++j) {
-    const double d = P[j * ldp + j];
-    const double rl = rsqrt_nr(d);
-    if (bad < 0 && !(d > 0.0)) bad = j;
-    const double v = (r < m && r >= j) ? (r == j ? d * rl : P[j * ldp + r] * rl) : 0.0;
-    if (r < m) colbuf[r] = v;
-    __syncthreads();                        // everyone has read the pivot; column j published
-    if (r < m && r >= j) P[j * ldp + r] = v;
-    if (r < m && r > j) {
-      const int ce = min(r, k - 1);
-      for (int c = j + 1; c <= ce; ++c) P[c * ldp + r] -= v * colbuf[c];
+  const int r = tid;                      // this thread's panel row
+  __shared__ double colbuf[SMALL_MAXM];   // multipliers L(c0.., j) of the current column
+  __shared__ double piv;
+  // Register-blocked left-looking factor, 8 columns at a time: the row's 8 entries of the block
+  // are updated by every earlier column (1 own load + 8 broadcast multipliers per 8 FMAs), then the
+  // block is factored right-looking with the pivot and the block rows' multipliers through shared
+  // memory (two barriers per column).
+  for (int c0 = 0; c0 < k; c0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) v[cc] = (r < m && c0 + cc < k4) ? P[(c0 + cc) * ldp + r] : 0.0;
+    for (int q = 0; q < c0; ++q) {
+      const double l = r < m ? P[q * ldp + r] : 0.0;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) v[cc] = fma(-l, P[q * ldp + min(c0 + cc, ldp - 1)], v[cc]);
     }
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const int j = c0 + cc;
+      if (j >= k) break;                  // uniform over the CTA
+      if (r == j) piv = v[cc];
+      __syncthreads();
+      const double d = piv;
+      const double rl = rsqrt_nr(d);
+      if (bad < 0 && !(d > 0.0)) bad = j;
+      v[cc] = r > j ? v[cc] * rl : (r == j ? d * rl : 0.0);
+      if (r > j && r < c0 + 8) colbuf[r] = v[cc];
+      __syncthreads();
+#pragma unroll
+      for (int c2 = cc + 1; c2 < 8; ++c2) v[c2] = fma(-v[cc], colbuf[min(c0 + c2, SMALL_MAXM - 1)], v[c2]);
+    }
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc)
+      if (r < m && c0 + cc < k) P[(c0 + cc) * ldp + r] = v[cc];
     __syncthreads();
   }
   if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[J] + bad));
