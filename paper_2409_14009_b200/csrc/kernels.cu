@@ -662,12 +662,15 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
     if (rr >= c) G[(long long)c * S.ld + rr] = P[c * ldp + rr];
   }
   if (t <= 0) return;
-  if (SMALL_DMMA_U) {
+#if SMALL_DMMA_U
+  {
     // U_J = L_R L_R^T on DMMA m8n8k4: work items of 8 U columns x 32 U rows (4 row tiles) dealt to
     // the warps; each is staged per warp in shared memory and RED-scattered column by column with
     // lanes over 32 consecutive U rows (runs of consecutive ancestor rows).  U row r = panel row k + r.
     const int nw = blockDim.x >> 5, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
+#if SMALL_DMMA_U == 1
     double* Ust = P + ldp * k4 + warp * 256;
+#endif
     const int nt8 = (t + 7) >> 3, nr32 = (t + 31) >> 5;
     int item = 0;
     for (int Jc = 0; Jc < nt8; ++Jc)
@@ -687,6 +690,26 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
             dmma(acc[i], ra < m ? P[(q + tg) * ldp + ra] : 0.0, b);
           }
         }
+#if SMALL_DMMA_U == 2
+        {                          // RED straight from the fragments: runs of 8 consecutive U rows
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int c = 8 * Jc + 2 * tg + v;
+            if (c >= t) continue;
+            const long long cbase = ucol_base[S.ucol + c];
+            const long long mbase = ucol_map[S.ucol + c];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int ur = 32 * I4 + 8 * i + g;
+              if (ur >= t || ur < c) continue;
+              double* d = panels + cbase + posmap[mbase + k + ur];
+              if (plain) *d -= acc[i][v];
+              else atomicAdd(d, -acc[i][v]);
+            }
+          }
+          continue;
+        }
+#else
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           Ust[(2 * tg) * 32 + 8 * i + g] = acc[i][0];
@@ -707,9 +730,11 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
           }
         }
         __syncwarp();
+#endif
       }
     return;
   }
+#else
   // U_J = L_R L_R^T: a work item is (8-column block cb, row r >= 8 cb); consecutive threads take
   // consecutive rows of the same column block, so each RED instruction of a warp covers a run of
   // consecutive U rows of one column = a run of consecutive ancestor rows (coalesced).
@@ -744,7 +769,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_kernel(const int* __restr
     }
     item += blockDim.x;
   }
-
+#endif
 }
 
 // ----------------------------------------------------------------------------------------------

@@ -98,13 +98,15 @@ constexpr int SMALL_MAXK = 64;
 constexpr int SMALL_MAXM = SMALL_THREADS;
 constexpr int SMALL_MAXELEMS = 12288;   // m*k doubles in shared memory (96 KB)
 #ifndef SMALL_DMMA_U
-#define SMALL_DMMA_U 0                    // small_kernel: U_J on DMMA tiles (measured slower: the
-#endif                                    // extra shared memory costs residency)
+// small_kernel U_J: 2 = DMMA tiles, RED straight from the fragments (default); 1 = DMMA tiles staged
+// through shared memory (slower: the staging costs residency); 0 = scalar FMAs
+#define SMALL_DMMA_U 2
+#endif
 // small_kernel shared memory: panel with row stride small_ldp(m) (4 mod 16 doubles: conflict-free
 // DMMA fragment loads) and k rounded up to 4 columns, then 8 x 32 doubles of U staging per warp.
 __host__ __device__ constexpr int small_ldp(int m) { return (m + 15) / 16 * 16 + 4; }
 __host__ __device__ constexpr int small_cta_smem(int m, int k) {
-  return small_ldp(m) * ((k + 3) & ~3) + (SMALL_DMMA_U ? 8 * 256 : 0);
+  return small_ldp(m) * ((k + 3) & ~3) + (SMALL_DMMA_U == 1 ? 8 * 256 : 0);
 }
 constexpr int SMALL_CTA_SMEM_MAX = 16384;   // >= small_cta_smem(m, k) for every m <= 256, m k <= SMALL_MAXELEMS
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,
