@@ -354,9 +354,11 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       // SPCHOL_SMALL_WARP=0): buckets by m k
       static const int bucket_max[] = {256, 1024, 4096, SMALL_MAXELEMS};
       auto bucket = [&](const SnInfo& I) {
-        if (h->small_warp && I.m <= h->small_warp_maxm) return I.m <= 32 ? 0 : (I.m <= 64 ? 1 : 2);
+        // warp kernel: by rows per lane and by k (the launch's shared memory follows its largest k)
+        if (h->small_warp && I.m <= h->small_warp_maxm)
+          return 3 * (I.k <= 16 ? 0 : I.k <= 32 ? 1 : 2) + (I.m <= 32 ? 0 : (I.m <= 64 ? 1 : 2));
         const int mk = I.m * I.k;
-        return 3 + (mk <= 256 ? 0 : mk <= 1024 ? 1 : mk <= 4096 ? 2 : 3);
+        return 9 + (mk <= 256 ? 0 : mk <= 1024 ? 1 : mk <= 4096 ? 2 : 3);
       };
       (void)bucket_max;
       bool forked = false;
@@ -366,7 +368,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       const int nsc = h->opt.deterministic ? colour_supernodes(h, sm, scol) : 1;
       if (!h->opt.deterministic) scol.assign(sm.size(), 0);
       for (int col = 0; col < nsc; ++col)
-      for (int bk = 0; bk < 7; ++bk) {
+      for (int bk = 0; bk < 13; ++bk) {
         long long s0 = (long long)h->small_sns.size();
         int mx = 0, mxm = 0, mxk = 0;
         double fsm = 0, bsm = 0;
@@ -377,7 +379,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
           const int mk = I.m * I.k;
           if (bucket(I) != bk) continue;
           h->small_sns.push_back(J);
-          mx = std::max(mx, bk < 3 ? mk : small_cta_smem(I.m, I.k));
+          mx = std::max(mx, bk < 9 ? mk : small_cta_smem(I.m, I.k));
           mxm = std::max(mxm, I.m);
           mxk = std::max(mxk, I.k);
           const double t = I.m - I.k;
@@ -395,7 +397,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         Launch L{K_SMALL, s0, (int)(s1 - s0), fsm, bsm, OP_LAUNCH, SB + 1, -1};
         L.aux = mx;
         L.aux2 = mxm;
-        L.aux3 = bk < 3 ? mxk : 0;
+        L.aux3 = bk < 9 ? mxk : 0;
         h->plan.push_back(L);
       }
     }

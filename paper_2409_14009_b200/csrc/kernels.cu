@@ -878,9 +878,9 @@ __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ 
     }
   if (t <= 0) return;
   // U_J = L_R L_R^T on the FP64 tensor core: per 8-column block Jc, the 8x8 tiles I >= Jc (DMMA
-  // m8n8k4 over K = k4), staged in shared memory, then RED-scattered column by column with lanes
-  // over rows (runs of consecutive ancestor rows).  U row r = panel row k + r.
-  double* Ust = Pw + LD * k4;           // 8 x 32 R
+  // m8n8k4 over K = k4), RED-scattered straight from the fragments (runs of 8 consecutive U rows =
+  // mostly consecutive ancestor rows; no staging memory, so more warps stay resident).
+  // U row r = panel row k + r.
   const int g = lane >> 2, tg = lane & 3, nt8 = (t + 7) >> 3;
   for (int Jc = 0; Jc < nt8; ++Jc) {
     double acc[4 * R][2];
@@ -897,29 +897,20 @@ __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ 
       }
     }
 #pragma unroll
-    for (int I = 0; I < 4 * R; ++I) {
-      if (I < Jc || I >= nt8) continue;
-      Ust[(2 * tg) * (32 * R) + 8 * I + g] = acc[I][0];
-      Ust[(2 * tg + 1) * (32 * R) + 8 * I + g] = acc[I][1];
-    }
-    __syncwarp();
-#pragma unroll
-    for (int c8 = 0; c8 < 8; ++c8) {
-      const int c = 8 * Jc + c8;
-      if (c >= t) break;
+    for (int v = 0; v < 2; ++v) {
+      const int c = 8 * Jc + 2 * tg + v;
+      if (c >= t) continue;
       const long long cbase = ucol_base[S.ucol + c];
       const long long mbase = ucol_map[S.ucol + c];
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const int r = lane + 32 * i;
-        if (r >= t || r < c) continue;
+      for (int I = 0; I < 4 * R; ++I) {
+        const int r = 8 * I + g;
+        if (I < Jc || I >= nt8 || r >= t || r < c) continue;
         double* d = panels + cbase + posmap[mbase + k + r];
-        const double u = Ust[c8 * (32 * R) + r];
-        if (plain) *d -= u;               // deterministic mode: conflict-free launch
-        else atomicAdd(d, -u);
+        if (plain) *d -= acc[I][v];       // deterministic mode: conflict-free launch
+        else atomicAdd(d, -acc[I][v]);
       }
     }
-    __syncwarp();
   }
 }
 
@@ -1810,7 +1801,7 @@ void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst
   if (count <= 0) return;
   if (maxk > 0 && maxm <= 128) {   // one warp per supernode
     const int R = maxm <= 32 ? 1 : (maxm <= 64 ? 2 : 4);
-    const int sm = ((32 * R + 4) * ((maxk + 3) & ~3) + 8 * 32 * R) * (int)sizeof(double);
+    const int sm = (32 * R + 4) * ((maxk + 3) & ~3) * (int)sizeof(double);
     if (R == 1) launch_prio(small_warp_kernel<1>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);
     else if (R == 2) launch_prio(small_warp_kernel<2>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);
     else launch_prio(small_warp_kernel<4>, count, 32, sm, st, prio, sns, sn, sfirst, panels, ucol_base, ucol_map, posmap, fail, plain);
