@@ -49,7 +49,7 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call);    \
   } while (0)
 
-enum LaunchKind { K_SMALL = 0, K_POTRF = 1, K_TRSM = 2, K_LOCAL = 3, K_SCATTER = 4, K_INIT = 5, K_RLB = 6, K_NKINDS = 7 };
+enum LaunchKind { K_SMALL = 0, K_POTRF = 1, K_TRSM = 2, K_LOCAL = 3, K_SCATTER = 4, K_INIT = 5, K_RLB = 6, K_INV = 7, K_NKINDS = 8 };
 }  // namespace
 
 // ------------------------------------------------------------------------------------- NCCL
@@ -209,6 +209,9 @@ struct spchol_handle {
                                  // per block column; C4 -0.45%, C5 -0.35%, but C3/C2 +1.3-1.5%: on the chain)
   int max_level = -1;            // SPCHOL_MAX_LEVEL=l: factor only levels <= l (diagnostics)
   bool small_warp = true;        // SPCHOL_SMALL_WARP=0: CTA-per-supernode small kernel for every size
+  bool trsm_subst = false;       // SPCHOL_TRSM_SUBST=1: TRSM by substitution with L_bb (POTRF without the
+                                 // inverse on the chain, the solve's inverses beside the factor); measured
+                                 // slower than the DMMA TRSM with kept inverses (C4 +5.5%, C2 +10%)
   int small_warp_maxm = 64;      // largest m of the warp-per-supernode kernel (SPCHOL_SMALL_WARP_MAXM <= 128)
   bool use_tma = false;          // SPCHOL_TMA=1: TMA + mbarrier tile kernels (measured ~2% slower)
   void* d_tmaps = nullptr;       // CUtensorMap per supernode panel (TMA boxes 16 x 8, 128B swizzle)
@@ -419,6 +422,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
     // NEXT is split further: NEXT_a = the first inner block of outer block S+1 (all the cdiv of the
     // next step needs) stays on stream 0; NEXT_b = its other columns runs at high priority on
     // stream 1 ahead of REST(S), and the first in-block update of S+1 (same entries) waits for it.
+    const long long level_p0 = (long long)h->ptasks.size();
     int pending_rest_ev = -1;      // event recorded after the latest REST launch on stream 1
     int pending_nextb_ev = -1;     // event recorded after the latest NEXT_b launch
     const bool split_next = !h->no_lookahead && !h->no_next_split;
@@ -540,6 +544,15 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       }
     }
     (void)pending_nextb_ev;
+    if (h->trsm_subst && (long long)h->ptasks.size() > level_p0) {
+      // the solve's diagonal-block inverses of this level, beside the factor (low priority side stream)
+      const int ev = h->nevents++, SIDE = 2 * 16 + SB + 1;
+      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, SB, ev});
+      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SIDE, ev});
+      const long long np = (long long)h->ptasks.size() - level_p0;
+      h->plan.push_back(Launch{K_INV, level_p0, (int)np, (double)np * NBMAX * NBMAX * NBMAX / 3.0, 16.0 * np * NBMAX * NBMAX,
+                               OP_LAUNCH, SIDE, -1});
+    }
     bool s1_used = false;
     for (size_t q = plan_before; q < h->plan.size(); ++q) s1_used |= h->plan[q].stream == SB + 1;
     if (s1_used) {  // join stream 1 (small-supernode launch and trailing updates) before the level's scatter
@@ -981,6 +994,8 @@ static int finish_handle(spchol_handle* h) {
   if (const char* e = getenv("SPCHOL_SOLVE_LEGACY")) h->legacy_solve = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_DIST_MINFLOPS")) h->dist_min_flops = atof(e);
   if (const char* e = getenv("SPCHOL_SMALL_WARP")) h->small_warp = atoi(e) != 0;
+  if (const char* e = getenv("SPCHOL_TRSM_SUBST")) h->trsm_subst = atoi(e) != 0;
+  if (!POTRF_MODES || h->use_tma) h->trsm_subst = false;
   if (const char* e = getenv("SPCHOL_SMALL_WARP_MAXM")) h->small_warp_maxm = std::max(0, std::min(128, atoi(e)));
   build_plan(h);
   if (h->opt.device < 0) return SPCHOL_OK;   // host-only analysis (no device state)
@@ -1251,10 +1266,16 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
                      h->d_posmap, h->d_fail, L.aux, L.aux2, h->opt.deterministic ? 1 : 0, ls, prio, L.aux3);
         break;
       case K_POTRF:
-        launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio);
+        launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio,
+                     h->trsm_subst ? 1 : 0);
+        break;
+      case K_INV:
+        launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio, 2);
         break;
       case K_TRSM:
-        if (h->use_tma)
+        if (h->trsm_subst)
+          launch_trsm_subst(h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, ls, prio);
+        else if (h->use_tma)
           launch_gemm_tma(MODE_TRSM, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_tmaps, h->d_tmap_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
         else
           launch_gemm(MODE_TRSM, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);

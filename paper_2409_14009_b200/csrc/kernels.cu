@@ -1183,6 +1183,10 @@ __device__ __forceinline__ void p8_double(double* As, int tid) {
   __syncthreads();
 }
 
+// PM = 0: factor + inverse (TRSM-as-GEMM reads the inverse); PM = 1: factor only (the substitution
+// TRSM reads L); PM = 2: inverse only, of the finished L in the panel (the solve's inverses, off
+// the critical path).
+template <int PM>
 __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* __restrict__ tasks,
                                                                 const SnInfo* __restrict__ sn,
                                                                 const int* __restrict__ sfirst, double* panels,
@@ -1211,6 +1215,10 @@ __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* 
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
   int bad = -1;
+  if (PM == 2) {   // L given: reciprocal pivots only
+    if (tid < NBMAX) rl[tid] = 1.0 / As[tid * P8_LD + tid];
+    __syncthreads();
+  } else {
   if (tid == 0) p8_diag(As, rl, 0, nb, bad);
   __syncthreads();
   for (int p = 0; p < NBMAX / 8; ++p) {
@@ -1255,7 +1263,9 @@ __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* 
     const int c = e / NBMAX, r = e % NBMAX;
     if (r >= c && r < nb && c < nb) P[(long long)c * S.ld + r] = As[r * P8_LD + c];
   }
+  if (PM == 1) return;
   __syncthreads();
+  }
   // inverse, level 0: the eight 8x8 diagonal blocks (column-oriented substitution per block)
   if (tid < NBMAX / 8) {
     const int b = 8 * tid;
@@ -1287,6 +1297,76 @@ __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* 
     W[e] = (r >= c && r < nb && c < nb) ? As[r * P8_LD + c] : 0.0;
   }
 }
+
+// ----------------------------------------------------------------------------------------------
+// trsm_subst_kernel (a4, "DTRSM"): L_{R,b} = A_{R,b} L_bb^{-T} by forward substitution with
+// L_bb itself, so POTRF need not form the inverse on the cdiv chain (the solve's inverses are made
+// beside the factor, potrf8_kernel<2>).  One CTA per 64-row tile (the MODE_TRSM task layout):
+// thread pair (2i, 2i+1) owns row i, each half 32 columns in registers; column sweep j = 0..nb-1:
+// the owning half scales x_j by 1/L_jj, the pair exchanges it by shuffle, both subtract
+// x_j L(q, j) from their columns q > j (L's column j contiguous in shared memory: 16-byte loads).
+// ----------------------------------------------------------------------------------------------
+constexpr int TS_LD = NBMAX + 2;                     // 66: 16-byte aligned columns
+constexpr int TRSM_SUBST_SMEM = (NBMAX * TS_LD + NBMAX) * (int)sizeof(double);
+__global__ void __launch_bounds__(128, 3) trsm_subst_kernel(const GTask* __restrict__ tasks,
+                                                             const SnInfo* __restrict__ sn, double* panels) {
+  pdl_enter();
+  extern __shared__ __align__(16) double ts_smem[];
+  double* Ls = ts_smem;                              // Ls[j * TS_LD + q] = L(c0 + q, c0 + j)
+  double* rinv = Ls + NBMAX * TS_LD;
+  const GTask T = tasks[blockIdx.x];
+  const SnInfo S = sn[T.sn];
+  const int nb = T.nb, tid = threadIdx.x, lane = tid & 31, i = tid >> 1, h = tid & 1;
+  const double* Lg = panels + S.off + (long long)T.c0 * S.ld + T.c0;
+  for (int e = tid; e < NBMAX * NBMAX; e += 128) {
+    const int j = e / NBMAX, q = e % NBMAX;
+    double* d = Ls + j * TS_LD + q;
+    if (j < nb && q < nb && q >= j) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(d);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(Lg + (long long)j * S.ld + q));
+    } else {
+      *d = 0.0;
+    }
+  }
+  const int r = T.r0 + i;
+  const bool rok = r < S.m && r >= T.s0;
+  double a[32];
+  double* Ag = panels + S.off + (long long)(T.c0 + 32 * h) * S.ld + r;
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) a[jj] = (rok && 32 * h + jj < nb) ? Ag[(long long)jj * S.ld] : 0.0;
+  asm volatile("cp.async.wait_all;\n" ::);
+  __syncthreads();
+  if (tid < NBMAX) rinv[tid] = tid < nb ? 1.0 / Ls[tid * TS_LD + tid] : 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = 32 * hh + jj;
+      if (j >= nb) break;                        // uniform
+      double x = 0.0;
+      if (h == hh) { a[jj] *= rinv[j]; x = a[jj]; }
+      x = __shfl_sync(0xffffffffu, x, (lane & ~1) | hh);
+      // columns q > j of this half: q = 32 h + jj2
+      const double2* lc = reinterpret_cast<const double2*>(Ls + j * TS_LD + 32 * h);
+#pragma unroll
+      for (int p2 = 0; p2 < 16; ++p2) {
+        const int q0 = 32 * h + 2 * p2;
+        if (q0 + 1 <= j) continue;               // both columns at or left of j
+        const double2 l = lc[p2];
+        if (q0 > j) a[2 * p2] = fma(-x, l.x, a[2 * p2]);
+        a[2 * p2 + 1] = fma(-x, l.y, a[2 * p2 + 1]);
+      }
+    }
+  }
+  if (rok) {
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj)
+      if (32 * h + jj < nb) Ag[(long long)jj * S.ld] = a[jj];
+  }
+}
+
+void launch_trsm_subst(const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio);
 
 __global__ void init_scatter_kernel(const double* __restrict__ vals, const long long* __restrict__ amap,
                                     long long nnz, double* panels) {
@@ -1710,7 +1790,10 @@ __global__ void gather_kernel(const double* __restrict__ src, const long long* _
 cudaError_t kernels_init_attributes() {
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM))) return e;
-  if ((e = cudaFuncSetAttribute(potrf8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF8_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(potrf8_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF8_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(potrf8_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF8_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(potrf8_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF8_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(trsm_subst_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSM_SUBST_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 1 + 4) * SMALL_MAXK + 8 * 32 * 1) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 2 + 4) * SMALL_MAXK + 8 * 32 * 2) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 4 + 4) * SMALL_MAXK + 8 * 32 * 4) * 8))) return e;
@@ -1784,15 +1867,22 @@ void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels
 }
 
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels, double* linv,
-                  unsigned long long* fail, cudaStream_t st, int prio) {
+                  unsigned long long* fail, cudaStream_t st, int prio, int mode) {
   if (ntasks <= 0) return;
 #if SPCHOL_POTRF4 == 2
   launch_prio(potrf4_kernel, ntasks, POTRF4_THREADS, 0, st, prio, tasks, sn, sfirst, panels, linv, fail);
 #elif SPCHOL_POTRF4
-  launch_prio(potrf8_kernel, ntasks, POTRF8_THREADS, POTRF8_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
+  if (mode == 1) launch_prio(potrf8_kernel<1>, ntasks, POTRF8_THREADS, POTRF8_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
+  else if (mode == 2) launch_prio(potrf8_kernel<2>, ntasks, POTRF8_THREADS, POTRF8_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
+  else launch_prio(potrf8_kernel<0>, ntasks, POTRF8_THREADS, POTRF8_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
 #else
   launch_prio(potrf_kernel, ntasks, POTRF_THREADS, POTRF_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
 #endif
+}
+
+void launch_trsm_subst(const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio) {
+  if (ntasks <= 0) return;
+  launch_prio(trsm_subst_kernel, ntasks, 128, TRSM_SUBST_SMEM, st, prio, tasks, sn, panels);
 }
 
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,

@@ -73,6 +73,7 @@ constexpr int POTRF4_THREADS = 160;
 #define SPCHOL_POTRF4 1
 #endif
 constexpr int POTRF_SMEM = 2 * NBMAX * (NBMAX + 1) * (int)sizeof(double);
+constexpr bool POTRF_MODES = SPCHOL_POTRF4 == 1;   // potrf8_kernel: factor-only / inverse-only modes
 
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels,
                  const double* linv, const long long* ucol_base, const long long* ucol_map,
@@ -91,8 +92,10 @@ void launch_gemm_tma(int mode, const GTask* tasks, int ntasks, const SnInfo* sn,
                      const void* tmap_linv, const long long* ucol_base, const long long* ucol_map, const int* posmap,
                      cudaStream_t st, int prio = 0);
 void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio = 0);
+// mode 0: factor + inverse, 1: factor only, 2: inverse of the finished block only (potrf8_kernel)
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels,
-                  double* linv, unsigned long long* fail, cudaStream_t st, int prio = 0);
+                  double* linv, unsigned long long* fail, cudaStream_t st, int prio = 0, int mode = 0);
+void launch_trsm_subst(const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio = 0);
 constexpr int SMALL_THREADS = 256;
 constexpr int SMALL_MAXK = 64;
 constexpr int SMALL_MAXM = SMALL_THREADS;
