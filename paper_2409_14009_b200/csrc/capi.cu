@@ -205,6 +205,8 @@ struct spchol_handle {
   bool no_lookahead = false;     // SPCHOL_NO_LOOKAHEAD=1 (diagnostics)
   bool no_next_split = false;    // SPCHOL_NO_NEXT_SPLIT=1: NEXT as one critical-stream launch (diagnostics)
   int rest_smem = 0;             // SPCHOL_REST_SMEM: dynamic shared memory of trailing-stream updates (bytes)
+  int left_inner_min = 16;       // SPCHOL_LEFT_INNER_MIN=n: left-looking in-block updates in levels with at
+                                 // least n large supernodes (0 = never); SPCHOL_LEFT_INNER=1: everywhere
   bool right_inner = true;       // SPCHOL_LEFT_INNER=1: left-looking in-block updates (one K <= 192 pass
                                  // per block column; C4 -0.45%, C5 -0.35%, but C3/C2 +1.3-1.5%: on the chain)
   int max_level = -1;            // SPCHOL_MAX_LEVEL=l: factor only levels <= l (diagnostics)
@@ -423,6 +425,15 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
     // next step needs) stays on stream 0; NEXT_b = its other columns runs at high priority on
     // stream 1 ahead of REST(S), and the first in-block update of S+1 (same entries) waits for it.
     const long long level_p0 = (long long)h->ptasks.size();
+    // in-block update direction for this level: left-looking (fewer read-modify-write passes) where
+    // the level has many large supernodes (bandwidth-bound, chains overlap), right-looking where a
+    // few large supernodes make the cdiv chain critical
+    bool left_inner = !h->right_inner;
+    if (h->left_inner_min > 0) {
+      int nbig = 0;
+      for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) nbig += !h->is_small[h->level_sns[x]];
+      left_inner = left_inner || nbig >= h->left_inner_min;
+    }
     int pending_rest_ev = -1;      // event recorded after the latest REST launch on stream 1
     int pending_nextb_ev = -1;     // event recorded after the latest NEXT_b launch
     const bool split_next = !h->no_lookahead && !h->no_next_split;
@@ -451,7 +462,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
           for (int r0 = c1 & ~1; r0 < I.m; r0 += TILE) h->gtasks.push_back(GTask{J, r0, c1, c0, nb, slot});
           ft += (double)(I.m - c1) * nb * nb;
           bt += 16.0 * (double)(I.m - c1) * nb;
-          if (!h->right_inner) {
+          if (left_inner) {
             // left-looking inside the outer block: before its POTRF, block column [c0, c1) takes
             // the updates of the block columns [C0, c0) in one K = c0 - C0 pass (each column
             // block is read and written once per outer block instead of once per inner step)
@@ -987,6 +998,7 @@ static int finish_handle(spchol_handle* h) {
   if (const char* e = getenv("SPCHOL_NO_LOOKAHEAD")) h->no_lookahead = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_NO_NEXT_SPLIT")) h->no_next_split = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_LEFT_INNER")) h->right_inner = atoi(e) == 0;
+  if (const char* e = getenv("SPCHOL_LEFT_INNER_MIN")) h->left_inner_min = std::max(0, atoi(e));
   if (const char* e = getenv("SPCHOL_REST_SMEM")) h->rest_smem = std::max(0, std::min(112 * 1024, atoi(e)));
   if (const char* e = getenv("SPCHOL_MAX_LEVEL")) h->max_level = atoi(e);
   if (const char* e = getenv("SPCHOL_TMA")) h->use_tma = atoi(e) != 0;
