@@ -18,6 +18,45 @@ import paper_2409_14009_b200 as sp  # noqa: E402
 from helpers import backward_error, panel_index_of_pattern  # noqa: E402
 
 
+def main_not_spd(name, world, frac):
+    """Rank-local pivot failure: every rank must report the same first failing column (the
+    all-reduce(min) of the fail flags), in the final and the caller's numbering."""
+    p = gen.make(name)
+    with sp.Solver.from_problem(p, device=-1) as h0:
+        pf = h0.spchol_export_symbolic()["perm_final"]
+    j0 = int(frac * (p.n - 1))
+    i0 = int(np.where(pf == j0)[0][0])
+    vals = p.values.copy()
+    vals[p.colptr[i0]] = -1.0
+    q = gen.Problem(p.name, p.n, p.colptr, p.rowidx, vals, p.perm)
+    expect = oracle.Oracle.from_problem(q).factor()
+    uid = sp.spchol_dist_nccl_unique_id()
+    hs = [sp.Solver.from_problem(q, dist_world=world, dist_rank=r) for r in range(world)]
+    got = [None] * world
+
+    def run(r):
+        try:
+            hs[r].spchol_dist_attach_nccl(uid)
+            hs[r].spchol_factor()
+            got[r] = "no error"
+        except sp.NotSPDError as e:
+            got[r] = (e.fail_col, e.fail_col_orig)
+        except Exception as e:  # noqa: BLE001
+            got[r] = repr(e)
+
+    th = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    if any(t.is_alive() for t in th):
+        print(json.dumps({"ok": False, "why": "hang"}), flush=True)
+        os._exit(3)
+    ok = expect == j0 and all(g == (j0, i0) for g in got)
+    print(json.dumps({"ok": ok, "expect": [j0, i0], "oracle": expect, "got": [list(g) if isinstance(g, tuple) else g
+                                                                            for g in got]}), flush=True)
+
+
 def main(name, world):
     prob = gen.make(name)
     uid = sp.spchol_dist_nccl_unique_id()
@@ -67,4 +106,7 @@ def main(name, world):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]))
+    if len(sys.argv) > 3:
+        main_not_spd(sys.argv[1], int(sys.argv[2]), float(sys.argv[3]))
+    else:
+        main(sys.argv[1], int(sys.argv[2]))

@@ -303,3 +303,24 @@ def test_device_footprint_query():
         assert nb < 64 * (h.query("PANEL_DOUBLES") + h.query("NNZ_A")) + (64 << 20)
     with sp.Solver.from_problem(prob, device=-1) as h:
         assert h.query("DEVICE_BYTES") == 0
+
+
+@pytest.mark.parametrize("name,world,frac,minflops", [("S4", 2, 0.1, "0"), ("S4", 4, 0.97, "0"), ("S5", 3, 0.5, None)])
+def test_distributed_not_spd_mock(name, world, frac, minflops):
+    """A failing pivot on one rank (in a subtree or in a distributed top supernode): every rank
+    reports the sequential first failing column (all-reduce(min) of the fail flags) through the
+    real NCCL code path over the single-process stand-in."""
+    import json
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ)
+    if minflops is not None:
+        env["SPCHOL_DIST_MINFLOPS"] = minflops
+    here = os.path.dirname(os.path.abspath(__file__))
+    p = subprocess.run([sys.executable, os.path.join(here, "mock_dist_run.py"), name, str(world), str(frac)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert lines, p.stdout[-2000:] + p.stderr[-2000:]
+    r = json.loads(lines[-1])
+    assert r["ok"], r
