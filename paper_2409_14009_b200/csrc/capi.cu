@@ -269,7 +269,10 @@ extern "C" const char* spchol_last_error(void) { return g_err.c_str(); }
 // instead of streaming the whole panel once per row band.
 template <class F>
 static void for_tiles(int rbase, int rend, int cbase, int cend, F emit) {
-  constexpr int SUPER = 8;
+#ifndef SPCHOL_SUPER
+#define SPCHOL_SUPER 8
+#endif
+  constexpr int SUPER = SPCHOL_SUPER;
   const int nr = rend > rbase ? (rend - rbase + TILE - 1) / TILE : 0;
   const int nc = cend > cbase ? (cend - cbase + TILE - 1) / TILE : 0;
   for (int I = 0; I < nr; I += SUPER)
