@@ -132,6 +132,18 @@ def dist_setup(args):
     return world, rank, local
 
 
+def self_launch(args):
+    """`bench.py --gpus N` (N > 1) started without a launcher: re-run this script under
+    torch.distributed.run with N local ranks (one process per GPU) and return its exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle (as it stands) on the host cores, a bounded sample per step."""
     import oracle
@@ -193,6 +205,10 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}")
 
     import torch
     import paper_2409_14009_b200 as sp
@@ -209,27 +225,17 @@ def main():
     t0 = time.perf_counter()
     dist_mode = "1 GPU"
     if world > 1:
-        # distributed factor of one matrix; if its NCCL setup fails on this box, every rank factors
-        # its own replica instead and the line says so (never silently)
-        try:
-            h = sp.Solver.from_problem(prob, device=dev, dist_world=world, dist_rank=rank)
-            uid = [sp.spchol_dist_nccl_unique_id() if rank == 0 else None]
-            torch.distributed.broadcast_object_list(uid, src=0)
-            h.spchol_dist_attach_nccl(uid[0])
-            ok = torch.tensor([1], device="cuda")
-        except Exception as e:  # noqa: BLE001
-            print(f"[rank {rank}] distributed setup failed: {e!r}", file=sys.stderr, flush=True)
-            ok = torch.tensor([0], device="cuda")
-        torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
-        if ok.item() == 1:
-            dist_mode = f"subtree-to-GPU x{world} + NCCL top all-reduce"
-        else:
-            h = sp.Solver.from_problem(prob, device=dev)
-            dist_mode = "replicas (distributed setup failed)"
+        # distributed factor of ONE matrix over the ranks; any setup failure ends the run (non-zero
+        # exit) — there is no replica fallback
+        h = sp.Solver.from_problem(prob, device=dev, dist_world=world, dist_rank=rank)
+        uid = [sp.spchol_dist_nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        h.spchol_dist_attach_nccl(uid[0])
+        dist_mode = (f"subtree-to-GPU x{world}: proportional mapping of the supernodal etree, top supernodes "
+                     f"distributed over their rank groups, NCCL exchanges")
     else:
         h = sp.Solver.from_problem(prob, device=dev)
     analyze_s = time.perf_counter() - t0
-    replicas = dist_mode.startswith("replicas")
     stream = torch.cuda.Stream()
     h.spchol_set_stream(stream.cuda_stream)
     F = float(h.query("FLOPS_EXACT"))
@@ -265,7 +271,7 @@ def main():
     fc, _ = h.spchol_factor_status()
     assert fc == -1
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
-    value = (world if replicas else 1) * F / (ms / 1e3) / 1e9   # distributed: one matrix (strong scaling)
+    value = F / (ms / 1e3) / 1e9   # distributed: one matrix (strong scaling)
     peak = fp64_peak()
 
     # ---- roofline of the dominant kernel (SYRK/GEMM + relind scatter), CUDA events per launch
@@ -335,7 +341,7 @@ def main():
         barrier()
         solve_ms = max_over_ranks(s0.elapsed_time(s1) / args.steps)
         e2e = {"solve_ms": solve_ms, "solve_GBps_L_read_twice": 2 * 8 * h.query("NNZ_L") / (solve_ms / 1e3) / 1e9,
-               "value": (world if replicas else 1) * F / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * (prob.nnz + prob.n),
+               "value": F / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * (prob.nnz + prob.n),
                "d2h_bytes_per_step": 8 * prob.n + 8, "seconds_per_step": e2e_s, "includes": "set_values(H2D) + factor + solve(H2D b, D2H x)",
                "backward_error": berr}
 
@@ -347,7 +353,7 @@ def main():
     line = {
         "metric": "numeric factor FP64 GFLOP/s (F_exact / factor time)",
         "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if world > 1 and not replicas else "weak",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": gen.CONFIGS[args.config]["desc"], "config_id": args.config, "n": prob.n,
                    "nnz_A_lower": prob.nnz, "nnz_L": h.query("NNZ_L"), "flops_exact": F, "flops_executed": Fexec,

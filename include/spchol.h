@@ -260,6 +260,12 @@ int spchol_dist_nccl_unique_id(void* out128);
 /* Attach an NCCL communicator (ncclCommInitRank over dist_world ranks, this handle's dist_rank;
  * collective: every rank must call it).  NCCL is loaded with dlopen (libnccl.so.2). */
 int spchol_dist_attach_nccl(spchol_handle* h, const void* unique_id128);
+/* Collective (every rank of the communicator must call it, in the same order relative to the other
+ * collective calls): assemble the whole factor on every rank after a successful multi-GPU factor.
+ * Value exports (panels, diagonal, CSC values) of a multi-GPU handle return STATE until it has run;
+ * the first solve after a factor runs it implicitly (so that solve is collective too).  No-op for
+ * dist_world == 1. */
+int spchol_dist_gather(spchol_handle* h);
 /* owner[NSUPER]: rank owning each supernode's subtree, -1 for the top supernodes (all 0 when
  * dist_world == 1); top_owner[NSUPER]: the rank that factors an undistributed top supernode, and
  * the rank owning block column 0 of a distributed one (block column C of a distributed top

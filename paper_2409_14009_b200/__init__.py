@@ -28,7 +28,7 @@ SPCHOL_ERR_STATE = -7
 Q = dict(N=0, NNZ_A=1, NNZ_L=2, NFUND=3, NSUPER=4, ADDED=5, NLEVELS=6, ROWS_LEN=7, NPAIRS=8,
          RELIND_LEN=9, PANEL_DOUBLES=10, NMERGES=11, FLOPS_EXACT=12, FLOPS_EXEC=13, LAUNCHES=14,
          UPDATE_ENTRIES=15, NBLOCKS=16, NMARKERS=17, NTOP_DIST=18, DEVICE_BYTES=19)
-KERNEL_KINDS = dict(small=0, potrf=1, trsm=2, local_update=3, syrk_scatter=4, init=5, rlb_update=6, inverse=7)
+KERNEL_KINDS = dict(small=0, potrf=1, trsm=2, local_update=3, syrk_scatter=4, init=5, rlb_update=6)
 
 # Every symbol include/spchol.h declares (checked by tests/test_capi_exports.py).
 EXPORTS = [
@@ -37,7 +37,7 @@ EXPORTS = [
     "spchol_set_stream", "spchol_factor_async", "spchol_factor_status", "spchol_factor",
     "spchol_solve", "spchol_solve_device", "spchol_query", "spchol_export_symbolic",
     "spchol_export_blocks", "spchol_export_panels", "spchol_export_panel", "spchol_export_diagonal", "spchol_enable_kernel_timing", "spchol_kernel_stats",
-    "spchol_kernel_trace", "spchol_dist_nccl_unique_id", "spchol_dist_attach_nccl", "spchol_export_mapping",
+    "spchol_kernel_trace", "spchol_dist_nccl_unique_id", "spchol_dist_attach_nccl", "spchol_dist_gather", "spchol_export_mapping",
     "spchol_factor_phase", "spchol_dist_debug_comm", "spchol_dist_debug_accumulate", "spchol_dist_plan_flops",
     "spchol_destroy", "spchol_last_error",
 ]
@@ -98,6 +98,7 @@ def lib():
         L.spchol_kernel_trace.argtypes = [vp, i64, ctypes.POINTER(i64), vp, vp, vp, vp]
         L.spchol_dist_nccl_unique_id.argtypes = [vp]
         L.spchol_dist_attach_nccl.argtypes = [vp, vp]
+        L.spchol_dist_gather.argtypes = [vp]
         L.spchol_export_mapping.argtypes = [vp, vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.spchol_factor_phase.argtypes = [vp, ctypes.c_int]
         L.spchol_dist_debug_accumulate.argtypes = [vp, vp, ctypes.c_int]
@@ -311,6 +312,9 @@ class Solver:
     def spchol_dist_attach_nccl(self, unique_id: bytes):
         buf = ctypes.create_string_buffer(bytes(unique_id), 128)
         _check(self._L.spchol_dist_attach_nccl(self._h, buf))
+
+    def spchol_dist_gather(self):
+        _check(self._L.spchol_dist_gather(self._h))
 
     def spchol_export_mapping(self, with_top_owner=False):
         owner = np.empty(self.spchol_query("NSUPER"), np.int32)

@@ -14,6 +14,9 @@
 
 #include <algorithm>
 #include <array>
+#include <climits>
+#include <cstdint>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -49,7 +52,7 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call);    \
   } while (0)
 
-enum LaunchKind { K_SMALL = 0, K_POTRF = 1, K_TRSM = 2, K_LOCAL = 3, K_SCATTER = 4, K_INIT = 5, K_RLB = 6, K_INV = 7, K_NKINDS = 8 };
+enum LaunchKind { K_SMALL = 0, K_POTRF = 1, K_TRSM = 2, K_LOCAL = 3, K_SCATTER = 4, K_INIT = 5, K_RLB = 6, K_NKINDS = 7 };
 }  // namespace
 
 // ------------------------------------------------------------------------------------- NCCL
@@ -81,29 +84,34 @@ struct NcclApi {
   nccl_errstr_t errstr = nullptr;
 };
 NcclApi g_nccl;
+std::mutex g_nccl_mu;   // handles (and the tests' rank threads) may attach concurrently
 constexpr int NCCL_SUM = 0, NCCL_MIN = 3, NCCL_UINT64 = 5, NCCL_FLOAT64 = 8;
+// Resolves every symbol into a local table first and publishes it (g_nccl.so last) under the lock.
 bool nccl_load(std::string& err) {
+  std::lock_guard<std::mutex> lock(g_nccl_mu);
   if (g_nccl.so) return true;
+  NcclApi api;
   // SPCHOL_NCCL_LIB: another NCCL build, or the tests' single-GPU stand-in (tests/mock_nccl)
   const char* alt = getenv("SPCHOL_NCCL_LIB");
   void* so = dlopen(alt && *alt ? alt : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!so) so = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
   if (!so) { err = std::string("cannot load NCCL: ") + dlerror(); return false; }
-  g_nccl.getid = (nccl_getid_t)dlsym(so, "ncclGetUniqueId");
-  g_nccl.init = (nccl_init_t)dlsym(so, "ncclCommInitRank");
-  g_nccl.allreduce = (nccl_allreduce_t)dlsym(so, "ncclAllReduce");
-  g_nccl.reduce = (nccl_reduce_t)dlsym(so, "ncclReduce");
-  g_nccl.send = (nccl_p2p_t)dlsym(so, "ncclSend");
-  g_nccl.bcast = (nccl_bcast_t)dlsym(so, "ncclBroadcast");
-  g_nccl.split = (nccl_split_t)dlsym(so, "ncclCommSplit");
-  g_nccl.recv = (nccl_p2p_t)dlsym(so, "ncclRecv");
-  g_nccl.group_start = (nccl_group_t)dlsym(so, "ncclGroupStart");
-  g_nccl.group_end = (nccl_group_t)dlsym(so, "ncclGroupEnd");
-  g_nccl.destroy = (nccl_destroy_t)dlsym(so, "ncclCommDestroy");
-  g_nccl.errstr = (nccl_errstr_t)dlsym(so, "ncclGetErrorString");
-  if (!g_nccl.getid || !g_nccl.init || !g_nccl.allreduce || !g_nccl.reduce || !g_nccl.send || !g_nccl.recv || !g_nccl.bcast || !g_nccl.split || !g_nccl.group_start ||
-      !g_nccl.group_end || !g_nccl.destroy) { err = "NCCL symbols missing"; return false; }
-  g_nccl.so = so;
+  api.getid = (nccl_getid_t)dlsym(so, "ncclGetUniqueId");
+  api.init = (nccl_init_t)dlsym(so, "ncclCommInitRank");
+  api.allreduce = (nccl_allreduce_t)dlsym(so, "ncclAllReduce");
+  api.reduce = (nccl_reduce_t)dlsym(so, "ncclReduce");
+  api.send = (nccl_p2p_t)dlsym(so, "ncclSend");
+  api.bcast = (nccl_bcast_t)dlsym(so, "ncclBroadcast");
+  api.split = (nccl_split_t)dlsym(so, "ncclCommSplit");
+  api.recv = (nccl_p2p_t)dlsym(so, "ncclRecv");
+  api.group_start = (nccl_group_t)dlsym(so, "ncclGroupStart");
+  api.group_end = (nccl_group_t)dlsym(so, "ncclGroupEnd");
+  api.destroy = (nccl_destroy_t)dlsym(so, "ncclCommDestroy");
+  api.errstr = (nccl_errstr_t)dlsym(so, "ncclGetErrorString");
+  if (!api.getid || !api.init || !api.allreduce || !api.reduce || !api.send || !api.recv || !api.bcast || !api.split || !api.group_start ||
+      !api.group_end || !api.destroy) { err = "NCCL symbols missing"; return false; }
+  api.so = so;
+  g_nccl = api;
   return true;
 }
 int nccl_fail(int r, const char* where) {
@@ -189,8 +197,6 @@ struct spchol_handle {
   std::vector<std::array<int, 2>> grp_keys;   // distinct rank groups [lo, hi) of the top supernodes (hi - lo < world)
   std::vector<void*> grp_comms;               // their NCCL communicators (ncclCommSplit; null if not a member)
   bool gathered = false;
-  struct SolveStep { int level; long long p0; int np; long long t0; int nt; };
-  std::vector<SolveStep> solve_steps;   // per (level, inner block step): POTRF and TRSM task ranges
   std::vector<int> small_level_off;     // small_sns range per level
   std::vector<STask> stasks;            // level solve tasks: forward of level l at [sfwd_off[l], sfwd_off[l+1]),
   std::vector<long long> sfwd_off, sbwd_off;   // backward at [sbwd_off[l], sbwd_off[l+1])
@@ -200,7 +206,6 @@ struct spchol_handle {
   SmallSolve* d_ssolve = nullptr;
   int* d_sflags = nullptr;              // forward flags | backward flags | backward chunk counts (nslots
                                         // each) | per-level tickets (2 * nlevels); zeroed per solve
-  bool legacy_solve = false;            // SPCHOL_SOLVE_LEGACY=1: per-block-step launches (diagnostics)
   int nevents = 0;
   bool no_lookahead = false;     // SPCHOL_NO_LOOKAHEAD=1 (diagnostics)
   bool no_next_split = false;    // SPCHOL_NO_NEXT_SPLIT=1: NEXT as one critical-stream launch (diagnostics)
@@ -211,9 +216,6 @@ struct spchol_handle {
                                  // per block column; C4 -0.45%, C5 -0.35%, but C3/C2 +1.3-1.5%: on the chain)
   int max_level = -1;            // SPCHOL_MAX_LEVEL=l: factor only levels <= l (diagnostics)
   bool small_warp = true;        // SPCHOL_SMALL_WARP=0: CTA-per-supernode small kernel for every size
-  bool trsm_subst = false;       // SPCHOL_TRSM_SUBST=1: TRSM by substitution with L_bb (POTRF without the
-                                 // inverse on the chain, the solve's inverses beside the factor); measured
-                                 // slower than the DMMA TRSM with kept inverses (C4 +5.5%, C2 +10%)
   int small_warp_maxm = 64;      // largest m of the warp-per-supernode kernel (SPCHOL_SMALL_WARP_MAXM <= 128)
   bool use_tma = false;          // SPCHOL_TMA=1: TMA + mbarrier tile kernels (measured ~2% slower)
   void* d_tmaps = nullptr;       // CUtensorMap per supernode panel (TMA boxes 16 x 8, 128B swizzle)
@@ -498,7 +500,6 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         }
       }
       long long p1 = (long long)h->ptasks.size(), t1 = (long long)h->gtasks.size();
-      if (record_solve && p1 > p0) h->solve_steps.push_back(spchol_handle::SolveStep{l, p0, (int)(p1 - p0), t0, (int)(t1 - t0)});
       if (!left.empty()) {   // left-looking in-block update of this step's block column, before its POTRF
         if (pending_nextb_ev >= 0) {   // same entries as NEXT_b
           h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SB, pending_nextb_ev});
@@ -558,15 +559,6 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       }
     }
     (void)pending_nextb_ev;
-    if (h->trsm_subst && (long long)h->ptasks.size() > level_p0) {
-      // the solve's diagonal-block inverses of this level, beside the factor (low priority side stream)
-      const int ev = h->nevents++, SIDE = 2 * 16 + SB + 1;
-      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, SB, ev});
-      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SIDE, ev});
-      const long long np = (long long)h->ptasks.size() - level_p0;
-      h->plan.push_back(Launch{K_INV, level_p0, (int)np, (double)np * NBMAX * NBMAX * NBMAX / 3.0, 16.0 * np * NBMAX * NBMAX,
-                               OP_LAUNCH, SIDE, -1});
-    }
     bool s1_used = false;
     for (size_t q = plan_before; q < h->plan.size(); ++q) s1_used |= h->plan[q].stream == SB + 1;
     if (s1_used) {  // join stream 1 (small-supernode launch and trailing updates) before the level's scatter
@@ -1006,11 +998,8 @@ static int finish_handle(spchol_handle* h) {
   if (const char* e = getenv("SPCHOL_MAX_LEVEL")) h->max_level = atoi(e);
   if (const char* e = getenv("SPCHOL_TMA")) h->use_tma = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_OUTER")) h->outer = std::max(1, atoi(e));
-  if (const char* e = getenv("SPCHOL_SOLVE_LEGACY")) h->legacy_solve = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_DIST_MINFLOPS")) h->dist_min_flops = atof(e);
   if (const char* e = getenv("SPCHOL_SMALL_WARP")) h->small_warp = atoi(e) != 0;
-  if (const char* e = getenv("SPCHOL_TRSM_SUBST")) h->trsm_subst = atoi(e) != 0;
-  if (!POTRF_MODES || h->use_tma) h->trsm_subst = false;
   if (const char* e = getenv("SPCHOL_SMALL_WARP_MAXM")) h->small_warp_maxm = std::max(0, std::min(128, atoi(e)));
   build_plan(h);
   if (h->opt.device < 0) return SPCHOL_OK;   // host-only analysis (no device state)
@@ -1077,6 +1066,58 @@ struct Reader {
   template <class T> bool sc(T& x) { return fread(&x, sizeof x, 1, f) == 1; }
   template <class T> bool v(std::vector<T>& x) { return rvec(f, x); }
 };
+// Consistency of a deserialised analysis before anything indexes with it: array lengths against
+// n / nsuper / nnzA, monotone pointer arrays with the right final values, every index in range.
+bool valid_symbolic(const Symbolic& S, std::string& why) {
+  const int64_t n = S.n, ns = S.nsuper;
+  auto bad = [&](const char* w) { why = w; return false; };
+  if (n < 1 || n > INT32_MAX || ns < 1 || ns > n || S.nnzA < n || S.nlevels < 1 || S.nlevels > ns) return bad("scalars");
+  auto len = [](const auto& v, int64_t x) { return (int64_t)v.size() == x; };
+  if (!len(S.post, n) || !len(S.parent3, n) || !len(S.cc3, n) || !len(S.perm_final, n) || !len(S.iperm_final, n) ||
+      !len(S.parent_final, n) || !len(S.cc_final, n) || !len(S.snode, n) || !len(S.sfirst, ns + 1) ||
+      !len(S.sparent, ns) || !len(S.rows_ptr, ns + 1) || !len(S.rel_ptr, ns + 1) || !len(S.level, ns) ||
+      !len(S.blk_ptr, ns + 1) || !len(S.a_col, S.nnzA) || !len(S.a_pos, S.nnzA))
+    return bad("array lengths");
+  auto in = [](int64_t v, int64_t lo, int64_t hi) { return v >= lo && v < hi; };
+  std::vector<char> seen(n, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    if (!in(S.perm_final[i], 0, n) || seen[S.perm_final[i]]) return bad("perm_final is not a permutation");
+    seen[S.perm_final[i]] = 1;
+    if (S.iperm_final[S.perm_final[i]] != i) return bad("iperm_final");
+    if (!in(S.snode[i], 0, ns) || !(S.parent_final[i] == -1 || in(S.parent_final[i], i + 1, n))) return bad("snode / parent");
+  }
+  if (S.sfirst[0] != 0 || S.sfirst[ns] != n || S.rows_ptr[0] != 0 || (int64_t)S.rows.size() != S.rows_ptr[ns] ||
+      S.rel_ptr[0] != 0 || (int64_t)S.rel_anc.size() != S.rel_ptr[ns] || !len(S.rel_q0, S.rel_ptr[ns]) ||
+      !len(S.rel_off, S.rel_ptr[ns] + 1) || S.blk_ptr[0] != 0 || !len(S.blk_q, S.blk_ptr[ns]) ||
+      !len(S.blk_len, S.blk_ptr[ns]) || !len(S.blk_anc, S.blk_ptr[ns]) || !len(S.blk_relind, S.blk_ptr[ns]))
+    return bad("pointer ends");
+  for (int64_t J = 0; J < ns; ++J) {
+    const int64_t k = S.sfirst[J + 1] - S.sfirst[J], m = S.rows_ptr[J + 1] - S.rows_ptr[J];
+    if (k < 1 || m < k || m > n || S.rel_ptr[J + 1] < S.rel_ptr[J] || S.blk_ptr[J + 1] < S.blk_ptr[J]) return bad("supernode shape");
+    if (!(S.sparent[J] == -1 || in(S.sparent[J], J + 1, ns)) || !in(S.level[J], 0, S.nlevels)) return bad("supernode tree");
+    for (int64_t q = S.rows_ptr[J]; q < S.rows_ptr[J + 1]; ++q)
+      if (!in(S.rows[q], 0, n) || (q > S.rows_ptr[J] && S.rows[q] <= S.rows[q - 1])) return bad("rows(J)");
+    for (int64_t c = 0; c < k; ++c)
+      if (S.rows[S.rows_ptr[J] + c] != S.sfirst[J] + c || S.snode[S.sfirst[J] + c] != J) return bad("rows(J) columns");
+    for (int64_t p = S.rel_ptr[J]; p < S.rel_ptr[J + 1]; ++p) {
+      if (!in(S.rel_anc[p], J + 1, ns) || !in(S.rel_q0[p], k, m)) return bad("relind pairs");
+      const int64_t mP = S.rows_ptr[S.rel_anc[p] + 1] - S.rows_ptr[S.rel_anc[p]];
+      if (S.rel_off[p + 1] < S.rel_off[p] || S.rel_off[p + 1] > (int64_t)S.relind.size()) return bad("rel_off");
+      for (int64_t x = S.rel_off[p]; x < S.rel_off[p + 1]; ++x)
+        if (!in(S.relind[x], 0, mP)) return bad("relind range");
+    }
+    for (int64_t b = S.blk_ptr[J]; b < S.blk_ptr[J + 1]; ++b)
+      if (!in(S.blk_anc[b], J + 1, ns) || !in(S.blk_q[b], k, m) || S.blk_len[b] < 1 || S.blk_q[b] + S.blk_len[b] > m)
+        return bad("RLB blocks");
+  }
+  if (S.rel_off.back() != (int64_t)S.relind.size()) return bad("relind length");
+  for (int64_t e = 0; e < S.nnzA; ++e) {
+    if (!in(S.a_col[e], 0, n)) return bad("a_col");
+    const int32_t J = S.snode[S.a_col[e]];
+    if (!in(S.a_pos[e], S.a_col[e] - S.sfirst[J], S.rows_ptr[J + 1] - S.rows_ptr[J])) return bad("a_pos");
+  }
+  return true;
+}
 }  // namespace
 
 extern "C" int spchol_save_analysis(const spchol_handle* h, const char* path) {
@@ -1105,6 +1146,8 @@ extern "C" int spchol_load_analysis(const char* path, const spchol_options* opt,
             fields(h->S, cap, r);
   fclose(f);
   if (!ok) { delete h; return fail(SPCHOL_ERR_VALIDATION, std::string("not a spchol analysis file: ") + path); }
+  std::string why;
+  if (!valid_symbolic(h->S, why)) { delete h; return fail(SPCHOL_ERR_VALIDATION, std::string("inconsistent analysis file (") + why + "): " + path); }
   h->opt.merge_cap = cap;   // the analysis was built with this cap
   int rc = finish_handle(h);
   if (rc != SPCHOL_OK) { delete h; return rc; }
@@ -1281,16 +1324,10 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
                      h->d_posmap, h->d_fail, L.aux, L.aux2, h->opt.deterministic ? 1 : 0, ls, prio, L.aux3);
         break;
       case K_POTRF:
-        launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio,
-                     h->trsm_subst ? 1 : 0);
-        break;
-      case K_INV:
-        launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio, 2);
+        launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio);
         break;
       case K_TRSM:
-        if (h->trsm_subst)
-          launch_trsm_subst(h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, ls, prio);
-        else if (h->use_tma)
+        if (h->use_tma)
           launch_gemm_tma(MODE_TRSM, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_tmaps, h->d_tmap_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
         else
           launch_gemm(MODE_TRSM, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
@@ -1420,45 +1457,23 @@ extern "C" int spchol_factor(spchol_handle* h, int64_t* fail_col, int64_t* fail_
 static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaStream_t st) {
   const Symbolic& S = h->S;
   launch_permute(h->d_perm, d_b, h->d_y, S.n, 0, st);
-  std::vector<std::pair<size_t, size_t>> lvl_steps(S.nlevels, {0, 0});
-  for (size_t q = 0; q < h->solve_steps.size(); ++q) {
-    auto& r = lvl_steps[h->solve_steps[q].level];
-    if (r.second == 0) r.first = q;
-    r.second = q + 1;
-  }
   const size_t NS = (size_t)std::max(1, h->nslots_total);
   int* fflag = h->d_sflags;
   int* bflag = fflag + NS;
   int* rcnt = bflag + NS;
   int* tickets = rcnt + NS;
-  if (!h->legacy_solve) CK(cudaMemsetAsync(h->d_sflags, 0, sizeof(int) * (3 * NS + 2 * (size_t)S.nlevels + 1), st));
+  CK(cudaMemsetAsync(h->d_sflags, 0, sizeof(int) * (3 * NS + 2 * (size_t)S.nlevels + 1), st));
   for (int l = 0; l < S.nlevels; ++l) {
     for (int cl = 0; cl < 3; ++cl)
       launch_solve_small(h->d_ssolve + h->ssolve_off[3 * l + cl], h->ssolve_off[3 * l + cl + 1] - h->ssolve_off[3 * l + cl],
                          cl, 0, h->d_rows, h->d_panels, h->d_y, st);
-    if (!h->legacy_solve) {
-      launch_solve_fwd_level(h->d_stasks + h->sfwd_off[l], (int)(h->sbwd_off[l] - h->sfwd_off[l]), tickets + 2 * l, fflag,
-                             h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, st);
-      continue;
-    }
-    for (size_t q = lvl_steps[l].first; q < lvl_steps[l].second; ++q) {
-      const auto& T = h->solve_steps[q];
-      launch_solve_diag(h->d_ptasks + T.p0, T.np, h->d_sfirst, h->d_linv, h->d_y, 0, st);
-      launch_solve_upd(h->d_gtasks + T.t0, T.nt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, 0, st);
-    }
+    launch_solve_fwd_level(h->d_stasks + h->sfwd_off[l], (int)(h->sbwd_off[l] - h->sfwd_off[l]), tickets + 2 * l, fflag,
+                           h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, st);
   }
   for (int l = S.nlevels - 1; l >= 0; --l) {
-    if (!h->legacy_solve) {
-      launch_solve_bwd_level(h->d_stasks + h->sbwd_off[l], (int)(h->sfwd_off[l + 1] - h->sbwd_off[l]), tickets + 2 * l + 1,
-                             bflag, rcnt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y,
-                             h->nb, st);
-    } else {
-      for (size_t q = lvl_steps[l].second; q > lvl_steps[l].first; --q) {
-        const auto& T = h->solve_steps[q - 1];
-        launch_solve_upd(h->d_gtasks + T.t0, T.nt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_y, 1, st);
-        launch_solve_diag(h->d_ptasks + T.p0, T.np, h->d_sfirst, h->d_linv, h->d_y, 1, st);
-      }
-    }
+    launch_solve_bwd_level(h->d_stasks + h->sbwd_off[l], (int)(h->sfwd_off[l + 1] - h->sbwd_off[l]), tickets + 2 * l + 1,
+                           bflag, rcnt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y,
+                           h->nb, st);
     for (int cl = 0; cl < 3; ++cl)
       launch_solve_small(h->d_ssolve + h->ssolve_off[3 * l + cl], h->ssolve_off[3 * l + cl + 1] - h->ssolve_off[3 * l + cl],
                          cl, 1, h->d_rows, h->d_panels, h->d_y, st);
@@ -1482,6 +1497,17 @@ static int gather_factor(spchol_handle* h) {
                                                    NCCL_FLOAT64, NCCL_SUM, h->nccl_comm, h->stream)))
     return nccl_fail(r, "ncclAllReduce(diagonal inverses)");
   h->gathered = true;
+  return SPCHOL_OK;
+}
+
+extern "C" int spchol_dist_gather(spchol_handle* h) {
+  if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
+  if (host_only(h) || !h->factored) return fail(SPCHOL_ERR_STATE, "gather before a successful factor");
+  if (h->world == 1) return SPCHOL_OK;
+  CK(cudaSetDevice(h->opt.device));
+  int rc = gather_factor(h);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(h->stream));
   return SPCHOL_OK;
 }
 
@@ -1606,6 +1632,14 @@ extern "C" int spchol_export_blocks(const spchol_handle* h, int64_t* blk_ptr, in
   return SPCHOL_OK;
 }
 
+// Multi-GPU: after a factor each rank holds only its share of L until the collective gather
+// (spchol_dist_gather, or the first solve) has run; value exports before that would be partial.
+static int need_gathered(const spchol_handle* h) {
+  if (h->world > 1 && h->factored && !h->gathered)
+    return fail(SPCHOL_ERR_STATE, "multi-GPU factor not gathered: call spchol_dist_gather (collective) first");
+  return SPCHOL_OK;
+}
+
 extern "C" int spchol_export_panels(const spchol_handle* h, int64_t* panel_off, int32_t* ld, double* panels) {
   if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
   if (host_only(h) && panels) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
@@ -1614,6 +1648,7 @@ extern "C" int spchol_export_panels(const spchol_handle* h, int64_t* panel_off, 
     if (ld) for (size_t J = 0; J < h->sn.size(); ++J) ld[J] = h->sn[J].ld;
     return SPCHOL_OK;
   }
+  if (panels && need_gathered(h)) return SPCHOL_ERR_STATE;
   CK(cudaSetDevice(h->opt.device));
   CK(cudaStreamSynchronize(h->stream));
   if (panel_off) for (size_t J = 0; J < h->panel_off.size(); ++J) panel_off[J] = h->panel_off[J];
@@ -1627,6 +1662,7 @@ extern "C" int spchol_export_panel(const spchol_handle* h, int32_t J, double* ou
   if (!h || !out) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
   if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
   if (J < 0 || J >= h->S.nsuper) return fail(SPCHOL_ERR_DIMENSION, "supernode index out of range");
+  if (need_gathered(h)) return SPCHOL_ERR_STATE;
   CK(cudaSetDevice(h->opt.device));
   CK(cudaStreamSynchronize(h->stream));
   const size_t cnt = (size_t)h->sn[J].ld * h->sn[J].k;   // panels need not be in supernode order
@@ -1642,6 +1678,7 @@ extern "C" int spchol_export_factor_csc(const spchol_handle* h, int64_t* Lp, int
   if (!h || !Lp) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
   if ((Lx || padding_nonzeros) && (host_only(h) || !h->factored))
     return fail(SPCHOL_ERR_STATE, "values need a successful factor on a device handle");
+  if ((Lx || padding_nonzeros) && need_gathered(h)) return SPCHOL_ERR_STATE;
   const Symbolic& S = h->S;
   const int64_t n = S.n;
   Lp[0] = 0;
@@ -1705,6 +1742,7 @@ extern "C" int spchol_export_factor_csc(const spchol_handle* h, int64_t* Lp, int
 extern "C" int spchol_export_diagonal(spchol_handle* h, double* diag) {
   if (!h || !diag) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
   if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
+  if (need_gathered(h)) return SPCHOL_ERR_STATE;
   CK(cudaSetDevice(h->opt.device));
   const Symbolic& S = h->S;
   if (!h->d_diag_idx) {

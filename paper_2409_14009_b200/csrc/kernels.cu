@@ -404,188 +404,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 4) gemm_tma_kernel(const GTask* 
 }
 
 // ----------------------------------------------------------------------------------------------
-// potrf_kernel: one CTA (4 warps) factors the nb x nb (nb <= 64) diagonal block [c0, c0+nb) of
-// supernode J ("DPOTRF") and forms X = L_bb^{-1} for TRSM-as-GEMM.  A block with nb < 64 is
-// padded with the identity (chol/inverse of blockdiag(A, I) = blockdiag(L, I)).
-// 2x2 blocking of the 64x64 block into 32x32 pieces keeps the dependent chain short:
-//   warp 0: L11 = chol(A11), X11 = L11^{-1}         (register rows + shuffles, no barriers)
-//   all:    L21 = A21 X11^T;  A22 -= L21 L21^T
-//   warp 0: L22 = chol(A22), X22 = L22^{-1}
-//   all:    T = L21 X11;  X21 = -X22 T
-// The strict upper triangle of the panel is padding and is never written.  X goes to the task's
-// workspace slot, column-major, ld 64, zero padded.  A pivot that is not > 0 (incl. NaN) records
-// its global column (final numbering) with atomicMin (a7).
-// ----------------------------------------------------------------------------------------------
-constexpr int PLD = NBMAX + 1;   // shared-memory column stride (doubles) of the 64x64 blocks
-
-// Cholesky of the 32x32 block at (b, b) of D (D[col][row]) by one warp: lane r owns row r.  The
-// step loop stays rolled (small code): the registers rotate so the current column is always a[0].
-__device__ __noinline__ void chol32_warp(double* D, int b, int lane, int* bad, double* rdiag) {
-  double a[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) a[c] = c <= lane ? D[(b + c) * PLD + b + lane] : 0.0;
-#pragma unroll 1
-  for (int j = 0; j < 32; ++j) {
-    const double d = __shfl_sync(0xffffffffu, a[0], j);
-    const double rl = rsqrt(d), l = d * rl;
-    if (*bad < 0 && !(d > 0.0)) *bad = b + j;
-    const double lrj = lane > j ? a[0] * rl : (lane == j ? l : 0.0);
-    if (lane >= j) D[(b + j) * PLD + b + lane] = lrj;
-    if (lane == j) rdiag[b + j] = rl;
-#pragma unroll
-    for (int c = 1; c < 32; ++c) {
-      const double lc = __shfl_sync(0xffffffffu, lrj, (j + c) & 31);
-      if (j + c <= lane) a[c] -= lrj * lc;
-    }
-#pragma unroll
-    for (int c = 0; c < 31; ++c) a[c] = a[c + 1];
-    a[31] = 0.0;
-  }
-}
-
-// X_bb = L_bb^{-1} for the 32x32 block at (b, b) by one warp: lane c solves L x = e_c, column
-// oriented (x_s final at step s, then eliminated from the rows below); registers rotate as above.
-__device__ __noinline__ void inv32_warp(const double* D, double* X, int b, int lane, const double* rdiag) {
-  double y[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) y[i] = i == lane ? 1.0 : 0.0;
-#pragma unroll 1
-  for (int s = 0; s < 32; ++s) {
-    const double xs = y[0] * rdiag[b + s];
-    X[(b + lane) * PLD + b + s] = xs;
-#pragma unroll
-    for (int i = 1; i < 32; ++i)
-      if (s + i < 32) y[i] -= D[(b + s) * PLD + b + s + i] * xs;
-#pragma unroll
-    for (int i = 0; i < 31; ++i) y[i] = y[i + 1];
-    y[31] = 0.0;
-  }
-}
-
-__global__ void __launch_bounds__(POTRF_THREADS, 4) potrf_kernel(const PTask* __restrict__ tasks,
-                                                                 const SnInfo* __restrict__ sn,
-                                                                 const int* __restrict__ sfirst, double* panels,
-                                                                 double* linv, unsigned long long* fail) {
-  pdl_enter();
-  extern __shared__ double psm[];
-  double* D = psm;                      // D[col * PLD + row]: A, then L (lower); upper-right 32x32 holds T
-  double* X = psm + NBMAX * PLD;        // X[col * PLD + row] = (L^{-1})(row, col)
-  __shared__ double rdiag[NBMAX];
-  const PTask T = tasks[blockIdx.x];
-  const SnInfo S = sn[T.sn];
-  const int nb = T.nb, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* P = panels + S.off + (long long)T.c0 * S.ld + T.c0;
-  for (int e = tid; e < NBMAX * NBMAX; e += POTRF_THREADS) {
-    const int c = e >> 6, r = e & 63;
-    double v = 0.0;
-    if (r >= c) v = (r < nb) ? (c < nb ? P[(long long)c * S.ld + r] : 0.0) : (r == c ? 1.0 : 0.0);
-    D[c * PLD + r] = v;
-    X[c * PLD + r] = 0.0;
-  }
-  int bad = -1;
-  __syncthreads();
-  if (warp == 0) {
-    chol32_warp(D, 0, lane, &bad, rdiag);
-    __syncwarp();
-    inv32_warp(D, X, 0, lane, rdiag);
-  }
-  __syncthreads();
-  // L21 = A21 X11^T: thread -> row i = 32 + (tid & 31), columns c = cg + 4m (cg = warp)
-  {
-    const int i = 32 + lane;
-    double arow[32];
-#pragma unroll
-    for (int p = 0; p < 32; ++p) arow[p] = D[p * PLD + i];
-    double out[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {   // (out[] needs static indices)
-      const int c = warp + 4 * m;
-      double s = 0.0;
-#pragma unroll
-      for (int p = 0; p < 32; ++p)
-        if (p <= c) s += arow[p] * X[p * PLD + c];      // X11(c, p)
-      out[m] = s;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int m = 0; m < 8; ++m) D[(warp + 4 * m) * PLD + i] = out[m];
-  }
-  __syncthreads();
-  // A22 -= L21 L21^T (lower): thread -> row i = 32 + lane, columns j = 32 + warp + 4m <= i
-  {
-    const int i = 32 + lane;
-    double lrow[32];
-#pragma unroll
-    for (int p = 0; p < 32; ++p) lrow[p] = D[p * PLD + i];
-#pragma unroll 1
-    for (int m = 0; m < 8; ++m) {
-      const int j = 32 + warp + 4 * m;
-      if (j > i) continue;
-      double s = 0.0;
-#pragma unroll
-      for (int p = 0; p < 32; ++p) s += lrow[p] * D[p * PLD + j];
-      D[j * PLD + i] -= s;
-    }
-  }
-  __syncthreads();
-  if (warp == 0) {
-    chol32_warp(D, 32, lane, &bad, rdiag);
-    __syncwarp();
-    inv32_warp(D, X, 32, lane, rdiag);
-  }
-  __syncthreads();
-  // T = L21 X11 (32x32), stored in D's upper-right block: T(q, c) at D[(32 + c) * PLD + q]
-  {
-    const int q = lane;
-    double lrow[32];
-#pragma unroll
-    for (int p = 0; p < 32; ++p) lrow[p] = D[p * PLD + 32 + q];
-#pragma unroll 1
-    for (int m = 0; m < 8; ++m) {
-      const int c = warp + 4 * m;
-      double s = 0.0;
-#pragma unroll
-      for (int p = 0; p < 32; ++p)
-        if (p >= c) s += lrow[p] * X[c * PLD + p];       // X11(p, c)
-      D[(32 + c) * PLD + q] = s;
-    }
-  }
-  __syncthreads();
-  // X21 = -X22 T: X(32 + i, c) = -sum_{q <= i} X22(i, q) T(q, c)
-  {
-    const int i = lane;
-    double xrow[32];
-#pragma unroll
-    for (int q = 0; q < 32; ++q) xrow[q] = q <= i ? X[(32 + q) * PLD + 32 + i] : 0.0;
-#pragma unroll 1
-    for (int m = 0; m < 8; ++m) {
-      const int c = warp + 4 * m;
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 32; ++q) s += xrow[q] * D[(32 + c) * PLD + q];
-      X[c * PLD + 32 + i] = -s;
-    }
-  }
-  // failure flag: any lane of warp 0 may hold it
-  if (warp == 0) {
-    int b2 = bad;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const int ob = __shfl_xor_sync(0xffffffffu, b2, o);
-      b2 = (b2 < 0) ? ob : (ob < 0 ? b2 : min(b2, ob));
-    }
-    if (lane == 0 && b2 >= 0 && b2 < nb) atomicMin(fail, (unsigned long long)(sfirst[T.sn] + T.c0 + b2));
-  }
-  __syncthreads();
-  for (int e = tid; e < NBMAX * NBMAX; e += POTRF_THREADS) {
-    const int c = e >> 6, r = e & 63;
-    const bool valid = r >= c && r < nb && c < nb;
-    if (valid) P[(long long)c * S.ld + r] = D[c * PLD + r];
-    linv[(long long)T.slot * (NBMAX * NBMAX) + e] = valid ? X[c * PLD + r] : 0.0;
-  }
-}
-
-// ----------------------------------------------------------------------------------------------
 // small_kernel: the whole RL step of one small supernode J per CTA (k_J <= 64, m_J <= 256,
 // m_J k_J <= SMALL_MAXELEMS), with the panel resident in shared memory:
 //   cdiv(J): unblocked right-looking Cholesky of the k x k block + TRSM of the rows below,
@@ -915,14 +733,6 @@ __global__ void __launch_bounds__(32) small_warp_kernel(const int* __restrict__ 
 }
 
 // ----------------------------------------------------------------------------------------------
-// potrf4_kernel: the same contract as potrf_kernel with a flatter dependency chain: 160 threads,
-// thread t < 136 owns one 4x4 register tile (bi, bj), bi >= bj, of the 64x64 lower triangle.
-// Cholesky, right-looking, step j: the owners of column j publish it (double-buffered shared
-// vector, ONE barrier per step), every thread scales its rows/columns by rsqrt(pivot) and applies
-// the rank-1 update to its tile.  Inverse, step s (forward substitution on I): the owners of row s
-// of X scale it by 1/L_ss and publish it; rows r > s subtract L(r,s) X(s,:).  160 threads x <= 96
-// registers fit the slot of one retiring GEMM CTA (lookahead co-scheduling).
-// ----------------------------------------------------------------------------------------------
 // 1/sqrt(d) to full FP64 precision: hardware approximation (MUFU.RSQ64H) + two Newton steps;
 // shorter dependent chain than rsqrt(double) (which also handles special cases).  d <= 0 or NaN
 // gives NaN/inf, which the caller flags as a failed pivot.
@@ -935,125 +745,9 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
   return y;
 }
 
-__global__ void __launch_bounds__(POTRF4_THREADS) potrf4_kernel(const PTask* __restrict__ tasks,
-                                                                const SnInfo* __restrict__ sn,
-                                                                const int* __restrict__ sfirst, double* panels,
-                                                                double* linv, unsigned long long* fail) {
-  pdl_enter();
-  __shared__ double vbuf[2][NBMAX];            // published column of L / row of X
-  __shared__ double Ls[NBMAX][NBMAX + 1];      // Ls[row][col] = L(row, col) after the Cholesky
-  __shared__ double invd[NBMAX];
-  const PTask T = tasks[blockIdx.x];
-  const SnInfo S = sn[T.sn];
-  const int nb = T.nb, tid = threadIdx.x;
-  const bool owner = tid < 136;
-  int bi = 0, bj = owner ? tid : 0;
-  while (bj > bi) { bj -= bi + 1; ++bi; }
-  const int r0 = 4 * bi, q0 = 4 * bj;
-  double* P = panels + S.off + (long long)T.c0 * S.ld + T.c0;
-  double a[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = r0 + i, c = q0 + q;
-      a[i][q] = (owner && r < nb && c < nb && r >= c) ? P[(long long)c * S.ld + r] : 0.0;
-    }
-  // Entries above the diagonal inside diagonal tiles are never read back; masking is done by zeroing
-  // the column multipliers of finished columns (a - x*0 == a exactly), so the updates run unguarded.
-  int bad = -1;
-  for (int jb = 0; jb < (nb + 3) / 4; ++jb) {
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const int j = 4 * jb + jj;
-      if (j >= nb) break;
-      double* col = vbuf[j & 1];
-      if (owner && bj == jb) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) col[r0 + i] = a[i][jj];
-      }
-      __syncthreads();
-      const double d = col[j];
-      const double rl = rsqrt_nr(d), l = d * rl;
-      if (bad < 0 && !(d > 0.0)) bad = j;
-      double lr[4], lc[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        lr[i] = col[r0 + i] * rl;
-        lc[i] = q0 + i > j ? col[q0 + i] * rl : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) a[i][q] = fma(-lr[i], lc[q], a[i][q]);
-      if (bj == jb) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i][jj] = r0 + i == j ? l : lr[i];
-      }
-      if (tid == 0) invd[j] = rl;
-    }
-  }
-  if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[T.sn] + T.c0 + bad));
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = r0 + i, c = q0 + q;
-      if (owner) Ls[r][c] = r >= c ? a[i][q] : 0.0;
-      if (owner && r < nb && c < nb && r >= c) P[(long long)c * S.ld + r] = a[i][q];
-    }
-  // inverse: x = identity on the block, forward substitution over pivot rows s
-  double x[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) x[i][q] = (owner && r0 + i == q0 + q && r0 + i < nb) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int sb = 0; sb < (nb + 3) / 4; ++sb) {
-#pragma unroll
-    for (int ss = 0; ss < 4; ++ss) {
-      const int s = 4 * sb + ss;
-      if (s >= nb) break;
-      double* row = vbuf[s & 1];
-      if (owner && bi == sb) {
-        const double is = invd[s];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          x[ss][q] *= is;
-          row[q0 + q] = x[ss][q];
-        }
-      }
-      __syncthreads();
-      double xs[4], lrs[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) xs[q] = q0 + q <= s ? row[q0 + q] : 0.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) lrs[i] = r0 + i > s ? Ls[r0 + i][s] : 0.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) x[i][q] = fma(-lrs[i], xs[q], x[i][q]);
-    }
-  }
-  double* W = linv + (long long)T.slot * (NBMAX * NBMAX);
-  for (int e = tid; e < NBMAX * NBMAX; e += POTRF4_THREADS) {
-    const int c = e / NBMAX, r = e % NBMAX;
-    if (r < c || r >= nb || c >= nb) W[e] = 0.0;
-  }
-  if (owner) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = r0 + i, c = q0 + q;
-        if (r >= c && r < nb && c < nb) W[c * NBMAX + r] = x[i][q];
-      }
-  }
-}
-
 // ----------------------------------------------------------------------------------------------
-// potrf8_kernel (default): the same contract as potrf4_kernel, blocked so that the sequential part
-// is short.  The 64x64 block (padding rows/columns >= nb are an identity) sits in shared memory,
+// potrf8_kernel: cdiv POTRF ("DPOTRF") of one <= 64-column diagonal block plus its inverse
+// X = L_bb^{-1} (TRSM-as-GEMM, solve), blocked so that the sequential part is short.  The 64x64 block (padding rows/columns >= nb are an identity) sits in shared memory,
 // row-major, and is factored right-looking in 8-column panels:
 //   * the 8x8 diagonal block of panel p is factored by ONE thread in registers (8 dependent
 //     rsqrt steps, no barrier);
@@ -1183,10 +877,6 @@ __device__ __forceinline__ void p8_double(double* As, int tid) {
   __syncthreads();
 }
 
-// PM = 0: factor + inverse (TRSM-as-GEMM reads the inverse); PM = 1: factor only (the substitution
-// TRSM reads L); PM = 2: inverse only, of the finished L in the panel (the solve's inverses, off
-// the critical path).
-template <int PM>
 __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* __restrict__ tasks,
                                                                 const SnInfo* __restrict__ sn,
                                                                 const int* __restrict__ sfirst, double* panels,
@@ -1215,10 +905,6 @@ __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* 
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
   int bad = -1;
-  if (PM == 2) {   // L given: reciprocal pivots only
-    if (tid < NBMAX) rl[tid] = 1.0 / As[tid * P8_LD + tid];
-    __syncthreads();
-  } else {
   if (tid == 0) p8_diag(As, rl, 0, nb, bad);
   __syncthreads();
   for (int p = 0; p < NBMAX / 8; ++p) {
@@ -1263,9 +949,7 @@ __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* 
     const int c = e / NBMAX, r = e % NBMAX;
     if (r >= c && r < nb && c < nb) P[(long long)c * S.ld + r] = As[r * P8_LD + c];
   }
-  if (PM == 1) return;
   __syncthreads();
-  }
   // inverse, level 0: the eight 8x8 diagonal blocks (column-oriented substitution per block)
   if (tid < NBMAX / 8) {
     const int b = 8 * tid;
@@ -1297,76 +981,6 @@ __global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* 
     W[e] = (r >= c && r < nb && c < nb) ? As[r * P8_LD + c] : 0.0;
   }
 }
-
-// ----------------------------------------------------------------------------------------------
-// trsm_subst_kernel (a4, "DTRSM"): L_{R,b} = A_{R,b} L_bb^{-T} by forward substitution with
-// L_bb itself, so POTRF need not form the inverse on the cdiv chain (the solve's inverses are made
-// beside the factor, potrf8_kernel<2>).  One CTA per 64-row tile (the MODE_TRSM task layout):
-// thread pair (2i, 2i+1) owns row i, each half 32 columns in registers; column sweep j = 0..nb-1:
-// the owning half scales x_j by 1/L_jj, the pair exchanges it by shuffle, both subtract
-// x_j L(q, j) from their columns q > j (L's column j contiguous in shared memory: 16-byte loads).
-// ----------------------------------------------------------------------------------------------
-constexpr int TS_LD = NBMAX + 2;                     // 66: 16-byte aligned columns
-constexpr int TRSM_SUBST_SMEM = (NBMAX * TS_LD + NBMAX) * (int)sizeof(double);
-__global__ void __launch_bounds__(128, 3) trsm_subst_kernel(const GTask* __restrict__ tasks,
-                                                             const SnInfo* __restrict__ sn, double* panels) {
-  pdl_enter();
-  extern __shared__ __align__(16) double ts_smem[];
-  double* Ls = ts_smem;                              // Ls[j * TS_LD + q] = L(c0 + q, c0 + j)
-  double* rinv = Ls + NBMAX * TS_LD;
-  const GTask T = tasks[blockIdx.x];
-  const SnInfo S = sn[T.sn];
-  const int nb = T.nb, tid = threadIdx.x, lane = tid & 31, i = tid >> 1, h = tid & 1;
-  const double* Lg = panels + S.off + (long long)T.c0 * S.ld + T.c0;
-  for (int e = tid; e < NBMAX * NBMAX; e += 128) {
-    const int j = e / NBMAX, q = e % NBMAX;
-    double* d = Ls + j * TS_LD + q;
-    if (j < nb && q < nb && q >= j) {
-      const unsigned sa = (unsigned)__cvta_generic_to_shared(d);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(Lg + (long long)j * S.ld + q));
-    } else {
-      *d = 0.0;
-    }
-  }
-  const int r = T.r0 + i;
-  const bool rok = r < S.m && r >= T.s0;
-  double a[32];
-  double* Ag = panels + S.off + (long long)(T.c0 + 32 * h) * S.ld + r;
-#pragma unroll
-  for (int jj = 0; jj < 32; ++jj) a[jj] = (rok && 32 * h + jj < nb) ? Ag[(long long)jj * S.ld] : 0.0;
-  asm volatile("cp.async.wait_all;\n" ::);
-  __syncthreads();
-  if (tid < NBMAX) rinv[tid] = tid < nb ? 1.0 / Ls[tid * TS_LD + tid] : 0.0;
-  __syncthreads();
-#pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-    for (int jj = 0; jj < 32; ++jj) {
-      const int j = 32 * hh + jj;
-      if (j >= nb) break;                        // uniform
-      double x = 0.0;
-      if (h == hh) { a[jj] *= rinv[j]; x = a[jj]; }
-      x = __shfl_sync(0xffffffffu, x, (lane & ~1) | hh);
-      // columns q > j of this half: q = 32 h + jj2
-      const double2* lc = reinterpret_cast<const double2*>(Ls + j * TS_LD + 32 * h);
-#pragma unroll
-      for (int p2 = 0; p2 < 16; ++p2) {
-        const int q0 = 32 * h + 2 * p2;
-        if (q0 + 1 <= j) continue;               // both columns at or left of j
-        const double2 l = lc[p2];
-        if (q0 > j) a[2 * p2] = fma(-x, l.x, a[2 * p2]);
-        a[2 * p2 + 1] = fma(-x, l.y, a[2 * p2 + 1]);
-      }
-    }
-  }
-  if (rok) {
-#pragma unroll
-    for (int jj = 0; jj < 32; ++jj)
-      if (32 * h + jj < nb) Ag[(long long)jj * S.ld] = a[jj];
-  }
-}
-
-void launch_trsm_subst(const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio);
 
 __global__ void init_scatter_kernel(const double* __restrict__ vals, const long long* __restrict__ amap,
                                     long long nnz, double* panels) {
@@ -1514,70 +1128,6 @@ __global__ void __launch_bounds__(32 * SW_WARPS, ROWS >= 8 ? 2 : 3) solve_bwd_sm
   }
   if (lane < I.k) y[I.f + lane] = t0;
   if (lane + 32 < I.k) y[I.f + lane + 32] = t1;
-}
-
-// Solve, large supernodes.  y_b := X y_b (forward) or X^T y_b (backward) for the 64-column block
-// [c0, c0+nb) of supernode J, X = L_bb^{-1} (kept from the factor's POTRF, column-major ld 64).
-__global__ void __launch_bounds__(64) solve_diag_kernel(const PTask* __restrict__ tasks, const int* __restrict__ sfirst,
-                                                        const double* __restrict__ linv, double* y, int transpose) {
-  __shared__ double yb[NBMAX];
-  const PTask T = tasks[blockIdx.x];
-  const int r = threadIdx.x, f = sfirst[T.sn] + T.c0;
-  const double* X = linv + (long long)T.slot * (NBMAX * NBMAX);
-  yb[r] = r < T.nb ? y[f + r] : 0.0;
-  __syncthreads();
-  double s = 0.0;
-  if (!transpose) {
-    for (int c = 0; c <= r && c < T.nb; ++c) s += X[c * NBMAX + r] * yb[c];
-  } else {
-    for (int c = r; c < T.nb; ++c) s += X[r * NBMAX + c] * yb[c];
-  }
-  if (r < T.nb) y[f + r] = s;
-}
-
-// Solve, large supernodes: rows [r0, r0+64) ∩ [s0 = c0+nb, m) of J's panel against block column
-// [c0, c0+nb).  Forward: y[rows(J)[q]] -= L(q, blk) y_b (RED: ancestors are shared by the level).
-// Backward: y_b -= L(rows, blk)^T y[rows] (partial sums per tile, RED into y_b).
-__global__ void __launch_bounds__(256) solve_upd_kernel(const GTask* __restrict__ tasks, const SnInfo* __restrict__ sn,
-                                                        const int* __restrict__ sfirst,
-                                                        const long long* __restrict__ rows_ptr,
-                                                        const int* __restrict__ rows, const double* __restrict__ panels,
-                                                        double* y, int transpose) {
-  __shared__ double vb[NBMAX];     // forward: y_b; backward: y at the tile rows
-  __shared__ double part[4][NBMAX];
-  const GTask T = tasks[blockIdx.x];
-  const SnInfo S = sn[T.sn];
-  const int tid = threadIdx.x, lane = tid & 63, grp = tid >> 6;
-  const int f = sfirst[T.sn];
-  const int* R = rows + rows_ptr[T.sn];
-  const double* L = panels + S.off + (long long)T.c0 * S.ld;
-  const int q = T.r0 + lane;
-  const bool rowok = q >= T.s0 && q < S.m;
-  if (!transpose) {
-    if (tid < NBMAX) vb[tid] = tid < T.nb ? y[f + T.c0 + tid] : 0.0;
-    __syncthreads();
-    double s = 0.0;
-    if (rowok)
-      for (int c = grp; c < T.nb; c += 4) s += L[(long long)c * S.ld + q] * vb[c];
-    part[grp][lane] = s;
-    __syncthreads();
-    if (grp == 0 && rowok) atomicAdd(y + R[q], -(part[0][lane] + part[1][lane] + part[2][lane] + part[3][lane]));
-  } else {
-    if (tid < NBMAX) vb[tid] = rowok ? y[R[q]] : 0.0;
-    __syncthreads();
-    // column c handled by group grp, lanes over rows; reduce over the 64 rows
-    for (int c = grp; c < T.nb; c += 4) {
-      double s = rowok ? L[(long long)c * S.ld + q] * vb[lane] : 0.0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if ((lane & 31) == 0) part[grp][(c >> 2) * 2 + (lane >> 5)] = s;   // two half-sums per column
-    }
-    __syncthreads();
-    if (tid < T.nb) {
-      const int c = tid, g = c & 3, slotc = (c >> 2) * 2;
-      atomicAdd(y + f + T.c0 + c, -(part[g][slotc] + part[g][slotc + 1]));
-    }
-  }
 }
 
 // ------------------------------------------------------------------ sync-free level solve (large)
@@ -1789,11 +1339,7 @@ __global__ void gather_kernel(const double* __restrict__ src, const long long* _
 // ---------------------------------------------------------------------------------------------- launchers
 cudaError_t kernels_init_attributes() {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM))) return e;
-  if ((e = cudaFuncSetAttribute(potrf8_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF8_SMEM))) return e;
-  if ((e = cudaFuncSetAttribute(potrf8_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF8_SMEM))) return e;
-  if ((e = cudaFuncSetAttribute(potrf8_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF8_SMEM))) return e;
-  if ((e = cudaFuncSetAttribute(trsm_subst_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSM_SUBST_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(potrf8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF8_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 1 + 4) * SMALL_MAXK + 8 * 32 * 1) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 2 + 4) * SMALL_MAXK + 8 * 32 * 2) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 4 + 4) * SMALL_MAXK + 8 * 32 * 4) * 8))) return e;
@@ -1867,23 +1413,11 @@ void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels
 }
 
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels, double* linv,
-                  unsigned long long* fail, cudaStream_t st, int prio, int mode) {
+                  unsigned long long* fail, cudaStream_t st, int prio) {
   if (ntasks <= 0) return;
-#if SPCHOL_POTRF4 == 2
-  launch_prio(potrf4_kernel, ntasks, POTRF4_THREADS, 0, st, prio, tasks, sn, sfirst, panels, linv, fail);
-#elif SPCHOL_POTRF4
-  if (mode == 1) launch_prio(potrf8_kernel<1>, ntasks, POTRF8_THREADS, POTRF8_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
-  else if (mode == 2) launch_prio(potrf8_kernel<2>, ntasks, POTRF8_THREADS, POTRF8_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
-  else launch_prio(potrf8_kernel<0>, ntasks, POTRF8_THREADS, POTRF8_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
-#else
-  launch_prio(potrf_kernel, ntasks, POTRF_THREADS, POTRF_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
-#endif
+  launch_prio(potrf8_kernel, ntasks, POTRF8_THREADS, POTRF8_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
 }
 
-void launch_trsm_subst(const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio) {
-  if (ntasks <= 0) return;
-  launch_prio(trsm_subst_kernel, ntasks, 128, TRSM_SUBST_SMEM, st, prio, tasks, sn, panels);
-}
 
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,
                   const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,
@@ -1953,14 +1487,6 @@ void launch_gather(const double* src, const long long* idx, double* out, long lo
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   gather_kernel<<<(int)blocks, 256, 0, st>>>(src, idx, out, n);
-}
-void launch_solve_diag(const PTask* tasks, int count, const int* sfirst, const double* linv, double* y, int transpose,
-                       cudaStream_t st) {
-  if (count > 0) solve_diag_kernel<<<count, 64, 0, st>>>(tasks, sfirst, linv, y, transpose);
-}
-void launch_solve_upd(const GTask* tasks, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
-                      const int* rows, const double* panels, double* y, int transpose, cudaStream_t st) {
-  if (count > 0) solve_upd_kernel<<<count, 256, 0, st>>>(tasks, sn, sfirst, rows_ptr, rows, panels, y, transpose);
 }
 void launch_permute(const int* perm, const double* in, double* out, long long n, int inverse, cudaStream_t st) {
   if (n <= 0) return;

@@ -1,7 +1,7 @@
 // sm_100a device kernels of the numeric RL factorization (arXiv 2409.14009, §II.A "RL").
 // P:n = PAPER.md line n.  All arithmetic is FP64 ("D" BLAS).
 //
-//   potrf_kernel        a3: cdiv POTRF of one <=64-column diagonal block in shared memory, plus its
+//   potrf8_kernel       a3: cdiv POTRF of one <=64-column diagonal block in shared memory, plus its
 //                       triangular inverse (used by TRSM-as-GEMM)               ("DPOTRF")
 //   gemm_kernel<MODE>   FP64 DMMA (mma.sync m8n8k4) 64x64 tile, cp.async 3-stage smem pipeline
 //     MODE_TRSM         a4: L_{R,b} = A_{R,b} L_bb^{-T}                          ("DTRSM")
@@ -67,13 +67,6 @@ constexpr int GEMM_THREADS = 128;  // 4 warps, 2x2, warp tile 32x32
 constexpr int GEMM_SMEM = 2 * STAGES * BK * LDS * (int)sizeof(double);
 static_assert(GEMM_SMEM >= TILE * (TILE + 4) * (int)sizeof(double), "the epilogue stages the 64x68 tile in the pipeline's shared memory");
 constexpr int NBMAX = 64;          // cdiv block width
-constexpr int POTRF_THREADS = 128;
-constexpr int POTRF4_THREADS = 160;
-#ifndef SPCHOL_POTRF4
-#define SPCHOL_POTRF4 1
-#endif
-constexpr int POTRF_SMEM = 2 * NBMAX * (NBMAX + 1) * (int)sizeof(double);
-constexpr bool POTRF_MODES = SPCHOL_POTRF4 == 1;   // potrf8_kernel: factor-only / inverse-only modes
 
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels,
                  const double* linv, const long long* ucol_base, const long long* ucol_map,
@@ -92,10 +85,8 @@ void launch_gemm_tma(int mode, const GTask* tasks, int ntasks, const SnInfo* sn,
                      const void* tmap_linv, const long long* ucol_base, const long long* ucol_map, const int* posmap,
                      cudaStream_t st, int prio = 0);
 void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio = 0);
-// mode 0: factor + inverse, 1: factor only, 2: inverse of the finished block only (potrf8_kernel)
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels,
-                  double* linv, unsigned long long* fail, cudaStream_t st, int prio = 0, int mode = 0);
-void launch_trsm_subst(const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio = 0);
+                  double* linv, unsigned long long* fail, cudaStream_t st, int prio = 0);
 constexpr int SMALL_THREADS = 256;
 constexpr int SMALL_MAXK = 64;
 constexpr int SMALL_MAXM = SMALL_THREADS;
@@ -124,10 +115,6 @@ struct SmallSolve {
 // rows_class 0 / 1 / 2: m <= 64 / 128 / 256 (rows per lane 2 / 4 / 8)
 void launch_solve_small(const SmallSolve* info, int count, int rows_class, int backward, const int* rows,
                         const double* panels, double* y, cudaStream_t st);
-void launch_solve_diag(const PTask* tasks, int count, const int* sfirst, const double* linv, double* y, int transpose,
-                       cudaStream_t st);
-void launch_solve_upd(const GTask* tasks, int count, const SnInfo* sn, const int* sfirst, const long long* rows_ptr,
-                      const int* rows, const double* panels, double* y, int transpose, cudaStream_t st);
 constexpr int SOLVE_THREADS = 256;
 constexpr int SOLVE_RCHUNK = 512;   // rows per backward kind-2 task
 void launch_solve_fwd_level(const STask* tasks, int ntasks, int* ticket, int* flag, const SnInfo* sn, const int* sfirst,

@@ -108,6 +108,17 @@ def test_save_load_analysis_roundtrip(tmp_path):
     bad = tmp_path / "bad.spchol"
     bad.write_bytes(b"not an analysis")
     assert _err(lambda: sp.Solver.spchol_load_analysis(bad, device=-1)) == sp.SPCHOL_ERR_VALIDATION
+    # a file with the right magic but truncated or corrupted contents is rejected before use
+    raw = bytearray(path.read_bytes())
+    import struct
+    n = struct.unpack_from("<q", raw, 16)[0]
+    corrupt = [bytes(raw[:len(raw) // 2]),                                  # truncated
+               bytes(raw[:-4] + struct.pack("<i", 0x7FFFFFFF)),             # last a_pos out of range
+               bytes(raw[:16] + struct.pack("<q", n + 1) + raw[24:]),       # n disagrees with the arrays
+               bytes(raw[:-8] + struct.pack("<ii", -5, 0))]                 # negative row position
+    for data in corrupt:
+        bad.write_bytes(data)
+        assert _err(lambda: sp.Solver.spchol_load_analysis(bad, device=-1)) == sp.SPCHOL_ERR_VALIDATION
 
 
 def test_deterministic_option_plan():
