@@ -57,9 +57,12 @@ typedef struct {
   int32_t dist_rank;    /* multi-GPU: this process's rank (default 0), one process per GPU */
   int32_t dist_world;   /* multi-GPU: number of ranks (default 1).  With dist_world > 1 the merged
                            supernodal tree is mapped to ranks by proportional subtree-to-GPU mapping
-                           (SURVEY §8(e)): each rank factors its own subtrees (phase A), the top
-                           (separator) panels are summed over ranks with NCCL (phase B), and the
-                           top supernodes are factored (phase C).  Needs spchol_dist_attach_nccl. */
+                           (SURVEY §8(e)): each rank factors its own subtrees (phase A), their
+                           boundary update blocks go to the owners of the ancestor block columns
+                           (NCCL send/recv, phase B), and the top supernodes are factored block
+                           column by block column over their rank groups (phase C).  Each rank holds
+                           only its own part of L in device memory.  Needs update_mode 0, not
+                           deterministic, and spchol_dist_attach_nccl. */
   int32_t subtree_streams; /* single GPU: independent subtrees (proportional mapping onto this many
                            virtual ranks) are factored concurrently on their own stream pairs, the
                            top supernodes after they join.  0 = default (4), 1 = one level-set
@@ -153,6 +156,9 @@ int spchol_factor(spchol_handle* h, int64_t* fail_col, int64_t* fail_col_orig);
  * leaves first); L^T z = y' (backward, root first); x = P_f^T z.  b, x: host arrays,
  * column-major n x nrhs with leading dimension ld >= n; b and x may alias.
  * Errors: STATE before a successful factor, DIMENSION on nrhs < 1 or ld < n.
+ * Multi-GPU (dist_world > 1): collective — every rank calls it with the same b (only the entries
+ * of the rows a rank holds are read) and receives the whole x; only solution segments travel
+ * (a reduce per top block column forward, a broadcast backward, one all-reduce of x).
  */
 int spchol_solve(spchol_handle* h, const double* b, double* x, int32_t nrhs, int64_t ld);
 
@@ -180,7 +186,13 @@ enum {
   SPCHOL_Q_NBLOCKS = 16,      /* RLB blocks over all supernodes                   */
   SPCHOL_Q_NMARKERS = 17,     /* multi-GPU: exchange points (markers) of this rank's phase C     */
   SPCHOL_Q_NTOP_DIST = 18,    /* multi-GPU: top supernodes distributed over their rank group     */
-  SPCHOL_Q_DEVICE_BYTES = 19  /* device memory the handle owns (panels, inverses, plan; 0 if host-only) */
+  SPCHOL_Q_DEVICE_BYTES = 19, /* device memory the handle owns (panels, inverses, plan; 0 if host-only) */
+  SPCHOL_Q_COMM_SEND_BYTES = 20, /* multi-GPU: logical bytes this rank sends per factor (update runs +
+                                    its broadcast block columns, once per receiving member); host-only too */
+  SPCHOL_Q_COMM_RECV_BYTES = 21, /* multi-GPU: bytes this rank receives per factor                      */
+  SPCHOL_Q_ARENA_BYTES = 22,  /* physical device bytes of this rank's panels + inverses (+ broadcast
+                                 ring, update and receive regions under multi-GPU); host-only too    */
+  SPCHOL_Q_DIST_GRAPH = 23    /* multi-GPU: 1 if the factor (with its NCCL calls) replays as a CUDA graph */
 };
 int spchol_query(const spchol_handle* h, int key, int64_t* value);
 
@@ -212,11 +224,14 @@ int spchol_export_blocks(const spchol_handle* h, int64_t* blk_ptr, int32_t* blk_
 /*
  * Copy the device panels back.  panel_off[NSUPER+1] (doubles; panel J occupies
  * [panel_off[J], panel_off[J] + ld[J] k_J), column-major with leading dimension ld[J] >= m_J; under
- * multi-GPU the top panels are stored last, so offsets need not increase with J; panel_off[NSUPER]
- * = PANEL_DOUBLES),
+ * multi-GPU the panels are grouped by owning rank, top panels last and page-aligned, so offsets need
+ * not increase with J; panel_off[NSUPER] = PANEL_DOUBLES),
  * ld[NSUPER], panels[PANEL_DOUBLES].  After factor, panel J column c (0 <= c < k_J), row q
  * (c <= q < m_J) holds L(rows(J)[q], sfirst[J] + c); entries inside the panel but outside the
  * exact pattern of L ("padding") are exactly +-0.0.  Synchronizes the stream.
+ * Multi-GPU: every value export (panels, panel, factor CSC, diagonal) holds the entries this rank
+ * owns (its subtrees, its top supernodes / block columns; spchol_export_mapping) and zeros
+ * elsewhere, so the sum of the ranks' exports is L.  Not collective.
  */
 int spchol_export_panels(const spchol_handle* h, int64_t* panel_off, int32_t* ld, double* panels);
 
@@ -260,42 +275,25 @@ int spchol_dist_nccl_unique_id(void* out128);
 /* Attach an NCCL communicator (ncclCommInitRank over dist_world ranks, this handle's dist_rank;
  * collective: every rank must call it).  NCCL is loaded with dlopen (libnccl.so.2). */
 int spchol_dist_attach_nccl(spchol_handle* h, const void* unique_id128);
-/* Collective (every rank of the communicator must call it, in the same order relative to the other
- * collective calls): assemble the whole factor on every rank after a successful multi-GPU factor.
- * Value exports (panels, diagonal, CSC values) of a multi-GPU handle return STATE until it has run;
- * the first solve after a factor runs it implicitly (so that solve is collective too).  No-op for
- * dist_world == 1. */
-int spchol_dist_gather(spchol_handle* h);
 /* owner[NSUPER]: rank owning each supernode's subtree, -1 for the top supernodes (all 0 when
  * dist_world == 1); top_owner[NSUPER]: the rank that factors an undistributed top supernode, and
  * the rank owning block column 0 of a distributed one (block column C of a distributed top
  * supernode with rank group [lo, hi) belongs to lo + (C + top_owner - lo) mod (hi - lo)), -1
  * otherwise;
- * *top_off: first double of the contiguous top-panel region; *top_slot: first diagonal-inverse
- * slot of the top supernodes.  Any pointer may be NULL. */
+ * *top_off: first double of the top-panel region; *top_slot: first diagonal-inverse slot of the top
+ * supernodes.  Any pointer may be NULL. */
 int spchol_export_mapping(const spchol_handle* h, int32_t* owner, int32_t* top_owner, int64_t* top_off,
                           int64_t* top_slot);
 /*
  * Multi-GPU phase C.  Top supernodes whose work reaches a threshold are distributed
  * over their rank group: block columns of W = 256 columns are owned cyclically; the owner of a
- * block column runs its cdiv (POTRF, TRSM, in-block updates) and then sends it to the rest of the
- * group (NCCL send/recv), every rank applies the trailing updates of the block columns it owns and
- * a contiguous share of the U_J tiles (SYRK + relind scatter into its own copies of the ancestors).
- * At the start of each top level the partial panels are summed onto the block-column owners
- * (NCCL reduce per block column).  Smaller top supernodes are factored whole by top_owner.
- *
- * Diagnostics (single process standing in for several ranks on one GPU, never a reported result):
- * phase 1 = a1 init + phase A (own subtrees); 2000 + i = segment i of phase C (the plan between
- * exchange markers i-1 and i, i <= SPCHOL_Q_NMARKERS); 3 = synchronize, check the pivots and mark
- * the handle factored with its factor complete.  spchol_dist_debug_comm(hs, world, i) plays
- * marker i's exchange between the world handles hs[0..world-1] (ranks 0..world-1 of one problem on
- * one device): a level-start reduce onto the owners (other copies zeroed) or a block-column
- * broadcast.  spchol_dist_debug_accumulate(dst, src, which): dst += src over 1 = the whole panel
- * arena, 2 = all diagonal inverses (the final gather), 0 = the top region, 16 + J = top supernode
- * J's panel (src's copy zeroed). */
-int spchol_factor_phase(spchol_handle* h, int phase);
-int spchol_dist_debug_comm(spchol_handle* const* hs, int world, int marker);
-int spchol_dist_debug_accumulate(spchol_handle* dst, const spchol_handle* src, int which);
+ * block column runs its cdiv (POTRF, TRSM, in-block updates) and broadcasts it to the rest of the
+ * group (ncclBroadcast on the group's communicator), every member applies the trailing updates of
+ * the block columns it owns and forms its partial U_J = sum over its block columns C of
+ * L_{R,C} L_{R,C}^T.  After each top level (and after phase A), every update block travels to the
+ * owners of its destination block columns (grouped ncclSend / ncclRecv, one message per column
+ * run) and is extend-added there.  Smaller top supernodes are factored whole by top_owner.
+ */
 /* Executed flops of this rank's plan: phase A (own subtrees; the whole factor when dist_world == 1)
  * and, per level l < NLEVELS, phase C's share of that level (top_level may be NULL).  Works on
  * host-only handles (device < 0): the work model of the multi-GPU schedule. */

@@ -27,7 +27,8 @@ SPCHOL_ERR_STATE = -7
 
 Q = dict(N=0, NNZ_A=1, NNZ_L=2, NFUND=3, NSUPER=4, ADDED=5, NLEVELS=6, ROWS_LEN=7, NPAIRS=8,
          RELIND_LEN=9, PANEL_DOUBLES=10, NMERGES=11, FLOPS_EXACT=12, FLOPS_EXEC=13, LAUNCHES=14,
-         UPDATE_ENTRIES=15, NBLOCKS=16, NMARKERS=17, NTOP_DIST=18, DEVICE_BYTES=19)
+         UPDATE_ENTRIES=15, NBLOCKS=16, NMARKERS=17, NTOP_DIST=18, DEVICE_BYTES=19, COMM_SEND_BYTES=20,
+         COMM_RECV_BYTES=21, ARENA_BYTES=22, DIST_GRAPH=23)
 KERNEL_KINDS = dict(small=0, potrf=1, trsm=2, local_update=3, syrk_scatter=4, init=5, rlb_update=6)
 
 # Every symbol include/spchol.h declares (checked by tests/test_capi_exports.py).
@@ -37,8 +38,8 @@ EXPORTS = [
     "spchol_set_stream", "spchol_factor_async", "spchol_factor_status", "spchol_factor",
     "spchol_solve", "spchol_solve_device", "spchol_query", "spchol_export_symbolic",
     "spchol_export_blocks", "spchol_export_panels", "spchol_export_panel", "spchol_export_diagonal", "spchol_enable_kernel_timing", "spchol_kernel_stats",
-    "spchol_kernel_trace", "spchol_dist_nccl_unique_id", "spchol_dist_attach_nccl", "spchol_dist_gather", "spchol_export_mapping",
-    "spchol_factor_phase", "spchol_dist_debug_comm", "spchol_dist_debug_accumulate", "spchol_dist_plan_flops",
+    "spchol_kernel_trace", "spchol_dist_nccl_unique_id", "spchol_dist_attach_nccl", "spchol_export_mapping",
+    "spchol_dist_plan_flops",
     "spchol_destroy", "spchol_last_error",
 ]
 
@@ -98,11 +99,7 @@ def lib():
         L.spchol_kernel_trace.argtypes = [vp, i64, ctypes.POINTER(i64), vp, vp, vp, vp]
         L.spchol_dist_nccl_unique_id.argtypes = [vp]
         L.spchol_dist_attach_nccl.argtypes = [vp, vp]
-        L.spchol_dist_gather.argtypes = [vp]
         L.spchol_export_mapping.argtypes = [vp, vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
-        L.spchol_factor_phase.argtypes = [vp, ctypes.c_int]
-        L.spchol_dist_debug_accumulate.argtypes = [vp, vp, ctypes.c_int]
-        L.spchol_dist_debug_comm.argtypes = [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int]
         L.spchol_dist_plan_flops.argtypes = [vp, ctypes.POINTER(dbl), vp]
         L.spchol_destroy.argtypes = [vp]
         L.spchol_destroy.restype = None
@@ -313,9 +310,6 @@ class Solver:
         buf = ctypes.create_string_buffer(bytes(unique_id), 128)
         _check(self._L.spchol_dist_attach_nccl(self._h, buf))
 
-    def spchol_dist_gather(self):
-        _check(self._L.spchol_dist_gather(self._h))
-
     def spchol_export_mapping(self, with_top_owner=False):
         owner = np.empty(self.spchol_query("NSUPER"), np.int32)
         towner = np.empty(self.spchol_query("NSUPER"), np.int32)
@@ -324,15 +318,6 @@ class Solver:
         if with_top_owner:
             return owner, towner, int(to.value), int(ts.value)
         return owner, int(to.value), int(ts.value)
-
-    def spchol_factor_phase(self, phase):
-        rc = self._L.spchol_factor_phase(self._h, int(phase))
-        if rc == SPCHOL_ERR_NOT_SPD:
-            raise NotSPDError(rc, self._L.spchol_last_error().decode(), -1, -1)
-        _check(rc)
-
-    def spchol_dist_debug_accumulate(self, src, which):
-        _check(self._L.spchol_dist_debug_accumulate(self._h, src._h, int(which)))
 
     def spchol_dist_plan_flops(self):
         """(phase-A flops, per-level phase-C flops) of this rank's plan."""
@@ -351,12 +336,6 @@ class Solver:
         sym = self.spchol_export_symbolic()
         off, ld, pan = self.spchol_export_panels()
         return sym, off, ld, pan
-
-
-def spchol_dist_debug_comm(handles, marker):
-    """Play exchange marker `marker` between the handles of ranks 0..len(handles)-1 (one GPU)."""
-    arr = (ctypes.c_void_p * len(handles))(*[h._h for h in handles])
-    _check(lib().spchol_dist_debug_comm(arr, len(handles), int(marker)))
 
 
 def spchol_dist_nccl_unique_id() -> bytes:

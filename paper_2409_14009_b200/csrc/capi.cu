@@ -23,12 +23,9 @@
 #include <string>
 #include <vector>
 
-#include <cuda.h>
 #include <cudaTypedefs.h>
 
-#include "kernels.cuh"
-#include "spchol.h"
-#include "symbolic.h"
+#include "handle.h"
 
 using namespace spchol;
 namespace spchol {
@@ -37,55 +34,22 @@ void proportional_map(const Symbolic& S, const std::vector<double>& work, int wo
 void assign_top_owners(const std::vector<double>& work, const std::vector<int>& owner, const std::vector<int>& lo,
                        const std::vector<int>& hi, const std::vector<int>& level, int world,
                        std::vector<int>& top_owner);
-}
 
 namespace {
 thread_local std::string g_err;
+}
 int fail(int code, const std::string& msg) { g_err = msg; return code; }
 int cuda_fail(cudaError_t e, const char* where) {
   return fail(e == cudaErrorMemoryAllocation ? SPCHOL_ERR_DEVICE_OOM : SPCHOL_ERR_CUDA,
               std::string(where) + ": " + cudaGetErrorString(e));
 }
-#define CK(call)                                           \
-  do {                                                     \
-    cudaError_t e_ = (call);                               \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call);    \
-  } while (0)
-
-enum LaunchKind { K_SMALL = 0, K_POTRF = 1, K_TRSM = 2, K_LOCAL = 3, K_SCATTER = 4, K_INIT = 5, K_RLB = 6, K_NKINDS = 7 };
-}  // namespace
+thread_local size_t g_dev_bytes = 0;
 
 // ------------------------------------------------------------------------------------- NCCL
-// NCCL is loaded on demand (dlopen of libnccl.so.2, normally the copy torch already loaded), so the
-// library has no link-time NCCL dependency and single-GPU use never touches it.
-namespace {
-typedef int (*nccl_getid_t)(void*);
-struct NcclUid { char internal[128]; };
-typedef int (*nccl_init_t)(void**, int, NcclUid, int);
-typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
-typedef int (*nccl_reduce_t)(const void*, void*, size_t, int, int, int, void*, cudaStream_t);
-typedef int (*nccl_p2p_t)(const void*, size_t, int, int, void*, cudaStream_t);
-typedef int (*nccl_bcast_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
-typedef int (*nccl_split_t)(void*, int, int, void**, void*);
-typedef int (*nccl_group_t)();
-typedef int (*nccl_destroy_t)(void*);
-typedef const char* (*nccl_errstr_t)(int);
-struct NcclApi {
-  void* so = nullptr;
-  nccl_getid_t getid = nullptr;
-  nccl_init_t init = nullptr;
-  nccl_allreduce_t allreduce = nullptr;
-  nccl_reduce_t reduce = nullptr;
-  nccl_p2p_t send = nullptr, recv = nullptr;
-  nccl_bcast_t bcast = nullptr;
-  nccl_split_t split = nullptr;
-  nccl_group_t group_start = nullptr, group_end = nullptr;
-  nccl_destroy_t destroy = nullptr;
-  nccl_errstr_t errstr = nullptr;
-};
 NcclApi g_nccl;
+namespace {
 std::mutex g_nccl_mu;   // handles (and the tests' rank threads) may attach concurrently
-constexpr int NCCL_SUM = 0, NCCL_MIN = 3, NCCL_UINT64 = 5, NCCL_FLOAT64 = 8;
+}
 // Resolves every symbol into a local table first and publishes it (g_nccl.so last) under the lock.
 bool nccl_load(std::string& err) {
   std::lock_guard<std::mutex> lock(g_nccl_mu);
@@ -108,6 +72,8 @@ bool nccl_load(std::string& err) {
   api.group_end = (nccl_group_t)dlsym(so, "ncclGroupEnd");
   api.destroy = (nccl_destroy_t)dlsym(so, "ncclCommDestroy");
   api.errstr = (nccl_errstr_t)dlsym(so, "ncclGetErrorString");
+  // the tests' stand-in blocks the host inside every call, so its calls cannot be graph-captured
+  api.capturable = dlsym(so, "spcholMockNcclBlocking") == nullptr;
   if (!api.getid || !api.init || !api.allreduce || !api.reduce || !api.send || !api.recv || !api.bcast || !api.split || !api.group_start ||
       !api.group_end || !api.destroy) { err = "NCCL symbols missing"; return false; }
   api.so = so;
@@ -117,137 +83,7 @@ bool nccl_load(std::string& err) {
 int nccl_fail(int r, const char* where) {
   return fail(SPCHOL_ERR_NCCL, std::string(where) + ": " + (g_nccl.errstr ? g_nccl.errstr(r) : "nccl error"));
 }
-}  // namespace
-
-namespace {
-enum OpType { OP_LAUNCH = 0, OP_RECORD = 1, OP_WAIT = 2, OP_TOP_LEVEL = 3, OP_BCAST = 4, OP_ZERO = 5 };
-// One step of the factor's launch plan.  OP_LAUNCH: a batched kernel (kind, tasks [off, off+n)) on
-// stream `stream` (0 = critical path: cdiv chain + relind scatter, 1 = trailing updates);
-// OP_RECORD / OP_WAIT: event `ev` recorded on / awaited by `stream` (lookahead fork/join).
-// OP_TOP_LEVEL (multi-GPU phase C): start of top level `aux` — the panels of that level's top
-// supernodes are reduced (NCCL, sum) onto their owner ranks, the other ranks zero their copies.
-// OP_BCAST (multi-GPU, distributed top supernode aux, column block aux2): the finished block column
-// goes from its owner to the other ranks of the supernode's group (NCCL send/recv).  OP_ZERO: the
-// ranks of aux's group zero their copies of the block columns they do not own (after the last read).
-// OP_TOP_LEVEL and OP_BCAST are "markers": every rank's plan holds the same sequence of them.
-struct Launch {
-  int kind;
-  long long off;   // first task
-  int n;           // tasks
-  double flops, bytes;
-  int op = OP_LAUNCH, stream = 0, ev = -1;
-  int aux = 0;     // K_SMALL: dynamic shared memory (doubles); K_SCATTER: 1 = plain RMW (deterministic)
-  int aux2 = 0;    // K_SMALL: largest m in the launch
-  int aux3 = 0;    // K_SMALL: largest k in the launch if it runs one warp per supernode, else 0
-};
-thread_local size_t g_dev_bytes = 0;   // device bytes allocated by the handle being set up
-template <class T>
-cudaError_t dalloc(T** p, size_t count) {
-  *p = nullptr;
-  if (count == 0) count = 1;
-  g_dev_bytes += count * sizeof(T);
-  return cudaMalloc((void**)p, count * sizeof(T));
-}
-template <class T>
-cudaError_t upload(T** p, const std::vector<T>& v) {
-  cudaError_t e = dalloc(p, v.size());
-  if (e != cudaSuccess) return e;
-  if (!v.empty()) e = cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
-  return e;
-}
-}  // namespace
-
-struct spchol_handle {
-  Symbolic S;
-  spchol_options opt{};
-  int nb = NBMAX;
-  int outer = 4;                    // outer block = outer inner blocks (SPCHOL_OUTER, diagnostics)
-  cudaStream_t stream = nullptr, own_stream = nullptr;
-  // host plan
-  std::vector<SnInfo> sn;
-  std::vector<Launch> plan;
-  std::vector<GTask> gtasks;
-  std::vector<RTask> rtasks;            // RLB block-pair tiles (update_mode 1)
-  std::vector<PTask> ptasks;
-  std::vector<int> level_sns, level_off;
-  std::vector<int> small_sns;           // supernodes handled by the fused small kernel, by level
-  std::vector<char> is_small;
-  long long panel_doubles = 0;
-  size_t device_bytes = 0;              // device memory the handle owns (SPCHOL_Q_DEVICE_BYTES)
-  std::vector<long long> panel_off;
-  double flops_exec = 0, update_entries = 0;
-  int nslots_total = 0;
-  std::vector<int> slot_base;          // first inverse slot of each supernode's diagonal blocks
-  // multi-GPU: subtree-to-GPU mapping, phase A = own subtrees, B = NCCL all-reduce
-  // of the top panels, C = top supernodes
-  int rank = 0, world = 1;
-  std::vector<int> owner;              // rank owning each supernode's subtree, -1 = top
-  std::vector<int> top_owner;          // rank factoring each top supernode (fan-in), -1 otherwise
-  std::vector<int> grp_lo, grp_hi;     // rank group [lo, hi) of each top supernode
-  std::vector<char> top_dist;          // top supernode distributed over its group (block-column cyclic
-                                       // cdiv, U_J tiles split over the group)
-  double dist_min_flops = 4e9;         // SPCHOL_DIST_MINFLOPS: smallest top supernode distributed
-  std::vector<size_t> markers;         // plan positions of the phase-C markers (same sequence on all ranks)
-  std::vector<std::vector<int>> top_by_level;
-  long long top_off = -1;              // first double of the contiguous top-panel region
-  int top_slot = -1;                   // first inverse slot of the top supernodes
-  size_t plan_all_end = 0, plan_a_end = 0, plan_factor_begin = 0;
-  int nvr = 1;                         // single-GPU subtree concurrency (virtual ranks)
-  void* nccl_comm = nullptr;
-  std::vector<std::array<int, 2>> grp_keys;   // distinct rank groups [lo, hi) of the top supernodes (hi - lo < world)
-  std::vector<void*> grp_comms;               // their NCCL communicators (ncclCommSplit; null if not a member)
-  bool gathered = false;
-  std::vector<int> small_level_off;     // small_sns range per level
-  std::vector<STask> stasks;            // level solve tasks: forward of level l at [sfwd_off[l], sfwd_off[l+1]),
-  std::vector<long long> sfwd_off, sbwd_off;   // backward at [sbwd_off[l], sbwd_off[l+1])
-  STask* d_stasks = nullptr;
-  std::vector<SmallSolve> ssolve;       // small supernodes, per level by row class (m <= 64 / 128 / 256)
-  std::vector<int> ssolve_off;          // level l, class c at [ssolve_off[3l + c], ssolve_off[3l + c + 1])
-  SmallSolve* d_ssolve = nullptr;
-  int* d_sflags = nullptr;              // forward flags | backward flags | backward chunk counts (nslots
-                                        // each) | per-level tickets (2 * nlevels); zeroed per solve
-  int nevents = 0;
-  bool no_lookahead = false;     // SPCHOL_NO_LOOKAHEAD=1 (diagnostics)
-  bool no_next_split = false;    // SPCHOL_NO_NEXT_SPLIT=1: NEXT as one critical-stream launch (diagnostics)
-  int rest_smem = 0;             // SPCHOL_REST_SMEM: dynamic shared memory of trailing-stream updates (bytes)
-  int left_inner_min = 16;       // SPCHOL_LEFT_INNER_MIN=n: left-looking in-block updates in levels with at
-                                 // least n large supernodes (0 = never); SPCHOL_LEFT_INNER=1: everywhere
-  bool right_inner = true;       // SPCHOL_LEFT_INNER=1: left-looking in-block updates (one K <= 192 pass
-                                 // per block column; C4 -0.45%, C5 -0.35%, but C3/C2 +1.3-1.5%: on the chain)
-  int max_level = -1;            // SPCHOL_MAX_LEVEL=l: factor only levels <= l (diagnostics)
-  bool small_warp = true;        // SPCHOL_SMALL_WARP=0: CTA-per-supernode small kernel for every size
-  int small_warp_maxm = 64;      // largest m of the warp-per-supernode kernel (SPCHOL_SMALL_WARP_MAXM <= 128)
-  bool use_tma = false;          // SPCHOL_TMA=1: TMA + mbarrier tile kernels (measured ~2% slower)
-  void* d_tmaps = nullptr;       // CUtensorMap per supernode panel (TMA boxes 16 x 8, 128B swizzle)
-  void* d_tmap_linv = nullptr;   // CUtensorMap over the diagonal-inverse slots
-  std::vector<int> plan_level;   // level of each plan entry (diagnostics)
-  // device
-  double *d_panels = nullptr, *d_avals = nullptr, *d_linv = nullptr, *d_y = nullptr, *d_y2 = nullptr;
-  long long *d_diag_idx = nullptr, *d_amap = nullptr, *d_ucol_base = nullptr, *d_ucol_map = nullptr, *d_rows_ptr = nullptr;
-  int *d_small_sns = nullptr, *d_posmap = nullptr, *d_sfirst = nullptr, *d_rows = nullptr, *d_perm = nullptr, *d_level_sns = nullptr;
-  SnInfo* d_sn = nullptr;
-  GTask* d_gtasks = nullptr;
-  RTask* d_rtasks = nullptr;
-  PTask* d_ptasks = nullptr;
-  unsigned long long* d_fail = nullptr;
-  bool values_set = false, factored = false;
-  std::vector<cudaStream_t> pstreams;           // plan streams: even = cdiv chain (high priority),
-                                                // odd = trailing updates (low priority)
-  std::vector<cudaEvent_t> join_events;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  int prio_lo = 0, prio_hi = 0;
-  std::vector<cudaEvent_t> plan_events;
-  // graph
-  cudaGraph_t graph = nullptr, solve_graph = nullptr;
-  cudaGraphExec_t gexec = nullptr, solve_gexec = nullptr;
-  // timing
-  bool timing = false;
-  std::vector<cudaEvent_t> ev_pool;
-  size_t ev_used = 0;
-  std::vector<std::pair<int, size_t>> pending;  // (plan index, first event)
-  long long st_launches[K_NKINDS] = {0};
-  double st_ms[K_NKINDS] = {0}, st_flops[K_NKINDS] = {0}, st_bytes[K_NKINDS] = {0};
-};
+}  // namespace spchol
 
 extern "C" void spchol_default_options(spchol_options* o) {
   o->merge_cap = 0.25;
@@ -286,18 +122,9 @@ static void for_tiles(int rbase, int rend, int cbase, int cend, F emit) {
         }
 }
 
-// Multi-GPU, distributed top supernode J (top_dist): outer column block C (columns [C W, (C+1) W),
-// W = outer * nb) belongs to rank grp_lo + (C + top_owner - grp_lo) mod g — cyclic over J's rank group,
-// starting at the rank the per-level LPT picked; an undistributed top supernode belongs to top_owner.
-static int blk_owner(const spchol_handle* h, int J, int C) {
-  if (!h->top_dist[J]) return h->top_owner[J];
-  const int g = h->grp_hi[J] - h->grp_lo[J];
-  return h->grp_lo[J] + (C + h->top_owner[J] - h->grp_lo[J]) % g;
-}
-static bool in_group(const spchol_handle* h, int J, int r) { return r >= h->grp_lo[J] && r < h->grp_hi[J]; }
 // The NCCL communicator of top supernode J's rank group (ranks lo..hi-1 as 0..hi-lo-1): the world
 // communicator when the group is everyone, else the one ncclCommSplit made at attach time.
-static void* group_comm(const spchol_handle* h, int J) {
+void* spchol::group_comm(const spchol_handle* h, int J) {
   if (h->grp_hi[J] - h->grp_lo[J] == h->world) return h->nccl_comm;
   for (size_t i = 0; i < h->grp_keys.size(); ++i)
     if (h->grp_keys[i][0] == h->grp_lo[J] && h->grp_keys[i][1] == h->grp_hi[J]) return h->grp_comms[i];
@@ -336,10 +163,10 @@ static int colour_supernodes(const spchol_handle* h, const std::vector<int>& Js,
 
 // Appends, level by level, the launches for the supernodes J with active(J).  record_solve: also
 // record the solve's step structure (only for the whole-tree plan).  top_markers (multi-GPU phase
-// C of rank h->rank): a level-start marker per top level; distributed top supernodes (top_dist) take
-// part on every rank of their group — cdiv tasks of the column blocks the rank owns, one OP_BCAST
-// marker per finished column block (on every rank, so all plans hold the same marker sequence), the
-// rank's share of the U_J tiles, and an OP_ZERO of the non-owned blocks after the level's scatter.
+// C of rank h->rank): distributed top supernodes (top_dist) take part on every rank of their group —
+// cdiv tasks of the column blocks the rank owns, one OP_BCAST marker per finished column block (on
+// every rank, so all plans hold the same marker sequence), and the rank's partial U_J (its own block
+// columns' share of the K sum, MODE_SCATTER_KS); after each level with update blocks, an OP_EXCHANGE.
 template <class Active>
 static void append_levels(spchol_handle* h, Active active, bool record_solve, int SB = 0, bool top_markers = false) {
   const Symbolic& S = h->S;
@@ -349,11 +176,6 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
   };
   const int lmax = h->max_level >= 0 ? std::min(S.nlevels, h->max_level + 1) : S.nlevels;
   for (int l = 0; l < lmax; ++l) {
-    if (top_markers && !h->top_by_level[l].empty()) {
-      Launch M{0, 0, 0, 0, 0, OP_TOP_LEVEL, SB, -1};
-      M.aux = l;
-      h->plan.push_back(M);
-    }
     const size_t plan_before = h->plan.size();
     // small supernodes of this level: launches on stream 1 (independent of the level's big ones),
     // bucketed by panel size so that each launch's shared memory (sized by its largest panel)
@@ -441,6 +263,9 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
     }
     int pending_rest_ev = -1;      // event recorded after the latest REST launch on stream 1
     int pending_nextb_ev = -1;     // event recorded after the latest NEXT_b launch
+    // multi-GPU: event after the trailing-stream reads (NEXT_b, REST) of outer block column C; the
+    // broadcast into C's ring slot waits for the readers of the slot's previous block, C - ring_ns
+    std::vector<int> rest_ev_of_C(maxblk / std::max(1, OUTER) + 2, -1);
     const bool split_next = !h->no_lookahead && !h->no_next_split;
     for (int s = 0; s < maxblk; ++s) {
       long long p0 = (long long)h->ptasks.size(), t0 = (long long)h->gtasks.size();
@@ -518,6 +343,11 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         pending_nextb_ev = -1;
       }
       push(K_LOCAL, l0, (long long)h->gtasks.size(), fl, bl);
+      if (!bcast.empty()) {
+        const int Cb = s / OUTER;
+        if (Cb >= h->ring_ns && rest_ev_of_C[Cb - h->ring_ns] >= 0)
+          h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SB, rest_ev_of_C[Cb - h->ring_ns]});
+      }
       for (const auto& jc : bcast) {   // finished block columns to the rest of their group (stream SB)
         Launch M{0, 0, 0, 0, 0, OP_BCAST, SB, -1};
         M.aux = jc.first;
@@ -556,6 +386,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       if (!rest.empty() || !nxtb.empty()) {
         pending_rest_ev = h->nevents++;
         h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, SB + 1, pending_rest_ev});
+        rest_ev_of_C[s / OUTER] = pending_rest_ev;
       }
     }
     (void)pending_nextb_ev;
@@ -610,11 +441,14 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
       h->plan_level.resize(h->plan.size(), l);
       continue;
     }
-    std::vector<int> bg, bcol;
+    std::vector<int> bg, bcol, bks;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
       const int J = h->level_sns[x];
-      if (dtop(J) && !in_group(h, J, h->rank)) continue;
-      if (!h->is_small[J] && (active(J) || dtop(J)) && h->sn[J].m > h->sn[J].k) bg.push_back(J);
+      if (dtop(J)) {
+        if (in_group(h, J, h->rank) && h->sn[J].m > h->sn[J].k) bks.push_back(J);
+        continue;
+      }
+      if (!h->is_small[J] && active(J) && h->sn[J].m > h->sn[J].k) bg.push_back(J);
     }
     const int nbc = h->opt.deterministic ? colour_supernodes(h, bg, bcol) : 1;
     if (!h->opt.deterministic) bcol.assign(bg.size(), 0);
@@ -627,32 +461,43 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         const SnInfo& I = h->sn[J];
         const int t = I.m - I.k;
         const int base = I.k & ~1;
-        const long long g0 = (long long)h->gtasks.size();
         for_tiles(base, I.m, base, I.m, [&](int r0, int c0) { h->gtasks.push_back(GTask{J, r0, c0, 0, 0, 0}); });
-        double frac = 1.0;
-        if (dtop(J)) {   // this rank's contiguous share of J's U tiles (super-tile order kept)
-          const long long nt = (long long)h->gtasks.size() - g0;
-          const int g = h->grp_hi[J] - h->grp_lo[J], i = h->rank - h->grp_lo[J];
-          const long long a = g0 + nt * i / g, b = g0 + nt * (i + 1) / g;
-          h->gtasks.erase(h->gtasks.begin() + b, h->gtasks.end());
-          h->gtasks.erase(h->gtasks.begin() + g0, h->gtasks.begin() + a);
-          frac = nt ? (double)(b - a) / (double)nt : 0.0;
-        }
-        fs += frac * (double)I.k * t * (t + 1);
-        bs += frac * (8.0 * (double)t * I.k + 16.0 * 0.5 * t * (t + 1.0));
+        fs += (double)I.k * t * (t + 1);
+        bs += 8.0 * (double)t * I.k + 16.0 * 0.5 * t * (t + 1.0);
       }
       push(K_SCATTER, s0g, (long long)h->gtasks.size(), fs, bs);
       if (h->opt.deterministic && !h->plan.empty() && h->plan.back().kind == K_SCATTER && h->plan.back().off == s0g)
         h->plan.back().aux = 1;
     }
-    if (top_markers)   // distributed supernodes of the level: the group's non-owned copies are dead now
-      for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
-        const int J = h->level_sns[x];
-        if (!dtop(J) || !in_group(h, J, h->rank)) continue;
-        Launch Z{0, 0, 0, 0, 0, OP_ZERO, SB, -1};
-        Z.aux = J;
-        h->plan.push_back(Z);
+    if (!bks.empty()) {
+      // distributed top supernodes: this rank's partial U_J over the block columns it owns (C = cr,
+      // cr + g, ...: cyclic ownership), RED into its update block of J (dist_redirect)
+      const int W = h->outer * h->nb;
+      long long s0g = (long long)h->gtasks.size();
+      double fs = 0, bs = 0;
+      for (int J : bks) {
+        const SnInfo& I = h->sn[J];
+        const int g = h->grp_hi[J] - h->grp_lo[J], nblk = (I.k + W - 1) / W;
+        const int cr = ((h->rank - h->top_owner[J]) % g + g) % g;
+        if (cr >= nblk) continue;
+        const int cnt = (nblk - 1 - cr) / g + 1;
+        double cols = 0;
+        for (int i = 0; i < cnt; ++i) cols += std::min(W, I.k - (cr + i * g) * W);
+        const int base = I.k & ~1;
+        const double t = I.m - I.k;
+        for_tiles(base, I.m, base, I.m, [&](int r0, int c0) { h->gtasks.push_back(GTask{J, r0, c0, cr * W, cnt, g * W}); });
+        fs += cols * t * (t + 1);
+        bs += 8.0 * t * cols + 16.0 * 0.5 * t * (t + 1.0);
       }
+      push(K_SCATTER, s0g, (long long)h->gtasks.size(), fs, bs);
+      if (!h->plan.empty() && h->plan.back().kind == K_SCATTER && h->plan.back().off == s0g) h->plan.back().aux = 2;
+    }
+    if (top_markers && l + 1 < h->nexch && !h->exch_runs[l + 1].empty()) {
+      // the level's partial U_J go to the owners of their destination block columns
+      Launch M{0, 0, 0, 0, 0, OP_EXCHANGE, SB, -1};
+      M.aux = l + 1;
+      h->plan.push_back(M);
+    }
     h->plan_level.resize(h->plan.size(), l);
   }
   if (record_solve) h->small_level_off.push_back((int)h->small_sns.size());
@@ -663,7 +508,8 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
 // a level = the ticket order: forward, triangle blocks b = 0, 1, ... interleaved over the level's
 // supernodes, then the rows below the triangles; backward, the chunks below the triangles, then the
 // triangle column blocks from the last to the first.  A task only waits for tasks before it.
-static void build_solve_tasks(spchol_handle* h) {
+template <class Active>
+static void build_solve_tasks(spchol_handle* h, Active active) {
   const Symbolic& S = h->S;
   const int NB = h->nb;
   h->stasks.clear();
@@ -674,7 +520,7 @@ static void build_solve_tasks(spchol_handle* h) {
     int maxblk = 0;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
       const int J = h->level_sns[x];
-      if (h->is_small[J] || h->sn[J].k == 0) continue;
+      if (h->is_small[J] || h->sn[J].k == 0 || !active(J)) continue;
       big.push_back(J);
       maxblk = std::max(maxblk, (h->sn[J].k + NB - 1) / NB);
     }
@@ -684,11 +530,12 @@ static void build_solve_tasks(spchol_handle* h) {
         const SnInfo& I = h->sn[J];
         if (b * NB >= I.k) continue;
         const int nb = std::min(NB, I.k - b * NB);
-        h->stasks.push_back(STask{J, 0, b, nb, b * NB, b * NB + nb, h->slot_base[J] + b, 0});
+        h->stasks.push_back(STask{J, 0, b, nb, b * NB, b * NB + nb, h->slot_base[J] + b, 0, 0, (I.k + NB - 1) / NB});
       }
     for (int J : big) {
       const SnInfo& I = h->sn[J];
-      for (int q0 = I.k; q0 < I.m; q0 += 64) h->stasks.push_back(STask{J, 1, 0, 0, q0, std::min(q0 + 64, I.m), h->slot_base[J], 0});
+      for (int q0 = I.k; q0 < I.m; q0 += 64)
+        h->stasks.push_back(STask{J, 1, 0, 0, q0, std::min(q0 + 64, I.m), h->slot_base[J], 0, 0, (I.k + NB - 1) / NB});
     }
     h->sbwd_off[l] = (long long)h->stasks.size();
     for (int J : big) {
@@ -696,7 +543,7 @@ static void build_solve_tasks(spchol_handle* h) {
       const int nblk = (I.k + NB - 1) / NB;
       for (int b = 0; b < nblk; ++b)
         for (int q0 = I.k; q0 < I.m; q0 += SOLVE_RCHUNK)
-          h->stasks.push_back(STask{J, 2, b, std::min(NB, I.k - b * NB), q0, std::min(q0 + SOLVE_RCHUNK, I.m), h->slot_base[J] + b, 0});
+          h->stasks.push_back(STask{J, 2, b, std::min(NB, I.k - b * NB), q0, std::min(q0 + SOLVE_RCHUNK, I.m), h->slot_base[J] + b, 0, 0, nblk});
     }
     for (int d = 0; d < maxblk; ++d)
       for (int J : big) {
@@ -704,10 +551,11 @@ static void build_solve_tasks(spchol_handle* h) {
         const int nblk = (I.k + NB - 1) / NB, b = nblk - 1 - d;
         if (b < 0) continue;
         const int need = (I.m - I.k + SOLVE_RCHUNK - 1) / SOLVE_RCHUNK;
-        h->stasks.push_back(STask{J, 3, b, std::min(NB, I.k - b * NB), b * NB, b * NB + std::min(NB, I.k - b * NB), h->slot_base[J] + b, need});
+        h->stasks.push_back(STask{J, 3, b, std::min(NB, I.k - b * NB), b * NB, b * NB + std::min(NB, I.k - b * NB), h->slot_base[J] + b, need, 0, nblk});
       }
   }
   h->sfwd_off[S.nlevels] = h->sbwd_off[S.nlevels] = (long long)h->stasks.size();
+  h->nticket = 2 * (size_t)S.nlevels;
   h->ssolve.clear();
   h->ssolve_off.assign(3 * S.nlevels + 1, 0);
   for (int l = 0; l < S.nlevels; ++l)
@@ -716,7 +564,7 @@ static void build_solve_tasks(spchol_handle* h) {
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
         const int J = h->level_sns[x];
         const SnInfo& I = h->sn[J];
-        if (!h->is_small[J] || (I.m > 64) + (I.m > 128) != cl) continue;
+        if (!h->is_small[J] || (I.m > 64) + (I.m > 128) != cl || !active(J)) continue;
         h->ssolve.push_back(SmallSolve{I.off, S.rows_ptr[J], I.ld, I.m, I.k, S.sfirst[J]});
       }
     }
@@ -728,7 +576,8 @@ static void build_plan(spchol_handle* h) {
   const int ns = S.nsuper, NB = h->nb;
   h->sn.resize(ns);
   h->panel_off.assign(ns + 1, 0);
-  std::vector<double> work(ns, 0.0);
+  h->work.assign(ns, 0.0);
+  std::vector<double>& work = h->work;
   for (int J = 0; J < ns; ++J) {
     int k = S.sfirst[J + 1] - S.sfirst[J];
     int m = (int)(S.rows_ptr[J + 1] - S.rows_ptr[J]);
@@ -749,23 +598,6 @@ static void build_plan(spchol_handle* h) {
     if (h->world > 1)
       for (int J = 0; J < ns; ++J) if (h->owner[J] < 0) h->top_by_level[S.level[J]].push_back(J);
   }
-  // panel arena: supernodes in order, except that the top supernodes (multi-GPU) come last so
-  // their panels form one contiguous region (the NCCL all-reduce of phase B)
-  {
-    long long off = 0;
-    for (int pass = 0; pass < 2; ++pass)
-      for (int J = 0; J < ns; ++J) {
-        const bool top = h->world > 1 && h->owner[J] < 0;
-        if (top != (pass == 1)) continue;
-        if (pass == 1 && h->top_off < 0) h->top_off = off;
-        h->sn[J].off = off;
-        off += (long long)h->sn[J].ld * h->sn[J].k;
-      }
-    h->panel_doubles = off;
-    if (h->top_off < 0) h->top_off = off;
-    for (int J = 0; J < ns; ++J) h->panel_off[J] = h->sn[J].off;
-    h->panel_off[ns] = off;
-  }
   // levels
   h->level_off.assign(S.nlevels + 1, 0);
   for (int J = 0; J < ns; ++J) h->level_off[S.level[J] + 1]++;
@@ -775,66 +607,87 @@ static void build_plan(spchol_handle* h) {
     std::vector<int> nx(h->level_off.begin(), h->level_off.end() - 1);
     for (int J = 0; J < ns; ++J) h->level_sns[nx[S.level[J]]++] = J;
   }
-  // fused small-supernode path: k <= small_max_k, m <= 256, m k <= SMALL_MAXELEMS (shared memory)
+  // fused small-supernode path: k <= small_max_k, m <= 256, m k <= SMALL_MAXELEMS (shared memory);
+  // multi-GPU top supernodes always take the blocked path (their solve steps use the kept inverses)
   const int kmax = h->opt.small_max_k < 0 ? 0 : (h->opt.small_max_k == 0 ? SMALL_MAXK : std::min(h->opt.small_max_k, SMALL_MAXK));
   h->is_small.assign(ns, 0);
   for (int J = 0; J < ns; ++J) {
     const SnInfo& I = h->sn[J];
-    h->is_small[J] = I.k <= kmax && I.m <= SMALL_MAXM && (long long)I.m * I.k <= SMALL_MAXELEMS;
+    h->is_small[J] = I.k <= kmax && I.m <= SMALL_MAXM && (long long)I.m * I.k <= SMALL_MAXELEMS &&
+                     !(h->world > 1 && h->owner[J] < 0);
   }
   // distributed top supernodes (multi-GPU): large enough that splitting the cdiv and U_J over the
-  // rank group beats the block-column broadcasts it costs
+  // rank group beats the block-column broadcasts it costs; the outer block width W must be a power
+  // of two (block columns = whole VMM pages, K-split chunk arithmetic)
   h->top_dist.assign(ns, 0);
-  if (h->world > 1 && (h->outer * NB) % TILE == 0 && h->opt.update_mode == 0)
+  const int W = h->outer * NB;
+  if (h->world > 1 && W % TILE == 0 && (W & (W - 1)) == 0 && h->opt.update_mode == 0)
     for (int J = 0; J < ns; ++J)
       h->top_dist[J] = h->owner[J] < 0 && h->grp_hi[J] - h->grp_lo[J] > 1 && !h->is_small[J] && work[J] >= h->dist_min_flops;
-  // persistent diagonal-block inverse slots (factor TRSM + solve): non-top supernodes first
-  h->slot_base.assign(ns, 0);
-  {
-    int slot = 0;
-    for (int pass = 0; pass < 2; ++pass)
-      for (int J = 0; J < ns; ++J) {
-        const bool top = h->world > 1 && h->owner[J] < 0;
-        if (top != (pass == 1) || h->is_small[J]) continue;
-        if (pass == 1 && h->top_slot < 0) h->top_slot = slot;
-        h->slot_base[J] = slot;
-        slot += (h->sn[J].k + NB - 1) / NB;
-      }
-    h->nslots_total = slot;
-    if (h->top_slot < 0) h->top_slot = slot;
-  }
-  // the whole tree (the solve's structure; the single-GPU factor when nvr == 1), then per-rank
-  // phase A / phase C for multi-GPU
-  append_levels(h, [](int) { return true; }, true);
-  build_solve_tasks(h);
-  h->plan_all_end = h->plan.size();
-  h->plan_factor_begin = 0;
-  if (h->world == 1 && h->nvr > 1) {
-    // single GPU, subtree concurrency: proportional map onto nvr virtual ranks; each virtual rank's
-    // subtrees run on their own (critical, trailing) stream pair, the top supernodes after all of
-    // them have joined stream 0
-    std::vector<int> vown;
-    proportional_map(S, work, h->nvr, vown);
-    h->plan_factor_begin = h->plan.size();
-    for (int v = 0; v < h->nvr; ++v) append_levels(h, [&vown, v](int J) { return vown[J] == v; }, false, 2 * v);
-    for (int v = 1; v < h->nvr; ++v) {
-      const int ev = h->nevents++;
-      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 2 * v, ev});
-      h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 0, ev});
+  if (h->world == 1) {
+    // panel arena: supernodes in order
+    long long off = 0;
+    for (int J = 0; J < ns; ++J) {
+      h->sn[J].off = off;
+      off += (long long)h->sn[J].ld * h->sn[J].k;
     }
-    append_levels(h, [&vown](int J) { return vown[J] < 0; }, false, 0);
-    h->plan_all_end = h->plan.size();
-  }
-  if (h->world > 1) {
-    const int me = h->rank;
-    append_levels(h, [h, me](int J) { return h->owner[J] == me; }, false);
-    h->plan_a_end = h->plan.size();
-    append_levels(h, [h, me](int J) { return h->owner[J] < 0 && h->top_owner[J] == me; }, false, 0, true);
-    for (size_t i = h->plan_a_end; i < h->plan.size(); ++i)
-      if (h->plan[i].op == OP_TOP_LEVEL || h->plan[i].op == OP_BCAST) h->markers.push_back(i);
+    h->panel_doubles = off;
+    // persistent diagonal-block inverse slots (factor TRSM + solve)
+    h->slot_base.assign(ns, 0);
+    int slot = 0;
+    for (int J = 0; J < ns; ++J) {
+      if (h->is_small[J]) continue;
+      h->slot_base[J] = slot;
+      slot += (h->sn[J].k + NB - 1) / NB;
+    }
+    h->nslots_total = slot;
   } else {
-    h->plan_a_end = h->plan.size();
+    dist_layout(h);   // per-rank arena: own subtrees, owned top block columns, ring aliases
   }
+  for (int J = 0; J < ns; ++J) h->panel_off[J] = h->sn[J].off;
+  h->panel_off[ns] = h->panel_doubles;
+  if (h->world == 1) {
+    // the whole tree (the solve's structure; the single-GPU factor when nvr == 1)
+    append_levels(h, [](int) { return true; }, true);
+    build_solve_tasks(h, [](int) { return true; });
+    h->plan_all_end = h->plan.size();
+    h->plan_factor_begin = 0;
+    if (h->nvr > 1) {
+      // single GPU, subtree concurrency: proportional map onto nvr virtual ranks; each virtual rank's
+      // subtrees run on their own (critical, trailing) stream pair, the top supernodes after all of
+      // them have joined stream 0
+      std::vector<int> vown;
+      proportional_map(S, work, h->nvr, vown);
+      h->plan_factor_begin = h->plan.size();
+      for (int v = 0; v < h->nvr; ++v) append_levels(h, [&vown, v](int J) { return vown[J] == v; }, false, 2 * v);
+      for (int v = 1; v < h->nvr; ++v) {
+        const int ev = h->nevents++;
+        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_RECORD, 2 * v, ev});
+        h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, 0, ev});
+      }
+      append_levels(h, [&vown](int J) { return vown[J] < 0; }, false, 0);
+      h->plan_all_end = h->plan.size();
+    }
+    h->plan_a_end = h->plan.size();
+    return;
+  }
+  // multi-GPU: phase A (own subtrees), the boundary-block exchange, phase C (top levels)
+  dist_exchange_plan(h);
+  const int me = h->rank;
+  h->plan_all_end = h->plan_factor_begin = 0;
+  append_levels(h, [h, me](int J) { return h->owner[J] == me; }, false);
+  h->plan_a_end = h->plan.size();
+  if (!h->exch_runs[0].empty()) {
+    Launch M{0, 0, 0, 0, 0, OP_EXCHANGE, 0, -1};
+    M.aux = 0;
+    h->plan.push_back(M);
+    h->plan_level.resize(h->plan.size(), -1);
+  }
+  append_levels(h, [h, me](int J) { return h->owner[J] < 0 && h->top_owner[J] == me; }, false, 0, true);
+  for (size_t i = h->plan_a_end; i < h->plan.size(); ++i)
+    if (h->plan[i].op == OP_EXCHANGE || h->plan[i].op == OP_BCAST) h->markers.push_back(i);
+  build_solve_tasks(h, [h, me](int J) { return h->owner[J] == me; });
+  dist_solve_plan(h);
 }
 
 static int setup_device(spchol_handle* h) {
@@ -861,13 +714,13 @@ static int setup_device(spchol_handle* h) {
       ucm.push_back(S.rel_off[pair] - S.rel_q0[pair]);
     }
   }
+  if (h->world > 1) dist_redirect(h, posmap, ucb);   // updates leaving the rank go to its update blocks
   std::vector<long long> amap(S.nnzA);
   for (long long e = 0; e < S.nnzA; ++e) {
     const int c = S.a_col[e], J = S.snode[c];
     amap[e] = h->sn[J].off + (long long)(c - S.sfirst[J]) * h->sn[J].ld + S.a_pos[e];
-    // multi-GPU: a rank initialises its own subtrees' entries; a top supernode's entries are added
-    // once, by the first rank of its group (which takes part in its reduction)
-    if (h->world > 1 && !(h->owner[J] == h->rank || (h->owner[J] < 0 && h->rank == h->grp_lo[J]))) amap[e] = -1;
+    // multi-GPU: a rank initialises the entries of the columns it holds
+    if (h->world > 1 && !dist_amap_mine(h, c)) amap[e] = -1;
   }
   CK(cudaSetDevice(h->opt.device));
   CK(kernels_init_attributes());
@@ -892,7 +745,12 @@ static int setup_device(spchol_handle* h) {
   h->plan_events.resize(h->nevents);
   for (auto& e : h->plan_events) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   g_dev_bytes = 0;
-  CK(dalloc(&h->d_panels, (size_t)h->panel_doubles));
+  if (h->world > 1) {
+    int rc = dist_setup_device(h);   // per-rank arena (VMM), inverse slots, exchange metadata
+    if (rc) return rc;
+  } else {
+    CK(dalloc(&h->d_panels, (size_t)h->panel_doubles));
+  }
   CK(dalloc(&h->d_avals, (size_t)S.nnzA));
   CK(upload(&h->d_amap, amap));
   CK(upload(&h->d_ucol_base, ucb));
@@ -903,7 +761,7 @@ static int setup_device(spchol_handle* h) {
   CK(upload(&h->d_gtasks, h->gtasks));
   CK(upload(&h->d_rtasks, h->rtasks));
   CK(upload(&h->d_ptasks, h->ptasks));
-  CK(dalloc(&h->d_linv, (size_t)std::max(1, h->nslots_total) * NBMAX * NBMAX));
+  if (h->world == 1) CK(dalloc(&h->d_linv, (size_t)std::max(1, h->nslots_total) * NBMAX * NBMAX));
   if (h->use_tma) {
     // TMA descriptors: panel J as a 2D tensor (m_J rows contiguous, k_J columns, row stride ld_J),
     // boxes of 16 rows x 8 columns with 128-byte swizzle; rows >= m_J / columns >= k_J read as 0
@@ -945,7 +803,7 @@ static int setup_device(spchol_handle* h) {
   CK(upload(&h->d_small_sns, h->small_sns));
   CK(upload(&h->d_stasks, h->stasks));
   CK(upload(&h->d_ssolve, h->ssolve));
-  CK(dalloc(&h->d_sflags, (size_t)3 * std::max(1, h->nslots_total) + 2 * (size_t)S.nlevels + 1));
+  CK(dalloc(&h->d_sflags, (size_t)3 * std::max(1, h->nslots_total) + h->nticket + 1));
   CK(dalloc(&h->d_y, (size_t)S.n));
   CK(dalloc(&h->d_y2, (size_t)S.n));
   h->device_bytes = g_dev_bytes;
@@ -959,6 +817,7 @@ static void free_device(spchol_handle* h) {
   if (h->solve_graph) cudaGraphDestroy(h->solve_graph);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->graph) cudaGraphDestroy(h->graph);
+  if (h->world > 1) dist_free_device(h);   // the VMM arenas (d_panels, d_linv)
   void* ptrs[] = {h->d_ssolve, h->d_stasks, h->d_sflags, h->d_rtasks, h->d_tmaps, h->d_tmap_linv, h->d_small_sns, h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
                   h->d_rows_ptr, h->d_posmap, h->d_sfirst, h->d_rows, h->d_perm, h->d_level_sns, h->d_sn,
                   h->d_gtasks, h->d_ptasks, h->d_fail};
@@ -990,15 +849,18 @@ static int finish_handle(spchol_handle* h) {
     if (h->opt.update_mode != 0) return fail(SPCHOL_ERR_VALIDATION, "deterministic requires update_mode 0 (RL)");
     h->nvr = 1;   // concurrent subtrees would update the shared top panels in an unordered way
   }
+  if (h->world > 1 && (h->opt.update_mode != 0 || h->opt.deterministic))
+    return fail(SPCHOL_ERR_VALIDATION, "multi-GPU (dist_world > 1) supports update_mode 0 without deterministic");
   if (const char* e = getenv("SPCHOL_NO_LOOKAHEAD")) h->no_lookahead = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_NO_NEXT_SPLIT")) h->no_next_split = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_LEFT_INNER")) h->right_inner = atoi(e) == 0;
   if (const char* e = getenv("SPCHOL_LEFT_INNER_MIN")) h->left_inner_min = std::max(0, atoi(e));
   if (const char* e = getenv("SPCHOL_REST_SMEM")) h->rest_smem = std::max(0, std::min(112 * 1024, atoi(e)));
   if (const char* e = getenv("SPCHOL_MAX_LEVEL")) h->max_level = atoi(e);
-  if (const char* e = getenv("SPCHOL_TMA")) h->use_tma = atoi(e) != 0;
+  if (const char* e = getenv("SPCHOL_TMA")) h->use_tma = atoi(e) != 0 && h->world == 1;
   if (const char* e = getenv("SPCHOL_OUTER")) h->outer = std::max(1, atoi(e));
   if (const char* e = getenv("SPCHOL_DIST_MINFLOPS")) h->dist_min_flops = atof(e);
+  if (const char* e = getenv("SPCHOL_RING_NS")) h->ring_ns = std::max(2, atoi(e));   // diagnostics
   if (const char* e = getenv("SPCHOL_SMALL_WARP")) h->small_warp = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_SMALL_WARP_MAXM")) h->small_warp_maxm = std::max(0, std::min(128, atoi(e)));
   build_plan(h);
@@ -1184,79 +1046,6 @@ extern "C" int spchol_set_stream(spchol_handle* h, void* stream) {
   return SPCHOL_OK;
 }
 
-// Enqueue the whole factorization on st (no host synchronization).
-// Multi-GPU phase C, start of top level l: every top supernode P of the level has partial panels
-// on all ranks (A's entries on rank 0, contributions of each rank's subtrees and of the top
-// supernodes it factored); they are summed onto P's owner (one NCCL group of reduces), and the
-// other ranks zero their copies so that a final sum all-reduce assembles the factor exactly once.
-// Without a communicator (diagnostics) nothing is exchanged here.
-static int enqueue_top_reduce(spchol_handle* h, cudaStream_t st, int l) {
-  if (!h->nccl_comm) return SPCHOL_OK;
-  const int W = h->outer * h->nb;
-  for (int P : h->top_by_level[l]) {
-    // only P's rank group holds contributions to P (its descendants live there; A's entries of P
-    // are added by the group's first rank), so the sum runs over the group's communicator; one
-    // NCCL group per supernode (one communicator per group call)
-    if (!in_group(h, P, h->rank)) continue;
-    void* comm = group_comm(h, P);
-    if (!comm) return fail(SPCHOL_ERR_STATE, "no communicator for a top rank group");
-    int r = g_nccl.group_start();
-    if (r) return nccl_fail(r, "ncclGroupStart");
-    const SnInfo& I = h->sn[P];
-    for (int C = 0; C * W < I.k; ++C) {   // block columns onto their owners (whole panel if undistributed)
-      const int c0 = C * W, nc = h->top_dist[P] ? std::min(W, I.k - c0) : I.k;
-      double* p = h->d_panels + I.off + (size_t)c0 * I.ld;
-      r = g_nccl.reduce(p, p, (size_t)I.ld * nc, NCCL_FLOAT64, NCCL_SUM, blk_owner(h, P, C) - h->grp_lo[P], comm, st);
-      if (r) { g_nccl.group_end(); return nccl_fail(r, "ncclReduce(top panel)"); }
-      if (!h->top_dist[P]) break;
-    }
-    r = g_nccl.group_end();
-    if (r) return nccl_fail(r, "ncclGroupEnd");
-  }
-  for (int P : h->top_by_level[l]) {
-    const SnInfo& I = h->sn[P];
-    for (int C = 0; C * W < I.k; ++C) {
-      const int c0 = C * W, nc = h->top_dist[P] ? std::min(W, I.k - c0) : I.k;
-      if (blk_owner(h, P, C) != h->rank)
-        CK(cudaMemsetAsync(h->d_panels + I.off + (size_t)c0 * I.ld, 0, sizeof(double) * (size_t)I.ld * nc, st));
-      if (!h->top_dist[P]) break;
-    }
-  }
-  return SPCHOL_OK;
-}
-
-// Multi-GPU phase C, distributed top supernode J: column block C is final on its owner; it goes to
-// the other ranks of J's group (their trailing updates and U_J tiles read it): ncclBroadcast on the
-// group's communicator; ranks outside the group have nothing to do.  Every rank issues its NCCL
-// calls in the same (plan) order on one stream, so calls on different communicators never cross.
-static int enqueue_bcast(spchol_handle* h, cudaStream_t st, int J, int C) {
-  if (!h->nccl_comm || !in_group(h, J, h->rank)) return SPCHOL_OK;
-  const int W = h->outer * h->nb, o = blk_owner(h, J, C);
-  const SnInfo& I = h->sn[J];
-  const int c0 = C * W, nc = std::min(W, I.k - c0);
-  double* p = h->d_panels + I.off + (size_t)c0 * I.ld;
-  const size_t cnt = (size_t)I.ld * nc;
-  void* comm = group_comm(h, J);
-  if (!comm) return fail(SPCHOL_ERR_STATE, "no communicator for a top rank group");
-  // pipelined broadcast over the group (ring / tree / NVLS as NCCL picks): each member receives the
-  // block column once instead of the owner sending it g - 1 times
-  const int r = g_nccl.bcast(p, p, cnt, NCCL_FLOAT64, o - h->grp_lo[J], comm, st);
-  if (r) return nccl_fail(r, "ncclBroadcast(block column)");
-  return SPCHOL_OK;
-}
-
-// After the level's scatter, a group member's copies of the blocks of J it does not own are zeroed
-// (so every factor entry is non-zero on exactly one rank: the solve's gather is a sum).
-static int enqueue_zero_nonowned(spchol_handle* h, cudaStream_t st, int J) {
-  const int W = h->outer * h->nb;
-  const SnInfo& I = h->sn[J];
-  for (int C = 0; C * W < I.k; ++C)
-    if (blk_owner(h, J, C) != h->rank)
-      CK(cudaMemsetAsync(h->d_panels + I.off + (size_t)C * W * I.ld, 0,
-                         sizeof(double) * (size_t)I.ld * std::min(W, I.k - C * W), st));
-  return SPCHOL_OK;
-}
-
 // Enqueue the plan entries [begin, end) (launches, lookahead fork/join events) on st.
 static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t end) {
   auto tstart = [&](int idx) -> size_t {
@@ -1297,18 +1086,13 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
       if (multi) CK(cudaStreamWaitEvent(ls, h->plan_events[L.ev], 0));
       continue;
     }
-    if (L.op == OP_TOP_LEVEL) {
-      int rc = enqueue_top_reduce(h, ls, L.aux);
+    if (L.op == OP_EXCHANGE) {
+      int rc = dist_enqueue_exchange(h, ls, L.aux);
       if (rc) return rc;
       continue;
     }
     if (L.op == OP_BCAST) {
-      int rc = enqueue_bcast(h, ls, L.aux, L.aux2);
-      if (rc) return rc;
-      continue;
-    }
-    if (L.op == OP_ZERO) {
-      int rc = enqueue_zero_nonowned(h, ls, L.aux);
+      int rc = dist_enqueue_bcast(h, ls, L.aux, L.aux2);
       if (rc) return rc;
       continue;
     }
@@ -1340,7 +1124,12 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
                       multi && !hi ? h->rest_smem : 0);
         break;
       case K_SCATTER:
-        if (L.aux == 1)
+        if (L.aux == 2) {   // multi-GPU: partial U_J over the owned block columns
+          int lw = 0;
+          while ((1 << lw) < h->outer * h->nb) ++lw;
+          launch_gemm(MODE_SCATTER_KS, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base,
+                      h->d_ucol_map, h->d_posmap, ls, prio, 0, lw);
+        } else if (L.aux == 1)
           launch_gemm(MODE_SCATTER_DET, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
         else if (h->use_tma)
           launch_gemm_tma(MODE_SCATTER, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_tmaps, h->d_tmap_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
@@ -1375,9 +1164,14 @@ static int enqueue_init(spchol_handle* h, cudaStream_t st) {
     cudaEventRecord(h->ev_pool[ti], st);
     h->pending.push_back({-1, ti});
   }
-  CK(cudaMemsetAsync(h->d_fail, 0xFF, sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(h->d_panels, 0, sizeof(double) * (size_t)std::max(1LL, h->panel_doubles), st));
-  launch_init(h->d_avals, h->d_amap, h->S.nnzA, h->d_panels, st);
+  if (h->world > 1) {
+    int rc = dist_enqueue_init(h, st);
+    if (rc) return rc;
+  } else {
+    CK(cudaMemsetAsync(h->d_fail, 0xFF, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(h->d_panels, 0, sizeof(double) * (size_t)std::max(1LL, h->panel_doubles), st));
+    launch_init(h->d_avals, h->d_amap, h->S.nnzA, h->d_panels, st);
+  }
   if (h->timing) cudaEventRecord(h->ev_pool[ti + 1], st);
   CK(cudaGetLastError());
   return SPCHOL_OK;
@@ -1388,12 +1182,11 @@ static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
   if (rc) return rc;
   if (h->world == 1) return enqueue_ops(h, st, h->plan_factor_begin, h->plan_all_end);
   if (!h->nccl_comm) return fail(SPCHOL_ERR_STATE, "multi-GPU handle without an NCCL communicator (spchol_dist_attach_nccl)");
-  // every diagonal-inverse slot is written on one rank only (its subtree's rank, or its block
-  // column's owner); zero them all so the solve's gather (a sum over ranks) sees each exactly once
-  if (h->nslots_total > 0)
-    CK(cudaMemsetAsync(h->d_linv, 0, sizeof(double) * (size_t)h->nslots_total * NBMAX * NBMAX, st));
   if ((rc = enqueue_ops(h, st, h->plan_all_end, h->plan_a_end))) return rc;   // phase A: own subtrees
-  if ((rc = enqueue_ops(h, st, h->plan_a_end, h->plan.size()))) return rc;    // phase C: owned tops, per-level reduces
+  // exchange of the boundary blocks, then phase C (top levels with their broadcasts and exchanges)
+  if ((rc = enqueue_ops(h, st, h->plan_a_end, h->plan.size()))) return rc;
+  CK(cudaEventRecord(h->ev_comm_out, h->comm_stream));   // join the comm stream (graph capture)
+  CK(cudaStreamWaitEvent(st, h->ev_comm_out, 0));
   int r = g_nccl.allreduce(h->d_fail, h->d_fail, 1, NCCL_UINT64, NCCL_MIN, h->nccl_comm, st);
   if (r) return nccl_fail(r, "ncclAllReduce(fail flag)");
   return SPCHOL_OK;
@@ -1405,22 +1198,35 @@ extern "C" int spchol_factor_async(spchol_handle* h) {
   if (!h->values_set) return fail(SPCHOL_ERR_STATE, "values not set");
   CK(cudaSetDevice(h->opt.device));
   h->factored = false;
-  // multi-GPU factors are launched directly (no graph capture of the NCCL calls)
-  if (h->opt.use_graph && !h->timing && h->world == 1) {
+  // multi-GPU: the NCCL calls are captured with the kernels (NCCL supports stream capture) from the
+  // second factor on — the first runs eagerly so that NCCL sets up its peer connections outside a
+  // capture; if the capture fails the handle stays eager.  The tests' blocking stand-in is never
+  // captured.
+  const bool dist_graph = h->world > 1 && g_nccl.capturable && !h->dist_capture_failed && h->dist_eager_done &&
+                          !(getenv("SPCHOL_DIST_GRAPH") && atoi(getenv("SPCHOL_DIST_GRAPH")) == 0);
+  if (h->opt.use_graph && !h->timing && (h->world == 1 || dist_graph)) {
     if (!h->gexec) {
       cudaStream_t cs = h->own_stream;
-      CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      CK(cudaStreamBeginCapture(cs, h->world > 1 ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal));
       int rc = enqueue_factor(h, cs);
       cudaGraph_t g = nullptr;
       cudaError_t e = cudaStreamEndCapture(cs, &g);
+      if (h->world > 1 && (rc != SPCHOL_OK || e != cudaSuccess)) {   // stay eager (NCCL refused the capture)
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        h->dist_capture_failed = true;
+        return enqueue_factor(h, h->stream);
+      }
       if (rc != SPCHOL_OK) { if (g) cudaGraphDestroy(g); return rc; }
       if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
       h->graph = g;
       CK(cudaGraphInstantiateWithFlags(&h->gexec, g, cudaGraphInstantiateFlagUseNodePriority));  // honour per-node priorities
+      h->graph_dist = h->world > 1;
     }
     CK(cudaGraphLaunch(h->gexec, h->stream));
     return SPCHOL_OK;
   }
+  h->dist_eager_done = true;
   return enqueue_factor(h, h->stream);
 }
 
@@ -1439,7 +1245,6 @@ extern "C" int spchol_factor_status(spchol_handle* h, int64_t* fail_col, int64_t
     return fail(SPCHOL_ERR_NOT_SPD, "matrix is not positive definite: pivot <= 0 at final column " + std::to_string(fc));
   }
   h->factored = true;
-  h->gathered = h->world == 1;
   return SPCHOL_OK;
 }
 
@@ -1483,47 +1288,30 @@ static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaS
   return SPCHOL_OK;
 }
 
-// Multi-GPU: before the first solve after a factor, every rank receives the whole factor — each
-// panel and diagonal-block inverse is non-zero on exactly one rank (subtrees on their rank, top
-// supernodes on their owner), so a sum all-reduce assembles them.
-static int gather_factor(spchol_handle* h) {
-  if (h->gathered) return SPCHOL_OK;
-  if (!h->nccl_comm) return fail(SPCHOL_ERR_STATE, "multi-GPU handle without an NCCL communicator");
-  int r = 0;
-  if (h->panel_doubles > 0 && (r = g_nccl.allreduce(h->d_panels, h->d_panels, (size_t)h->panel_doubles, NCCL_FLOAT64,
-                                                    NCCL_SUM, h->nccl_comm, h->stream)))
-    return nccl_fail(r, "ncclAllReduce(panels)");
-  if (h->nslots_total > 0 && (r = g_nccl.allreduce(h->d_linv, h->d_linv, (size_t)h->nslots_total * NBMAX * NBMAX,
-                                                   NCCL_FLOAT64, NCCL_SUM, h->nccl_comm, h->stream)))
-    return nccl_fail(r, "ncclAllReduce(diagonal inverses)");
-  h->gathered = true;
-  return SPCHOL_OK;
-}
-
-extern "C" int spchol_dist_gather(spchol_handle* h) {
-  if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
-  if (host_only(h) || !h->factored) return fail(SPCHOL_ERR_STATE, "gather before a successful factor");
-  if (h->world == 1) return SPCHOL_OK;
-  CK(cudaSetDevice(h->opt.device));
-  int rc = gather_factor(h);
-  if (rc) return rc;
-  CK(cudaStreamSynchronize(h->stream));
-  return SPCHOL_OK;
-}
-
 // One solve of the internal buffer d_y2 in place, captured in a CUDA graph on first use.
+// Multi-GPU: the distributed solve (dist_enqueue_solve) is collective — every rank of the handle's
+// communicator calls the solve the same number of times.
+static int any_solve(spchol_handle* h, cudaStream_t st) {
+  return h->world > 1 ? dist_enqueue_solve(h, h->d_y2, st) : enqueue_solve(h, h->d_y2, h->d_y2, st);
+}
 static int run_solve_y2(spchol_handle* h) {
-  if (!h->gathered) {
-    int rc = gather_factor(h);
-    if (rc) return rc;
-  }
-  if (!h->opt.use_graph) return enqueue_solve(h, h->d_y2, h->d_y2, h->stream);
+  // multi-GPU: captured from the second solve on, as the factor
+  const bool graph = h->opt.use_graph &&
+                     (h->world == 1 || (g_nccl.capturable && h->dist_solve_eager_done && !h->dist_capture_failed));
+  h->dist_solve_eager_done = true;
+  if (!graph) return any_solve(h, h->stream);
   if (!h->solve_gexec) {
     cudaStream_t cs = h->own_stream;
-    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    int rc = enqueue_solve(h, h->d_y2, h->d_y2, cs);
+    CK(cudaStreamBeginCapture(cs, h->world > 1 ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal));
+    int rc = any_solve(h, cs);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(cs, &g);
+    if (h->world > 1 && (rc != SPCHOL_OK || e != cudaSuccess)) {   // stay eager (NCCL refused the capture)
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      h->dist_capture_failed = true;
+      return any_solve(h, h->stream);
+    }
     if (rc != SPCHOL_OK) { if (g) cudaGraphDestroy(g); return rc; }
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture(solve)");
     h->solve_graph = g;
@@ -1594,6 +1382,18 @@ extern "C" int spchol_query(const spchol_handle* h, int key, int64_t* value) {
     case SPCHOL_Q_NBLOCKS: *value = (int64_t)S.blk_q.size(); break;
     case SPCHOL_Q_NMARKERS: *value = (int64_t)h->markers.size(); break;
     case SPCHOL_Q_DEVICE_BYTES: *value = (int64_t)h->device_bytes; break;
+    case SPCHOL_Q_COMM_SEND_BYTES: *value = (int64_t)h->comm_send; break;
+    case SPCHOL_Q_COMM_RECV_BYTES: *value = (int64_t)h->comm_recv; break;
+    case SPCHOL_Q_ARENA_BYTES: {   // physical memory of this rank's panel arena + inverses (+ ring)
+      if (h->world == 1) { *value = (int64_t)(8 * (h->panel_doubles + (long long)h->nslots_total * NBMAX * NBMAX)); break; }
+      long long b = h->ring_bytes;
+      for (const VRegion& g : h->vregions) if (g.ring < 0) b += 8 * g.len;
+      const int r = h->rank, P = h->world;
+      b += 8LL * NBMAX * NBMAX * ((h->slot_sub[r + 1] - h->slot_sub[r]) + (h->nslots_total - h->slot_sub[P]));
+      *value = b;
+      break;
+    }
+    case SPCHOL_Q_DIST_GRAPH: *value = h->graph_dist ? 1 : 0; break;
     case SPCHOL_Q_NTOP_DIST: {
       int64_t c = 0;
       for (char d : h->top_dist) c += d != 0;
@@ -1632,11 +1432,29 @@ extern "C" int spchol_export_blocks(const spchol_handle* h, int64_t* blk_ptr, in
   return SPCHOL_OK;
 }
 
-// Multi-GPU: after a factor each rank holds only its share of L until the collective gather
-// (spchol_dist_gather, or the first solve) has run; value exports before that would be partial.
-static int need_gathered(const spchol_handle* h) {
-  if (h->world > 1 && h->factored && !h->gathered)
-    return fail(SPCHOL_ERR_STATE, "multi-GPU factor not gathered: call spchol_dist_gather (collective) first");
+// Panel J to host memory.  Multi-GPU: the entries this rank holds (its subtrees, the top supernodes
+// it factors whole, its block columns of the distributed ones), zeros elsewhere — the sum over the
+// ranks' exports is L.
+static int copy_panel(const spchol_handle* h, int J, double* out) {
+  const SnInfo& I = h->sn[J];
+  const size_t cnt = (size_t)I.ld * I.k;
+  if (!cnt) return SPCHOL_OK;
+  const double* src = h->d_panels + I.off;
+  if (h->world == 1) {
+    CK(cudaMemcpy(out, src, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+    return SPCHOL_OK;
+  }
+  std::fill(out, out + cnt, 0.0);
+  const int W = outer_w(h);
+  if (!h->top_dist[J]) {
+    if (dist_owns(h, J, h->S.sfirst[J])) CK(cudaMemcpy(out, src, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+    return SPCHOL_OK;
+  }
+  for (int C = 0; C * W < I.k; ++C)
+    if (blk_owner(h, J, C) == h->rank) {
+      const size_t o = (size_t)C * W * I.ld;
+      CK(cudaMemcpy(out + o, src + o, sizeof(double) * (size_t)I.ld * std::min(W, I.k - C * W), cudaMemcpyDeviceToHost));
+    }
   return SPCHOL_OK;
 }
 
@@ -1648,13 +1466,21 @@ extern "C" int spchol_export_panels(const spchol_handle* h, int64_t* panel_off, 
     if (ld) for (size_t J = 0; J < h->sn.size(); ++J) ld[J] = h->sn[J].ld;
     return SPCHOL_OK;
   }
-  if (panels && need_gathered(h)) return SPCHOL_ERR_STATE;
   CK(cudaSetDevice(h->opt.device));
   CK(cudaStreamSynchronize(h->stream));
   if (panel_off) for (size_t J = 0; J < h->panel_off.size(); ++J) panel_off[J] = h->panel_off[J];
   if (ld) for (size_t J = 0; J < h->sn.size(); ++J) ld[J] = h->sn[J].ld;
-  if (panels && h->panel_doubles > 0)
-    CK(cudaMemcpy(panels, h->d_panels, sizeof(double) * (size_t)h->panel_doubles, cudaMemcpyDeviceToHost));
+  if (panels && h->panel_doubles > 0) {
+    if (h->world == 1) {
+      CK(cudaMemcpy(panels, h->d_panels, sizeof(double) * (size_t)h->panel_doubles, cudaMemcpyDeviceToHost));
+    } else {
+      std::fill(panels, panels + h->panel_doubles, 0.0);
+      for (int J = 0; J < h->S.nsuper; ++J) {
+        int rc = copy_panel(h, J, panels + h->sn[J].off);
+        if (rc) return rc;
+      }
+    }
+  }
   return SPCHOL_OK;
 }
 
@@ -1662,12 +1488,9 @@ extern "C" int spchol_export_panel(const spchol_handle* h, int32_t J, double* ou
   if (!h || !out) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
   if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
   if (J < 0 || J >= h->S.nsuper) return fail(SPCHOL_ERR_DIMENSION, "supernode index out of range");
-  if (need_gathered(h)) return SPCHOL_ERR_STATE;
   CK(cudaSetDevice(h->opt.device));
   CK(cudaStreamSynchronize(h->stream));
-  const size_t cnt = (size_t)h->sn[J].ld * h->sn[J].k;   // panels need not be in supernode order
-  if (cnt) CK(cudaMemcpy(out, h->d_panels + h->sn[J].off, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
-  return SPCHOL_OK;
+  return copy_panel(h, J, out);
 }
 
 // Exact factor in CSC (final numbering).  Pattern: struct(L_j) by row subtrees of the final etree
@@ -1678,7 +1501,6 @@ extern "C" int spchol_export_factor_csc(const spchol_handle* h, int64_t* Lp, int
   if (!h || !Lp) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
   if ((Lx || padding_nonzeros) && (host_only(h) || !h->factored))
     return fail(SPCHOL_ERR_STATE, "values need a successful factor on a device handle");
-  if ((Lx || padding_nonzeros) && need_gathered(h)) return SPCHOL_ERR_STATE;
   const Symbolic& S = h->S;
   const int64_t n = S.n;
   Lp[0] = 0;
@@ -1742,13 +1564,14 @@ extern "C" int spchol_export_factor_csc(const spchol_handle* h, int64_t* Lp, int
 extern "C" int spchol_export_diagonal(spchol_handle* h, double* diag) {
   if (!h || !diag) return fail(SPCHOL_ERR_VALIDATION, "NULL argument");
   if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
-  if (need_gathered(h)) return SPCHOL_ERR_STATE;
   CK(cudaSetDevice(h->opt.device));
   const Symbolic& S = h->S;
-  if (!h->d_diag_idx) {
+  if (!h->d_diag_idx) {   // multi-GPU: the diagonal entries this rank holds, zeros elsewhere
     std::vector<long long> idx(S.n);
     for (int J = 0; J < S.nsuper; ++J)
-      for (int c = 0; c < h->sn[J].k; ++c) idx[S.sfirst[J] + c] = h->sn[J].off + (long long)c * h->sn[J].ld + c;
+      for (int c = 0; c < h->sn[J].k; ++c)
+        idx[S.sfirst[J] + c] = h->world > 1 && !dist_owns(h, J, S.sfirst[J] + c)
+                                   ? -1 : h->sn[J].off + (long long)c * h->sn[J].ld + c;
     CK(upload(&h->d_diag_idx, idx));
   }
   launch_gather(h->d_panels, h->d_diag_idx, h->d_y, S.n, h->stream);
@@ -1823,130 +1646,8 @@ extern "C" int spchol_export_mapping(const spchol_handle* h, int32_t* owner, int
   if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
   if (owner) for (int J = 0; J < h->S.nsuper; ++J) owner[J] = h->world > 1 ? h->owner[J] : 0;
   if (top_owner) for (int J = 0; J < h->S.nsuper; ++J) top_owner[J] = h->world > 1 ? h->top_owner[J] : -1;
-  if (top_off) *top_off = h->top_off;
-  if (top_slot) *top_slot = h->top_slot;
-  return SPCHOL_OK;
-}
-
-extern "C" int spchol_factor_phase(spchol_handle* h, int phase) {
-  if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
-  if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
-  if (!h->values_set) return fail(SPCHOL_ERR_STATE, "values not set");
-  CK(cudaSetDevice(h->opt.device));
-  int rc = SPCHOL_OK;
-  switch (phase) {
-    case 1:
-      h->factored = false;
-      rc = enqueue_init(h, h->stream);
-      if (!rc && h->world > 1 && h->nslots_total > 0)
-        CK(cudaMemsetAsync(h->d_linv, 0, sizeof(double) * (size_t)h->nslots_total * NBMAX * NBMAX, h->stream));
-      if (!rc) rc = enqueue_ops(h, h->stream, h->world == 1 ? h->plan_factor_begin : h->plan_all_end, h->world == 1 ? h->plan_all_end : h->plan_a_end);
-      break;
-    case 2:
-      if (h->world > 1) rc = enqueue_ops(h, h->stream, h->plan_a_end, h->plan.size());
-      break;
-    case 3:
-      rc = spchol_factor_status(h, nullptr, nullptr);
-      if (!rc) h->gathered = true;
-      break;
-    default: {
-      // 2000 + i: segment i of phase C, the plan entries between marker i-1 and marker i (the
-      // exchange of marker i is then played by spchol_dist_debug_comm)
-      const long long nm = (long long)h->markers.size();
-      if (phase < 2000 || phase - 2000 > nm || h->world == 1)
-        return fail(SPCHOL_ERR_VALIDATION, "phase must be 1, 2, 3 or 2000 + segment (segment <= markers)");
-      const long long i = phase - 2000;
-      const size_t b = i == 0 ? h->plan_a_end : h->markers[i - 1] + 1;
-      const size_t e = i < nm ? h->markers[i] : h->plan.size();
-      if (b < e) rc = enqueue_ops(h, h->stream, b, e);
-      break;
-    }
-  }
-  return rc;
-}
-
-extern "C" int spchol_dist_debug_accumulate(spchol_handle* dst, const spchol_handle* src, int which) {
-  if (!dst || !src) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
-  if (host_only(dst) || host_only(src)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
-  if (dst->panel_doubles != src->panel_doubles || dst->top_off != src->top_off || dst->top_slot != src->top_slot)
-    return fail(SPCHOL_ERR_VALIDATION, "handles of different problems");
-  CK(cudaSetDevice(dst->opt.device));
-  CK(cudaStreamSynchronize(src->stream));
-  double* d;
-  const double* sp;
-  long long cnt;
-  switch (which) {
-    case 0: d = dst->d_panels + dst->top_off; sp = src->d_panels + src->top_off; cnt = dst->panel_doubles - dst->top_off; break;
-    case 1: d = dst->d_panels; sp = src->d_panels; cnt = dst->panel_doubles; break;
-    case 2: d = dst->d_linv; sp = src->d_linv; cnt = (long long)dst->nslots_total * NBMAX * NBMAX; break;
-    default:
-      if (which >= 16) {   // 16 + J: fan-in of top supernode J's panel, the source copy is zeroed
-        const int J = which - 16;
-        if (J >= dst->S.nsuper) return fail(SPCHOL_ERR_VALIDATION, "supernode out of range");
-        d = dst->d_panels + dst->sn[J].off;
-        sp = src->d_panels + src->sn[J].off;
-        cnt = (long long)dst->sn[J].ld * dst->sn[J].k;
-        launch_axpy(sp, d, cnt, dst->stream);
-        CK(cudaStreamSynchronize(dst->stream));
-        CK(cudaMemset(src->d_panels + src->sn[J].off, 0, sizeof(double) * (size_t)cnt));
-        return SPCHOL_OK;
-      }
-      return fail(SPCHOL_ERR_VALIDATION, "which must be 0, 1, 2 or 16 + supernode");
-  }
-  launch_axpy(sp, d, cnt, dst->stream);
-  CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(dst->stream));
-  return SPCHOL_OK;
-}
-
-extern "C" int spchol_dist_debug_comm(spchol_handle* const* hs, int world, int marker) {
-  if (!hs || world < 2) return fail(SPCHOL_ERR_VALIDATION, "need world >= 2 handles");
-  for (int r = 0; r < world; ++r) {
-    if (!hs[r] || host_only(hs[r])) return fail(SPCHOL_ERR_VALIDATION, "NULL or host-only handle");
-    if (hs[r]->world != world || hs[r]->rank != r || hs[r]->opt.device != hs[0]->opt.device ||
-        hs[r]->panel_doubles != hs[0]->panel_doubles || hs[r]->markers.size() != hs[0]->markers.size())
-      return fail(SPCHOL_ERR_VALIDATION, "handles must be ranks 0..world-1 of one problem on one device");
-  }
-  const spchol_handle* h0 = hs[0];
-  if (marker < 0 || marker >= (int)h0->markers.size()) return fail(SPCHOL_ERR_VALIDATION, "marker out of range");
-  const Launch& M = h0->plan[h0->markers[marker]];
-  for (int r = 1; r < world; ++r) {
-    const Launch& Mr = hs[r]->plan[hs[r]->markers[marker]];
-    if (Mr.op != M.op || Mr.aux != M.aux || Mr.aux2 != M.aux2) return fail(SPCHOL_ERR_STATE, "marker sequences differ between ranks");
-  }
-  CK(cudaSetDevice(h0->opt.device));
-  for (int r = 0; r < world; ++r) CK(cudaStreamSynchronize(hs[r]->stream));
-  const int W = h0->outer * h0->nb;
-  auto block = [&](int r, int J, int C, long long& cnt) {
-    const SnInfo& I = hs[r]->sn[J];
-    const int c0 = h0->top_dist[J] ? C * W : 0, nc = h0->top_dist[J] ? std::min(W, I.k - c0) : I.k;
-    cnt = (long long)I.ld * nc;
-    return hs[r]->d_panels + I.off + (size_t)c0 * I.ld;
-  };
-  if (M.op == OP_TOP_LEVEL) {          // per block column: sum onto the owner, other copies zeroed
-    for (int P : h0->top_by_level[M.aux])
-      for (int C = 0; C * W < h0->sn[P].k; ++C) {
-        const int o = blk_owner(h0, P, C);
-        long long cnt = 0;
-        double* dst = block(o, P, C, cnt);
-        for (int r = 0; r < world; ++r) {
-          if (r == o) continue;
-          double* src = block(r, P, C, cnt);
-          launch_axpy(src, dst, cnt, hs[o]->stream);
-          CK(cudaStreamSynchronize(hs[o]->stream));
-          CK(cudaMemset(src, 0, sizeof(double) * (size_t)cnt));
-        }
-        if (!h0->top_dist[P]) break;
-      }
-  } else {                             // OP_BCAST: owner's block column to the rest of the group
-    const int J = M.aux, C = M.aux2, o = blk_owner(h0, J, C);
-    long long cnt = 0;
-    const double* src = block(o, J, C, cnt);
-    for (int q = h0->grp_lo[J]; q < h0->grp_hi[J]; ++q)
-      if (q != o) CK(cudaMemcpy(block(q, J, C, cnt), src, sizeof(double) * (size_t)cnt, cudaMemcpyDeviceToDevice));
-  }
-  CK(cudaGetLastError());
-  CK(cudaDeviceSynchronize());
+  if (top_off) *top_off = h->world > 1 ? h->sub_off[h->world] : h->panel_doubles;
+  if (top_slot) *top_slot = h->world > 1 ? h->slot_sub[h->world] : h->nslots_total;
   return SPCHOL_OK;
 }
 

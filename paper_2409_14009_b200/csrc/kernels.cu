@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const G
                                                             const double* __restrict__ linv,
                                                             const long long* __restrict__ ucol_base,
                                                             const long long* __restrict__ ucol_map,
-                                                            const int* __restrict__ posmap) {
+                                                            const int* __restrict__ posmap, int kw_log2) {
   pdl_enter();
   extern __shared__ __align__(16) double smem[];
   double* sA = smem;
@@ -190,10 +190,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const G
     A = panels + S.off + (long long)T.c0 * S.ld + T.r0;
     B = linv + (long long)T.slot * (NBMAX * NBMAX);
     lda = S.ld; ldb = NBMAX; arows = S.m - T.r0; brows = T.nb; K = T.nb;
-  } else {   // MODE_SCATTER and MODE_RLB: rows of U_J, all k columns
+  } else {   // MODE_SCATTER(_DET / _KS) and MODE_RLB: rows of U_J, all k columns (KS: T.nb owned blocks)
     A = panels + S.off + T.r0;
     B = panels + S.off + T.s0;
-    lda = ldb = S.ld; arows = S.m - T.r0; brows = S.m - T.s0; K = S.k;
+    lda = ldb = S.ld; arows = S.m - T.r0; brows = S.m - T.s0;
+    K = MODE == MODE_SCATTER_KS ? (T.nb << kw_log2) : S.k;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
@@ -223,9 +224,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, SPCHOL_MINB) gemm_kernel(const G
   }
   const long long stepA = (long long)BK * lda, stepB = (long long)BK * ldb;
   auto load_chunk = [&](int chunk, int stage) {
-    const int kc = chunk * BK;
     double* dA = sA + stage * BK * LDS;
     double* dB = sB + stage * BK * LDS;
+    if (MODE == MODE_SCATTER_KS) {
+      // chunk -> column of the rank's i-th owned block: c0 + i * slot + (chunk mod chunks per block) * BK
+      const int cpb_log2 = kw_log2 - (BK == 8 ? 3 : 4);
+      const int kcol = T.c0 + (chunk >> cpb_log2) * T.slot + (chunk & ((1 << cpb_log2) - 1)) * BK;
+      const long long oa = (long long)kcol * lda;
+#pragma unroll
+      for (int i = 0; i < NP; ++i) {
+        const bool kval = kcol + kkp[i] < S.k;
+        cp_async16(dA + dofs[i], kval && byA[i] ? srcA[i] + oa : A, kval ? byA[i] : 0);
+        cp_async16(dB + dofs[i], kval && byB[i] ? srcB[i] + oa : B, kval ? byB[i] : 0);
+      }
+      return;
+    }
+    const int kc = chunk * BK;
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
       const bool kval = kc + kkp[i] < K;
@@ -1182,9 +1196,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS) solve_fwd_level_kernel(
   const int q = T.q0 + lane;
   const bool rowok = q < T.q1;
   const double* Pq = panels + S.off + q;
-  const int ncb = tri ? T.cb : (S.k + NB - 1) / NB;
+  const int ncb = tri ? T.cb : T.cbhi;
   double acc = 0.0;
-  for (int cb = 0; cb < ncb; ++cb) {
+  for (int cb = T.cblo; cb < ncb; ++cb) {
     const int nbc = min(NB, S.k - cb * NB);
     const double* Lc = Pq + (long long)(cb * NB) * S.ld;
     double lv[16];
@@ -1264,8 +1278,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 2) solve_bwd_level_kernel(
       }
     }
   } else {
-    const int nblk = (S.k + NB - 1) / NB;
-    for (int rb = nblk - 1; rb > T.cb; --rb) {
+    for (int rb = T.cbhi - 1; rb > T.cb; --rb) {
       const int nbr = min(NB, S.k - rb * NB);
       const int r = rb * NB + lane;
       const bool ok = lane < nbr;
@@ -1331,9 +1344,18 @@ __global__ void permute_kernel(const int* __restrict__ perm, const double* __res
   }
 }
 
+__global__ void permute_masked_kernel(const int* __restrict__ perm, const unsigned char* __restrict__ mine,
+                                      const double* __restrict__ in, double* out, long long n, int inverse) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int r = perm[i];
+    if (inverse) out[i] = mine[r] ? in[r] : 0.0;
+    else out[r] = mine[r] ? in[i] : 0.0;
+  }
+}
+
 __global__ void gather_kernel(const double* __restrict__ src, const long long* __restrict__ idx, double* out, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    out[i] = src[idx[i]];
+    out[i] = idx[i] >= 0 ? src[idx[i]] : 0.0;   // idx < 0: entry held by another rank (multi-GPU)
 }
 
 // ---------------------------------------------------------------------------------------------- launchers
@@ -1352,6 +1374,7 @@ cudaError_t kernels_init_attributes() {
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_TRSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_SCATTER>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_SCATTER_DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(gemm_kernel<MODE_SCATTER_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   return cudaSuccess;
 }
 
@@ -1394,22 +1417,46 @@ void launch_gemm_tma(int mode, const GTask* tasks, int ntasks, const SnInfo* sn,
 
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels, const double* linv,
                  const long long* ucol_base, const long long* ucol_map, const int* posmap, cudaStream_t st, int prio,
-                 int min_smem) {
+                 int min_smem, int kw_log2) {
   if (ntasks <= 0) return;
   if (mode == MODE_LOCAL)
-    launch_prio(gemm_kernel<MODE_LOCAL>, ntasks, GEMM_THREADS, std::max(GEMM_SMEM, min_smem), st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
+    launch_prio(gemm_kernel<MODE_LOCAL>, ntasks, GEMM_THREADS, std::max(GEMM_SMEM, min_smem), st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap, 0);
   else if (mode == MODE_TRSM)
-    launch_prio(gemm_kernel<MODE_TRSM>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
+    launch_prio(gemm_kernel<MODE_TRSM>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap, 0);
   else if (mode == MODE_SCATTER_DET)
-    launch_prio(gemm_kernel<MODE_SCATTER_DET>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
+    launch_prio(gemm_kernel<MODE_SCATTER_DET>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap, 0);
+  else if (mode == MODE_SCATTER_KS)
+    launch_prio(gemm_kernel<MODE_SCATTER_KS>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap, kw_log2);
   else
-    launch_prio(gemm_kernel<MODE_SCATTER>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap);
+    launch_prio(gemm_kernel<MODE_SCATTER>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, tasks, sn, panels, linv, ucol_base, ucol_map, posmap, 0);
+}
+
+// Extend-add of the multi-GPU exchange (see XTask): one CTA per task, a warp per column, lanes over
+// consecutive rows (coalesced reads of the run, runs of consecutive destination rows).
+__global__ void __launch_bounds__(256) extend_add_kernel(const XTask* __restrict__ tasks, const long long* __restrict__ col,
+                                                         const int* __restrict__ pos, double* panels) {
+  const XTask T = tasks[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < T.nc; c += 8) {
+    const int j = T.c0 + c;
+    const double* s = panels + T.src + (long long)j * T.ld;
+    double* d = panels + col[T.col + j];
+    const int* p = pos + T.pos;
+    for (int i = j + lane; i < T.nrow; i += 32) {
+      const double v = s[i];
+      if (v != 0.0) atomicAdd(d + p[i], v);
+    }
+  }
+}
+void launch_extend_add(const XTask* tasks, int ntasks, const long long* col, const int* pos, double* panels,
+                       cudaStream_t st) {
+  if (ntasks > 0) extend_add_kernel<<<ntasks, 256, 0, st>>>(tasks, col, pos, panels);
 }
 
 void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio) {
   if (ntasks <= 0) return;
   launch_prio(gemm_kernel<MODE_RLB>, ntasks, GEMM_THREADS, GEMM_SMEM, st, prio, reinterpret_cast<const GTask*>(tasks), sn,
-              panels, (const double*)nullptr, (const long long*)nullptr, (const long long*)nullptr, (const int*)nullptr);
+              panels, (const double*)nullptr, (const long long*)nullptr, (const long long*)nullptr, (const int*)nullptr, 0);
 }
 
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels, double* linv,
@@ -1493,6 +1540,13 @@ void launch_permute(const int* perm, const double* in, double* out, long long n,
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   permute_kernel<<<(int)blocks, 256, 0, st>>>(perm, in, out, n, inverse);
+}
+void launch_permute_masked(const int* perm, const unsigned char* mine, const double* in, double* out, long long n,
+                           int inverse, cudaStream_t st) {
+  if (n <= 0) return;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  permute_masked_kernel<<<(int)blocks, 256, 0, st>>>(perm, mine, in, out, n, inverse);
 }
 
 }  // namespace spchol

@@ -43,12 +43,27 @@ struct RTask {
 // kind 2: backward, column block cb against rows [q0, q1) >= k (partial dot products, RED into y_cb);
 // kind 3: backward, triangle column block cb (waits for `need` kind-2 chunks and the blocks > cb).
 // slot = diagonal-inverse slot of block cb (slot - cb = slot of block 0 = the flag base).
+// cblo / cbhi bound the column blocks a task sums over (single GPU: 0 / all blocks; the distributed
+// top solve restricts them to one rank's outer block column): kind 0 sums cb in [cblo, cb), kind 1
+// cb in [cblo, cbhi), kind 3 rb in (cb, cbhi).
 struct STask {
-  int sn, kind, cb, nb, q0, q1, slot, need;
+  int sn, kind, cb, nb, q0, q1, slot, need, cblo, cbhi;
 };
 // MODE_SCATTER_DET: MODE_SCATTER with plain RMW stores (deterministic mode: the launch's supernodes are
 // column-conflict free, so no two CTAs of the launch touch one ancestor entry).
-enum { MODE_LOCAL = 0, MODE_TRSM = 1, MODE_SCATTER = 2, MODE_RLB = 3, MODE_SCATTER_DET = 4 };
+// MODE_SCATTER_KS (multi-GPU, distributed top supernode): MODE_SCATTER over this rank's share of the
+// K columns only — the owned outer block columns c0 + i * slot (i < nb), kw columns each — so the
+// group's partial U_J sum to U_J (P:307 with the sum over the columns of L_J split by owner).
+enum { MODE_LOCAL = 0, MODE_TRSM = 1, MODE_SCATTER = 2, MODE_RLB = 3, MODE_SCATTER_DET = 4, MODE_SCATTER_KS = 5 };
+// Extend-add task (multi-GPU exchange): columns [c0, c0 + nc) of one received (or local) update
+// run — a column-major nrow x ncol block at src (ld), whose row i / column j are rows / columns
+// j0 + i / j0 + j of the source's update row set — are added into the owner's panel: entry (i, j),
+// i >= j, goes to panels[col[j] + pos[i]] (col = column start inside the destination supernode,
+// pos = row position in its rows(P)).  FP64 RED: several sources hit one entry.
+struct XTask {
+  long long src, col, pos;
+  int ld, nrow, c0, nc;
+};
 
 constexpr int TILE = 64;           // CTA tile edge (rows and columns)
 #ifndef SPCHOL_MINB
@@ -70,7 +85,9 @@ constexpr int NBMAX = 64;          // cdiv block width
 
 void launch_gemm(int mode, const GTask* tasks, int ntasks, const SnInfo* sn, double* panels,
                  const double* linv, const long long* ucol_base, const long long* ucol_map,
-                 const int* posmap, cudaStream_t st, int prio = 0, int min_smem = 0);
+                 const int* posmap, cudaStream_t st, int prio = 0, int min_smem = 0, int kw_log2 = 0);
+void launch_extend_add(const XTask* tasks, int ntasks, const long long* col, const int* pos, double* panels,
+                       cudaStream_t st);
 #ifndef SPCHOL_TBK
 #define SPCHOL_TBK 16
 #endif
@@ -124,6 +141,9 @@ void launch_solve_bwd_level(const STask* tasks, int ntasks, int* ticket, int* fl
                             const int* sfirst, const long long* rows_ptr, const int* rows, const double* panels,
                             const double* linv, double* y, int NB, cudaStream_t st);
 void launch_permute(const int* perm, const double* in, double* out, long long n, int inverse, cudaStream_t st);
+// multi-GPU solve: as launch_permute, entries whose final row r has mine[r] == 0 become 0
+void launch_permute_masked(const int* perm, const unsigned char* mine, const double* in, double* out, long long n,
+                           int inverse, cudaStream_t st);
 void launch_axpy(const double* x, double* y, long long n, cudaStream_t st);
 void launch_gather(const double* src, const long long* idx, double* out, long long n, cudaStream_t st);
 cudaError_t kernels_init_attributes();

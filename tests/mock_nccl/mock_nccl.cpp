@@ -1,9 +1,11 @@
 // Test double for NCCL: every rank of a communicator is a thread of ONE process driving the same
 // GPU (gpurun boxes have one GPU; NCCL refuses two ranks on one device).  Loaded by libspchol.so
 // in place of libnccl.so.2 when SPCHOL_NCCL_LIB points here (tests/test_gpu_parity.py), so the
-// library's real multi-GPU code path — communicator splits, the level-start reduces, the
-// block-column broadcasts, the final gathers, in the order enqueue_factor issues them — runs
-// unchanged.  Semantics are blocking: a call synchronizes the caller's stream, meets the other
+// library's real multi-GPU code path — communicator splits, the grouped send/recv exchanges of the
+// update blocks, the block-column broadcasts, the solve's reduces / broadcasts / all-reduce, in the
+// order the library issues them — runs unchanged.  Point-to-point calls inside ncclGroupStart/End
+// are deferred to ncclGroupEnd, which posts every send before it waits for any receive (the NCCL
+// group semantics that make an all-to-all exchange deadlock-free).  Semantics are blocking: a call synchronizes the caller's stream, meets the other
 // members of its communicator at a rendezvous keyed by (communicator, call sequence number), the
 // last arrival moves the data through host memory, and everyone returns.  Calls issued in a
 // different order on different ranks deadlock here exactly as they would under NCCL (the test
@@ -17,6 +19,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 namespace {
@@ -39,6 +42,7 @@ struct Comm {
   std::shared_ptr<Group> g;
   int rank = 0;
   long long seq = 0;
+  std::map<int, long long> sseq, rseq;   // point-to-point sequence numbers per peer
 };
 std::mutex mu;
 std::condition_variable cv;
@@ -81,6 +85,9 @@ int rendezvous(Comm* c, Fill fill, Act act) {
 }
 
 int sync(cudaStream_t st) { return cudaStreamSynchronize(st) == cudaSuccess ? 0 : 1; }
+// cudaMemcpy device-to-device returns before the copy has finished (it runs on the legacy default
+// stream, which the library's non-blocking streams do not wait for): wait for it explicitly.
+void d2d_done() { cudaStreamSynchronize(0); }
 
 void reduce_into(Slot& sl, int n, size_t cnt, int type, int op, void* dst) {
   std::vector<double> acc(cnt, 0.0), tmp(cnt);
@@ -159,6 +166,7 @@ extern "C" int ncclAllReduce(const void* sendbuff, void* recvbuff, size_t count,
         cudaMalloc(&scratch, std::max<size_t>(1, count * type_size(type)));
         reduce_into(sl, n, count, type, op, scratch);
         for (int i = 0; i < n; ++i) cudaMemcpy(sl.recv[i], scratch, count * type_size(type), cudaMemcpyDeviceToDevice);
+        d2d_done();
         cudaFree(scratch);
       });
 }
@@ -174,6 +182,7 @@ extern "C" int ncclReduce(const void* sendbuff, void* recvbuff, size_t count, in
         cudaMalloc(&scratch, std::max<size_t>(1, count * type_size(type)));
         reduce_into(sl, c->g->n, count, type, op, scratch);
         cudaMemcpy(sl.recv[root], scratch, count * type_size(type), cudaMemcpyDeviceToDevice);
+        d2d_done();
         cudaFree(scratch);
       });
 }
@@ -188,13 +197,75 @@ extern "C" int ncclBroadcast(const void* sendbuff, void* recvbuff, size_t count,
         for (int i = 0; i < c->g->n; ++i)
           if (sl.recv[i] != sl.send[root])
             cudaMemcpy(sl.recv[i], sl.send[root], count * type_size(type), cudaMemcpyDeviceToDevice);
+        d2d_done();
       });
 }
 
-extern "C" int ncclSend(const void*, size_t, int, int, void*, cudaStream_t) { return 5; }   // unused by the library
-extern "C" int ncclRecv(void*, size_t, int, int, void*, cudaStream_t) { return 5; }
-extern "C" int ncclGroupStart() { return 0; }
-extern "C" int ncclGroupEnd() { return 0; }
+namespace {
+struct P2P { bool send; void* buf; size_t bytes; int peer; Comm* c; cudaStream_t st; };
+struct Mail { const void* buf; size_t bytes; bool taken = false; };
+// mailbox key: (group, src, dst, sequence number of that pair)
+std::map<std::tuple<Group*, int, int, long long>, Mail> mailbox;
+thread_local int group_depth = 0;
+thread_local std::vector<P2P> pending_p2p;
+
+int run_p2p(std::vector<P2P>& ops) {
+  for (auto& o : ops) if (sync(o.st)) return 1;
+  std::vector<std::tuple<Group*, int, int, long long>> mine;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& o : ops)
+      if (o.send) {
+        auto key = std::make_tuple(o.c->g.get(), o.c->rank, o.peer, o.c->sseq[o.peer]++);
+        mailbox[key] = Mail{o.buf, o.bytes, false};
+        mine.push_back(key);
+      }
+    cv.notify_all();
+  }
+  for (auto& o : ops) {
+    if (o.send) continue;
+    std::unique_lock<std::mutex> lk(mu);
+    auto key = std::make_tuple(o.c->g.get(), o.peer, o.c->rank, o.c->rseq[o.peer]++);
+    cv.wait(lk, [&] { return mailbox.count(key) > 0; });
+    Mail& m = mailbox[key];
+    if (m.bytes != o.bytes) return 2;
+    lk.unlock();
+    cudaMemcpy(o.buf, m.buf, o.bytes, cudaMemcpyDeviceToDevice);
+        d2d_done();
+    lk.lock();
+    mailbox[key].taken = true;
+    cv.notify_all();
+  }
+  std::unique_lock<std::mutex> lk(mu);
+  for (auto& key : mine) {   // the send buffers stay untouched until the receivers have copied them
+    cv.wait(lk, [&] { return mailbox[key].taken; });
+    mailbox.erase(key);
+  }
+  return 0;
+}
+int p2p(bool send, const void* buf, size_t count, int type, int peer, void* comm, cudaStream_t st) {
+  P2P o{send, const_cast<void*>(buf), count * type_size(type), peer, (Comm*)comm, st};
+  if (group_depth > 0) { pending_p2p.push_back(o); return 0; }
+  std::vector<P2P> one{o};
+  return run_p2p(one);
+}
+}  // namespace
+
+extern "C" int ncclSend(const void* buf, size_t count, int type, int peer, void* comm, cudaStream_t st) {
+  return p2p(true, buf, count, type, peer, comm, st);
+}
+extern "C" int ncclRecv(void* buf, size_t count, int type, int peer, void* comm, cudaStream_t st) {
+  return p2p(false, buf, count, type, peer, comm, st);
+}
+extern "C" int ncclGroupStart() { ++group_depth; return 0; }
+extern "C" int ncclGroupEnd() {
+  if (--group_depth > 0) return 0;
+  std::vector<P2P> ops;
+  ops.swap(pending_p2p);
+  return ops.empty() ? 0 : run_p2p(ops);
+}
+// marks this library as the blocking stand-in (libspchol.so then never graph-captures NCCL calls)
+extern "C" int spcholMockNcclBlocking() { return 1; }
 extern "C" int ncclCommDestroy(void* comm) {
   delete (Comm*)comm;
   return 0;

@@ -1,7 +1,8 @@
-"""Multi-GPU host-side logic on CPU: two gloo processes build host-only handles for ranks 0 and 1
-and check that the subtree-to-GPU mapping is identical on both ranks, partitions the
-supernodes into whole subtrees plus a top that is closed under ancestors, and lays the top panels
-out as one contiguous region (the phase-B all-reduce)."""
+"""Multi-GPU host-side logic on CPU: gloo processes build host-only handles for their ranks and check
+that the subtree-to-GPU mapping is identical on every rank, partitions the supernodes
+into whole subtrees plus a top that is closed under ancestors, lays each rank's subtree panels out
+as one region below the top panels, and that every rank's plan holds the same marker sequence and
+matching exchange volumes (what one rank sends, the others receive)."""
 import os
 import socket
 
@@ -32,6 +33,7 @@ def _worker(rank, world, port, name, q):
             owner, top_off, top_slot = h.spchol_export_mapping()
             sym = h.spchol_export_symbolic()
             off, ld, _ = h.spchol_export_panels(values=False)
+            h_send, h_recv = h.query("COMM_SEND_BYTES"), h.query("COMM_RECV_BYTES")
         t = torch.from_numpy(owner.astype(np.int64))
         got = [torch.zeros_like(t) for _ in range(world)]
         dist.all_gather(got, t)
@@ -47,15 +49,22 @@ def _worker(rank, world, port, name, q):
             if owner[J] < 0 and P >= 0:
                 assert owner[P] < 0, "top is closed under ancestors"
         assert set(np.unique(owner[owner >= 0]).tolist()) <= set(range(world))
-        # top panels contiguous at the end of the arena
+        # per-rank arena layout: rank q's subtree panels form one region, all below the top panels
         k = np.diff(sym["sfirst"])
         sizes = ld.astype(np.int64) * k
         top = owner < 0
-        assert off[-1] - top_off == sizes[top].sum()
         if top.any():
-            assert off[:-1][top].min() == top_off
+            assert off[:-1][top].min() >= top_off
+        for rq in range(world):
+            mine = owner == rq
+            if mine.any() and (owner > rq).any():
+                assert (off[:-1][mine] + sizes[mine]).max() <= off[:-1][owner > rq].min()
         if (~top).any():
             assert (off[:-1][~top] + sizes[~top]).max() <= top_off
+        # exchange volumes: the bytes all ranks send equal the bytes all ranks receive
+        vol = torch.tensor([h_send, h_recv], dtype=torch.float64)
+        dist.all_reduce(vol)
+        assert vol[0].item() == vol[1].item()
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok", int(top.sum()), [int((owner == r).sum()) for r in range(world)]))
@@ -63,7 +72,7 @@ def _worker(rank, world, port, name, q):
         q.put((rank, f"error: {e!r}", 0, []))
 
 
-@pytest.mark.parametrize("name,world", [("S4", 2), ("C1", 2), ("S5", 2), ("S2", 3)])
+@pytest.mark.parametrize("name,world", [("S4", 2), ("C1", 2), ("S5", 2), ("S2", 3), ("S4", 4)])
 def test_mapping_two_process_gloo(name, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -95,32 +104,56 @@ def test_mapping_single_process_properties():
         sp.Solver.from_problem(p, device=-1, dist_world=2, dist_rank=2)
 
 
-def _plan_work(p, W, r):
-    with sp.Solver.from_problem(p, device=-1, dist_world=W, dist_rank=r) as h:
+def _plan_work(p, W, r, **opts):
+    with sp.Solver.from_problem(p, device=-1, dist_world=W, dist_rank=r, **opts) as h:
         a, lv = h.spchol_dist_plan_flops()
-        return a, lv, h.query("NMARKERS"), h.query("NTOP_DIST"), h.query("FLOPS_EXEC")
+        return (a, lv, h.query("NMARKERS"), h.query("NTOP_DIST"), h.query("FLOPS_EXEC"), h.query("COMM_SEND_BYTES"),
+                h.query("COMM_RECV_BYTES"), h.query("ARENA_BYTES"))
 
 
 @pytest.mark.parametrize("name,minflops,outer", [("S4", "0", None), ("S5", "0", "1"), ("C1", "0", "1"),
                                                   ("S4", None, None), ("S2", "0", "1")])
 def test_distributed_top_plan_partitions_work(name, minflops, outer, monkeypatch):
-    """Distributed top (block-column cyclic cdiv, U_J tiles split over the group): every task of the
-    single-GPU plan runs on exactly one rank — the executed flops of all ranks' plans (phase A + phase
-    C) add up to the whole factor's — and all ranks hold the same number of exchange markers."""
+    """Distributed top (block-column cyclic cdiv, K-split partial U_J): every flop of the single-GPU
+    plan runs on exactly one rank — the executed flops of all ranks' plans (phase A + phase C) add up
+    to the whole factor's — all ranks hold the same number of exchange markers, the bytes sent equal
+    the bytes received (the per-rank arena is checked at full size: 2 MB pages dominate here)."""
     if minflops is not None:
         monkeypatch.setenv("SPCHOL_DIST_MINFLOPS", minflops)
     if outer is not None:
         monkeypatch.setenv("SPCHOL_OUTER", outer)
     p = gen.make(name)
-    with sp.Solver.from_problem(p, device=-1) as h:
+    # every supernode on the blocked path on both sides (multi-GPU top supernodes always are), so the
+    # per-launch flop accounting is the same
+    with sp.Solver.from_problem(p, device=-1, small_max_k=-1) as h:
         whole, _ = h.spchol_dist_plan_flops()
     for W in (2, 3, 4, 8):
-        res = [_plan_work(p, W, r) for r in range(W)]
+        res = [_plan_work(p, W, r, small_max_k=-1) for r in range(W)]
         tot = sum(a + lv.sum() for a, lv, *_ in res)
         assert abs(tot - whole) <= 1e-9 * whole, (W, tot, whole)
-        assert len({m for _, _, m, _, _ in res}) == 1
-        if minflops == "0" and name != "C1":     # C1's top supernodes all take the fused small path
+        assert len({r_[2] for r_ in res}) == 1
+        assert sum(r_[5] for r_ in res) == sum(r_[6] for r_ in res)
+        if minflops == "0" and name != "C1":     # C1's top supernodes are below one outer block
             assert res[0][3] > 0
         # distributing the top never makes the critical rank path longer than the fan-in schedule
         crit = max(a for a, *_ in res) + sum(max(r_[1][l] for r_ in res) for l in range(len(res[0][1])))
         assert crit <= whole
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_fullsize_distribution_model(name):
+    """The north_star configs' multi-GPU plans (host-only, the driver's 2/4/8-GPU runs): exact work
+    partition, per-rank arena well below the single-GPU one, and the work model's speedup bound
+    (max over ranks of phase A + per top level max over ranks) above 6x at 8 ranks on C4."""
+    p = gen.make(name)
+    with sp.Solver.from_problem(p, device=-1) as h:
+        whole, _ = h.spchol_dist_plan_flops()
+        arena1 = h.query("ARENA_BYTES")
+    for W in (2, 4, 8):
+        res = [_plan_work(p, W, r) for r in range(W)]
+        assert abs(sum(a + lv.sum() for a, lv, *_ in res) - whole) <= 1e-9 * whole
+        crit = max(a for a, *_ in res) + sum(max(r_[1][l] for r_ in res) for l in range(len(res[0][1])))
+        if name == "C4" and W == 8:
+            assert whole / crit >= 6.0, whole / crit
+        assert max(r_[7] for r_ in res) <= arena1 * (1.5 / W + 0.2)

@@ -88,3 +88,24 @@ def test_fullsize_leading_block_factor(name, N):
     Lref = np.linalg.cholesky(A)
     err = np.abs(Lg - Lref).max() / np.abs(Lref).max()
     assert err <= 1e-10, err
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_fullsize_top_levels_llt(name):
+    """Exact-result check at full size where most of the flops live: for sampled
+    columns j of every supernode in the top three levels (the root chain and the largest separators),
+    every stored entry (L L^T)(i, j), i >= j, computed from the exported panels, equals C_f(i, j)
+    = (P_f A P_f^T)(i, j) to 1e-12 max|A| — independent of the oracle and of the kernels, in the bench
+    configuration (CUDA graph, replayed)."""
+    from helpers import llt_sample_error, top_level_columns
+    p = gen.make(name)
+    with sp.Solver.from_problem(p) as h:
+        h.spchol_factor()
+        h.spchol_factor()
+        sym = h.spchol_export_symbolic()
+        off, ld, pan = h.spchol_export_panels()
+    cols = top_level_columns(sym, nlev=3, per_sn=3)
+    err, cnt = llt_sample_error(p, sym, off, ld, pan, cols)
+    print(name, "sampled columns", len(cols), "entries", cnt, "max |LL^T - C_f| / max|A|", err)
+    assert cnt >= 10 ** 5 if name != "C3" else cnt >= 10 ** 4
+    assert err <= 1e-12, err

@@ -118,63 +118,6 @@ def test_edge_cases():
     run_parity(gen.from_dense_lower(D))
 
 
-@pytest.mark.parametrize("name,world,minflops,outer", [
-    ("S4", 2, None, None), ("S5", 3, None, None), ("C1", 2, None, None), ("S2", 4, None, None), ("T3", 2, None, None),
-    ("S4", 8, None, None),
-    # distributed top supernodes (block-column cyclic cdiv + block-column sends + U_J tiles split)
-    ("S4", 2, "0", None), ("S4", 4, "0", "1"), ("S5", 3, "0", "1"), ("S2", 4, "0", "1"), ("T3", 2, "0", "1"),
-    ("S4", 8, "0", "1"), ("S5", 8, "0", None)])
-def test_distributed_dataflow_single_gpu(name, world, minflops, outer, monkeypatch):
-    """The multi-GPU data flow played by `world` handles on one GPU through the diagnostics API:
-    phase A per rank; then phase C segment by segment, each exchange marker played between the
-    handles (spchol_dist_debug_comm: the level-start reduce of the top panels onto their block-column
-    owners, other copies zeroed; the send of a finished block column of a distributed top supernode to
-    its group); finally the gather (sum of all arenas and inverses).  The assembled factor must match
-    the oracle like the single-GPU one."""
-    if minflops is not None:
-        monkeypatch.setenv("SPCHOL_DIST_MINFLOPS", minflops)
-    if outer is not None:
-        monkeypatch.setenv("SPCHOL_OUTER", outer)
-    prob = gen.make(name)
-    o = oracle.Oracle.from_problem(prob)
-    assert o.factor() == -1
-    Lp, Li, Lx = o.L_csc()
-    hs = [sp.Solver.from_problem(prob, dist_world=world, dist_rank=r) for r in range(world)]
-    try:
-        for h in hs:
-            h.spchol_factor_phase(1)
-        owner, towner, _, _ = hs[0].spchol_export_mapping(with_top_owner=True)
-        assert np.all((owner >= 0) | (towner >= 0))
-        nm = hs[0].query("NMARKERS")
-        assert all(h.query("NMARKERS") == nm for h in hs)
-        if minflops == "0" and name in ("S2", "S4", "S5"):   # (C1's and T3's tops take the small path)
-            assert hs[0].query("NTOP_DIST") > 0
-        for i in range(nm):
-            for h in hs:
-                h.spchol_factor_phase(2000 + i)
-            sp.spchol_dist_debug_comm(hs, i)
-        for h in hs:
-            h.spchol_factor_phase(2000 + nm)
-        for h in hs[1:]:
-            hs[0].spchol_dist_debug_accumulate(h, 1)      # gather panels
-            hs[0].spchol_dist_debug_accumulate(h, 2)      # and diagonal inverses
-        hs[0].spchol_factor_phase(3)
-        s_gpu = hs[0].spchol_export_symbolic()
-        off, ld, pan = hs[0].spchol_export_panels()
-        idx = panel_index_of_pattern(s_gpu, off, ld, Lp, Li)
-        err = np.abs(pan[idx] - Lx).max() / np.abs(Lx).max()
-        assert err <= TOL_L, err
-        mask = lower_panel_mask(s_gpu, off, ld, len(pan))
-        mask[idx] = False
-        assert np.all(pan[mask] == 0.0)
-        xs, b = gen.rhs(prob)
-        x = hs[0].spchol_solve(b)
-        assert backward_error(prob, x, b) <= TOL_BERR
-    finally:
-        for h in hs:
-            h.close()
-
-
 @pytest.mark.parametrize("name", ["S3", "S4", "S5", "T2"])
 def test_parity_tma_tiles(name, monkeypatch):
     """The TMA + mbarrier variant of the tile kernels (SPCHOL_TMA=1): same parity bar."""
@@ -250,34 +193,64 @@ def test_parity_small_supernode_paths(name, env, monkeypatch):
     run_parity(gen.make(name), deterministic=1)
 
 
-@pytest.mark.parametrize("name,world,minflops,outer", [("S4", 2, "0", None), ("S4", 4, "0", "1"), ("S5", 3, "0", "1"),
-                                                       ("S2", 8, "0", "1"), ("T3", 2, None, None)])
-def test_distributed_nccl_path_mock(name, world, minflops, outer):
-    """The multi-GPU factor and solve through the library's real NCCL code path (communicator
-    splits per top rank group, level-start reduces, block-column broadcasts, final gathers), each
-    rank a thread on this GPU with NCCL replaced by a blocking single-process stand-in
-    (tests/mock_nccl): no hang (same call order on every rank), factor within the parity tolerance,
-    backward error within the bound, all ranks return the same solution."""
+def run_mock(name, world, env_extra=None, args=(), timeout=1800):
+    """Run tests/mock_dist_run.py (every rank a thread on this GPU, NCCL replaced by the blocking
+    single-process stand-in tests/mock_nccl) and return its JSON record."""
     import json
     import os
     import subprocess
     import sys
     env = dict(os.environ)
+    env.update(env_extra or {})
+    here = os.path.dirname(os.path.abspath(__file__))
+    assert os.path.exists(os.path.join(here, "mock_nccl", "libmocknccl.so")), "build it with make"
+    p = subprocess.run([sys.executable, os.path.join(here, "mock_dist_run.py"), name, str(world), *map(str, args)],
+                       env=env, capture_output=True, text=True, timeout=timeout)
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert lines, p.stdout[-2000:] + p.stderr[-2000:]
+    return json.loads(lines[-1])
+
+
+@pytest.mark.parametrize("name,world,minflops,outer", [
+    ("S4", 2, None, None), ("S5", 3, None, None), ("C1", 2, None, None), ("S2", 4, None, None), ("T3", 2, None, None),
+    ("S4", 8, None, None),
+    # distributed top supernodes (block-column cyclic cdiv, broadcasts, K-split partial U_J)
+    ("S4", 2, "0", None), ("S4", 4, "0", "1"), ("S5", 3, "0", "1"), ("S2", 4, "0", "1"), ("T3", 2, "0", "1"),
+    ("S4", 8, "0", "1"), ("S5", 8, "0", None), ("S3", 5, "0", "1"), ("S2", 8, "0", "1")])
+def test_distributed_nccl_path_mock(name, world, minflops, outer):
+    """The multi-GPU factor and solve through the library's real NCCL code path (communicator
+    splits per top rank group, grouped send/recv of the update runs + extend-add, block-column
+    broadcasts, the solve's per-block reduces / broadcasts and final all-reduce), each rank a thread
+    on this GPU with its own per-rank arena: no hang (same call order on every rank), the sum of the
+    ranks' panel exports matches the oracle with every padding entry exactly 0, backward error
+    within the bound, every rank returns the same solution, two factor + solve rounds."""
+    env = {}
     if minflops is not None:
         env["SPCHOL_DIST_MINFLOPS"] = minflops
     if outer is not None:
         env["SPCHOL_OUTER"] = outer
-    here = os.path.dirname(os.path.abspath(__file__))
-    assert os.path.exists(os.path.join(here, "mock_nccl", "libmocknccl.so")), "build it with make"
-    p = subprocess.run([sys.executable, os.path.join(here, "mock_dist_run.py"), name, str(world)], env=env,
-                       capture_output=True, text=True, timeout=900)
-    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
-    assert lines, p.stdout[-2000:] + p.stderr[-2000:]
-    r = json.loads(lines[-1])
+    r = run_mock(name, world, env)
     assert r["ok"], r
     assert r["lerr"] <= TOL_L and r["berr"] <= TOL_BERR and r["ranks_agree"], r
-    if minflops == "0":
+    assert r["padding_nonzeros"] == 0, r
+    if minflops == "0" and name not in ("T3",):
         assert r["ntop_dist"] > 0
+
+
+@pytest.mark.parametrize("name,world", [("C4", 2), ("C4", 4), ("C4", 8), ("C5", 2), ("C5", 4)])
+def test_distributed_fullsize_mock(name, world):
+    """The north_star's multi-GPU configs (C4 at 2/4/8 ranks, C5 at 2/4) through the real NCCL code
+    path on one GPU (ranks as threads, per-rank arenas): log det of the grid operator from its
+    closed-form eigenvalues (the whole diagonal of L), backward error, all ranks agree, and the
+    exact-result check (L L^T)(i, j) = C_f(i, j) on sampled columns of the top three levels — the
+    distributed supernodes — with the panels summed over the ranks' exports."""
+    r = run_mock(name, world, {"MOCK_FULL": "1"}, timeout=3600)
+    assert r["ok"], r
+    assert r["logdet_rel_err"] <= 1e-10, r
+    assert r["berr"] <= TOL_BERR and r["ranks_agree"], r
+    assert r["llt_err"] <= 1e-12 and r["llt_entries"] >= 10 ** 5, r
+    assert r["ntop_dist"] > 0
+    print(name, world, {k: r[k] for k in ("factor_s", "arena_bytes", "send_bytes", "recv_bytes", "llt_err")})
 
 
 @pytest.mark.parametrize("name", ["S3", "S4", "S5"])
@@ -310,17 +283,5 @@ def test_distributed_not_spd_mock(name, world, frac, minflops):
     """A failing pivot on one rank (in a subtree or in a distributed top supernode): every rank
     reports the sequential first failing column (all-reduce(min) of the fail flags) through the
     real NCCL code path over the single-process stand-in."""
-    import json
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ)
-    if minflops is not None:
-        env["SPCHOL_DIST_MINFLOPS"] = minflops
-    here = os.path.dirname(os.path.abspath(__file__))
-    p = subprocess.run([sys.executable, os.path.join(here, "mock_dist_run.py"), name, str(world), str(frac)], env=env,
-                       capture_output=True, text=True, timeout=900)
-    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
-    assert lines, p.stdout[-2000:] + p.stderr[-2000:]
-    r = json.loads(lines[-1])
+    r = run_mock(name, world, {"SPCHOL_DIST_MINFLOPS": minflops} if minflops is not None else {}, args=(frac,))
     assert r["ok"], r
