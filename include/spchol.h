@@ -192,7 +192,10 @@ enum {
   SPCHOL_Q_COMM_RECV_BYTES = 21, /* multi-GPU: bytes this rank receives per factor                      */
   SPCHOL_Q_ARENA_BYTES = 22,  /* physical device bytes of this rank's panels + inverses (+ broadcast
                                  ring, update and receive regions under multi-GPU); host-only too    */
-  SPCHOL_Q_DIST_GRAPH = 23    /* multi-GPU: 1 if the factor (with its NCCL calls) replays as a CUDA graph */
+  SPCHOL_Q_DIST_GRAPH = 23,   /* multi-GPU: 1 if the factor (with its NCCL calls) replays as a CUDA graph */
+  SPCHOL_Q_COMM_B_SEND_BYTES = 24, /* multi-GPU: bytes this rank sends in the boundary-block exchange
+                                      after phase A (SURVEY §8(e) phase B); host-only too               */
+  SPCHOL_Q_COMM_B_RECV_BYTES = 25  /* ... receives in it                                                 */
 };
 int spchol_query(const spchol_handle* h, int key, int64_t* value);
 

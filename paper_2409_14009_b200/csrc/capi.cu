@@ -1394,6 +1394,8 @@ extern "C" int spchol_query(const spchol_handle* h, int key, int64_t* value) {
       break;
     }
     case SPCHOL_Q_DIST_GRAPH: *value = h->graph_dist ? 1 : 0; break;
+    case SPCHOL_Q_COMM_B_SEND_BYTES: *value = (int64_t)h->comm_b_send; break;
+    case SPCHOL_Q_COMM_B_RECV_BYTES: *value = (int64_t)h->comm_b_recv; break;
     case SPCHOL_Q_NTOP_DIST: {
       int64_t c = 0;
       for (char d : h->top_dist) c += d != 0;

@@ -295,13 +295,13 @@ void dist_exchange_plan(spchol_handle* h) {
   if (h->upd_doubles) h->vregions.push_back({h->upd_off, h->upd_doubles, -1});
   if (h->recv_doubles) h->vregions.push_back({h->recv_off, h->recv_doubles, -1});
   // communication volume of this rank per factor (exchanges + broadcasts)
-  h->comm_send = h->comm_recv = 0;
+  h->comm_send = h->comm_recv = h->comm_b_send = h->comm_b_recv = 0;
   for (const XRun& X : h->xrun) {
     const double by = 8.0 * X.ld * (X.j1 - X.j0);
-    const int src = h->xblk[X.blk].src;
-    if (src == X.dst) continue;
-    if (src == r) h->comm_send += by;
-    if (X.dst == r) h->comm_recv += by;
+    const XBlk& B = h->xblk[X.blk];
+    if (B.src == X.dst) continue;
+    if (B.src == r) { h->comm_send += by; if (B.exch == 0) h->comm_b_send += by; }
+    if (X.dst == r) { h->comm_recv += by; if (B.exch == 0) h->comm_b_recv += by; }
   }
   for (int J = 0; J < ns; ++J) {
     if (!h->top_dist[J] || !in_group(h, J, r)) continue;

@@ -187,6 +187,7 @@ struct spchol_handle {
   std::vector<long long> xt_off, xcol;
   std::vector<int> xpos;
   double comm_send = 0, comm_recv = 0; // bytes per factor, this rank (exchanges + broadcasts)
+  double comm_b_send = 0, comm_b_recv = 0;   // ... of the boundary-block exchange after phase A
   int ring_ns = 3;                     // ring slots per distributed top supernode
   // distributed solve
   std::vector<spchol::TStep> tsteps;
