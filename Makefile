@@ -15,7 +15,7 @@ gen/libgen.so: gen/gen.c
 
 oracle: oracle/liboracle.so
 oracle/liboracle.so: oracle/oracle.c
-	gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC -o $@ $< -lm
+	gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC -pthread -o $@ $< -lm
 
 SPCHOL_SRC := $(wildcard $(CSRC)/*.cu) $(wildcard $(CSRC)/*.cpp)
 SPCHOL_HDR := $(wildcard $(CSRC)/*.h) $(wildcard $(CSRC)/*.cuh) include/spchol.h

@@ -34,6 +34,8 @@ def lib():
                                    ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_int]
         L.orc_numeric.restype = ctypes.c_int
         L.orc_numeric.argtypes = [ctypes.c_void_p, _I64]
+        L.orc_numeric_parallel.restype = ctypes.c_int
+        L.orc_numeric_parallel.argtypes = [ctypes.c_void_p, ctypes.c_int, _I64]
         L.orc_solve.restype = ctypes.c_int
         L.orc_solve.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.orc_free.restype = None
@@ -140,9 +142,14 @@ class Oracle:
                                self._arr("merge_cost", nm, np.int64).tolist()))
         return d
 
-    def factor(self):
+    def factor(self, threads=None):
+        """O9.  threads=None: the serial build; threads=T: the level-parallel build on T threads
+        (bit-identical L, the separately timed CPU baseline)."""
         fc = ctypes.c_int64(-1)
-        rc = self._L.orc_numeric(self._h, ctypes.byref(fc))
+        if threads is None:
+            rc = self._L.orc_numeric(self._h, ctypes.byref(fc))
+        else:
+            rc = self._L.orc_numeric_parallel(self._h, int(threads), ctypes.byref(fc))
         if rc == -3:
             return int(fc.value)
         if rc != 0:

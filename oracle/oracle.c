@@ -596,6 +596,146 @@ int orc_numeric(orc_t* o, int64_t* fail_col) {
   return rc;
 }
 
+/*
+ * O9, level-parallel build (the separately timed CPU baseline, SURVEY §8(d) "oracle-timed"): the
+ * same scalar column computation as orc_numeric — w = C_f(:,j); for every k < j with L(j,k) != 0,
+ * ascending, w -= L(:,k) L(j,k); pivot; scale — so every column is computed with the same
+ * operations in the same order and L is bit-identical to the serial build.  Columns of equal
+ * height in the elimination tree depend only on lower heights, so each height level is
+ * split over nthreads POSIX threads (dynamic column assignment, one private accumulator each).
+ * Returns as orc_numeric; *fail_col = the smallest failing column (the serial first failure:
+ * a column computed from a failed one is larger, it is an ancestor).
+ */
+#include <pthread.h>
+typedef struct {
+  orc_t* o;
+  const int64_t* rp; const int32_t* rk; const int64_t* rpos;   /* row lists: (k, position of j in column k) */
+  const int32_t* lvl_cols; int64_t lo, hi;                    /* current level's columns */
+  int64_t next;                                               /* next column index (atomic) */
+  int64_t fail;                                               /* smallest failing column so far */
+  pthread_mutex_t mu;
+  pthread_barrier_t bar_start, bar_end;
+  int stop;
+} par_t;
+typedef struct { par_t* P; double* w; } par_arg_t;
+
+static void par_column(par_t* P, double* w, int64_t j) {
+  orc_t* o = P->o;
+  const int64_t* Lp = o->Lp; const int32_t* Li = o->Li; double* Lx = o->Lx;
+  for (int64_t p = o->Cp[j]; p < o->Cp[j + 1]; ++p) w[o->Ci[p]] = o->Cx[p];
+  for (int64_t a = P->rp[j]; a < P->rp[j + 1]; ++a) {
+    int32_t k = P->rk[a];
+    int64_t pk = P->rpos[a];          /* Li[pk] == j */
+    double ljk = Lx[pk];
+    for (int64_t p = pk; p < Lp[k + 1]; ++p) w[Li[p]] -= Lx[p] * ljk;
+  }
+  double d = w[j];
+  w[j] = 0.0;
+  if (!(d > 0.0)) {
+    pthread_mutex_lock(&P->mu);
+    if (P->fail < 0 || j < P->fail) P->fail = j;
+    pthread_mutex_unlock(&P->mu);
+    for (int64_t p = Lp[j] + 1; p < Lp[j + 1]; ++p) w[Li[p]] = 0.0;
+    Lx[Lp[j]] = NAN;
+    for (int64_t p = Lp[j] + 1; p < Lp[j + 1]; ++p) Lx[p] = NAN;
+    return;
+  }
+  double ljj = sqrt(d);
+  Lx[Lp[j]] = ljj;
+  for (int64_t p = Lp[j] + 1; p < Lp[j + 1]; ++p) { Lx[p] = w[Li[p]] / ljj; w[Li[p]] = 0.0; }
+}
+
+static void* par_worker(void* arg) {
+  par_arg_t* A = (par_arg_t*)arg;
+  par_t* P = A->P;
+  for (;;) {
+    pthread_barrier_wait(&P->bar_start);
+    if (P->stop) break;
+    for (;;) {
+      int64_t i = __atomic_fetch_add(&P->next, 1, __ATOMIC_RELAXED);
+      if (i >= P->hi) break;
+      par_column(P, A->w, P->lvl_cols[i]);
+    }
+    pthread_barrier_wait(&P->bar_end);
+  }
+  return NULL;
+}
+
+int orc_numeric_parallel(orc_t* o, int nthreads, int64_t* fail_col) {
+  int64_t n = o->n;
+  *fail_col = -1;
+  if (!o->Lp || !o->Cx) return -2;
+  if (nthreads < 1) nthreads = 1;
+  if (!o->Lx) o->Lx = (double*)malloc(sizeof(double) * (size_t)(o->Lp[n] ? o->Lp[n] : 1));
+  const int64_t* Lp = o->Lp; const int32_t* Li = o->Li;
+  /* row lists of L (k ascending, as the serial build takes them) */
+  int64_t* rp = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+  for (int64_t k = 0; k < n; ++k) for (int64_t p = Lp[k] + 1; p < Lp[k + 1]; ++p) rp[Li[p] + 1]++;
+  for (int64_t j = 0; j < n; ++j) rp[j + 1] += rp[j];
+  int32_t* rk = (int32_t*)malloc(sizeof(int32_t) * (size_t)(rp[n] ? rp[n] : 1));
+  int64_t* rpos = (int64_t*)malloc(sizeof(int64_t) * (size_t)(rp[n] ? rp[n] : 1));
+  int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+  for (int64_t j = 0; j < n; ++j) fill[j] = rp[j];
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t p = Lp[k] + 1; p < Lp[k + 1]; ++p) { int32_t i = Li[p]; rk[fill[i]] = (int32_t)k; rpos[fill[i]++] = p; }
+  /* etree heights (parent > child), columns grouped by height */
+  int32_t* h = (int32_t*)calloc((size_t)n + 1, sizeof(int32_t));
+  int32_t H = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    int32_t par = o->parent_final[j];
+    if (par >= 0 && h[par] < h[j] + 1) h[par] = h[j] + 1;
+    if (h[j] + 1 > H) H = h[j] + 1;
+  }
+  int64_t* lp = (int64_t*)calloc((size_t)H + 1, sizeof(int64_t));
+  for (int64_t j = 0; j < n; ++j) lp[h[j] + 1]++;
+  for (int32_t l = 0; l < H; ++l) lp[l + 1] += lp[l];
+  int32_t* cols = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  for (int64_t j = 0; j < n; ++j) fill[j] = 0;
+  {
+    int64_t* nx = (int64_t*)malloc(sizeof(int64_t) * (size_t)(H + 1));
+    for (int32_t l = 0; l <= H; ++l) nx[l] = lp[l];
+    for (int64_t j = 0; j < n; ++j) cols[nx[h[j]]++] = (int32_t)j;
+    free(nx);
+  }
+  par_t P;
+  memset(&P, 0, sizeof(P));
+  P.o = o; P.rp = rp; P.rk = rk; P.rpos = rpos; P.lvl_cols = cols; P.fail = -1;
+  pthread_mutex_init(&P.mu, NULL);
+  pthread_barrier_init(&P.bar_start, NULL, (unsigned)nthreads);
+  pthread_barrier_init(&P.bar_end, NULL, (unsigned)nthreads);
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
+  par_arg_t* args = (par_arg_t*)malloc(sizeof(par_arg_t) * (size_t)nthreads);
+  for (int t = 0; t < nthreads; ++t) {
+    args[t].P = &P;
+    args[t].w = (double*)calloc((size_t)n + 1, sizeof(double));
+    if (t > 0) pthread_create(&th[t], NULL, par_worker, &args[t]);
+  }
+  for (int32_t l = 0; l < H; ++l) {
+    P.lo = lp[l]; P.hi = lp[l + 1]; P.next = lp[l];
+    if (nthreads == 1 || P.hi - P.lo == 1) {   /* a chain column: no hand-off */
+      for (int64_t i = P.lo; i < P.hi; ++i) par_column(&P, args[0].w, cols[i]);
+      continue;
+    }
+    pthread_barrier_wait(&P.bar_start);
+    for (;;) {
+      int64_t i = __atomic_fetch_add(&P.next, 1, __ATOMIC_RELAXED);
+      if (i >= P.hi) break;
+      par_column(&P, args[0].w, cols[i]);
+    }
+    pthread_barrier_wait(&P.bar_end);
+  }
+  P.stop = 1;
+  if (nthreads > 1) pthread_barrier_wait(&P.bar_start);
+  for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+  for (int t = 0; t < nthreads; ++t) free(args[t].w);
+  free(args); free(th);
+  pthread_barrier_destroy(&P.bar_start); pthread_barrier_destroy(&P.bar_end); pthread_mutex_destroy(&P.mu);
+  free(rp); free(rk); free(rpos); free(fill); free(h); free(lp); free(cols);
+  *fail_col = P.fail;
+  o->numeric_done = P.fail < 0;
+  return P.fail < 0 ? 0 : -3;
+}
+
 /* O10: x = P_f^T L^{-T} L^{-1} P_f b */
 int orc_solve(const orc_t* o, const double* b, double* x) {
   if (!o->numeric_done) return -7;

@@ -377,3 +377,33 @@ def test_oracle_solve_backward_error(name):
         np.add.at(rowsum, cols[off], np.abs(p.values[off]))
         Anorm = rowsum.max()
     assert np.abs(r).max() / (Anorm * np.abs(x).max()) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["C1", "S2", "S4", "S5", "T2"])
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_parallel_oracle_bit_identical(name, threads):
+    """The level-parallel O9 build (the timed CPU baseline) computes every column with the
+    serial build's operations in the same order: L is bitwise equal, on any thread count."""
+    p = gen.make(name)
+    a = oracle.Oracle.from_problem(p)
+    assert a.factor() == -1
+    La = a.L_csc()[2].copy()
+    b = oracle.Oracle.from_problem(p)
+    assert b.factor(threads=threads) == -1
+    assert np.array_equal(La, b.L_csc()[2])
+
+
+@pytest.mark.parametrize("threads", [1, 4])
+def test_parallel_oracle_not_spd(threads):
+    """The parallel build reports the serial build's first failing column (recipe R8)."""
+    p = gen.make("S4")
+    a = oracle.Oracle.from_problem(p)
+    pf = a.symbolic()["perm_final"]
+    for frac in (0.1, 0.6, 0.99):
+        j0 = int(frac * (p.n - 1))
+        i0 = int(np.where(pf == j0)[0][0])
+        vals = p.values.copy()
+        vals[p.colptr[i0]] = -1.0
+        q = gen.Problem(p.name, p.n, p.colptr, p.rowidx, vals, p.perm)
+        assert oracle.Oracle.from_problem(q).factor() == j0
+        assert oracle.Oracle.from_problem(q).factor(threads=threads) == j0
