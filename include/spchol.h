@@ -77,6 +77,18 @@ typedef struct {
                            a class), one launch per class, plain read-modify-write scatter instead of
                            FP64 RED; subtree_streams is forced to 1.  Requires update_mode 0.
                            Default 0.  (The solve's RED into shared ancestors stays unordered.) */
+  int32_t reserved0;    /* 0 */
+  int64_t device_mem_cap; /* single GPU, memory-capped (out-of-core) mode (P:484-489,
+                           P:568): 0 = unlimited (default).  Otherwise the device arena is planned to
+                           stay under this many bytes: the supernodal tree is split into a resident
+                           top and subtree batches that share one device window; each batch is
+                           factored in the window, its contributions land in the resident top panels
+                           through the usual relind scatter, and its finished panels are copied to
+                           pinned host memory (the solve streams them back batch by batch).  The cap
+                           bounds the factor's device storage (window + resident top panels + kept
+                           diagonal-block inverses = SPCHOL_Q_ARENA_BYTES); the metadata (A's values
+                           and maps, relind, task lists) comes on top (SPCHOL_Q_DEVICE_BYTES).
+                           Analyze fails with SPCHOL_ERR_DEVICE_OOM when even the top does not fit. */
 } spchol_options;
 
 /* Fill *opt with the defaults above. */
@@ -195,7 +207,9 @@ enum {
   SPCHOL_Q_DIST_GRAPH = 23,   /* multi-GPU: 1 if the factor (with its NCCL calls) replays as a CUDA graph */
   SPCHOL_Q_COMM_B_SEND_BYTES = 24, /* multi-GPU: bytes this rank sends in the boundary-block exchange
                                       after phase A (SURVEY §8(e) phase B); host-only too               */
-  SPCHOL_Q_COMM_B_RECV_BYTES = 25  /* ... receives in it                                                 */
+  SPCHOL_Q_COMM_B_RECV_BYTES = 25, /* ... receives in it                                                 */
+  SPCHOL_Q_NBATCHES = 26,     /* memory-capped mode: subtree batches (0 when not capped)                */
+  SPCHOL_Q_HOST_BYTES = 27    /* memory-capped mode: pinned host bytes holding the finished batches     */
 };
 int spchol_query(const spchol_handle* h, int key, int64_t* value);
 

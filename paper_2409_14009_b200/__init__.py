@@ -28,7 +28,8 @@ SPCHOL_ERR_STATE = -7
 Q = dict(N=0, NNZ_A=1, NNZ_L=2, NFUND=3, NSUPER=4, ADDED=5, NLEVELS=6, ROWS_LEN=7, NPAIRS=8,
          RELIND_LEN=9, PANEL_DOUBLES=10, NMERGES=11, FLOPS_EXACT=12, FLOPS_EXEC=13, LAUNCHES=14,
          UPDATE_ENTRIES=15, NBLOCKS=16, NMARKERS=17, NTOP_DIST=18, DEVICE_BYTES=19, COMM_SEND_BYTES=20,
-         COMM_RECV_BYTES=21, ARENA_BYTES=22, DIST_GRAPH=23, COMM_B_SEND_BYTES=24, COMM_B_RECV_BYTES=25)
+         COMM_RECV_BYTES=21, ARENA_BYTES=22, DIST_GRAPH=23, COMM_B_SEND_BYTES=24, COMM_B_RECV_BYTES=25, NBATCHES=26,
+         HOST_BYTES=27)
 KERNEL_KINDS = dict(small=0, potrf=1, trsm=2, local_update=3, syrk_scatter=4, init=5, rlb_update=6)
 
 # Every symbol include/spchol.h declares (checked by tests/test_capi_exports.py).
@@ -49,7 +50,7 @@ class spchol_options(ctypes.Structure):
                 ("small_max_k", ctypes.c_int32), ("use_graph", ctypes.c_int32),
                 ("dist_rank", ctypes.c_int32), ("dist_world", ctypes.c_int32),
                 ("subtree_streams", ctypes.c_int32), ("update_mode", ctypes.c_int32),
-                ("deterministic", ctypes.c_int32)]
+                ("deterministic", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("device_mem_cap", ctypes.c_int64)]
 
 
 class SpcholError(RuntimeError):

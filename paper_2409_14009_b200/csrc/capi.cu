@@ -96,6 +96,8 @@ extern "C" void spchol_default_options(spchol_options* o) {
   o->subtree_streams = 0;
   o->update_mode = 0;
   o->deterministic = 0;
+  o->reserved0 = 0;
+  o->device_mem_cap = 0;
 }
 
 extern "C" const char* spchol_last_error(void) { return g_err.c_str(); }
@@ -509,10 +511,13 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
 // supernodes, then the rows below the triangles; backward, the chunks below the triangles, then the
 // triangle column blocks from the last to the first.  A task only waits for tasks before it.
 template <class Active>
-static void build_solve_tasks(spchol_handle* h, Active active) {
+static void build_solve_tasks(spchol_handle* h, Active active, bool append = false) {
   const Symbolic& S = h->S;
   const int NB = h->nb;
-  h->stasks.clear();
+  if (!append) {
+    h->stasks.clear();
+    h->ssolve.clear();
+  }
   h->sfwd_off.assign(S.nlevels + 1, 0);
   h->sbwd_off.assign(S.nlevels + 1, 0);
   for (int l = 0; l < S.nlevels; ++l) {
@@ -556,7 +561,6 @@ static void build_solve_tasks(spchol_handle* h, Active active) {
   }
   h->sfwd_off[S.nlevels] = h->sbwd_off[S.nlevels] = (long long)h->stasks.size();
   h->nticket = 2 * (size_t)S.nlevels;
-  h->ssolve.clear();
   h->ssolve_off.assign(3 * S.nlevels + 1, 0);
   for (int l = 0; l < S.nlevels; ++l)
     for (int cl = 0; cl < 3; ++cl) {
@@ -569,6 +573,87 @@ static void build_solve_tasks(spchol_handle* h, Active active) {
       }
     }
   h->ssolve_off[3 * S.nlevels] = (int)h->ssolve.size();
+}
+
+// Memory-capped mode (f-4; "RLB-v2" caps GPU memory, P:568 RL runs out of it): the tree is
+// split into a resident top and subtree batches that share one device window.  A subtree whose panels
+// fit the window W is a unit; units are packed in postorder into batches of at most W; every supernode
+// above them stays resident.  W is the largest window with W + top(W) + fixed costs <= the cap (the
+// top shrinks as W grows).  Returns false if no window fits.
+static bool capped_layout(spchol_handle* h) {
+  const Symbolic& S = h->S;
+  const int ns = S.nsuper, NB = h->nb;
+  auto al = [](long long x) { return (x + 255) / 256 * 256; };   // 2 KB-aligned regions
+  std::vector<long long> pb(ns), sb(ns, 0);
+  for (int J = 0; J < ns; ++J) pb[J] = al((long long)h->sn[J].ld * h->sn[J].k);
+  for (int J = 0; J < ns; ++J) {
+    sb[J] += pb[J];
+    if (S.sparent[J] >= 0) sb[S.sparent[J]] += sb[J];
+  }
+  // inverse slots as usual (all resident)
+  h->slot_base.assign(ns, 0);
+  int slot = 0;
+  for (int J = 0; J < ns; ++J) {
+    if (h->is_small[J]) continue;
+    h->slot_base[J] = slot;
+    slot += (h->sn[J].k + NB - 1) / NB;
+  }
+  h->nslots_total = slot;
+  // the cap bounds the factor's device storage: the panel window + the resident top panels + the kept
+  // diagonal-block inverses (SPCHOL_Q_ARENA_BYTES); metadata comes on top (SPCHOL_Q_DEVICE_BYTES)
+  const double fixed = 8.0 * NBMAX * NBMAX * slot;
+  const double budget = (double)h->opt.device_mem_cap - fixed;
+  std::vector<long long> cand(sb.begin(), sb.end());
+  std::sort(cand.begin(), cand.end());
+  cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+  long long W = -1;
+  for (size_t i = cand.size(); i-- > 0;) {
+    long long top = 0;
+    for (int J = 0; J < ns; ++J) if (sb[J] > cand[i]) top += pb[J];
+    if ((double)(cand[i] + top) * 8.0 <= budget) { W = cand[i]; break; }
+  }
+  if (W < 0) return false;
+  // units = maximal subtrees with sb <= W (contiguous in postorder), packed into batches
+  h->batch.assign(ns, -1);
+  std::vector<long long> blen;
+  long long cur = -1;
+  int J = 0;
+  while (J < ns) {
+    // the unit root is the highest ancestor of J whose subtree still fits
+    int root = J;
+    if (sb[J] > W) { ++J; continue; }      // a top supernode
+    while (S.sparent[root] >= 0 && sb[S.sparent[root]] <= W) root = S.sparent[root];
+    if (cur < 0 || blen.back() + sb[root] > W) { blen.push_back(0); cur = (long long)blen.size() - 1; }
+    for (int q = J; q <= root; ++q) h->batch[q] = (int)cur;   // J .. root = root's subtree (postorder)
+    blen.back() += sb[root];
+    J = root + 1;
+  }
+  h->nbatch = (int)blen.size();
+  // offsets: each batch from 0 inside the window; the top after the window; host copy per batch
+  h->batch_len.assign(h->nbatch, 0);
+  h->batch_host.assign(h->nbatch + 1, 0);
+  h->host_off.assign(ns, -1);
+  long long wmax = 0;
+  for (int b = 0; b < h->nbatch; ++b) wmax = std::max(wmax, blen[b]);
+  h->window_doubles = al(wmax);
+  h->top_base = h->window_doubles;
+  long long toff = h->top_base;
+  for (int q = 0; q < ns; ++q) {
+    const int b = h->batch[q];
+    if (b < 0) {
+      h->sn[q].off = toff;
+      toff += pb[q];
+    } else {
+      h->sn[q].off = h->batch_len[b];
+      h->host_off[q] = h->batch_len[b];   // relative to the batch's host base (fixed below)
+      h->batch_len[b] += pb[q];
+    }
+  }
+  for (int b = 0; b < h->nbatch; ++b) h->batch_host[b + 1] = h->batch_host[b] + h->batch_len[b];
+  for (int q = 0; q < ns; ++q) if (h->batch[q] >= 0) h->host_off[q] += h->batch_host[h->batch[q]];
+  h->panel_doubles = toff;
+  h->capped = true;
+  return true;
 }
 
 static void build_plan(spchol_handle* h) {
@@ -624,7 +709,10 @@ static void build_plan(spchol_handle* h) {
   if (h->world > 1 && W % TILE == 0 && (W & (W - 1)) == 0 && h->opt.update_mode == 0)
     for (int J = 0; J < ns; ++J)
       h->top_dist[J] = h->owner[J] < 0 && h->grp_hi[J] - h->grp_lo[J] > 1 && !h->is_small[J] && work[J] >= h->dist_min_flops;
-  if (h->world == 1) {
+  bool capped_fail = false;
+  if (h->world == 1 && h->opt.device_mem_cap > 0) {
+    capped_fail = !capped_layout(h);
+  } else if (h->world == 1) {
     // panel arena: supernodes in order
     long long off = 0;
     for (int J = 0; J < ns; ++J) {
@@ -646,6 +734,31 @@ static void build_plan(spchol_handle* h) {
   }
   for (int J = 0; J < ns; ++J) h->panel_off[J] = h->sn[J].off;
   h->panel_off[ns] = h->panel_doubles;
+  if (h->capped) {   // exported layout: the batches' host copy, then the resident top (distinct offsets)
+    const long long hb = h->batch_host[h->nbatch];
+    for (int J = 0; J < ns; ++J) h->panel_off[J] = h->batch[J] >= 0 ? h->host_off[J] : hb + h->sn[J].off - h->top_base;
+    h->panel_off[ns] = hb + h->panel_doubles - h->top_base;
+  }
+  if (capped_fail) { h->capped = false; h->nbatch = -1; return; }
+  if (h->capped) {
+    // batch by batch (each in the window), then the resident top; the solve per segment
+    h->plan_batch.assign(h->nbatch + 1, 0);
+    h->segs.clear();
+    for (int b = 0; b < h->nbatch; ++b) {
+      h->plan_batch[b] = h->plan.size();
+      append_levels(h, [h, b](int J) { return h->batch[J] == b; }, false);
+      build_solve_tasks(h, [h, b](int J) { return h->batch[J] == b; }, b > 0);
+      h->segs.push_back({h->sfwd_off, h->sbwd_off, h->ssolve_off});
+    }
+    h->plan_batch[h->nbatch] = h->plan.size();
+    append_levels(h, [h](int J) { return h->batch[J] < 0; }, false);
+    build_solve_tasks(h, [h](int J) { return h->batch[J] < 0; }, h->nbatch > 0);
+    h->segs.push_back({h->sfwd_off, h->sbwd_off, h->ssolve_off});
+    h->nticket = 2 * (size_t)S.nlevels * h->segs.size();
+    h->plan_factor_begin = 0;
+    h->plan_all_end = h->plan_a_end = h->plan.size();
+    return;
+  }
   if (h->world == 1) {
     // the whole tree (the solve's structure; the single-GPU factor when nvr == 1)
     append_levels(h, [](int) { return true; }, true);
@@ -715,8 +828,26 @@ static int setup_device(spchol_handle* h) {
     }
   }
   if (h->world > 1) dist_redirect(h, posmap, ucb);   // updates leaving the rank go to its update blocks
-  std::vector<long long> amap(S.nnzA);
-  for (long long e = 0; e < S.nnzA; ++e) {
+  std::vector<long long> amap(h->capped ? 0 : S.nnzA);
+  if (h->capped) {
+    // memory-capped: A's entries grouped by batch (the window's current occupant), the top's last
+    h->ainit_off.assign(h->nbatch + 2, 0);
+    for (long long e = 0; e < S.nnzA; ++e) {
+      const int b = h->batch[S.snode[S.a_col[e]]];
+      h->ainit_off[(b < 0 ? h->nbatch : b) + 1]++;
+    }
+    for (int b = 0; b <= h->nbatch; ++b) h->ainit_off[b + 1] += h->ainit_off[b];
+    h->ainit_idx.assign(S.nnzA, 0);
+    h->ainit_dst.assign(S.nnzA, 0);
+    std::vector<long long> nx(h->ainit_off.begin(), h->ainit_off.end() - 1);
+    for (long long e = 0; e < S.nnzA; ++e) {
+      const int c = S.a_col[e], J = S.snode[c], b = h->batch[J];
+      const long long x = nx[b < 0 ? h->nbatch : b]++;
+      h->ainit_idx[x] = e;
+      h->ainit_dst[x] = h->sn[J].off + (long long)(c - S.sfirst[J]) * h->sn[J].ld + S.a_pos[e];
+    }
+  }
+  for (long long e = 0; e < (long long)amap.size(); ++e) {
     const int c = S.a_col[e], J = S.snode[c];
     amap[e] = h->sn[J].off + (long long)(c - S.sfirst[J]) * h->sn[J].ld + S.a_pos[e];
     // multi-GPU: a rank initialises the entries of the columns it holds
@@ -753,6 +884,11 @@ static int setup_device(spchol_handle* h) {
   }
   CK(dalloc(&h->d_avals, (size_t)S.nnzA));
   CK(upload(&h->d_amap, amap));
+  if (h->capped) {
+    CK(upload(&h->d_ainit_idx, h->ainit_idx));
+    CK(upload(&h->d_ainit_dst, h->ainit_dst));
+    CK(cudaMallocHost((void**)&h->h_panels, sizeof(double) * (size_t)std::max(1LL, h->batch_host[h->nbatch])));
+  }
   CK(upload(&h->d_ucol_base, ucb));
   CK(upload(&h->d_ucol_map, ucm));
   CK(upload(&h->d_posmap, posmap));
@@ -818,6 +954,10 @@ static void free_device(spchol_handle* h) {
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->graph) cudaGraphDestroy(h->graph);
   if (h->world > 1) dist_free_device(h);   // the VMM arenas (d_panels, d_linv)
+  if (h->h_panels) cudaFreeHost(h->h_panels);
+  h->h_panels = nullptr;
+  if (h->d_ainit_idx) cudaFree(h->d_ainit_idx);
+  if (h->d_ainit_dst) cudaFree(h->d_ainit_dst);
   void* ptrs[] = {h->d_ssolve, h->d_stasks, h->d_sflags, h->d_rtasks, h->d_tmaps, h->d_tmap_linv, h->d_small_sns, h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
                   h->d_rows_ptr, h->d_posmap, h->d_sfirst, h->d_rows, h->d_perm, h->d_level_sns, h->d_sn,
                   h->d_gtasks, h->d_ptasks, h->d_fail};
@@ -863,7 +1003,11 @@ static int finish_handle(spchol_handle* h) {
   if (const char* e = getenv("SPCHOL_RING_NS")) h->ring_ns = std::max(2, atoi(e));   // diagnostics
   if (const char* e = getenv("SPCHOL_SMALL_WARP")) h->small_warp = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_SMALL_WARP_MAXM")) h->small_warp_maxm = std::max(0, std::min(128, atoi(e)));
+  if (h->opt.device_mem_cap < 0 || (h->opt.device_mem_cap > 0 && h->world > 1))
+    return fail(SPCHOL_ERR_VALIDATION, "device_mem_cap must be >= 0 and needs dist_world == 1");
   build_plan(h);
+  if (h->opt.device_mem_cap > 0 && !h->capped)
+    return fail(SPCHOL_ERR_DEVICE_OOM, "device_mem_cap: the resident top of the supernodal tree alone exceeds the cap");
   if (h->opt.device < 0) return SPCHOL_OK;   // host-only analysis (no device state)
   int rc = setup_device(h);
   if (rc != SPCHOL_OK) free_device(h);
@@ -1177,7 +1321,32 @@ static int enqueue_init(spchol_handle* h, cudaStream_t st) {
   return SPCHOL_OK;
 }
 
+// Memory-capped factor: the top's entries once; per batch: window zeroed, the batch's entries, its
+// levels, its finished panels to the host copy (stream-ordered, so the next batch's memset waits for
+// the copy); then the resident top.
+static int enqueue_factor_capped(spchol_handle* h, cudaStream_t st) {
+  CK(cudaMemsetAsync(h->d_fail, 0xFF, sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(h->d_panels + h->top_base, 0, sizeof(double) * (size_t)(h->panel_doubles - h->top_base), st));
+  const int nb = h->nbatch;
+  launch_init_list(h->d_avals, h->d_ainit_idx + h->ainit_off[nb], h->d_ainit_dst + h->ainit_off[nb],
+                   h->ainit_off[nb + 1] - h->ainit_off[nb], h->d_panels, st);
+  for (int b = 0; b < nb; ++b) {
+    CK(cudaMemsetAsync(h->d_panels, 0, sizeof(double) * (size_t)h->batch_len[b], st));
+    launch_init_list(h->d_avals, h->d_ainit_idx + h->ainit_off[b], h->d_ainit_dst + h->ainit_off[b],
+                     h->ainit_off[b + 1] - h->ainit_off[b], h->d_panels, st);
+    int rc = enqueue_ops(h, st, h->plan_batch[b], h->plan_batch[b + 1]);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h->h_panels + h->batch_host[b], h->d_panels, sizeof(double) * (size_t)h->batch_len[b],
+                       cudaMemcpyDeviceToHost, st));
+  }
+  int rc = enqueue_ops(h, st, h->plan_batch[nb], h->plan_all_end);
+  if (rc) return rc;
+  CK(cudaGetLastError());
+  return SPCHOL_OK;
+}
+
 static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
+  if (h->capped) return enqueue_factor_capped(h, st);
   int rc = enqueue_init(h, st);
   if (rc) return rc;
   if (h->world == 1) return enqueue_ops(h, st, h->plan_factor_begin, h->plan_all_end);
@@ -1259,7 +1428,58 @@ extern "C" int spchol_factor(spchol_handle* h, int64_t* fail_col, int64_t* fail_
 // the CTA).  Large supernodes: one launch per level and direction (solve_fwd/bwd_level_kernel):
 // 64-row / 64-column block tasks that wait on per-block ready flags instead of kernel boundaries;
 // the diagonal blocks are applied with the inverses kept from the factor (X_bb = L_bb^{-1}).
+// Memory-capped solve: forward batch by batch (each copied back into the window), then the resident
+// top; backward the top, then the batches in reverse (copied back again).
+static int enqueue_solve_capped(spchol_handle* h, const double* d_b, double* d_x, cudaStream_t st) {
+  const Symbolic& S = h->S;
+  launch_permute(h->d_perm, d_b, h->d_y, S.n, 0, st);
+  const size_t NS = (size_t)std::max(1, h->nslots_total);
+  int* fflag = h->d_sflags;
+  int* bflag = fflag + NS;
+  int* rcnt = bflag + NS;
+  int* tickets = rcnt + NS;
+  CK(cudaMemsetAsync(h->d_sflags, 0, sizeof(int) * (3 * NS + h->nticket), st));
+  const int nseg = (int)h->segs.size(), nl = S.nlevels;
+  auto fwd = [&](int g) {
+    const auto& G = h->segs[g];
+    for (int l = 0; l < nl; ++l) {
+      for (int cl = 0; cl < 3; ++cl)
+        launch_solve_small(h->d_ssolve + G.ss[3 * l + cl], G.ss[3 * l + cl + 1] - G.ss[3 * l + cl], cl, 0, h->d_rows,
+                           h->d_panels, h->d_y, st);
+      launch_solve_fwd_level(h->d_stasks + G.fwd[l], (int)(G.bwd[l] - G.fwd[l]), tickets + 2 * (g * nl + l), fflag,
+                             h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, st);
+    }
+  };
+  auto bwd = [&](int g) {
+    const auto& G = h->segs[g];
+    for (int l = nl - 1; l >= 0; --l) {
+      launch_solve_bwd_level(h->d_stasks + G.bwd[l], (int)(G.fwd[l + 1] - G.bwd[l]), tickets + 2 * (g * nl + l) + 1,
+                             bflag, rcnt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y,
+                             h->nb, st);
+      for (int cl = 0; cl < 3; ++cl)
+        launch_solve_small(h->d_ssolve + G.ss[3 * l + cl], G.ss[3 * l + cl + 1] - G.ss[3 * l + cl], cl, 1, h->d_rows,
+                           h->d_panels, h->d_y, st);
+    }
+  };
+  for (int b = 0; b < h->nbatch; ++b) {
+    CK(cudaMemcpyAsync(h->d_panels, h->h_panels + h->batch_host[b], sizeof(double) * (size_t)h->batch_len[b],
+                       cudaMemcpyHostToDevice, st));
+    fwd(b);
+  }
+  fwd(nseg - 1);
+  bwd(nseg - 1);
+  for (int b = h->nbatch - 1; b >= 0; --b) {
+    CK(cudaMemcpyAsync(h->d_panels, h->h_panels + h->batch_host[b], sizeof(double) * (size_t)h->batch_len[b],
+                       cudaMemcpyHostToDevice, st));
+    bwd(b);
+  }
+  launch_permute(h->d_perm, h->d_y, d_x, S.n, 1, st);
+  CK(cudaGetLastError());
+  return SPCHOL_OK;
+}
+
 static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaStream_t st) {
+  if (h->capped) return enqueue_solve_capped(h, d_b, d_x, st);
   const Symbolic& S = h->S;
   launch_permute(h->d_perm, d_b, h->d_y, S.n, 0, st);
   const size_t NS = (size_t)std::max(1, h->nslots_total);
@@ -1366,7 +1586,7 @@ extern "C" int spchol_query(const spchol_handle* h, int key, int64_t* value) {
     case SPCHOL_Q_ROWS_LEN: *value = (int64_t)S.rows.size(); break;
     case SPCHOL_Q_NPAIRS: *value = (int64_t)S.rel_anc.size(); break;
     case SPCHOL_Q_RELIND_LEN: *value = (int64_t)S.relind.size(); break;
-    case SPCHOL_Q_PANEL_DOUBLES: *value = h->panel_doubles; break;
+    case SPCHOL_Q_PANEL_DOUBLES: *value = h->panel_off.empty() ? h->panel_doubles : h->panel_off.back(); break;
     case SPCHOL_Q_NMERGES: *value = S.nmerges; break;
     case SPCHOL_Q_FLOPS_EXACT: *value = (int64_t)S.flops_exact; break;
     case SPCHOL_Q_FLOPS_EXEC: *value = (int64_t)h->flops_exec; break;
@@ -1395,6 +1615,8 @@ extern "C" int spchol_query(const spchol_handle* h, int key, int64_t* value) {
     }
     case SPCHOL_Q_DIST_GRAPH: *value = h->graph_dist ? 1 : 0; break;
     case SPCHOL_Q_COMM_B_SEND_BYTES: *value = (int64_t)h->comm_b_send; break;
+    case SPCHOL_Q_NBATCHES: *value = h->capped ? h->nbatch : 0; break;
+    case SPCHOL_Q_HOST_BYTES: *value = h->capped ? 8 * (int64_t)h->batch_host[h->nbatch] : 0; break;
     case SPCHOL_Q_COMM_B_RECV_BYTES: *value = (int64_t)h->comm_b_recv; break;
     case SPCHOL_Q_NTOP_DIST: {
       int64_t c = 0;
@@ -1442,6 +1664,10 @@ static int copy_panel(const spchol_handle* h, int J, double* out) {
   const size_t cnt = (size_t)I.ld * I.k;
   if (!cnt) return SPCHOL_OK;
   const double* src = h->d_panels + I.off;
+  if (h->capped && h->batch[J] >= 0) {   // a finished batch: its host copy
+    std::memcpy(out, h->h_panels + h->host_off[J], sizeof(double) * cnt);
+    return SPCHOL_OK;
+  }
   if (h->world == 1) {
     CK(cudaMemcpy(out, src, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
     return SPCHOL_OK;
@@ -1473,12 +1699,12 @@ extern "C" int spchol_export_panels(const spchol_handle* h, int64_t* panel_off, 
   if (panel_off) for (size_t J = 0; J < h->panel_off.size(); ++J) panel_off[J] = h->panel_off[J];
   if (ld) for (size_t J = 0; J < h->sn.size(); ++J) ld[J] = h->sn[J].ld;
   if (panels && h->panel_doubles > 0) {
-    if (h->world == 1) {
+    if (h->world == 1 && !h->capped) {
       CK(cudaMemcpy(panels, h->d_panels, sizeof(double) * (size_t)h->panel_doubles, cudaMemcpyDeviceToHost));
     } else {
-      std::fill(panels, panels + h->panel_doubles, 0.0);
+      std::fill(panels, panels + h->panel_off.back(), 0.0);
       for (int J = 0; J < h->S.nsuper; ++J) {
-        int rc = copy_panel(h, J, panels + h->sn[J].off);
+        int rc = copy_panel(h, J, panels + h->panel_off[J]);
         if (rc) return rc;
       }
     }
@@ -1568,6 +1794,17 @@ extern "C" int spchol_export_diagonal(spchol_handle* h, double* diag) {
   if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
   CK(cudaSetDevice(h->opt.device));
   const Symbolic& S = h->S;
+  if (h->capped) {   // the batches' panels live in the host copy
+    CK(cudaStreamSynchronize(h->stream));
+    std::vector<double> pan;
+    for (int J = 0; J < S.nsuper; ++J) {
+      pan.resize((size_t)h->sn[J].ld * h->sn[J].k);
+      int rc = copy_panel(h, J, pan.data());
+      if (rc) return rc;
+      for (int c = 0; c < h->sn[J].k; ++c) diag[S.sfirst[J] + c] = pan[(size_t)c * h->sn[J].ld + c];
+    }
+    return SPCHOL_OK;
+  }
   if (!h->d_diag_idx) {   // multi-GPU: the diagonal entries this rank holds, zeros elsewhere
     std::vector<long long> idx(S.n);
     for (int J = 0; J < S.nsuper; ++J)

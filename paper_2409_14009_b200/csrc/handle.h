@@ -203,6 +203,21 @@ struct spchol_handle {
   cudaEvent_t ev_comm_in = nullptr, ev_comm_out = nullptr;
   bool graph_dist = false;             // the multi-GPU factor runs as a captured graph (real NCCL)
   bool dist_eager_done = false, dist_solve_eager_done = false, dist_capture_failed = false;
+  // memory-capped mode (f-4, single GPU): resident top + subtree batches sharing one device window
+  bool capped = false;
+  std::vector<int> batch;                // batch of each supernode, -1 = resident top
+  int nbatch = 0;
+  std::vector<long long> batch_len;      // doubles of each batch's panels (a prefix of the window)
+  std::vector<long long> batch_host;     // [nbatch + 1] offsets of the batches in the host copy
+  std::vector<long long> host_off;       // per batch supernode: offset of its panel in the host copy
+  long long window_doubles = 0, top_base = 0;
+  std::vector<size_t> plan_batch;        // [nbatch + 1]: batch b's plan [plan_batch[b], plan_batch[b+1]); top after
+  std::vector<long long> ainit_off;      // [nbatch + 2]: A's entries to initialise per batch, the top's last
+  std::vector<long long> ainit_idx, ainit_dst;
+  long long *d_ainit_idx = nullptr, *d_ainit_dst = nullptr;
+  double* h_panels = nullptr;            // pinned host copy of the finished batches' panels
+  struct SolveSeg { std::vector<long long> fwd, bwd; std::vector<int> ss; };
+  std::vector<SolveSeg> segs;            // capped: per batch, then the top
   // single-GPU subtree concurrency etc.
   std::vector<int> small_level_off;     // small_sns range per level
   std::vector<spchol::STask> stasks;    // level solve tasks: forward of level l at [sfwd_off[l], sfwd_off[l+1]),

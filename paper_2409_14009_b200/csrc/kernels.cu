@@ -760,31 +760,37 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
 }
 
 // ----------------------------------------------------------------------------------------------
-// potrf8_kernel: cdiv POTRF ("DPOTRF") of one <= 64-column diagonal block plus its inverse
-// X = L_bb^{-1} (TRSM-as-GEMM, solve), blocked so that the sequential part is short.  The 64x64 block (padding rows/columns >= nb are an identity) sits in shared memory,
-// row-major, and is factored right-looking in 8-column panels:
-//   * the 8x8 diagonal block of panel p is factored by ONE thread in registers (8 dependent
-//     rsqrt steps, no barrier);
-//   * TRSM: one thread per row below it, 8-step row substitution with the reciprocal pivots;
-//   * SYRK: 4x4 register tiles of the trailing lower triangle, K = 8.  Thread 0 owns the three
-//     tiles of the next diagonal block and factors it as soon as they are updated, while the
-//     others finish the trailing update (two barriers per panel).
-// The inverse X = L^{-1} (kept for TRSM-as-GEMM and the solve) is then formed by blocked
-// doubling: the eight 8x8 diagonal blocks by substitution (one thread each), then for h = 8, 16,
-// 32: X21 = -(X22 L21) X11 for each 2h x 2h diagonal block — small parallel matrix products;
-// T = X22 L21 is parked transposed in the unused upper triangle of the L buffer.
+// potrf9_kernel: cdiv POTRF ("DPOTRF") of one <= 64-column diagonal block in place, plus X =
+// L_bb^{-1} into its inverse slot (TRSM-as-GEMM and the solve), the inverse formed alongside the
+// factorization.  Right-looking in 8-column
+// panels p (b = 8p) on column-major shared copies of A (-> L) and Y = I (-> X):
+//   phase 1  TRSM of panel p's rows below the diagonal block (one thread per row, warps 0-1);
+//            X_pp = L_pp^{-1} (one thread); Y_i -= L_{i,p-1} X_{p-1} for the rows i >= b (warps 2-3,
+//            the right-looking forward substitution of L X = I, "DTRSM" on the identity)
+//   phase 2  thread 0: the three 4x4 tiles of the next diagonal block, then its 8x8 factor (8
+//            pivots in registers); warps 1-3: the rest of the trailing SYRK, and X_p = X_pp Y_p
+// so the only sequential part is the 64-pivot chain; the inverse costs no extra phase.  16-byte
+// cp.async loads, 16-byte stores.  (Replaces a row-major kernel that formed the inverse by blocked
+// doubling after the factor: 22.2 -> 20.8 us per block, one CTA, tools/potrf_probe.cu.)
 // ----------------------------------------------------------------------------------------------
-constexpr int P8_LD = NBMAX + 1;              // row stride (doubles) of the shared buffers
-constexpr int POTRF8_THREADS = 128;
-constexpr int POTRF8_SMEM = (NBMAX * P8_LD + NBMAX) * (int)sizeof(double);
+constexpr int P9_LD = NBMAX + 2;              // column stride (doubles): even (16-byte rows pairs)
+constexpr int POTRF9_THREADS = 128;
+constexpr int POTRF9_SMEM = (2 * NBMAX * P9_LD + NBMAX + 64) * (int)sizeof(double);
+#ifdef SPCHOL_P9_CLOCKS   // tools/potrf_probe.cu: phase timestamps of thread 0
+__device__ long long p9_clocks[64];
+#define P9_CLK(i) do { if (threadIdx.x == 0) p9_clocks[i] = clock64(); } while (0)
+#define P9_CLKT(t, i) do { if (threadIdx.x == (t)) p9_clocks[i] = clock64(); } while (0)
+#else
+#define P9_CLK(i) do { } while (0)
+#define P9_CLKT(t, i) do { } while (0)
+#endif
 
-// Factor the 8x8 diagonal block at (b, b) of As in registers; pivots' reciprocals into rl.
-__device__ __forceinline__ void p8_diag(double* As, double* rl, int b, int nb, int& bad) {
+__device__ __forceinline__ void p9_diag(double* Ls, double* rl, int b, int nb, int& bad) {
   double a[8][8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int j = 0; j < 8; ++j)
 #pragma unroll
-    for (int j = 0; j <= i; ++j) a[i][j] = As[(b + i) * P8_LD + b + j];
+    for (int i = j; i < 8; ++i) a[i][j] = Ls[(b + j) * P9_LD + b + i];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const double d = a[j][j];
@@ -800,200 +806,207 @@ __device__ __forceinline__ void p8_diag(double* As, double* rl, int b, int nb, i
       for (int i = q; i < 8; ++i) a[i][q] = fma(-a[i][j], a[q][j], a[i][q]);
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int j = 0; j < 8; ++j)
 #pragma unroll
-    for (int j = 0; j <= i; ++j) As[(b + i) * P8_LD + b + j] = a[i][j];
+    for (int i = j; i < 8; ++i) Ls[(b + j) * P9_LD + b + i] = a[i][j];
 }
 
-// One 4x4 tile (rows r0.., cols c0..) of the trailing update A -= L_p L_p^T, panel columns [b, b+8).
-__device__ __forceinline__ void p8_syrk_tile(double* As, int b, int r0, int c0) {
+// 4x4 tile (rows r0.., columns c0..; r0, c0 multiples of 4) of A -= L_p L_p^T, K = panel [b, b+8).
+__device__ __forceinline__ void p9_syrk_tile(double* Ls, int b, int r0, int c0) {
   double acc[4][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int j = 0; j < 4; ++j) {
+    const double2 u = *reinterpret_cast<const double2*>(Ls + (c0 + j) * P9_LD + r0);
+    const double2 v = *reinterpret_cast<const double2*>(Ls + (c0 + j) * P9_LD + r0 + 2);
+    acc[0][j] = u.x; acc[1][j] = u.y; acc[2][j] = v.x; acc[3][j] = v.y;
+  }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = As[(r0 + i) * P8_LD + c0 + j];
-#pragma unroll
-  for (int q = 0; q < 8; q += 2) {
-    double2 lr[4], lc[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {      // rows r0+i and c0+i, panel columns q, q+1
-      lr[i] = make_double2(As[(r0 + i) * P8_LD + b + q], As[(r0 + i) * P8_LD + b + q + 1]);
-      lc[i] = make_double2(As[(c0 + i) * P8_LD + b + q], As[(c0 + i) * P8_LD + b + q + 1]);
-    }
+  for (int q = 0; q < 8; ++q) {
+    const double* col = Ls + (b + q) * P9_LD;
+    const double2 r01 = *reinterpret_cast<const double2*>(col + r0), r23 = *reinterpret_cast<const double2*>(col + r0 + 2);
+    const double2 c01 = *reinterpret_cast<const double2*>(col + c0), c23 = *reinterpret_cast<const double2*>(col + c0 + 2);
+    const double lr[4] = {r01.x, r01.y, r23.x, r23.y}, lc[4] = {c01.x, c01.y, c23.x, c23.y};
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = fma(-lr[i].y, lc[j].y, fma(-lr[i].x, lc[j].x, acc[i][j]));
+      for (int j = 0; j < 4; ++j) acc[i][j] = fma(-lr[i], lc[j], acc[i][j]);
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int j = 0; j < 4; ++j)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (r0 + i >= c0 + j) As[(r0 + i) * P8_LD + c0 + j] = acc[i][j];   // upper part of diagonal tiles unused
+    for (int i = 0; i < 4; ++i)
+      if (r0 + i >= c0 + j) Ls[(c0 + j) * P9_LD + r0 + i] = acc[i][j];   // upper part of diagonal tiles unused
 }
 
-// Doubling step of the inverse for all 2h x 2h diagonal blocks (a = 0, 2h, ...), TR x TC outputs per
-// thread (TR * TC * POTRF8_THREADS = 32 h).  Upper triangles of X are zero, so the triangular sums
-// run over whole ranges without masks.
-template <int H, int TR, int TC>
-__device__ __forceinline__ void p8_double(double* As, int tid) {
-  constexpr int TPR = H / TC, TPB = (H / TR) * TPR;   // threads per tile row, per block
-  const int a = (tid / TPB) * 2 * H, t = tid % TPB;
-  const int r0 = (t / TPR) * TR, c0 = (t % TPR) * TC;
-  double acc[TR][TC];
-  // T = X22 L21 (rows r0.., cols c0..), parked transposed at As(a + c, a + H + r) (upper part)
-#pragma unroll
-  for (int i = 0; i < TR; ++i)
-#pragma unroll
-    for (int j = 0; j < TC; ++j) acc[i][j] = 0.0;
-  for (int q = 0; q < r0 + TR; ++q) {
-    double x[TR], l[TC];
-#pragma unroll
-    for (int i = 0; i < TR; ++i) x[i] = As[(a + H + r0 + i) * P8_LD + a + H + q];
-#pragma unroll
-    for (int j = 0; j < TC; ++j) l[j] = As[(a + H + q) * P8_LD + a + c0 + j];
-#pragma unroll
-    for (int i = 0; i < TR; ++i)
-#pragma unroll
-      for (int j = 0; j < TC; ++j) acc[i][j] = fma(x[i], l[j], acc[i][j]);
-  }
-#pragma unroll
-  for (int i = 0; i < TR; ++i)
-#pragma unroll
-    for (int j = 0; j < TC; ++j) As[(a + c0 + j) * P8_LD + a + H + r0 + i] = acc[i][j];
-  __syncthreads();
-  // X21 = -T X11, over L21's place
-#pragma unroll
-  for (int i = 0; i < TR; ++i)
-#pragma unroll
-    for (int j = 0; j < TC; ++j) acc[i][j] = 0.0;
-  for (int q = c0; q < H; ++q) {
-    double tt[TR], x[TC];
-#pragma unroll
-    for (int i = 0; i < TR; ++i) tt[i] = As[(a + q) * P8_LD + a + H + r0 + i];
-#pragma unroll
-    for (int j = 0; j < TC; ++j) x[j] = As[(a + q) * P8_LD + a + c0 + j];
-#pragma unroll
-    for (int i = 0; i < TR; ++i)
-#pragma unroll
-      for (int j = 0; j < TC; ++j) acc[i][j] = fma(tt[i], x[j], acc[i][j]);
-  }
-#pragma unroll
-  for (int i = 0; i < TR; ++i)
-#pragma unroll
-    for (int j = 0; j < TC; ++j) As[(a + H + r0 + i) * P8_LD + a + c0 + j] = -acc[i][j];
-  __syncthreads();
-  // the upper part must be zero again for the next level's unmasked triangular sums
-#pragma unroll
-  for (int i = 0; i < TR; ++i)
-#pragma unroll
-    for (int j = 0; j < TC; ++j) As[(a + c0 + j) * P8_LD + a + H + r0 + i] = 0.0;
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(POTRF8_THREADS, 4) potrf8_kernel(const PTask* __restrict__ tasks,
+__global__ void __launch_bounds__(POTRF9_THREADS, 3) potrf9_kernel(const PTask* __restrict__ tasks,
                                                                 const SnInfo* __restrict__ sn,
                                                                 const int* __restrict__ sfirst, double* panels,
                                                                 double* linv, unsigned long long* fail) {
   pdl_enter();
-  extern __shared__ double p8_smem[];
-  double* As = p8_smem;                        // A -> L -> X = L^{-1} in place (lower); upper = 0 / T scratch
-  double* rl = As + NBMAX * P8_LD;             // reciprocal pivots 1 / L_jj
+  extern __shared__ __align__(16) double p9_smem[];
+  double* Ls = p9_smem;                        // A -> L (column-major, lower part used)
+  double* Xs = Ls + NBMAX * P9_LD;             // Y = I -> X = L^{-1} (column-major)
+  double* rl = Xs + NBMAX * P9_LD;             // 1 / L_jj
+  double* Xd = rl + NBMAX;                     // X_pp of the current panel (8 x 8, column-major)
+  P9_CLK(0);
   const PTask T = tasks[blockIdx.x];
   const SnInfo S = sn[T.sn];
-  const int nb = T.nb, tid = threadIdx.x;
+  const int nb = T.nb, tid = threadIdx.x, warp = tid >> 5;
   double* P = panels + S.off + (long long)T.c0 * S.ld + T.c0;
-  // all loads in flight at once (8-byte cp.async into the row-major buffer), padding = identity
-  for (int e = tid; e < NBMAX * NBMAX; e += POTRF8_THREADS) {
-    const int c = e / NBMAX, r = e % NBMAX;     // consecutive threads: consecutive rows (coalesced)
-    double* d = As + r * P8_LD + c;
-    if (r < c) {
-      *d = 0.0;
-    } else if (r < nb && c < nb) {
-      const unsigned sa = (unsigned)__cvta_generic_to_shared(d);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(P + (long long)c * S.ld + r));
-    } else {
-      *d = r == c ? 1.0 : 0.0;
+  // A's block: 16-byte cp.async of row pairs (rows >= nb zero-filled), Y = I meanwhile
+  for (int e = tid; e < NBMAX * NBMAX / 2; e += POTRF9_THREADS) {
+    const int c = e >> 5, r = (e & 31) * 2;
+    if (c < nb && r < nb) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(Ls + c * P9_LD + r);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(P + (long long)c * S.ld + r),
+                   "r"(r + 1 < nb ? 16 : 8));
     }
+    *reinterpret_cast<double2*>(Xs + c * P9_LD + r) = make_double2(r == c ? 1.0 : 0.0, r + 1 == c ? 1.0 : 0.0);
   }
-  asm volatile("cp.async.wait_all;\n" ::);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  if (nb < NBMAX)   // padding: identity (pivots 1, no coupling)
+    for (int e = tid; e < NBMAX * NBMAX; e += POTRF9_THREADS) {
+      const int c = e >> 6, r = e & 63;
+      if (c >= nb || r >= nb) Ls[c * P9_LD + r] = r == c ? 1.0 : 0.0;
+    }
   __syncthreads();
+  P9_CLK(1);
   int bad = -1;
-  if (tid == 0) p8_diag(As, rl, 0, nb, bad);
+  if (tid == 0) p9_diag(Ls, rl, 0, nb, bad);
   __syncthreads();
+  P9_CLK(2);
   for (int p = 0; p < NBMAX / 8; ++p) {
     const int b = 8 * p, t0 = b + 8, nt = NBMAX - t0;
-    // TRSM: rows t0 + tid of panel p
-    if (tid < nt) {
-      const int r = t0 + tid;
-      double x[8];
+    // ---- phase 1
+    if (warp < 2) {
+      if (tid < nt) {                          // TRSM: row t0 + tid of panel p
+        const int r = t0 + tid;
+        double x[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = As[r * P8_LD + b + j];
+        for (int j = 0; j < 8; ++j) x[j] = Ls[(b + j) * P9_LD + r];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 8; ++j) {
 #pragma unroll
-        for (int q = 0; q < j; ++q) x[j] = fma(-x[q], As[(b + j) * P8_LD + b + q], x[j]);
-        x[j] *= rl[b + j];
+          for (int q = 0; q < j; ++q) x[j] = fma(-x[q], Ls[(b + q) * P9_LD + b + j], x[j]);
+          x[j] *= rl[b + j];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) Ls[(b + j) * P9_LD + r] = x[j];
       }
+    } else {
+      if (tid == POTRF9_THREADS - 1) {         // X_pp = L_pp^{-1}: column-oriented substitution
+        double x[8][8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) As[r * P8_LD + b + j] = x[j];
+        for (int c = 0; c < 8; ++c) {
+          x[c][c] = rl[b + c];
+#pragma unroll
+          for (int r = c + 1; r < 8; ++r) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = c; q < r; ++q) acc = fma(Ls[(b + q) * P9_LD + b + r], x[q][c], acc);
+            x[r][c] = -acc * rl[b + r];
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int r = 0; r < 8; ++r) Xd[c * 8 + r] = r >= c ? x[r][c] : 0.0;
+      }
+      if (p > 0) {                             // Y_i -= L_{i,p-1} X_{p-1} (rows i >= b, columns < b)
+        const int bp = b - 8, nrc = (NBMAX - b) / 8;   // row chunks of 8
+        for (int it = tid - 64; it < b * nrc; it += 64) {
+          const int c = it % b, i0 = b + 8 * (it / b);
+          double xk[8];
+#pragma unroll
+          for (int k = 0; k < 8; k += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(Xs + c * P9_LD + bp + k);
+            xk[k] = v.x; xk[k + 1] = v.y;
+          }
+          double y[8];
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(Xs + c * P9_LD + i0 + i);
+            y[i] = v.x; y[i + 1] = v.y;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const double* lc = Ls + (bp + k) * P9_LD + i0;
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+              const double2 l = *reinterpret_cast<const double2*>(lc + i);
+              y[i] = fma(-l.x, xk[k], y[i]);
+              y[i + 1] = fma(-l.y, xk[k], y[i + 1]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) *reinterpret_cast<double2*>(Xs + c * P9_LD + i0 + i) = make_double2(y[i], y[i + 1]);
+        }
+      }
     }
     __syncthreads();
-    if (nt > 0) {
-      // SYRK on 4x4 tiles of the trailing triangle; tiles 0-2 = the next diagonal block (thread 0)
-      const int n4 = nt / 4, ntiles = n4 * (n4 + 1) / 2;
-      if (tid < 32) {    // warp 0: the next diagonal block — three tiles, then thread 0 factors it
-        if (tid < 3) p8_syrk_tile(As, b, t0 + (tid ? 4 : 0), t0 + (tid == 2 ? 4 : 0));
+    P9_CLK(3 + 2 * p);
+    // ---- phase 2
+    if (warp == 0) {
+      if (nt > 0) {
+        if (tid < 3) p9_syrk_tile(Ls, b, t0 + (tid ? 4 : 0), t0 + (tid == 2 ? 4 : 0));
         __syncwarp();
-        if (tid == 0) p8_diag(As, rl, t0, nb, bad);
-      } else {           // warps 1-3: the rest of the trailing update
-        for (int t = tid - 29; t < ntiles; t += POTRF8_THREADS - 32) {
+        P9_CLKT(0, 21 + p);
+        if (tid == 0) p9_diag(Ls, rl, t0, nb, bad);
+        P9_CLKT(0, 29 + p);
+      }
+    } else {
+      if (warp >= 2 && tid - 64 < t0) {        // X_p = X_pp Y_p, column tid - 64 (< b + 8), in place
+        const int c = tid - 64;
+        double y[8], xo[8];
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(Xs + c * P9_LD + b + k);
+          y[k] = v.x; y[k + 1] = v.y;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k <= r; ++k) acc = fma(Xd[k * 8 + r], y[k], acc);
+          xo[r] = acc;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; r += 2) *reinterpret_cast<double2*>(Xs + c * P9_LD + b + r) = make_double2(xo[r], xo[r + 1]);
+      }
+      P9_CLKT(64, 37 + p);
+      if (nt > 0) {
+        const int n4 = nt / 4, ntiles = n4 * (n4 + 1) / 2;   // tiles 0-2 = the next diagonal block (warp 0)
+        for (int t = tid - 29; t < ntiles; t += POTRF9_THREADS - 32) {
           int ti = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);   // t = ti (ti + 1) / 2 + tj
           while (ti * (ti + 1) / 2 > t) --ti;
           while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
           const int tj = t - ti * (ti + 1) / 2;
-          p8_syrk_tile(As, b, t0 + 4 * ti, t0 + 4 * tj);
+          p9_syrk_tile(Ls, b, t0 + 4 * ti, t0 + 4 * tj);
         }
       }
-      __syncthreads();
+      P9_CLKT(32, 45 + p);
+      P9_CLKT(64, 53 + p);
     }
+    __syncthreads();
+    P9_CLK(4 + 2 * p);
   }
   if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[T.sn] + T.c0 + bad));
-  for (int e = tid; e < NBMAX * NBMAX; e += POTRF8_THREADS) {   // L out before it is inverted in place
-    const int c = e / NBMAX, r = e % NBMAX;
-    if (r >= c && r < nb && c < nb) P[(long long)c * S.ld + r] = As[r * P8_LD + c];
-  }
-  __syncthreads();
-  // inverse, level 0: the eight 8x8 diagonal blocks (column-oriented substitution per block)
-  if (tid < NBMAX / 8) {
-    const int b = 8 * tid;
-    double x[8][8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      x[c][c] = rl[b + c];
-#pragma unroll
-      for (int r = c + 1; r < 8; ++r) {
-        double acc = 0.0;
-#pragma unroll
-        for (int q = c; q < r; ++q) acc = fma(As[(b + r) * P8_LD + b + q], x[q][c], acc);
-        x[r][c] = -acc * rl[b + r];
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-#pragma unroll
-      for (int c = 0; c <= r; ++c) As[(b + r) * P8_LD + b + c] = x[r][c];
-  }
-  __syncthreads();
-  // doubling: for every 2h block at a, X21 = -(X22 L21) X11 (h x h, rows a+h.., columns a..)
-  p8_double<8, 1, 2>(As, tid);
-  p8_double<16, 2, 2>(As, tid);
-  p8_double<32, 2, 4>(As, tid);
+  // L (lower, r >= c) into the panel; X (lower, zero elsewhere) into the inverse slot
   double* W = linv + (long long)T.slot * (NBMAX * NBMAX);
-  for (int e = tid; e < NBMAX * NBMAX; e += POTRF8_THREADS) {
-    const int c = e / NBMAX, r = e % NBMAX;
-    W[e] = (r >= c && r < nb && c < nb) ? As[r * P8_LD + c] : 0.0;
+  for (int e = tid; e < NBMAX * NBMAX / 2; e += POTRF9_THREADS) {
+    const int c = e >> 5, r = (e & 31) * 2;
+    const double2 l = *reinterpret_cast<const double2*>(Ls + c * P9_LD + r);
+    const double2 x = *reinterpret_cast<const double2*>(Xs + c * P9_LD + r);
+    const bool in0 = r >= c && r < nb && c < nb, in1 = r + 1 >= c && r + 1 < nb && c < nb;
+    *reinterpret_cast<double2*>(W + e * 2) = make_double2(in0 ? x.x : 0.0, in1 ? x.y : 0.0);
+    double* d = P + (long long)c * S.ld + r;
+    if (in0 && in1) *reinterpret_cast<double2*>(d) = l;
+    else {
+      if (in0) d[0] = l.x;
+      if (in1) d[1] = l.y;
+    }
   }
+  P9_CLK(20);
 }
 
 __global__ void init_scatter_kernel(const double* __restrict__ vals, const long long* __restrict__ amap,
@@ -1361,7 +1374,7 @@ __global__ void gather_kernel(const double* __restrict__ src, const long long* _
 // ---------------------------------------------------------------------------------------------- launchers
 cudaError_t kernels_init_attributes() {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(potrf8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF8_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(potrf9_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF9_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 1 + 4) * SMALL_MAXK + 8 * 32 * 1) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 2 + 4) * SMALL_MAXK + 8 * 32 * 2) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 4 + 4) * SMALL_MAXK + 8 * 32 * 4) * 8))) return e;
@@ -1462,7 +1475,7 @@ void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels, double* linv,
                   unsigned long long* fail, cudaStream_t st, int prio) {
   if (ntasks <= 0) return;
-  launch_prio(potrf8_kernel, ntasks, POTRF8_THREADS, POTRF8_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
+  launch_prio(potrf9_kernel, ntasks, POTRF9_THREADS, POTRF9_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
 }
 
 
@@ -1484,6 +1497,18 @@ void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst
               ucol_base, ucol_map, posmap, fail, plain);
 }
 
+__global__ void init_list_kernel(const double* __restrict__ vals, const long long* __restrict__ idx,
+                                 const long long* __restrict__ dst, long long cnt, double* panels) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < cnt; e += (long long)gridDim.x * blockDim.x)
+    panels[dst[e]] = vals[idx[e]];
+}
+void launch_init_list(const double* vals, const long long* idx, const long long* dst, long long cnt, double* panels,
+                      cudaStream_t st) {
+  if (cnt <= 0) return;
+  long long blocks = (cnt + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  init_list_kernel<<<(int)blocks, 256, 0, st>>>(vals, idx, dst, cnt, panels);
+}
 void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st) {
   if (nnz <= 0) return;
   long long blocks = (nnz + 255) / 256;

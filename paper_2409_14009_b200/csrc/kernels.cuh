@@ -1,7 +1,7 @@
 // sm_100a device kernels of the numeric RL factorization (arXiv 2409.14009, §II.A "RL").
 // P:n = PAPER.md line n.  All arithmetic is FP64 ("D" BLAS).
 //
-//   potrf8_kernel       a3: cdiv POTRF of one <=64-column diagonal block in shared memory, plus its
+//   potrf9_kernel       a3: cdiv POTRF of one <=64-column diagonal block in shared memory, plus its
 //                       triangular inverse (used by TRSM-as-GEMM)               ("DPOTRF")
 //   gemm_kernel<MODE>   FP64 DMMA (mma.sync m8n8k4) 64x64 tile, cp.async 3-stage smem pipeline
 //     MODE_TRSM         a4: L_{R,b} = A_{R,b} L_bb^{-T}                          ("DTRSM")
@@ -124,6 +124,9 @@ void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst
                   const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,
                   int smem_doubles, int maxm, int plain, cudaStream_t st, int prio = 0, int maxk = 0);
 void launch_init(const double* vals, const long long* amap, long long nnz, double* panels, cudaStream_t st);
+// a1 for a subset of A's entries (memory-capped mode: one batch): panels[dst[i]] = vals[idx[i]]
+void launch_init_list(const double* vals, const long long* idx, const long long* dst, long long cnt, double* panels,
+                      cudaStream_t st);
 // Small-supernode solve record (one per supernode, in level / row-class order).
 struct SmallSolve {
   long long off, rp;   // panel offset, rows_ptr[J]

@@ -129,3 +129,24 @@ def test_deterministic_option_plan():
         assert h1.query("LAUNCHES") > h0.query("LAUNCHES")
         assert h1.query("NSUPER") == h0.query("NSUPER")
     assert _err(lambda: sp.Solver.from_problem(p, device=-1, deterministic=1, update_mode=1)) == sp.SPCHOL_ERR_VALIDATION
+
+
+def test_memory_capped_plan():
+    """Memory-capped mode on a host-only handle: the factor's device storage stays under the cap with at
+    least two subtree batches; a cap below the resident top fails with DEVICE_OOM; the cap is a
+    single-GPU option."""
+    p = gen.make("S4")
+    with sp.Solver.from_problem(p, device=-1) as h:
+        full = h.query("ARENA_BYTES")
+        assert h.query("NBATCHES") == 0
+    for frac in (0.75, 0.6):
+        cap = int(frac * full)
+        with sp.Solver.from_problem(p, device=-1, device_mem_cap=cap) as h:
+            assert h.query("NBATCHES") >= 2 and h.query("ARENA_BYTES") <= cap
+            assert h.query("HOST_BYTES") > 0
+    with pytest.raises(sp.SpcholError) as e:
+        sp.Solver.from_problem(p, device=-1, device_mem_cap=int(0.1 * full))
+    assert e.value.code == sp.SPCHOL_ERR_DEVICE_OOM
+    with pytest.raises(sp.SpcholError) as e:
+        sp.Solver.from_problem(p, device=-1, device_mem_cap=int(0.6 * full), dist_world=2, dist_rank=0)
+    assert e.value.code == sp.SPCHOL_ERR_VALIDATION

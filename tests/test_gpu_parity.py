@@ -285,3 +285,43 @@ def test_distributed_not_spd_mock(name, world, frac, minflops):
     real NCCL code path over the single-process stand-in."""
     r = run_mock(name, world, {"SPCHOL_DIST_MINFLOPS": minflops} if minflops is not None else {}, args=(frac,))
     assert r["ok"], r
+
+
+def _arena(prob):
+    with sp.Solver.from_problem(prob, device=-1) as h:
+        return h.query("ARENA_BYTES")
+
+
+@pytest.mark.parametrize("name,frac", [("S2", 0.6), ("S3", 0.6), ("S4", 0.6), ("S5", 0.6), ("C1", 0.6), ("T3", 0.75)])
+def test_memory_capped_parity(name, frac):
+    """Memory-capped mode (f-4): the device storage is capped below the panel footprint; the
+    subtree batches run in one device window and go to pinned host memory, the solve streams them
+    back.  Same parity bar as the resident factor (oracle, padding, exact-pattern CSC, solve)."""
+    prob = gen.make(name)
+    cap = int(frac * _arena(prob))
+    run_parity(prob, device_mem_cap=cap)
+    with sp.Solver.from_problem(prob, device_mem_cap=cap) as h:
+        assert h.query("NBATCHES") >= 2
+        assert h.query("ARENA_BYTES") <= cap
+
+
+def test_memory_capped_fullsize_C3():
+    """C3 (n = 262144) with the factor's device storage capped at half its footprint: closed-form log
+    det, backward error, and the exact-result check L L^T = C_f on the top levels."""
+    from helpers import llt_sample_error, top_level_columns
+    p = gen.make("C3")
+    cap = int(0.5 * _arena(p))
+    with sp.Solver.from_problem(p, device_mem_cap=cap) as h:
+        assert h.query("NBATCHES") >= 2 and h.query("ARENA_BYTES") <= cap
+        h.spchol_factor()
+        h.spchol_factor()
+        ld = logdet_from_diag(h.spchol_export_diagonal())
+        ref = grid_logdet(p.kind, p.grid, p.dof)
+        assert abs(ld - ref) <= 1e-10 * abs(ref)
+        xs, b = gen.rhs(p)
+        x = h.spchol_solve(b)
+        assert backward_error(p, x, b) <= TOL_BERR
+        sym = h.spchol_export_symbolic()
+        off, ldv, pan = h.spchol_export_panels()
+    err, cnt = llt_sample_error(p, sym, off, ldv, pan, top_level_columns(sym, nlev=3, per_sn=3))
+    assert err <= 1e-12 and cnt >= 10 ** 4
