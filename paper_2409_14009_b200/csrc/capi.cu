@@ -940,8 +940,8 @@ static int setup_device(spchol_handle* h) {
   CK(upload(&h->d_stasks, h->stasks));
   CK(upload(&h->d_ssolve, h->ssolve));
   CK(dalloc(&h->d_sflags, (size_t)3 * std::max(1, h->nslots_total) + h->nticket + 1));
-  CK(dalloc(&h->d_y, (size_t)S.n));
-  CK(dalloc(&h->d_y2, (size_t)S.n));
+  CK(dalloc(&h->d_y, (size_t)S.n * SOLVE_NRMAX));
+  CK(dalloc(&h->d_y2, (size_t)S.n * SOLVE_NRMAX));
   h->device_bytes = g_dev_bytes;
   return SPCHOL_OK;
 }
@@ -949,8 +949,10 @@ static int setup_device(spchol_handle* h) {
 static void free_device(spchol_handle* h) {
   for (void* c : h->grp_comms) if (c && g_nccl.destroy) g_nccl.destroy(c);
   if (h->nccl_comm && g_nccl.destroy) g_nccl.destroy(h->nccl_comm);
-  if (h->solve_gexec) cudaGraphExecDestroy(h->solve_gexec);
-  if (h->solve_graph) cudaGraphDestroy(h->solve_graph);
+  for (int i = 0; i < 3; ++i) {
+    if (h->solve_gexec[i]) cudaGraphExecDestroy(h->solve_gexec[i]);
+    if (h->solve_graph[i]) cudaGraphDestroy(h->solve_graph[i]);
+  }
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->graph) cudaGraphDestroy(h->graph);
   if (h->world > 1) dist_free_device(h);   // the VMM arenas (d_panels, d_linv)
@@ -1430,9 +1432,9 @@ extern "C" int spchol_factor(spchol_handle* h, int64_t* fail_col, int64_t* fail_
 // the diagonal blocks are applied with the inverses kept from the factor (X_bb = L_bb^{-1}).
 // Memory-capped solve: forward batch by batch (each copied back into the window), then the resident
 // top; backward the top, then the batches in reverse (copied back again).
-static int enqueue_solve_capped(spchol_handle* h, const double* d_b, double* d_x, cudaStream_t st) {
+static int enqueue_solve_capped(spchol_handle* h, const double* d_b, double* d_x, int nr, cudaStream_t st) {
   const Symbolic& S = h->S;
-  launch_permute(h->d_perm, d_b, h->d_y, S.n, 0, st);
+  launch_permute(h->d_perm, d_b, h->d_y, S.n, nr, 0, st);
   const size_t NS = (size_t)std::max(1, h->nslots_total);
   int* fflag = h->d_sflags;
   int* bflag = fflag + NS;
@@ -1445,9 +1447,9 @@ static int enqueue_solve_capped(spchol_handle* h, const double* d_b, double* d_x
     for (int l = 0; l < nl; ++l) {
       for (int cl = 0; cl < 3; ++cl)
         launch_solve_small(h->d_ssolve + G.ss[3 * l + cl], G.ss[3 * l + cl + 1] - G.ss[3 * l + cl], cl, 0, h->d_rows,
-                           h->d_panels, h->d_y, st);
+                           h->d_panels, h->d_y, nr, st);
       launch_solve_fwd_level(h->d_stasks + G.fwd[l], (int)(G.bwd[l] - G.fwd[l]), tickets + 2 * (g * nl + l), fflag,
-                             h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, st);
+                             h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, nr, st);
     }
   };
   auto bwd = [&](int g) {
@@ -1455,10 +1457,10 @@ static int enqueue_solve_capped(spchol_handle* h, const double* d_b, double* d_x
     for (int l = nl - 1; l >= 0; --l) {
       launch_solve_bwd_level(h->d_stasks + G.bwd[l], (int)(G.fwd[l + 1] - G.bwd[l]), tickets + 2 * (g * nl + l) + 1,
                              bflag, rcnt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y,
-                             h->nb, st);
+                             h->nb, nr, st);
       for (int cl = 0; cl < 3; ++cl)
         launch_solve_small(h->d_ssolve + G.ss[3 * l + cl], G.ss[3 * l + cl + 1] - G.ss[3 * l + cl], cl, 1, h->d_rows,
-                           h->d_panels, h->d_y, st);
+                           h->d_panels, h->d_y, nr, st);
     }
   };
   for (int b = 0; b < h->nbatch; ++b) {
@@ -1473,15 +1475,15 @@ static int enqueue_solve_capped(spchol_handle* h, const double* d_b, double* d_x
                        cudaMemcpyHostToDevice, st));
     bwd(b);
   }
-  launch_permute(h->d_perm, h->d_y, d_x, S.n, 1, st);
+  launch_permute(h->d_perm, h->d_y, d_x, S.n, nr, 1, st);
   CK(cudaGetLastError());
   return SPCHOL_OK;
 }
 
-static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaStream_t st) {
-  if (h->capped) return enqueue_solve_capped(h, d_b, d_x, st);
+static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, int nr, cudaStream_t st) {
+  if (h->capped) return enqueue_solve_capped(h, d_b, d_x, nr, st);
   const Symbolic& S = h->S;
-  launch_permute(h->d_perm, d_b, h->d_y, S.n, 0, st);
+  launch_permute(h->d_perm, d_b, h->d_y, S.n, nr, 0, st);
   const size_t NS = (size_t)std::max(1, h->nslots_total);
   int* fflag = h->d_sflags;
   int* bflag = fflag + NS;
@@ -1491,53 +1493,73 @@ static int enqueue_solve(spchol_handle* h, const double* d_b, double* d_x, cudaS
   for (int l = 0; l < S.nlevels; ++l) {
     for (int cl = 0; cl < 3; ++cl)
       launch_solve_small(h->d_ssolve + h->ssolve_off[3 * l + cl], h->ssolve_off[3 * l + cl + 1] - h->ssolve_off[3 * l + cl],
-                         cl, 0, h->d_rows, h->d_panels, h->d_y, st);
+                         cl, 0, h->d_rows, h->d_panels, h->d_y, nr, st);
     launch_solve_fwd_level(h->d_stasks + h->sfwd_off[l], (int)(h->sbwd_off[l] - h->sfwd_off[l]), tickets + 2 * l, fflag,
-                           h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, st);
+                           h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, nr, st);
   }
   for (int l = S.nlevels - 1; l >= 0; --l) {
     launch_solve_bwd_level(h->d_stasks + h->sbwd_off[l], (int)(h->sfwd_off[l + 1] - h->sbwd_off[l]), tickets + 2 * l + 1,
                            bflag, rcnt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y,
-                           h->nb, st);
+                           h->nb, nr, st);
     for (int cl = 0; cl < 3; ++cl)
       launch_solve_small(h->d_ssolve + h->ssolve_off[3 * l + cl], h->ssolve_off[3 * l + cl + 1] - h->ssolve_off[3 * l + cl],
-                         cl, 1, h->d_rows, h->d_panels, h->d_y, st);
+                         cl, 1, h->d_rows, h->d_panels, h->d_y, nr, st);
   }
-  launch_permute(h->d_perm, h->d_y, d_x, S.n, 1, st);
+  launch_permute(h->d_perm, h->d_y, d_x, S.n, nr, 1, st);
   CK(cudaGetLastError());
   return SPCHOL_OK;
 }
 
 // One solve of the internal buffer d_y2 in place, captured in a CUDA graph on first use.
 // Multi-GPU: the distributed solve (dist_enqueue_solve) is collective — every rank of the handle's
-// communicator calls the solve the same number of times.
-static int any_solve(spchol_handle* h, cudaStream_t st) {
-  return h->world > 1 ? dist_enqueue_solve(h, h->d_y2, st) : enqueue_solve(h, h->d_y2, h->d_y2, st);
+// communicator calls the solve the same number of times (and with the same nrhs).
+static int any_solve(spchol_handle* h, int nr, cudaStream_t st) {
+  return h->world > 1 ? dist_enqueue_solve(h, h->d_y2, nr, st) : enqueue_solve(h, h->d_y2, h->d_y2, nr, st);
 }
-static int run_solve_y2(spchol_handle* h) {
+// One solve of the nr right-hand sides staged in d_y2 (column-major, ld n), in place; captured in a
+// CUDA graph per nr on first use.
+static int run_solve_y2(spchol_handle* h, int nr) {
   // multi-GPU: captured from the second solve on, as the factor
   const bool graph = h->opt.use_graph &&
                      (h->world == 1 || (g_nccl.capturable && h->dist_solve_eager_done && !h->dist_capture_failed));
   h->dist_solve_eager_done = true;
-  if (!graph) return any_solve(h, h->stream);
-  if (!h->solve_gexec) {
+  if (!graph) return any_solve(h, nr, h->stream);
+  const int gi = nr == 4 ? 2 : nr == 2 ? 1 : 0;
+  if (!h->solve_gexec[gi]) {
     cudaStream_t cs = h->own_stream;
     CK(cudaStreamBeginCapture(cs, h->world > 1 ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal));
-    int rc = any_solve(h, cs);
+    int rc = any_solve(h, nr, cs);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(cs, &g);
     if (h->world > 1 && (rc != SPCHOL_OK || e != cudaSuccess)) {   // stay eager (NCCL refused the capture)
       if (g) cudaGraphDestroy(g);
       cudaGetLastError();
       h->dist_capture_failed = true;
-      return any_solve(h, h->stream);
+      return any_solve(h, nr, h->stream);
     }
     if (rc != SPCHOL_OK) { if (g) cudaGraphDestroy(g); return rc; }
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture(solve)");
-    h->solve_graph = g;
-    CK(cudaGraphInstantiateWithFlags(&h->solve_gexec, g, 0));
+    h->solve_graph[gi] = g;
+    CK(cudaGraphInstantiateWithFlags(&h->solve_gexec[gi], g, 0));
   }
-  CK(cudaGraphLaunch(h->solve_gexec, h->stream));
+  CK(cudaGraphLaunch(h->solve_gexec[gi], h->stream));
+  return SPCHOL_OK;
+}
+
+// nrhs right-hand sides in blocks of 4, 2, 1 (each block one pass over L).
+static int solve_blocks(spchol_handle* h, const double* b, double* x, int32_t nrhs, int64_t ld, cudaMemcpyKind kin,
+                        cudaMemcpyKind kout) {
+  const size_t n = (size_t)h->S.n;
+  for (int r0 = 0; r0 < nrhs;) {
+    const int left = nrhs - r0, nr = left >= 4 ? 4 : left >= 2 ? 2 : 1;
+    CK(cudaMemcpy2DAsync(h->d_y2, n * sizeof(double), b + (size_t)r0 * ld, (size_t)ld * sizeof(double), n * sizeof(double),
+                         nr, kin, h->stream));
+    int rc = run_solve_y2(h, nr);
+    if (rc != SPCHOL_OK) return rc;
+    CK(cudaMemcpy2DAsync(x + (size_t)r0 * ld, (size_t)ld * sizeof(double), h->d_y2, n * sizeof(double), n * sizeof(double),
+                         nr, kout, h->stream));
+    r0 += nr;
+  }
   return SPCHOL_OK;
 }
 
@@ -1546,14 +1568,7 @@ extern "C" int spchol_solve_device(spchol_handle* h, const double* d_b, double* 
   if (host_only(h) || !h->factored) return fail(SPCHOL_ERR_STATE, "solve before a successful factor");
   if (nrhs < 1 || ld < h->S.n) return fail(SPCHOL_ERR_DIMENSION, "nrhs < 1 or ld < n");
   CK(cudaSetDevice(h->opt.device));
-  const size_t nbytes = sizeof(double) * (size_t)h->S.n;
-  for (int r = 0; r < nrhs; ++r) {
-    CK(cudaMemcpyAsync(h->d_y2, d_b + (size_t)r * ld, nbytes, cudaMemcpyDeviceToDevice, h->stream));
-    int rc = run_solve_y2(h);
-    if (rc != SPCHOL_OK) return rc;
-    CK(cudaMemcpyAsync(d_x + (size_t)r * ld, h->d_y2, nbytes, cudaMemcpyDeviceToDevice, h->stream));
-  }
-  return SPCHOL_OK;
+  return solve_blocks(h, d_b, d_x, nrhs, ld, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice);
 }
 
 extern "C" int spchol_solve(spchol_handle* h, const double* b, double* x, int32_t nrhs, int64_t ld) {
@@ -1561,13 +1576,8 @@ extern "C" int spchol_solve(spchol_handle* h, const double* b, double* x, int32_
   if (host_only(h) || !h->factored) return fail(SPCHOL_ERR_STATE, "solve before a successful factor");
   if (nrhs < 1 || ld < h->S.n) return fail(SPCHOL_ERR_DIMENSION, "nrhs < 1 or ld < n");
   CK(cudaSetDevice(h->opt.device));
-  const size_t nbytes = sizeof(double) * (size_t)h->S.n;
-  for (int r = 0; r < nrhs; ++r) {
-    CK(cudaMemcpyAsync(h->d_y2, b + (size_t)r * ld, nbytes, cudaMemcpyHostToDevice, h->stream));
-    int rc = run_solve_y2(h);
-    if (rc != SPCHOL_OK) return rc;
-    CK(cudaMemcpyAsync(x + (size_t)r * ld, h->d_y2, nbytes, cudaMemcpyDeviceToHost, h->stream));
-  }
+  int rc = solve_blocks(h, b, x, nrhs, ld, cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost);
+  if (rc) return rc;
   CK(cudaStreamSynchronize(h->stream));
   return SPCHOL_OK;
 }

@@ -564,7 +564,7 @@ int dist_enqueue_bcast(spchol_handle* h, cudaStream_t st, int J, int C) {
 }
 
 // Distributed solve of the permuted system in place on d_y2 (original numbering in and out).
-int dist_enqueue_solve(spchol_handle* h, double* d_y2, cudaStream_t st) {
+int dist_enqueue_solve(spchol_handle* h, double* d_y2, int nr, cudaStream_t st) {
   if (!h->nccl_comm) return fail(SPCHOL_ERR_STATE, "multi-GPU handle without an NCCL communicator");
   const Symbolic& S = h->S;
   const size_t NS = (size_t)std::max(1, h->nslots_total);
@@ -573,45 +573,45 @@ int dist_enqueue_solve(spchol_handle* h, double* d_y2, cudaStream_t st) {
   int* rcnt = bflag + NS;
   int* tickets = rcnt + NS;
   CK(cudaMemsetAsync(h->d_sflags, 0, sizeof(int) * (3 * NS + h->nticket), st));
-  launch_permute_masked(h->d_perm, h->d_row_mine, d_y2, h->d_y, S.n, 0, st);   // b counted once: on its row's owner
+  launch_permute_masked(h->d_perm, h->d_row_mine, d_y2, h->d_y, S.n, nr, 0, st);   // b counted once: on its row's owner
   for (int l = 0; l < S.nlevels; ++l) {
     for (int cl = 0; cl < 3; ++cl)
       launch_solve_small(h->d_ssolve + h->ssolve_off[3 * l + cl], h->ssolve_off[3 * l + cl + 1] - h->ssolve_off[3 * l + cl],
-                         cl, 0, h->d_rows, h->d_panels, h->d_y, st);
+                         cl, 0, h->d_rows, h->d_panels, h->d_y, nr, st);
     launch_solve_fwd_level(h->d_stasks + h->sfwd_off[l], (int)(h->sbwd_off[l] - h->sfwd_off[l]), tickets + 2 * l, fflag,
-                           h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, st);
+                           h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, nr, st);
   }
   int* tt = tickets + 2 * S.nlevels;
   for (size_t s = 0; s < h->tsteps.size(); ++s) {   // forward: the block's partial sums onto its owner
     const TStep& T = h->tsteps[s];
     if (!in_group(h, T.J, h->rank)) continue;
-    double* yb = h->d_y + S.sfirst[T.J] + T.c0;
-    const int rc = g_nccl.reduce(yb, yb, (size_t)(T.c1 - T.c0), NCCL_FLOAT64, NCCL_SUM, T.o - h->grp_lo[T.J], group_comm(h, T.J), st);
+    double* yb = h->d_y + (size_t)(S.sfirst[T.J] + T.c0) * nr;
+    const int rc = g_nccl.reduce(yb, yb, (size_t)(T.c1 - T.c0) * nr, NCCL_FLOAT64, NCCL_SUM, T.o - h->grp_lo[T.J], group_comm(h, T.J), st);
     if (rc) return nccl_fail(rc, "ncclReduce(solve block)");
     if (T.o == h->rank)
       launch_solve_fwd_level(h->d_stasks + T.f0, (int)(T.f1 - T.f0), tt + 2 * s, fflag, h->d_sn, h->d_sfirst, h->d_rows_ptr,
-                             h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, st);
+                             h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, nr, st);
   }
   for (size_t s = h->tsteps.size(); s-- > 0;) {   // backward: the block's solution to the group
     const TStep& T = h->tsteps[s];
     if (!in_group(h, T.J, h->rank)) continue;
     if (T.o == h->rank)
       launch_solve_bwd_level(h->d_stasks + T.b0, (int)(T.b1 - T.b0), tt + 2 * s + 1, bflag, rcnt, h->d_sn, h->d_sfirst,
-                             h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, st);
-    double* yb = h->d_y + S.sfirst[T.J] + T.c0;
-    const int rc = g_nccl.bcast(yb, yb, (size_t)(T.c1 - T.c0), NCCL_FLOAT64, T.o - h->grp_lo[T.J], group_comm(h, T.J), st);
+                             h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y, h->nb, nr, st);
+    double* yb = h->d_y + (size_t)(S.sfirst[T.J] + T.c0) * nr;
+    const int rc = g_nccl.bcast(yb, yb, (size_t)(T.c1 - T.c0) * nr, NCCL_FLOAT64, T.o - h->grp_lo[T.J], group_comm(h, T.J), st);
     if (rc) return nccl_fail(rc, "ncclBroadcast(solve block)");
   }
   for (int l = S.nlevels - 1; l >= 0; --l) {
     launch_solve_bwd_level(h->d_stasks + h->sbwd_off[l], (int)(h->sfwd_off[l + 1] - h->sbwd_off[l]), tickets + 2 * l + 1,
                            bflag, rcnt, h->d_sn, h->d_sfirst, h->d_rows_ptr, h->d_rows, h->d_panels, h->d_linv, h->d_y,
-                           h->nb, st);
+                           h->nb, nr, st);
     for (int cl = 0; cl < 3; ++cl)
       launch_solve_small(h->d_ssolve + h->ssolve_off[3 * l + cl], h->ssolve_off[3 * l + cl + 1] - h->ssolve_off[3 * l + cl],
-                         cl, 1, h->d_rows, h->d_panels, h->d_y, st);
+                         cl, 1, h->d_rows, h->d_panels, h->d_y, nr, st);
   }
-  launch_permute_masked(h->d_perm, h->d_row_mine, h->d_y, d_y2, S.n, 1, st);   // each component from its holder
-  const int rc = g_nccl.allreduce(d_y2, d_y2, (size_t)S.n, NCCL_FLOAT64, NCCL_SUM, h->nccl_comm, st);
+  launch_permute_masked(h->d_perm, h->d_row_mine, h->d_y, d_y2, S.n, nr, 1, st);   // each component from its holder
+  const int rc = g_nccl.allreduce(d_y2, d_y2, (size_t)S.n * nr, NCCL_FLOAT64, NCCL_SUM, h->nccl_comm, st);
   if (rc) return nccl_fail(rc, "ncclAllReduce(solution)");
   CK(cudaGetLastError());
   return SPCHOL_OK;

@@ -261,8 +261,8 @@ struct spchol_handle {
   int prio_lo = 0, prio_hi = 0;
   std::vector<cudaEvent_t> plan_events;
   // graph
-  cudaGraph_t graph = nullptr, solve_graph = nullptr;
-  cudaGraphExec_t gexec = nullptr, solve_gexec = nullptr;
+  cudaGraph_t graph = nullptr, solve_graph[3] = {nullptr, nullptr, nullptr};   // solve: per nr = 1, 2, 4
+  cudaGraphExec_t gexec = nullptr, solve_gexec[3] = {nullptr, nullptr, nullptr};
   // timing
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -301,6 +301,6 @@ void dist_free_device(spchol_handle* h);
 int dist_enqueue_init(spchol_handle* h, cudaStream_t st);
 int dist_enqueue_exchange(spchol_handle* h, cudaStream_t st, int e);
 int dist_enqueue_bcast(spchol_handle* h, cudaStream_t st, int J, int C);
-int dist_enqueue_solve(spchol_handle* h, double* d_y2, cudaStream_t st);
+int dist_enqueue_solve(spchol_handle* h, double* d_y2, int nr, cudaStream_t st);
 bool dist_owns(const spchol_handle* h, int J, int col);  // this rank holds column col of supernode J
 }  // namespace spchol

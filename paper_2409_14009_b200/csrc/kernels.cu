@@ -1036,24 +1036,29 @@ __device__ __forceinline__ void sw_load_cols(double (&Lb)[CH][ROWS], const doubl
     }
 }
 
-template <int ROWS, int CH>
-__device__ __forceinline__ void sw_fwd_cols(const double (&Lb)[CH][ROWS], double (&v)[ROWS], double dinv0, double dinv1,
-                                            int k, int c0, int lane) {
+// Right-hand-side blocks: the solve's work vector y holds NR right-hand sides interleaved
+// (y[i * NR + r] = component i of right-hand side r), so one pass over L serves all NR of them.
+template <int ROWS, int CH, int NR>
+__device__ __forceinline__ void sw_fwd_cols(const double (&Lb)[CH][ROWS], double (&v)[ROWS][NR], double dinv0,
+                                            double dinv1, int k, int c0, int lane) {
 #pragma unroll
   for (int j = 0; j < CH; ++j) {
     const int c = c0 + j;
     if (c >= k) break;
     const bool lo = c < 32;
-    const double yc = __shfl_sync(0xffffffffu, lo ? v[0] : v[ROWS > 1 ? 1 : 0], c & 31);
-    const double xc = yc * __shfl_sync(0xffffffffu, lo ? dinv0 : dinv1, c & 31);
-    if (lane == (c & 31)) { if (lo) v[0] = xc; else v[ROWS > 1 ? 1 : 0] = xc; }
+    const double dc = __shfl_sync(0xffffffffu, lo ? dinv0 : dinv1, c & 31);
 #pragma unroll
-    for (int i = 0; i < ROWS; ++i) v[i] -= Lb[j][i] * xc;
+    for (int r = 0; r < NR; ++r) {
+      const double xc = __shfl_sync(0xffffffffu, lo ? v[0][r] : v[ROWS > 1 ? 1 : 0][r], c & 31) * dc;
+      if (lane == (c & 31)) { if (lo) v[0][r] = xc; else v[ROWS > 1 ? 1 : 0][r] = xc; }
+#pragma unroll
+      for (int i = 0; i < ROWS; ++i) v[i][r] -= Lb[j][i] * xc;
+    }
   }
 }
 
 // Forward: y_J := L_JJ^{-1} y_J, then y[rows(J)[r]] -= (L_RJ y_J)_r (RED: ancestors are shared).
-template <int ROWS>
+template <int ROWS, int NR>
 __global__ void __launch_bounds__(32 * SW_WARPS, ROWS >= 4 ? 2 : 3) solve_fwd_small_kernel(const SmallSolve* __restrict__ info, int count,
                                                                         const int* __restrict__ rows,
                                                                         const double* __restrict__ panels, double* y) {
@@ -1066,30 +1071,34 @@ __global__ void __launch_bounds__(32 * SW_WARPS, ROWS >= 4 ? 2 : 3) solve_fwd_sm
   sw_load_cols<ROWS, CH>(La, P, I.ld, I.m, I.k, 0, lane);
   const double dinv0 = lane < I.k ? 1.0 / P[(long long)lane * I.ld + lane] : 0.0;
   const double dinv1 = lane + 32 < I.k ? 1.0 / P[(long long)(lane + 32) * I.ld + lane + 32] : 0.0;
-  double v[ROWS];
+  double v[ROWS][NR];
 #pragma unroll
   for (int i = 0; i < ROWS; ++i) {
-    const int r = lane + 32 * i;
-    v[i] = r < I.k ? y[I.f + r] : 0.0;
+    const int q = lane + 32 * i;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) v[i][r] = q < I.k ? y[(long long)(I.f + q) * NR + r] : 0.0;
   }
   for (int c0 = 0; c0 < I.k; c0 += 2 * CH) {
     sw_load_cols<ROWS, CH>(Lb, P, I.ld, I.m, I.k, c0 + CH, lane);
-    sw_fwd_cols<ROWS, CH>(La, v, dinv0, dinv1, I.k, c0, lane);
+    sw_fwd_cols<ROWS, CH, NR>(La, v, dinv0, dinv1, I.k, c0, lane);
     if (c0 + CH >= I.k) break;
     sw_load_cols<ROWS, CH>(La, P, I.ld, I.m, I.k, c0 + 2 * CH, lane);
-    sw_fwd_cols<ROWS, CH>(Lb, v, dinv0, dinv1, I.k, c0 + CH, lane);
+    sw_fwd_cols<ROWS, CH, NR>(Lb, v, dinv0, dinv1, I.k, c0 + CH, lane);
   }
   const int* R = rows + I.rp;
 #pragma unroll
   for (int i = 0; i < ROWS; ++i) {
-    const int r = lane + 32 * i;
-    if (r < I.k) y[I.f + r] = v[i];
-    else if (r < I.m) atomicAdd(y + R[r], v[i]);
+    const int q = lane + 32 * i;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      if (q < I.k) y[(long long)(I.f + q) * NR + r] = v[i][r];
+      else if (q < I.m) atomicAdd(y + (long long)R[q] * NR + r, v[i][r]);
+    }
   }
 }
 
 // Backward: y_J := L_JJ^{-T} (y_J - L_RJ^T y_R).
-template <int ROWS>
+template <int ROWS, int NR>
 __global__ void __launch_bounds__(32 * SW_WARPS, ROWS >= 8 ? 2 : 3) solve_bwd_small_kernel(const SmallSolve* __restrict__ info, int count,
                                                                         const int* __restrict__ rows,
                                                                         const double* __restrict__ panels, double* y) {
@@ -1099,41 +1108,53 @@ __global__ void __launch_bounds__(32 * SW_WARPS, ROWS >= 8 ? 2 : 3) solve_bwd_sm
   const SmallSolve I = info[w];
   const double* P = panels + I.off;
   const int* R = rows + I.rp;
-  double yr[ROWS];   // y at the rows below the triangle (final values of the ancestors)
+  double yr[ROWS][NR];   // y at the rows below the triangle (final values of the ancestors)
 #pragma unroll
   for (int i = 0; i < ROWS; ++i) {
-    const int r = lane + 32 * i;
-    yr[i] = (r >= I.k && r < I.m) ? y[R[r]] : 0.0;
+    const int q = lane + 32 * i;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) yr[i][r] = (q >= I.k && q < I.m) ? y[(long long)R[q] * NR + r] : 0.0;
   }
-  // t_c = y_c - sum_{r >= k} L_rc y_r: lane c (and c + 32) keeps t_c
-  double t0 = lane < I.k ? y[I.f + lane] : 0.0, t1 = lane + 32 < I.k ? y[I.f + lane + 32] : 0.0;
+  // t_c = y_c - sum_{q >= k} L_qc y_q: lane c (and c + 32) keeps t_c
+  double t0[NR], t1[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    t0[r] = lane < I.k ? y[(long long)(I.f + lane) * NR + r] : 0.0;
+    t1[r] = lane + 32 < I.k ? y[(long long)(I.f + lane + 32) * NR + r] : 0.0;
+  }
   const double dinv0 = lane < I.k ? 1.0 / P[(long long)lane * I.ld + lane] : 0.0;
   const double dinv1 = lane + 32 < I.k ? 1.0 / P[(long long)(lane + 32) * I.ld + lane + 32] : 0.0;
   if (I.m > I.k)
     for (int c0 = 0; c0 < I.k; c0 += CH) {
-      double sj[CH];
+      double sj[CH][NR];
 #pragma unroll
       for (int j = 0; j < CH; ++j) {
         const int c = c0 + j;
-        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) sj[j][r] = 0.0;
 #pragma unroll
         for (int i = 0; i < ROWS; ++i) {
-          const int r = lane + 32 * i;
-          if (c < I.k && r >= I.k && r < I.m) s += P[(long long)c * I.ld + r] * yr[i];
+          const int q = lane + 32 * i;
+          const double l = (c < I.k && q >= I.k && q < I.m) ? P[(long long)c * I.ld + q] : 0.0;
+#pragma unroll
+          for (int r = 0; r < NR; ++r) sj[j][r] += l * yr[i][r];
         }
-        sj[j] = s;
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-        for (int j = 0; j < CH; ++j) sj[j] += __shfl_xor_sync(0xffffffffu, sj[j], o);
+        for (int j = 0; j < CH; ++j)
+#pragma unroll
+          for (int r = 0; r < NR; ++r) sj[j][r] += __shfl_xor_sync(0xffffffffu, sj[j][r], o);
 #pragma unroll
       for (int j = 0; j < CH; ++j) {
         const int c = c0 + j;
-        if (c < I.k && lane == (c & 31)) { if (c < 32) t0 -= sj[j]; else t1 -= sj[j]; }
+        if (c < I.k && lane == (c & 31))
+#pragma unroll
+          for (int r = 0; r < NR; ++r) { if (c < 32) t0[r] -= sj[j][r]; else t1[r] -= sj[j][r]; }
       }
     }
-  // triangle, right-looking transposed: x_c = t_c / L_cc, then t_r -= L_cr x_c for r < c
+  // triangle, right-looking transposed: x_c = t_c / L_cc, then t_q -= L_cq x_c for q < c
   for (int c1 = I.k; c1 > 0; c1 -= 8) {   // columns c1-1 .. c1-8
     double L0[8], L1[8];
 #pragma unroll
@@ -1147,14 +1168,21 @@ __global__ void __launch_bounds__(32 * SW_WARPS, ROWS >= 8 ? 2 : 3) solve_bwd_sm
       const int c = c1 - 1 - j;
       if (c < 0) break;
       const bool lo = c < 32;
-      const double xc = __shfl_sync(0xffffffffu, lo ? t0 : t1, c & 31) * __shfl_sync(0xffffffffu, lo ? dinv0 : dinv1, c & 31);
-      if (lane == (c & 31)) { if (lo) t0 = xc; else t1 = xc; }
-      t0 -= L0[j] * xc;
-      t1 -= L1[j] * xc;
+      const double dc = __shfl_sync(0xffffffffu, lo ? dinv0 : dinv1, c & 31);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const double xc = __shfl_sync(0xffffffffu, lo ? t0[r] : t1[r], c & 31) * dc;
+        if (lane == (c & 31)) { if (lo) t0[r] = xc; else t1[r] = xc; }
+        t0[r] -= L0[j] * xc;
+        t1[r] -= L1[j] * xc;
+      }
     }
   }
-  if (lane < I.k) y[I.f + lane] = t0;
-  if (lane + 32 < I.k) y[I.f + lane + 32] = t1;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    if (lane < I.k) y[(long long)(I.f + lane) * NR + r] = t0[r];
+    if (lane + 32 < I.k) y[(long long)(I.f + lane + 32) * NR + r] = t1[r];
+  }
 }
 
 // ------------------------------------------------------------------ sync-free level solve (large)
@@ -1187,15 +1215,16 @@ __device__ __forceinline__ void stage_inverse(double* Xs, const double* X) {
 }
 
 // Forward, one level: kind 0 = triangle row block b: x_b = X_b (y_b - sum_{c<b} L_bc x_c);
-// kind 1 = rows [q0, q1) below the triangle: y[rows(J)[q]] -= sum_c L_qc x_c.
+// kind 1 = rows [q0, q1) below the triangle: y[rows(J)[q]] -= sum_c L_qc x_c.  NR right-hand sides.
 // Thread (lane = tid & 63, grp = tid >> 6): row q0 + lane, columns grp + 4j of each block.
+template <int NR>
 __global__ void __launch_bounds__(SOLVE_THREADS) solve_fwd_level_kernel(
     const STask* __restrict__ tasks, int* ticket, int* flag, const SnInfo* __restrict__ sn,
     const int* __restrict__ sfirst, const long long* __restrict__ rows_ptr, const int* __restrict__ rows,
     const double* __restrict__ panels, const double* __restrict__ linv, double* y, int NB) {
   __shared__ double Xs[NBMAX * XLD];
-  __shared__ double xs[NBMAX];
-  __shared__ double part[4][NBMAX];
+  __shared__ double xs[NBMAX][NR];
+  __shared__ double part[4][NBMAX][NR];
   __shared__ int s_task;
   const int tid = threadIdx.x, lane = tid & 63, grp = tid >> 6;
   if (tid == 0) s_task = atomicAdd(ticket, 1);
@@ -1210,7 +1239,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS) solve_fwd_level_kernel(
   const bool rowok = q < T.q1;
   const double* Pq = panels + S.off + q;
   const int ncb = tri ? T.cb : T.cbhi;
-  double acc = 0.0;
+  double acc[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r] = 0.0;
   for (int cb = T.cblo; cb < ncb; ++cb) {
     const int nbc = min(NB, S.k - cb * NB);
     const double* Lc = Pq + (long long)(cb * NB) * S.ld;
@@ -1222,49 +1253,71 @@ __global__ void __launch_bounds__(SOLVE_THREADS) solve_fwd_level_kernel(
     }
     if (tid == 0) wait_geq(flag + slot0 + cb, 1);
     __syncthreads();
-    if (tid < NBMAX) xs[tid] = tid < nbc ? __ldcg(y + f + cb * NB + tid) : 0.0;
+    for (int e = tid; e < NBMAX * NR; e += SOLVE_THREADS) {
+      const int c = e / NR;
+      xs[c][e % NR] = c < nbc ? __ldcg(y + (long long)(f + cb * NB) * NR + e) : 0.0;
+    }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc += lv[j] * xs[grp + 4 * j];
+    for (int j = 0; j < 16; ++j)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) acc[r] += lv[j] * xs[grp + 4 * j][r];
   }
-  part[grp][lane] = acc;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) part[grp][lane][r] = acc[r];
   __syncthreads();
   if (tri) {
     const int nb = T.nb, b0 = T.cb * NB;
-    if (tid < NBMAX)
-      xs[tid] = tid < nb ? __ldcg(y + f + b0 + tid) - (part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid]) : 0.0;
+    for (int e = tid; e < NBMAX * NR; e += SOLVE_THREADS) {
+      const int c = e / NR, r = e % NR;
+      xs[c][r] = c < nb ? __ldcg(y + (long long)(f + b0) * NR + e) -
+                              (part[0][c][r] + part[1][c][r] + part[2][c][r] + part[3][c][r]) : 0.0;
+    }
     cp_async_wait_all();
     __syncthreads();
-    double s = 0.0;
+    double s[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) s[r] = 0.0;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int c = grp + 4 * j;
-      if (c <= lane && c < nb) s += Xs[c * XLD + lane] * xs[c];
+      if (c <= lane && c < nb) {
+        const double xv = Xs[c * XLD + lane];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) s[r] += xv * xs[c][r];
+      }
     }
-    part[grp][lane] = s;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) part[grp][lane][r] = s[r];
     __syncthreads();
-    if (tid < nb) y[f + b0 + tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
+    for (int e = tid; e < nb * NR; e += SOLVE_THREADS) {
+      const int c = e / NR, r = e % NR;
+      y[(long long)(f + b0) * NR + e] = part[0][c][r] + part[1][c][r] + part[2][c][r] + part[3][c][r];
+    }
     __syncthreads();
     if (tid == 0) {
       __threadfence();
       st_release(flag + T.slot, 1);
     }
   } else if (grp == 0 && rowok) {
-    atomicAdd(y + rows[rows_ptr[T.sn] + q], -(part[0][lane] + part[1][lane] + part[2][lane] + part[3][lane]));
+    const long long yq = (long long)rows[rows_ptr[T.sn] + q] * NR;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) atomicAdd(y + yq + r, -(part[0][lane][r] + part[1][lane][r] + part[2][lane][r] + part[3][lane][r]));
   }
 }
 
 // Backward, one level: kind 2 = y_cb -= L(q0:q1, cb)^T y[rows(J)[q0:q1]] (RED), then count;
 // kind 3 = x_cb = X_cb^T (y_cb - sum_{r>cb} L_{r,cb}^T x_r) once all kind-2 chunks of cb are in.
 // Thread (lane, grp): row lane of a 64-row chunk, columns grp + 4j; sums reduced over the lanes.
-__global__ void __launch_bounds__(SOLVE_THREADS, 2) solve_bwd_level_kernel(
+template <int NR>
+__global__ void __launch_bounds__(SOLVE_THREADS, NR >= 4 ? 1 : 2) solve_bwd_level_kernel(
     const STask* __restrict__ tasks, int* ticket, int* flag, int* rcnt, const SnInfo* __restrict__ sn,
     const int* __restrict__ sfirst, const long long* __restrict__ rows_ptr, const int* __restrict__ rows,
     const double* __restrict__ panels, const double* __restrict__ linv, double* y, int NB) {
   __shared__ double Xs[NBMAX * XLD];
-  __shared__ double xs[NBMAX];
-  __shared__ double part[4][NBMAX];
-  __shared__ double red[4][16][2];
+  __shared__ double xs[NBMAX][NR];
+  __shared__ double part[4][NBMAX][NR];
+  __shared__ double red[4][16][2][NR];
   __shared__ int s_task;
   const int tid = threadIdx.x, lane = tid & 63, grp = tid >> 6;
   if (tid == 0) s_task = atomicAdd(ticket, 1);
@@ -1277,49 +1330,65 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 2) solve_bwd_level_kernel(
   const int c0 = T.cb * NB, nbc = T.nb;
   const double* P = panels + S.off + (long long)c0 * S.ld;
   if (tri) stage_inverse(Xs, linv + (long long)T.slot * (NBMAX * NBMAX));
-  double acc[16];
+  double acc[16][NR];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+  for (int j = 0; j < 16; ++j)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[j][r] = 0.0;
   if (!tri) {
     const int* R = rows + rows_ptr[T.sn];
-    for (int r = T.q0 + lane; r < T.q1; r += 64) {
-      const double yv = y[R[r]];
+    for (int q = T.q0 + lane; q < T.q1; q += 64) {
+      double yv[NR];
+      const long long yq = (long long)R[q] * NR;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) yv[r] = y[yq + r];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int c = grp + 4 * j;
-        if (c < nbc) acc[j] += P[(long long)c * S.ld + r] * yv;
+        const double l = c < nbc ? P[(long long)c * S.ld + q] : 0.0;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) acc[j][r] += l * yv[r];
       }
     }
   } else {
     for (int rb = T.cbhi - 1; rb > T.cb; --rb) {
       const int nbr = min(NB, S.k - rb * NB);
-      const int r = rb * NB + lane;
+      const int q = rb * NB + lane;
       const bool ok = lane < nbr;
       double lv[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int c = grp + 4 * j;
-        lv[j] = (ok && c < nbc) ? P[(long long)c * S.ld + r] : 0.0;
+        lv[j] = (ok && c < nbc) ? P[(long long)c * S.ld + q] : 0.0;
       }
       if (tid == 0) wait_geq(flag + slot0 + rb, 1);
       __syncthreads();
-      if (tid < NBMAX) xs[tid] = tid < nbr ? __ldcg(y + f + rb * NB + tid) : 0.0;
+      for (int e = tid; e < NBMAX * NR; e += SOLVE_THREADS) {
+        const int c = e / NR;
+        xs[c][e % NR] = c < nbr ? __ldcg(y + (long long)(f + rb * NB) * NR + e) : 0.0;
+      }
       __syncthreads();
-      const double xv = xs[lane];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] += lv[j] * xv;
+      for (int j = 0; j < 16; ++j)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) acc[j][r] += lv[j] * xs[lane][r];
     }
   }
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    double v = acc[j];
+  for (int j = 0; j < 16; ++j)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((tid & 31) == 0) red[grp][j][(tid >> 5) & 1] = v;
-  }
+    for (int r = 0; r < NR; ++r) {
+      double v = acc[j][r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((tid & 31) == 0) red[grp][j][(tid >> 5) & 1][r] = v;
+    }
   __syncthreads();
   if (!tri) {
-    if (tid < nbc) atomicAdd(y + f + c0 + tid, -(red[tid & 3][tid >> 2][0] + red[tid & 3][tid >> 2][1]));
+    for (int e = tid; e < nbc * NR; e += SOLVE_THREADS) {
+      const int c = e / NR, r = e % NR;
+      atomicAdd(y + (long long)(f + c0) * NR + e, -(red[c & 3][c >> 2][0][r] + red[c & 3][c >> 2][1][r]));
+    }
     __syncthreads();
     if (tid == 0) {
       __threadfence();
@@ -1330,18 +1399,30 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 2) solve_bwd_level_kernel(
   if (tid == 0 && T.need > 0) wait_geq(rcnt + T.slot, T.need);
   cp_async_wait_all();
   __syncthreads();
-  if (tid < NBMAX)
-    xs[tid] = tid < nbc ? __ldcg(y + f + c0 + tid) - (red[tid & 3][tid >> 2][0] + red[tid & 3][tid >> 2][1]) : 0.0;
+  for (int e = tid; e < NBMAX * NR; e += SOLVE_THREADS) {
+    const int c = e / NR, r = e % NR;
+    xs[c][r] = c < nbc ? __ldcg(y + (long long)(f + c0) * NR + e) - (red[c & 3][c >> 2][0][r] + red[c & 3][c >> 2][1][r]) : 0.0;
+  }
   __syncthreads();
-  double s = 0.0;   // x_i = sum_{j >= i} X(j, i) v_j, thread i = lane, j = grp + 4jj
+  double s[NR];   // x_i = sum_{j >= i} X(j, i) v_j, thread i = lane, j = grp + 4jj
+#pragma unroll
+  for (int r = 0; r < NR; ++r) s[r] = 0.0;
 #pragma unroll
   for (int jj = 0; jj < 16; ++jj) {
     const int j = grp + 4 * jj;
-    if (j >= lane && j < nbc) s += Xs[lane * XLD + j] * xs[j];
+    if (j >= lane && j < nbc) {
+      const double xv = Xs[lane * XLD + j];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) s[r] += xv * xs[j][r];
+    }
   }
-  part[grp][lane] = s;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) part[grp][lane][r] = s[r];
   __syncthreads();
-  if (tid < nbc) y[f + c0 + tid] = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
+  for (int e = tid; e < nbc * NR; e += SOLVE_THREADS) {
+    const int c = e / NR, r = e % NR;
+    y[(long long)(f + c0) * NR + e] = part[0][c][r] + part[1][c][r] + part[2][c][r] + part[3][c][r];
+  }
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -1349,20 +1430,23 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 2) solve_bwd_level_kernel(
   }
 }
 
+// The solve's work vector: NR right-hand sides interleaved in final order, y[pf[i] * NR + r] = b[r * n + i].
 __global__ void permute_kernel(const int* __restrict__ perm, const double* __restrict__ in, double* out, long long n,
-                               int inverse) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    if (inverse) out[i] = in[perm[i]];   // x[i] = z[pf[i]]
-    else out[perm[i]] = in[i];           // y[pf[i]] = b[i]
+                               int nr, int inverse) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * nr; e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e % n, r = e / n;
+    if (inverse) out[e] = in[(long long)perm[i] * nr + r];   // x[r][i] = z[pf[i]][r]
+    else out[(long long)perm[i] * nr + r] = in[e];            // y[pf[i]][r] = b[r][i]
   }
 }
 
 __global__ void permute_masked_kernel(const int* __restrict__ perm, const unsigned char* __restrict__ mine,
-                                      const double* __restrict__ in, double* out, long long n, int inverse) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const int r = perm[i];
-    if (inverse) out[i] = mine[r] ? in[r] : 0.0;
-    else out[r] = mine[r] ? in[i] : 0.0;
+                                      const double* __restrict__ in, double* out, long long n, int nr, int inverse) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * nr; e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e % n, r = e / n;
+    const int q = perm[i];
+    if (inverse) out[e] = mine[q] ? in[(long long)q * nr + r] : 0.0;
+    else out[(long long)q * nr + r] = mine[q] ? in[e] : 0.0;
   }
 }
 
@@ -1518,31 +1602,38 @@ void launch_init(const double* vals, const long long* amap, long long nnz, doubl
 
 void launch_solve_fwd_level(const STask* tasks, int ntasks, int* ticket, int* flag, const SnInfo* sn, const int* sfirst,
                             const long long* rows_ptr, const int* rows, const double* panels, const double* linv,
-                            double* y, int NB, cudaStream_t st) {
-  if (ntasks > 0)
-    solve_fwd_level_kernel<<<ntasks, SOLVE_THREADS, 0, st>>>(tasks, ticket, flag, sn, sfirst, rows_ptr, rows, panels,
-                                                             linv, y, NB);
+                            double* y, int NB, int nr, cudaStream_t st) {
+  if (ntasks <= 0) return;
+  auto k = nr == 4 ? solve_fwd_level_kernel<4> : nr == 2 ? solve_fwd_level_kernel<2> : solve_fwd_level_kernel<1>;
+  k<<<ntasks, SOLVE_THREADS, 0, st>>>(tasks, ticket, flag, sn, sfirst, rows_ptr, rows, panels, linv, y, NB);
 }
 void launch_solve_bwd_level(const STask* tasks, int ntasks, int* ticket, int* flag, int* rcnt, const SnInfo* sn,
                             const int* sfirst, const long long* rows_ptr, const int* rows, const double* panels,
-                            const double* linv, double* y, int NB, cudaStream_t st) {
-  if (ntasks > 0)
-    solve_bwd_level_kernel<<<ntasks, SOLVE_THREADS, 0, st>>>(tasks, ticket, flag, rcnt, sn, sfirst, rows_ptr, rows,
-                                                             panels, linv, y, NB);
+                            const double* linv, double* y, int NB, int nr, cudaStream_t st) {
+  if (ntasks <= 0) return;
+  auto k = nr == 4 ? solve_bwd_level_kernel<4> : nr == 2 ? solve_bwd_level_kernel<2> : solve_bwd_level_kernel<1>;
+  k<<<ntasks, SOLVE_THREADS, 0, st>>>(tasks, ticket, flag, rcnt, sn, sfirst, rows_ptr, rows, panels, linv, y, NB);
 }
-void launch_solve_small(const SmallSolve* info, int count, int rows_class, int backward, const int* rows,
-                        const double* panels, double* y, cudaStream_t st) {
-  if (count <= 0) return;
+template <int NR>
+static void solve_small_nr(const SmallSolve* info, int count, int rows_class, int backward, const int* rows,
+                           const double* panels, double* y, cudaStream_t st) {
   const int grid = (count + SW_WARPS - 1) / SW_WARPS, thr = 32 * SW_WARPS;
   if (!backward) {
-    if (rows_class == 0) solve_fwd_small_kernel<2><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
-    else if (rows_class == 1) solve_fwd_small_kernel<4><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
-    else solve_fwd_small_kernel<8><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+    if (rows_class == 0) solve_fwd_small_kernel<2, NR><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+    else if (rows_class == 1) solve_fwd_small_kernel<4, NR><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+    else solve_fwd_small_kernel<8, NR><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
   } else {
-    if (rows_class == 0) solve_bwd_small_kernel<2><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
-    else if (rows_class == 1) solve_bwd_small_kernel<4><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
-    else solve_bwd_small_kernel<8><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+    if (rows_class == 0) solve_bwd_small_kernel<2, NR><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+    else if (rows_class == 1) solve_bwd_small_kernel<4, NR><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
+    else solve_bwd_small_kernel<8, NR><<<grid, thr, 0, st>>>(info, count, rows, panels, y);
   }
+}
+void launch_solve_small(const SmallSolve* info, int count, int rows_class, int backward, const int* rows,
+                        const double* panels, double* y, int nr, cudaStream_t st) {
+  if (count <= 0) return;
+  if (nr == 4) solve_small_nr<4>(info, count, rows_class, backward, rows, panels, y, st);
+  else if (nr == 2) solve_small_nr<2>(info, count, rows_class, backward, rows, panels, y, st);
+  else solve_small_nr<1>(info, count, rows_class, backward, rows, panels, y, st);
 }
 __global__ void axpy_kernel(const double* __restrict__ x, double* y, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -1560,18 +1651,18 @@ void launch_gather(const double* src, const long long* idx, double* out, long lo
   if (blocks > 148 * 8) blocks = 148 * 8;
   gather_kernel<<<(int)blocks, 256, 0, st>>>(src, idx, out, n);
 }
-void launch_permute(const int* perm, const double* in, double* out, long long n, int inverse, cudaStream_t st) {
+void launch_permute(const int* perm, const double* in, double* out, long long n, int nr, int inverse, cudaStream_t st) {
   if (n <= 0) return;
-  long long blocks = (n + 255) / 256;
+  long long blocks = (n * nr + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  permute_kernel<<<(int)blocks, 256, 0, st>>>(perm, in, out, n, inverse);
+  permute_kernel<<<(int)blocks, 256, 0, st>>>(perm, in, out, n, nr, inverse);
 }
 void launch_permute_masked(const int* perm, const unsigned char* mine, const double* in, double* out, long long n,
-                           int inverse, cudaStream_t st) {
+                           int nr, int inverse, cudaStream_t st) {
   if (n <= 0) return;
-  long long blocks = (n + 255) / 256;
+  long long blocks = (n * nr + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  permute_masked_kernel<<<(int)blocks, 256, 0, st>>>(perm, mine, in, out, n, inverse);
+  permute_masked_kernel<<<(int)blocks, 256, 0, st>>>(perm, mine, in, out, n, nr, inverse);
 }
 
 }  // namespace spchol

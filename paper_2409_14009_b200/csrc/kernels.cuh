@@ -133,20 +133,23 @@ struct SmallSolve {
   int ld, m, k, f;     // f = first column
 };
 // rows_class 0 / 1 / 2: m <= 64 / 128 / 256 (rows per lane 2 / 4 / 8)
+// Solves run on NR = nr in {1, 2, 4} right-hand sides at once, interleaved: y[i * nr + r].
+constexpr int SOLVE_NRMAX = 4;
 void launch_solve_small(const SmallSolve* info, int count, int rows_class, int backward, const int* rows,
-                        const double* panels, double* y, cudaStream_t st);
+                        const double* panels, double* y, int nr, cudaStream_t st);
 constexpr int SOLVE_THREADS = 256;
 constexpr int SOLVE_RCHUNK = 512;   // rows per backward kind-2 task
 void launch_solve_fwd_level(const STask* tasks, int ntasks, int* ticket, int* flag, const SnInfo* sn, const int* sfirst,
                             const long long* rows_ptr, const int* rows, const double* panels, const double* linv,
-                            double* y, int NB, cudaStream_t st);
+                            double* y, int NB, int nr, cudaStream_t st);
 void launch_solve_bwd_level(const STask* tasks, int ntasks, int* ticket, int* flag, int* rcnt, const SnInfo* sn,
                             const int* sfirst, const long long* rows_ptr, const int* rows, const double* panels,
-                            const double* linv, double* y, int NB, cudaStream_t st);
-void launch_permute(const int* perm, const double* in, double* out, long long n, int inverse, cudaStream_t st);
+                            const double* linv, double* y, int NB, int nr, cudaStream_t st);
+// in: nr columns of n (column-major, ld n) in the caller's order <-> out: interleaved in final order
+void launch_permute(const int* perm, const double* in, double* out, long long n, int nr, int inverse, cudaStream_t st);
 // multi-GPU solve: as launch_permute, entries whose final row r has mine[r] == 0 become 0
 void launch_permute_masked(const int* perm, const unsigned char* mine, const double* in, double* out, long long n,
-                           int inverse, cudaStream_t st);
+                           int nr, int inverse, cudaStream_t st);
 void launch_axpy(const double* x, double* y, long long n, cudaStream_t st);
 void launch_gather(const double* src, const long long* idx, double* out, long long n, cudaStream_t st);
 cudaError_t kernels_init_attributes();

@@ -325,3 +325,39 @@ def test_memory_capped_fullsize_C3():
         off, ldv, pan = h.spchol_export_panels()
     err, cnt = llt_sample_error(p, sym, off, ldv, pan, top_level_columns(sym, nlev=3, per_sn=3))
     assert err <= 1e-12 and cnt >= 10 ** 4
+
+
+@pytest.mark.parametrize("name", ["S4", "S5", "C1", "T2"])
+@pytest.mark.parametrize("nrhs", [1, 3, 16])
+@pytest.mark.parametrize("capped", [False, True])
+def test_multi_rhs_solve(name, nrhs, capped):
+    """f-1, multiple right-hand sides: nrhs columns with leading dimension ld > n, solved in
+    blocks of 4 / 2 / 1 (one pass over L per block), in place (b aliasing x) and out of place; every
+    column against the oracle's scalar solve and within the backward-error bound.  Resident and
+    memory-capped factor."""
+    import ctypes
+    prob = gen.make(name)
+    o = oracle.Oracle.from_problem(prob)
+    assert o.factor() == -1
+    n, ld = prob.n, prob.n + 5
+    rng = np.random.default_rng(nrhs)
+    B = np.zeros((nrhs, ld))                       # column r at B[r, :n] (column-major, ld)
+    B[:, :n] = rng.uniform(-1, 1, (nrhs, n))
+    opts = {}
+    if capped and name == "T2":
+        pytest.skip("T2's resident top alone is above any cap below its footprint")
+    if capped:
+        with sp.Solver.from_problem(prob, device=-1) as h0:
+            opts["device_mem_cap"] = int(0.6 * h0.query("ARENA_BYTES"))
+    with sp.Solver.from_problem(prob, **opts) as h:
+        assert h.spchol_factor() == (-1, -1)
+        X = np.full_like(B, 7.0)
+        assert h._L.spchol_solve(h._h, sp._vp(B), sp._vp(X), nrhs, ld) == 0
+        Y = B.copy()
+        assert h._L.spchol_solve(h._h, sp._vp(Y), sp._vp(Y), nrhs, ld) == 0       # aliased b == x
+        for r in range(nrhs):
+            xr = o.solve(B[r, :n])
+            assert np.abs(X[r, :n] - xr).max() <= 1e-10 * np.abs(xr).max()
+            assert np.abs(X[r, :n] - Y[r, :n]).max() <= 1e-12 * np.abs(xr).max()   # FP64 RED: rounding order varies
+            assert backward_error(prob, X[r, :n], B[r, :n]) <= TOL_BERR
+        assert np.all(X[:, n:] == 7.0)             # the padding rows of the ld are untouched
