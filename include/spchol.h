@@ -77,7 +77,11 @@ typedef struct {
                            a class), one launch per class, plain read-modify-write scatter instead of
                            FP64 RED; subtree_streams is forced to 1.  Requires update_mode 0.
                            Default 0.  (The solve's RED into shared ancestors stays unordered.) */
-  int32_t reserved0;    /* 0 */
+  int32_t partition_refinement; /* 1 = reorder the columns inside each supernode after merging so that the
+                           rows every descendant has in it form fewer consecutive runs (fewer RLB
+                           blocks; reading R14 in DESIGN.md).  Changes the final
+                           permutation (and so the exact factor's pattern inside the panels), not
+                           the panel storage.  Default 0. */
   int64_t device_mem_cap; /* single GPU, memory-capped (out-of-core) mode (P:484-489,
                            P:568): 0 = unlimited (default).  Otherwise the device arena is planned to
                            stay under this many bytes: the supernodal tree is split into a resident

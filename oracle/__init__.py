@@ -32,6 +32,9 @@ def lib():
         L.orc_symbolic.restype = ctypes.c_void_p
         L.orc_symbolic.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_int]
+        L.orc_symbolic_pr.restype = ctypes.c_void_p
+        L.orc_symbolic_pr.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.orc_numeric.restype = ctypes.c_int
         L.orc_numeric.argtypes = [ctypes.c_void_p, _I64]
         L.orc_numeric_parallel.restype = ctypes.c_int
@@ -69,16 +72,18 @@ class OracleError(RuntimeError):
 
 
 class Oracle:
-    """Runs O1-O8 on construction; ``factor()`` runs O9, ``solve()`` O10."""
+    """Runs O1-O8 on construction (O7b partition refinement with pr=1); ``factor()`` runs O9,
+    ``solve()`` O10."""
 
-    def __init__(self, n, colptr, rowidx, values=None, perm=None, cap=0.25, rule=0, keep_L=True):
+    def __init__(self, n, colptr, rowidx, values=None, perm=None, cap=0.25, rule=0, keep_L=True, pr=0):
         self._L = lib()
         self._keep = [np.ascontiguousarray(colptr, np.int64), np.ascontiguousarray(rowidx, np.int32),
                       None if values is None else np.ascontiguousarray(values, np.float64),
                       None if perm is None else np.ascontiguousarray(perm, np.int32)]
         cp, ri, vx, pm = self._keep
         self.n = int(n)
-        h = self._L.orc_symbolic(self.n, _vp(cp), _vp(ri), _vp(vx), _vp(pm), float(cap), int(rule), int(keep_L))
+        h = self._L.orc_symbolic_pr(self.n, _vp(cp), _vp(ri), _vp(vx), _vp(pm), float(cap), int(rule), int(keep_L),
+                                    int(pr))
         if not h:
             raise OracleError("oracle symbolic self-check failed")
         self._h = h

@@ -21,6 +21,10 @@
  *   O6 greedy merge       pairs (J, p(J)), minimum new fill first, stop before cumulative growth
  *                         exceeds cap * nnz(L)  (readings R3-R6)
  *   O7 final permutation  postorder of the merged supernodal tree (reading R6)
+ *   O7b partition refinement (optional, pr = 1, reading R14): the
+ *                         columns inside each supernode P are reordered: the ordered partition
+ *                         [cols(P)] is refined by S_J = R_J n cols(P) for every J with S_J nonempty,
+ *                         J ascending, each part X becoming (X n S_J, X \ S_J), order kept inside
  *   O8 relind             relind(J,P)[q] = (m_P - 1) - position of rows(J)[q] in rows(P),
  *                         for the rows of J that are >= f_P ("distance from the bottom")
  *   O9 numeric            scalar left-looking column Cholesky of C_f = P_f A P_f^T on its exact
@@ -241,8 +245,59 @@ void orc_free(orc_t* o);
  * keep_L: also build the exact structure of L in final numbering (needed by orc_numeric).
  * values may be NULL (then orc_numeric is unavailable).
  */
+orc_t* orc_symbolic_pr(int64_t n, const int64_t* Ap, const int32_t* Ai, const double* Ax,
+                       const int32_t* perm, double cap, int rule, int keep_L, int pr);
 orc_t* orc_symbolic(int64_t n, const int64_t* Ap, const int32_t* Ai, const double* Ax,
                     const int32_t* perm, double cap, int rule, int keep_L) {
+  return orc_symbolic_pr(n, Ap, Ai, Ax, perm, cap, rule, keep_L, 0);
+}
+
+/*
+ * O7b (reading R14): partition refinement of the columns inside every supernode.  Input: the O7
+ * supernodes (sfirst) and rows(J) in O7 labels.  Output newlab[O7 label] = refined label.  Plain
+ * version: the whole ordered partition of P is rebuilt for every refining set.
+ */
+static void partition_refinement(int64_t n, int32_t ns, const int32_t* sfirst, const int64_t* rows_ptr,
+                                 const int32_t* rows, int32_t* newlab) {
+  int32_t* snode = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  for (int32_t s = 0; s < ns; ++s) for (int32_t c = sfirst[s]; c < sfirst[s + 1]; ++c) snode[c] = s;
+  int32_t* ord = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));     /* per P: its columns in order */
+  char* brk = (char*)calloc((size_t)n + 1, 1);                                  /* brk[i]: a part starts at ord[i] */
+  char* inS = (char*)calloc((size_t)n + 1, 1);
+  int32_t* tmp = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+  char* tbrk = (char*)calloc((size_t)n + 1, 1);
+  for (int64_t c = 0; c < n; ++c) ord[c] = (int32_t)c;
+  for (int32_t s = 0; s < ns; ++s) brk[sfirst[s]] = 1;
+  for (int32_t J = 0; J < ns; ++J) {
+    int64_t k = sfirst[J + 1] - sfirst[J];
+    for (int64_t q = rows_ptr[J] + k; q < rows_ptr[J + 1];) {
+      int32_t P = snode[rows[q]];
+      int64_t q1 = q;
+      while (q1 < rows_ptr[J + 1] && snode[rows[q1]] == P) { inS[rows[q1]] = 1; ++q1; }   /* S_J */
+      /* rebuild P's ordered partition: every part X -> (X n S_J, X \ S_J) */
+      int32_t a = sfirst[P], b = sfirst[P + 1], w = a;
+      for (int32_t i = a; i < b;) {
+        int32_t e = i + 1;
+        while (e < b && !brk[e]) ++e;                 /* part [i, e) */
+        int32_t w0 = w;
+        for (int32_t x = i; x < e; ++x) if (inS[ord[x]]) tmp[w++] = ord[x];
+        int32_t w1 = w;
+        for (int32_t x = i; x < e; ++x) if (!inS[ord[x]]) tmp[w++] = ord[x];
+        if (w1 > w0) tbrk[w0] = 1;
+        if (w > w1) tbrk[w1] = 1;
+        i = e;
+      }
+      for (int32_t i = a; i < b; ++i) { ord[i] = tmp[i]; brk[i] = tbrk[i]; tbrk[i] = 0; }
+      for (int64_t x = q; x < q1; ++x) inS[rows[x]] = 0;
+      q = q1;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) newlab[ord[i]] = (int32_t)i;
+  free(snode); free(ord); free(brk); free(inS); free(tmp); free(tbrk);
+}
+
+orc_t* orc_symbolic_pr(int64_t n, const int64_t* Ap, const int32_t* Ai, const double* Ax,
+                       const int32_t* perm, double cap, int rule, int keep_L, int pr) {
   orc_t* o = (orc_t*)calloc(1, sizeof(orc_t));
   o->n = n;
   int32_t* ident = NULL;
@@ -441,14 +496,33 @@ orc_t* orc_symbolic(int64_t n, const int64_t* Ap, const int32_t* Ai, const doubl
     free(gof); free(stack); free(hd); free(head); free(nxt); free(gcnt); free(gcols); free(gsuper);
     free(gparent); free(gmin); free(gl);
   }
+  /* O7b partition refinement: relabel the columns inside each supernode, rows(J) re-sorted */
+  if (pr) {
+    int32_t* newlab = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    partition_refinement(n, o->nsuper, o->sfirst, o->rows_ptr, o->rows, newlab);
+    for (int64_t j = 0; j < n; ++j) o->o7[j] = newlab[o->o7[j]];
+    for (int64_t x = 0; x < o->rows_ptr[o->nsuper]; ++x) o->rows[x] = newlab[o->rows[x]];
+    for (int32_t s = 0; s < o->nsuper; ++s)
+      qsort(o->rows + o->rows_ptr[s], (size_t)(o->rows_ptr[s + 1] - o->rows_ptr[s]), sizeof(int32_t), cmp_i32);
+    free(newlab);
+  }
   /* final permutation and exact etree / cc in final numbering */
   o->perm_final = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
   for (int64_t i = 0; i < n; ++i) o->perm_final[i] = o->o7[ipost[perm[i]]];
   o->parent_final = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
   o->cc_final = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
-  for (int64_t j = 0; j < n; ++j) {
-    o->parent_final[o->o7[j]] = o->parent3[j] == -1 ? -1 : o->o7[o->parent3[j]];
-    o->cc_final[o->o7[j]] = o->cc3[j];
+  if (!pr) {   /* O7 is an equivalent (topological) reordering: the O3 etree relabelled */
+    for (int64_t j = 0; j < n; ++j) {
+      o->parent_final[o->o7[j]] = o->parent3[j] == -1 ? -1 : o->o7[o->parent3[j]];
+      o->cc_final[o->o7[j]] = o->cc3[j];
+    }
+  } else {     /* a reordering inside supernodes can change the exact structure: row-merge again */
+    int64_t *Fp; int32_t* Fi;
+    permute_lower(n, Ap, Ai, NULL, o->perm_final, &Fp, &Fi, NULL);
+    rowmerge(n, Fp, Fi, o->parent_final, o->cc_final, NULL, 0, NULL, NULL);
+    free(Fp); free(Fi);
+    o->nnzL = 0; o->flops = 0.0;   /* the exact factor actually computed */
+    for (int64_t j = 0; j < n; ++j) { o->nnzL += o->cc_final[j]; o->flops += (double)o->cc_final[j] * (double)o->cc_final[j]; }
   }
   /* O8 relind */
   {

@@ -50,7 +50,7 @@ class spchol_options(ctypes.Structure):
                 ("small_max_k", ctypes.c_int32), ("use_graph", ctypes.c_int32),
                 ("dist_rank", ctypes.c_int32), ("dist_world", ctypes.c_int32),
                 ("subtree_streams", ctypes.c_int32), ("update_mode", ctypes.c_int32),
-                ("deterministic", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("device_mem_cap", ctypes.c_int64)]
+                ("deterministic", ctypes.c_int32), ("partition_refinement", ctypes.c_int32), ("device_mem_cap", ctypes.c_int64)]
 
 
 class SpcholError(RuntimeError):

@@ -8,6 +8,7 @@
 //   fundamental supernodes [LNP93]                           (reading R1)
 //   greedy child-parent merging with an indexed heap         (readings R3-R6)
 //   final permutation = postorder of the merged tree         (reading R6)
+//   optional partition refinement inside the supernodes       (reading R14)
 //   rows(J) by supernodal symbolic factorization on the merged partition
 //   relind(J,P) via indmap                                    (indmap P:38-39)
 //   level sets (heights) of the merged supernodal tree      (north_star: level-set scheduling)
@@ -122,7 +123,7 @@ struct IHeap {
 }  // namespace
 
 int analyze_symbolic(int64_t n, const int64_t* colptr, const int32_t* rowidx, const int32_t* perm_in,
-                     double cap, Symbolic& S, std::string& err) {
+                     double cap, int pr, Symbolic& S, std::string& err) {
   if (n < 0) { err = "n < 0"; return SPCHOL_ERR_DIMENSION; }
   if (n >= INT32_MAX) { err = "n must be < 2^31"; return SPCHOL_ERR_DIMENSION; }
   if (!colptr || (n > 0 && !rowidx)) { err = "NULL pattern arrays"; return SPCHOL_ERR_VALIDATION; }
@@ -371,6 +372,75 @@ int analyze_symbolic(int64_t n, const int64_t* colptr, const int32_t* rowidx, co
       for (int32_t c = f; c <= l; ++c) S.rows[w++] = c;
       for (int32_t i : extra) S.rows[w++] = i;
     }
+  }
+  // ---- partition refinement (reading R14): per supernode P, the ordered partition of cols(P) is
+  // refined by S_J = R_J n cols(P), J ascending, each touched part split stably into (in S, not in
+  // S).  Parts are position ranges [pstart, pend); only the parts S_J touches are visited.
+  if (pr) {
+    std::vector<int32_t> ord(n), where(n), pstart(n), pend(n), tmp(n);
+    std::vector<char> inS(n, 0), touched(n, 0);
+    for (int64_t i = 0; i < n; ++i) { ord[i] = (int32_t)i; where[i] = (int32_t)i; }
+    for (int32_t P = 0; P < ns; ++P)
+      for (int32_t i = S.sfirst[P]; i < S.sfirst[P + 1]; ++i) { pstart[i] = S.sfirst[P]; pend[i] = S.sfirst[P + 1]; }
+    std::vector<int32_t> parts;
+    for (int32_t J = 0; J < ns; ++J) {
+      const int64_t k = S.sfirst[J + 1] - S.sfirst[J];
+      const int32_t* r = S.rows.data() + S.rows_ptr[J];
+      const int64_t m = S.rows_ptr[J + 1] - S.rows_ptr[J];
+      for (int64_t q = k; q < m;) {
+        const int32_t P = S.snode[r[q]];
+        int64_t q1 = q;
+        parts.clear();
+        for (; q1 < m && S.snode[r[q1]] == P; ++q1) {
+          inS[r[q1]] = 1;
+          const int32_t a = pstart[where[r[q1]]];
+          if (!touched[a]) { touched[a] = 1; parts.push_back(a); }
+        }
+        for (int32_t a : parts) {
+          touched[a] = 0;
+          const int32_t e = pend[a];
+          int32_t w = a;
+          for (int32_t i = a; i < e; ++i) if (inS[ord[i]]) tmp[w++] = ord[i];
+          const int32_t mid = w;
+          for (int32_t i = a; i < e; ++i) if (!inS[ord[i]]) tmp[w++] = ord[i];
+          for (int32_t i = a; i < e; ++i) { ord[i] = tmp[i]; where[ord[i]] = i; }
+          if (mid < e) {   // both halves nonempty (mid > a: the part held an element of S)
+            for (int32_t i = a; i < mid; ++i) pend[i] = mid;
+            for (int32_t i = mid; i < e; ++i) pstart[i] = mid;
+          }
+        }
+        for (int64_t x = q; x < q1; ++x) inS[r[x]] = 0;
+        q = q1;
+      }
+    }
+    // relabel: newlab = position; rows(J) re-sorted; P_f and the A -> C_f map recomputed
+    std::vector<int32_t>& newlab = where;
+    for (int64_t x = 0; x < S.rows_ptr[ns]; ++x) S.rows[x] = newlab[S.rows[x]];
+    for (int32_t sn = 0; sn < ns; ++sn) std::sort(S.rows.begin() + S.rows_ptr[sn], S.rows.begin() + S.rows_ptr[sn + 1]);
+    for (int64_t i = 0; i < n; ++i) { S.perm_final[i] = newlab[S.perm_final[i]]; S.iperm_final[S.perm_final[i]] = (int32_t)i; }
+    { Pat tmp2; std::swap(Cf, tmp2); }
+    permute_pattern(n, colptr, rowidx, S.perm_final.data(), true, true, Cf);
+    // the exact factor's structure in the refined order: Liu's etree, then column counts by
+    // walking every row subtree (row i: from each k with C_f(i,k) != 0 up the etree to i)
+    std::vector<int32_t> anc(n, -1);
+    for (int64_t j = 0; j < n; ++j) {
+      S.parent_final[j] = -1;
+      for (int64_t p = Cf.rp[j]; p < Cf.rp[j + 1]; ++p) {
+        int32_t rr = Cf.rj[p];
+        if (rr >= j) continue;
+        while (anc[rr] != -1 && anc[rr] != j) { int32_t nx = anc[rr]; anc[rr] = (int32_t)j; rr = nx; }
+        if (anc[rr] == -1) { anc[rr] = (int32_t)j; S.parent_final[rr] = (int32_t)j; }
+      }
+    }
+    std::vector<int32_t> mark(n, -1);
+    for (int64_t j = 0; j < n; ++j) S.cc_final[j] = 1;
+    for (int64_t i = 0; i < n; ++i) {
+      mark[i] = (int32_t)i;
+      for (int64_t p = Cf.rp[i]; p < Cf.rp[i + 1]; ++p)
+        for (int32_t kk = Cf.rj[p]; kk >= 0 && mark[kk] != i; kk = S.parent_final[kk]) { mark[kk] = (int32_t)i; S.cc_final[kk]++; }
+    }
+    S.nnzL = 0; S.flops_exact = 0.0;
+    for (int64_t j = 0; j < n; ++j) { S.nnzL += S.cc_final[j]; S.flops_exact += (double)S.cc_final[j] * (double)S.cc_final[j]; }
   }
   // ---- levels (height from the leaves)
   S.level.assign(ns, 0);

@@ -96,7 +96,7 @@ extern "C" void spchol_default_options(spchol_options* o) {
   o->subtree_streams = 0;
   o->update_mode = 0;
   o->deterministic = 0;
-  o->reserved0 = 0;
+  o->partition_refinement = 0;
   o->device_mem_cap = 0;
 }
 
@@ -1023,7 +1023,7 @@ extern "C" int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* r
   spchol_handle* h = new spchol_handle();
   if (opt) h->opt = *opt; else spchol_default_options(&h->opt);
   std::string err;
-  int rc = analyze_symbolic(n, colptr, rowidx, perm, h->opt.merge_cap, h->S, err);
+  int rc = analyze_symbolic(n, colptr, rowidx, perm, h->opt.merge_cap, h->opt.partition_refinement, h->S, err);
   if (rc != SPCHOL_OK) { delete h; return fail(rc, err); }
   rc = finish_handle(h);
   if (rc != SPCHOL_OK) { delete h; return rc; }

@@ -39,7 +39,8 @@ struct Symbolic {
 };
 
 // Returns 0 or an SPCHOL_ERR_* code; err receives a message.
+// pr = 1: partition refinement of the columns inside the supernodes (reading R14)
 int analyze_symbolic(int64_t n, const int64_t* colptr, const int32_t* rowidx, const int32_t* perm,
-                     double cap, Symbolic& S, std::string& err);
+                     double cap, int pr, Symbolic& S, std::string& err);
 
 }  // namespace spchol

@@ -17,10 +17,10 @@ KEYS = ["post", "parent3", "cc3", "ffirst", "fgroup", "perm_final", "sfirst", "s
         "rel_ptr", "rel_anc", "rel_q0", "rel_off", "relind", "parent_final", "cc_final"]
 
 
-def compare(prob, cap=0.25):
-    with sp.Solver.from_problem(prob, device=-1, merge_cap=cap) as h:
+def compare(prob, cap=0.25, pr=0):
+    with sp.Solver.from_problem(prob, device=-1, merge_cap=cap, partition_refinement=pr) as h:
         a = h.spchol_export_symbolic()
-        o = oracle.Oracle.from_problem(prob, cap=cap, keep_L=True)
+        o = oracle.Oracle.from_problem(prob, cap=cap, keep_L=True, pr=pr)
         b = o.symbolic()
         for k in KEYS:
             assert np.array_equal(a[k], b[k]), k
@@ -40,6 +40,19 @@ def compare(prob, cap=0.25):
 @pytest.mark.parametrize("name", ["C1", "T1", "T2", "T3", "S2", "S3", "S4", "S5"])
 def test_analyze_small_configs(name):
     compare(gen.make(name))
+
+
+@pytest.mark.parametrize("name", ["C1", "T1", "T2", "T3", "S2", "S3", "S4", "S5"])
+def test_analyze_partition_refinement(name):
+    """Partition refinement (reading R14): the product's touched-parts refinement against the oracle's
+    whole-partition rebuild (O7b) — bit-exact, including the exact structure of the refined order."""
+    compare(gen.make(name), pr=1)
+
+
+@pytest.mark.parametrize("block", range(0, 3))
+def test_analyze_partition_refinement_random(block):
+    for trial in range(block * 100, block * 100 + 100):
+        compare(gen.random_spd(5000 + trial), pr=1)
 
 
 @pytest.mark.parametrize("cap", [-1.0, 0.0, 0.05, 0.25, 1.0, 10.0])

@@ -17,7 +17,7 @@ TOL_BERR = 1e-12   # north_star: ||Ax-b|| / (||A|| ||x||) <= 1e-12
 
 
 def run_parity(prob, **opts):
-    o = oracle.Oracle.from_problem(prob)
+    o = oracle.Oracle.from_problem(prob, pr=opts.get("partition_refinement", 0))
     s_or = o.symbolic()
     assert o.factor() == -1
     Lp, Li, Lx = o.L_csc()
@@ -361,3 +361,12 @@ def test_multi_rhs_solve(name, nrhs, capped):
             assert np.abs(X[r, :n] - Y[r, :n]).max() <= 1e-12 * np.abs(xr).max()   # FP64 RED: rounding order varies
             assert backward_error(prob, X[r, :n], B[r, :n]) <= TOL_BERR
         assert np.all(X[:, n:] == 7.0)             # the padding rows of the ld are untouched
+
+
+@pytest.mark.parametrize("name", ["S2", "S3", "S4", "S5", "T2"])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_parity_partition_refinement(name, mode):
+    """Partition refinement (f-2, reading R14) with RL (mode 0) and RLB (mode 1):
+    bit-exact symbolic arrays against the oracle's O7b, the factor of the refined order within the
+    parity bar, padding exactly 0, solve within the backward-error bound."""
+    run_parity(gen.make(name), partition_refinement=1, update_mode=mode)

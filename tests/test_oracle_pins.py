@@ -407,3 +407,70 @@ def test_parallel_oracle_not_spd(threads):
         q = gen.Problem(p.name, p.n, p.colptr, p.rowidx, vals, p.perm)
         assert oracle.Oracle.from_problem(q).factor() == j0
         assert oracle.Oracle.from_problem(q).factor(threads=threads) == j0
+
+
+# ---------------------------------------------------------------- O7b partition refinement (R14)
+def test_fig1_partition_refinement():
+    """Hand-derived refined column order of Fig. 1's cap-0.25 supernodes (tests/golden/fig1.json)."""
+    p = fig1_problem()
+    o = oracle.Oracle.from_problem(p, cap=0.25, rule=0, pr=1)
+    s = o.symbolic()
+    final = []
+    for J in range(o.nsuper):
+        final.append([int(np.where(s["perm_final"] == c)[0][0]) + 1 for c in range(s["sfirst"][J], s["sfirst"][J + 1])])
+    assert final == FIG1["partition_refinement_cap025"]["value"]
+
+
+@pytest.mark.parametrize("trial", range(0, 60))
+def test_partition_refinement_random_corpus(trial):
+    """PR only reorders columns inside the supernodes (same partition, same column sets); the exact
+    structure of the refined order matches dense boolean elimination; the factor matches LAPACK; the
+    exact pattern stays inside the panels; relind / RLB invariants hold; and the first refining set of
+    every supernode ends up as a prefix of its columns."""
+    p = gen.random_spd(2000 + trial)
+    o0 = oracle.Oracle.from_problem(p, cap=0.25)
+    o = oracle.Oracle.from_problem(p, cap=0.25, pr=1)
+    s0, s = o0.symbolic(), o.symbolic()
+    assert np.array_equal(s0["sfirst"], s["sfirst"]) and np.array_equal(s0["sparent"], s["sparent"])
+    ip0, ip = np.argsort(s0["perm_final"]), np.argsort(s["perm_final"])
+    sf = s["sfirst"]
+    for J in range(o.nsuper):
+        assert sorted(ip0[sf[J]:sf[J + 1]]) == sorted(ip[sf[J]:sf[J + 1]])
+    C = permuted_dense(p, s["perm_final"])
+    M, cc, par = brute_symbolic(C)
+    assert s["cc_final"].tolist() == cc and s["parent_final"].tolist() == par
+    assert o.nnzL == sum(cc)
+    assert o.factor() == -1
+    L = dense_of(o.L_csc(), p.n)
+    Lref = np.linalg.cholesky(C)
+    assert np.abs(L - Lref).max() <= 1e-13 * max(1.0, np.abs(Lref).max())
+    assert np.all(Lref[~M] == 0.0)
+    rp, rows = s["rows_ptr"], s["rows"]
+    inpanel = np.zeros((p.n, p.n), bool)
+    for J in range(o.nsuper):
+        r = rows[rp[J]:rp[J + 1]]
+        for c in range(sf[J], sf[J + 1]):
+            inpanel[r[r >= c], c] = True
+    assert np.all(inpanel[np.tril(Lref) != 0])
+    # first refining set of each supernode P = its columns in R_J of the smallest such J: a prefix
+    snode = np.repeat(np.arange(o.nsuper), np.diff(sf))
+    seen = set()
+    for J in range(o.nsuper):
+        R = rows[rp[J] + (sf[J + 1] - sf[J]):rp[J + 1]]
+        for P in np.unique(snode[R]):
+            if P in seen:
+                continue
+            seen.add(P)
+            SJ = np.sort(R[snode[R] == P])
+            assert SJ.tolist() == list(range(sf[P], sf[P] + len(SJ)))
+    # relind (P:188-190) and RLB block invariants in the refined numbering
+    for J in range(o.nsuper):
+        r = rows[rp[J]:rp[J + 1]]
+        for q in range(s["rel_ptr"][J], s["rel_ptr"][J + 1]):
+            P, q0 = s["rel_anc"][q], s["rel_q0"][q]
+            rel = s["relind"][s["rel_off"][q]:s["rel_off"][q + 1]]
+            rP = rows[rp[P]:rp[P + 1]]
+            assert np.all(np.diff(rel) < 0) and rP[len(rP) - 1 - rel].tolist() == r[q0:].tolist()
+        for b in range(s["blk_ptr"][J], s["blk_ptr"][J + 1]):
+            blk = r[s["blk_q"][b]:s["blk_q"][b] + s["blk_len"][b]]
+            assert np.all(np.diff(blk) == 1)
