@@ -305,9 +305,14 @@ def main():
     achieved = sd["flops"] / (sd["ms"] / 1e3) / 1e12 if sd["ms"] > 0 else 0.0
     traffic = None
     if os.path.exists(TRAFFIC_FILE):
+        # ncu-measured DRAM bytes per launch of the dominant kernel (profiles/roofline_traffic.json),
+        # used only while the kernel source is the one it was measured on (else null, not stale)
+        import hashlib
         with open(TRAFFIC_FILE) as f:
             tr = json.load(f)
-        if tr.get("config") == args.config and tr.get("kernel") == dom:
+        with open(os.path.join(ROOT, "paper_2409_14009_b200", "csrc", "kernels.cu"), "rb") as f:
+            same_src = hashlib.sha256(f.read()).hexdigest() == tr.get("kernels_cu_sha256")
+        if tr.get("config") == args.config and tr.get("kernel") == dom and same_src:
             traffic = tr.get("traffic_bytes_per_launch")
     step_ms_timed = sum(v["ms"] for v in stats.values()) / args.steps
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak["dmma_tflops_burst"], "unit": "TFLOP/s",

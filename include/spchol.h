@@ -178,8 +178,9 @@ int spchol_factor(spchol_handle* h, int64_t* fail_col, int64_t* fail_col_orig);
  */
 int spchol_solve(spchol_handle* h, const double* b, double* x, int32_t nrhs, int64_t ld);
 
-/* Same with device arrays, enqueued on the handle's stream (no synchronization). */
-int spchol_solve_device(spchol_handle* h, const double* d_b, double* d_x, int32_t nrhs, int64_t ld);
+/* Same with device arrays, enqueued on `stream` (a cudaStream_t; NULL = the handle's stream, see
+ * spchol_set_stream); no host synchronization. */
+int spchol_solve_device(spchol_handle* h, const double* d_b, double* d_x, int32_t nrhs, int64_t ld, void* stream);
 
 /* ---------------- introspection / parity exports ---------------- */
 enum {
@@ -291,6 +292,12 @@ int spchol_kernel_trace(spchol_handle* h, int64_t cap, int64_t* count, int32_t* 
                         int32_t* ntasks, double* ms);
 
 /* ---------------- multi-GPU (one process per GPU) ---------------- */
+/* Process-wide multi-GPU setup: this process is rank `rank` of `world`, and
+ * `nccl_unique_id` (128 bytes, from spchol_dist_nccl_unique_id on one rank, broadcast by the caller)
+ * names the communicator.  Every later spchol_analyze / spchol_load_analysis whose options keep the
+ * default dist_world == 1 then builds a rank of that world and attaches the communicator itself, so
+ * those calls become collective.  world == 1 clears the setting.  VALIDATION on bad arguments. */
+int spchol_dist_init(int32_t rank, int32_t world, const void* nccl_unique_id);
 /* Create an NCCL unique id (128 bytes) on one rank; the caller broadcasts it to the others. */
 int spchol_dist_nccl_unique_id(void* out128);
 /* Attach an NCCL communicator (ncclCommInitRank over dist_world ranks, this handle's dist_rank;

@@ -39,7 +39,8 @@ EXPORTS = [
     "spchol_set_stream", "spchol_factor_async", "spchol_factor_status", "spchol_factor",
     "spchol_solve", "spchol_solve_device", "spchol_query", "spchol_export_symbolic",
     "spchol_export_blocks", "spchol_export_panels", "spchol_export_panel", "spchol_export_diagonal", "spchol_enable_kernel_timing", "spchol_kernel_stats",
-    "spchol_kernel_trace", "spchol_dist_nccl_unique_id", "spchol_dist_attach_nccl", "spchol_export_mapping",
+    "spchol_kernel_trace", "spchol_dist_init", "spchol_dist_nccl_unique_id", "spchol_dist_attach_nccl",
+    "spchol_export_mapping",
     "spchol_dist_plan_flops",
     "spchol_destroy", "spchol_last_error",
 ]
@@ -87,7 +88,8 @@ def lib():
         L.spchol_factor_status.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.spchol_factor.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.spchol_solve.argtypes = [vp, vp, vp, i32, i64]
-        L.spchol_solve_device.argtypes = [vp, vp, vp, i32, i64]
+        L.spchol_solve_device.argtypes = [vp, vp, vp, i32, i64, vp]
+        L.spchol_dist_init.argtypes = [i32, i32, vp]
         L.spchol_query.argtypes = [vp, ctypes.c_int, ctypes.POINTER(i64)]
         L.spchol_export_symbolic.argtypes = [vp] * 19
         L.spchol_export_panels.argtypes = [vp, vp, vp, vp]
@@ -232,9 +234,10 @@ class Solver:
         _check(self._L.spchol_solve(self._h, _vp(bb), _vp(x), nrhs, self.n))
         return x
 
-    def spchol_solve_device(self, d_b: int, d_x: int, nrhs: int = 1, ld: int | None = None):
+    def spchol_solve_device(self, d_b: int, d_x: int, nrhs: int = 1, ld: int | None = None, stream: int | None = None):
         _check(self._L.spchol_solve_device(self._h, ctypes.c_void_p(d_b), ctypes.c_void_p(d_x), nrhs,
-                                           self.n if ld is None else ld))
+                                           self.n if ld is None else ld,
+                                           ctypes.c_void_p(stream) if stream else None))
 
     def spchol_query(self, key):
         v = ctypes.c_int64()
@@ -337,6 +340,12 @@ class Solver:
         sym = self.spchol_export_symbolic()
         off, ld, pan = self.spchol_export_panels()
         return sym, off, ld, pan
+
+
+def spchol_dist_init(rank: int, world: int, unique_id: bytes | None = None):
+    """Process-wide multi-GPU setup: later analyze calls with the default dist_world build this rank."""
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128) if unique_id is not None else None
+    _check(lib().spchol_dist_init(int(rank), int(world), buf))
 
 
 def spchol_dist_nccl_unique_id() -> bytes:

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "handle.h"
 
@@ -38,6 +39,12 @@ void assign_top_owners(const std::vector<double>& work, const std::vector<int>& 
 namespace {
 thread_local std::string g_err;
 }
+// NVTX ranges (SURVEY §5 tracing): analyze, factor (enqueue or graph launch), each level's plan
+// range when enqueued eagerly, solve, exchanges; visible in Nsight Systems / ncu --nvtx.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 int fail(int code, const std::string& msg) { g_err = msg; return code; }
 int cuda_fail(cudaError_t e, const char* where) {
   return fail(e == cudaErrorMemoryAllocation ? SPCHOL_ERR_DEVICE_OOM : SPCHOL_ERR_CUDA,
@@ -1016,12 +1023,42 @@ static int finish_handle(spchol_handle* h) {
   return rc;
 }
 
+// spchol_dist_init: the process's rank / world / communicator id, applied by later analyze calls
+namespace {
+struct DistInit { bool set = false; int32_t rank = 0, world = 1; char uid[128]; };
+DistInit g_dist_init;
+std::mutex g_dist_init_mu;
+}
+extern "C" int spchol_dist_init(int32_t rank, int32_t world, const void* nccl_unique_id) {
+  std::lock_guard<std::mutex> lock(g_dist_init_mu);
+  if (world == 1) { g_dist_init.set = false; return SPCHOL_OK; }
+  if (world < 1 || rank < 0 || rank >= world || !nccl_unique_id) return fail(SPCHOL_ERR_VALIDATION, "need 0 <= rank < world and an id");
+  g_dist_init.set = true;
+  g_dist_init.rank = rank;
+  g_dist_init.world = world;
+  std::memcpy(g_dist_init.uid, nccl_unique_id, 128);
+  return SPCHOL_OK;
+}
+// apply spchol_dist_init to options left at dist_world == 1; returns whether to attach afterwards
+static bool apply_dist_init(spchol_options& o, char* uid) {
+  std::lock_guard<std::mutex> lock(g_dist_init_mu);
+  if (!g_dist_init.set || o.dist_world != 1) return false;
+  o.dist_rank = g_dist_init.rank;
+  o.dist_world = g_dist_init.world;
+  std::memcpy(uid, g_dist_init.uid, 128);
+  return true;
+}
+extern "C" int spchol_dist_attach_nccl(spchol_handle* h, const void* unique_id128);
+
 extern "C" int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* rowidx, const double* values,
                               const int32_t* perm, const spchol_options* opt, spchol_handle** out) {
   if (!out) return fail(SPCHOL_ERR_VALIDATION, "out is NULL");
   *out = nullptr;
   spchol_handle* h = new spchol_handle();
   if (opt) h->opt = *opt; else spchol_default_options(&h->opt);
+  char uid[128];
+  const bool attach = apply_dist_init(h->opt, uid);
+  Nvtx nv("spchol_analyze");
   std::string err;
   int rc = analyze_symbolic(n, colptr, rowidx, perm, h->opt.merge_cap, h->opt.partition_refinement, h->S, err);
   if (rc != SPCHOL_OK) { delete h; return fail(rc, err); }
@@ -1029,6 +1066,10 @@ extern "C" int spchol_analyze(int64_t n, const int64_t* colptr, const int32_t* r
   if (rc != SPCHOL_OK) { delete h; return rc; }
   if (values && h->opt.device >= 0) {
     rc = spchol_set_values(h, values);
+    if (rc != SPCHOL_OK) { free_device(h); delete h; return rc; }
+  }
+  if (attach && h->opt.device >= 0) {
+    rc = spchol_dist_attach_nccl(h, uid);
     if (rc != SPCHOL_OK) { free_device(h); delete h; return rc; }
   }
   *out = h;
@@ -1147,6 +1188,8 @@ extern "C" int spchol_load_analysis(const char* path, const spchol_options* opt,
   if (!f) return fail(SPCHOL_ERR_VALIDATION, std::string("cannot open ") + path);
   spchol_handle* h = new spchol_handle();
   if (opt) h->opt = *opt; else spchol_default_options(&h->opt);
+  char uid[128];
+  const bool attach = apply_dist_init(h->opt, uid);
   uint64_t magic = 0, fmt = 0;
   double cap = 0;
   Reader r{f};
@@ -1159,6 +1202,10 @@ extern "C" int spchol_load_analysis(const char* path, const spchol_options* opt,
   h->opt.merge_cap = cap;   // the analysis was built with this cap
   int rc = finish_handle(h);
   if (rc != SPCHOL_OK) { delete h; return rc; }
+  if (attach && h->opt.device >= 0) {
+    rc = spchol_dist_attach_nccl(h, uid);
+    if (rc != SPCHOL_OK) { spchol_destroy(h); return rc; }
+  }
   *out = h;
   return SPCHOL_OK;
 }
@@ -1221,9 +1268,17 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
     for (size_t q = 0; q < used.size(); ++q)
       if (used[q]) CK(cudaStreamWaitEvent(h->pstreams[q], h->ev_fork, 0));
   }
+  int cur_level = -2;
   for (size_t i = begin; i < end; ++i) {
     const Launch& L = h->plan[i];
     cudaStream_t ls = multi ? h->pstreams[L.stream] : st;
+    if (i < h->plan_level.size() && h->plan_level[i] != cur_level) {   // one NVTX range per level
+      if (cur_level != -2) nvtxRangePop();
+      cur_level = h->plan_level[i];
+      char nm[32];
+      std::snprintf(nm, sizeof nm, "level %d", cur_level);
+      nvtxRangePushA(nm);
+    }
     if (L.op == OP_RECORD) {
       if (multi) CK(cudaEventRecord(h->plan_events[L.ev], ls));
       continue;
@@ -1285,6 +1340,7 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
     }
     tstop(ti);
   }
+  if (cur_level != -2) nvtxRangePop();
   if (multi) {   // join every stream the range used back into st (required under capture)
     for (size_t q = 0; q < used.size(); ++q)
       if (used[q]) {
@@ -1364,6 +1420,7 @@ static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
 }
 
 extern "C" int spchol_factor_async(spchol_handle* h) {
+  Nvtx nv("spchol_factor");
   if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
   if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
   if (!h->values_set) return fail(SPCHOL_ERR_STATE, "values not set");
@@ -1549,6 +1606,7 @@ static int run_solve_y2(spchol_handle* h, int nr) {
 // nrhs right-hand sides in blocks of 4, 2, 1 (each block one pass over L).
 static int solve_blocks(spchol_handle* h, const double* b, double* x, int32_t nrhs, int64_t ld, cudaMemcpyKind kin,
                         cudaMemcpyKind kout) {
+  Nvtx nv("spchol_solve");
   const size_t n = (size_t)h->S.n;
   for (int r0 = 0; r0 < nrhs;) {
     const int left = nrhs - r0, nr = left >= 4 ? 4 : left >= 2 ? 2 : 1;
@@ -1563,12 +1621,17 @@ static int solve_blocks(spchol_handle* h, const double* b, double* x, int32_t nr
   return SPCHOL_OK;
 }
 
-extern "C" int spchol_solve_device(spchol_handle* h, const double* d_b, double* d_x, int32_t nrhs, int64_t ld) {
+extern "C" int spchol_solve_device(spchol_handle* h, const double* d_b, double* d_x, int32_t nrhs, int64_t ld,
+                                   void* stream) {
   if (!h) return fail(SPCHOL_ERR_VALIDATION, "NULL handle");
   if (host_only(h) || !h->factored) return fail(SPCHOL_ERR_STATE, "solve before a successful factor");
   if (nrhs < 1 || ld < h->S.n) return fail(SPCHOL_ERR_DIMENSION, "nrhs < 1 or ld < n");
   CK(cudaSetDevice(h->opt.device));
-  return solve_blocks(h, d_b, d_x, nrhs, ld, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice);
+  cudaStream_t keep = h->stream;
+  if (stream) h->stream = (cudaStream_t)stream;
+  const int rc = solve_blocks(h, d_b, d_x, nrhs, ld, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice);
+  h->stream = keep;
+  return rc;
 }
 
 extern "C" int spchol_solve(spchol_handle* h, const double* b, double* x, int32_t nrhs, int64_t ld) {

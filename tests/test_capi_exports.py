@@ -150,3 +150,24 @@ def test_memory_capped_plan():
     with pytest.raises(sp.SpcholError) as e:
         sp.Solver.from_problem(p, device=-1, device_mem_cap=int(0.6 * full), dist_world=2, dist_rank=0)
     assert e.value.code == sp.SPCHOL_ERR_VALIDATION
+
+
+def test_dist_init_process_default():
+    """spchol_dist_init: later analyze calls with the default dist_world build that rank
+    of that world (host-only handles: no communicator is attached); world 1 clears the setting; bad
+    arguments are VALIDATION errors."""
+    p = gen.make("S4")
+    with pytest.raises(sp.SpcholError):
+        sp.spchol_dist_init(3, 2, b"\0" * 128)
+    try:
+        sp.spchol_dist_init(1, 3, b"\1" * 128)
+        with sp.Solver.from_problem(p, device=-1) as h:
+            owner, _, _ = h.spchol_export_mapping()
+            assert owner.max() == 2 and (owner < 0).any()
+            assert h.query("NMARKERS") > 0
+        with sp.Solver.from_problem(p, device=-1, dist_world=2, dist_rank=0) as h:   # explicit options win
+            assert h.spchol_export_mapping()[0].max() == 1
+    finally:
+        sp.spchol_dist_init(0, 1, None)
+    with sp.Solver.from_problem(p, device=-1) as h:
+        assert (h.spchol_export_mapping()[0] == 0).all()
