@@ -767,8 +767,8 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
 //   phase 1  TRSM of panel p's rows below the diagonal block (one thread per row, warps 0-1);
 //            X_pp = L_pp^{-1} (one thread); Y_i -= L_{i,p-1} X_{p-1} for the rows i >= b (warps 2-3,
 //            the right-looking forward substitution of L X = I, "DTRSM" on the identity)
-//   phase 2  thread 0: the three 4x4 tiles of the next diagonal block, then its 8x8 factor (8
-//            pivots in registers); warps 1-3: the rest of the trailing SYRK, and X_p = X_pp Y_p
+//   phase 2  thread 0: the next diagonal block's update by the panel and its 8x8 factor, in
+//            registers (8 pivots); warps 1-3: the rest of the trailing SYRK, and X_p = X_pp Y_p
 // so the only sequential part is the 64-pivot chain; the inverse costs no extra phase.  16-byte
 // cp.async loads, 16-byte stores.  (Replaces a row-major kernel that formed the inverse by blocked
 // doubling after the factor: 22.2 -> 20.8 us per block, one CTA, tools/potrf_probe.cu.)
@@ -785,12 +785,32 @@ __device__ long long p9_clocks[64];
 #define P9_CLKT(t, i) do { } while (0)
 #endif
 
-__device__ __forceinline__ void p9_diag(double* Ls, double* rl, int b, int nb, int& bad) {
+// 8x8 diagonal block at b: (optionally) its update by the previous panel [bp, bp + 8), then its
+// factor, all in one thread's registers; pivots' reciprocals into rl.
+template <bool UPD>
+__device__ __forceinline__ void p9_diag(double* Ls, double* rl, int b, int nb, int& bad, int bp = 0) {
   double a[8][8];
 #pragma unroll
   for (int j = 0; j < 8; ++j)
 #pragma unroll
     for (int i = j; i < 8; ++i) a[i][j] = Ls[(b + j) * P9_LD + b + i];
+  if (UPD) {   // A_bb -= L_{b,p} L_{b,p}^T (the panel rows just TRSM'd): 36 x 8 independent FMAs
+    double l[8][8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(Ls + (bp + q) * P9_LD + b + i);
+        l[i][q] = v.x;
+        l[i + 1][q] = v.y;
+      }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int i = j; i < 8; ++i) a[i][j] = fma(-l[i][q], l[j][q], a[i][j]);
+  }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const double d = a[j][j];
@@ -872,7 +892,7 @@ __global__ void __launch_bounds__(POTRF9_THREADS, 3) potrf9_kernel(const PTask* 
   __syncthreads();
   P9_CLK(1);
   int bad = -1;
-  if (tid == 0) p9_diag(Ls, rl, 0, nb, bad);
+  if (tid == 0) p9_diag<false>(Ls, rl, 0, nb, bad);
   __syncthreads();
   P9_CLK(2);
   for (int p = 0; p < NBMAX / 8; ++p) {
@@ -948,10 +968,9 @@ __global__ void __launch_bounds__(POTRF9_THREADS, 3) potrf9_kernel(const PTask* 
     // ---- phase 2
     if (warp == 0) {
       if (nt > 0) {
-        if (tid < 3) p9_syrk_tile(Ls, b, t0 + (tid ? 4 : 0), t0 + (tid == 2 ? 4 : 0));
-        __syncwarp();
+        // the next diagonal block: its update by this panel and its factor in thread 0's registers
         P9_CLKT(0, 21 + p);
-        if (tid == 0) p9_diag(Ls, rl, t0, nb, bad);
+        if (tid == 0) p9_diag<true>(Ls, rl, t0, nb, bad, b);
         P9_CLKT(0, 29 + p);
       }
     } else {

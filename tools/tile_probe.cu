@@ -10,7 +10,7 @@ __global__ void tile_k(long long* out, int nlanes, int variant) {
     if (variant == 0) p9_syrk_tile(sm, 0, 8 + 4 * (threadIdx.x % 3), 8);
     else {
       int bad = -1;
-      p9_diag(sm, sm + NBMAX * P9_LD, 8, 64, bad);
+      p9_diag<true>(sm, sm + NBMAX * P9_LD, 8, 64, bad, 0);
     }
   }
   __syncwarp();
@@ -28,7 +28,7 @@ int main() {
         long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
         if (h < best) best = h;
       }
-      printf("%s lanes=%d: %lld cycles\n", v == 0 ? "syrk tile" : "diag 8x8", nl, best);
+      printf("%s lanes=%d: %lld cycles\n", v == 0 ? "syrk tile" : "diag 8x8 + update", nl, best);
     }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
