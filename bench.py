@@ -207,6 +207,34 @@ def cpu_baseline(args, seconds_hint=True):
                       f"serial one) on {cores} threads"}
 
 
+def dry_run(args):
+    """Host-only plans of all N ranks (the multi-GPU schedule without a GPU): per rank the executed
+    flops of phase A and phase C, exchange markers, per-rank arena and communication volume; checks
+    that the ranks' plans pair up (same marker count) and partition the single-GPU work."""
+    import paper_2409_14009_b200 as sp
+    prob = gen.make(args.config)
+    with sp.Solver.from_problem(prob, device=-1) as h:
+        whole, _ = h.spchol_dist_plan_flops()
+        arena1 = h.query("ARENA_BYTES")
+    ranks = []
+    for r in range(args.gpus):
+        with sp.Solver.from_problem(prob, device=-1, dist_world=args.gpus, dist_rank=r) as h:
+            a, lv = h.spchol_dist_plan_flops()
+            ranks.append({"rank": r, "phase_a_flops": a, "phase_c_flops": float(lv.sum()), "level_flops": lv.tolist(),
+                          "markers": h.query("NMARKERS"), "arena_GB": h.query("ARENA_BYTES") / 1e9,
+                          "send_GB": h.query("COMM_SEND_BYTES") / 1e9, "recv_GB": h.query("COMM_RECV_BYTES") / 1e9,
+                          "top_distributed": h.query("NTOP_DIST")})
+    nl = len(ranks[0]["level_flops"])
+    crit = max(x["phase_a_flops"] for x in ranks) + sum(max(x["level_flops"][l] for x in ranks) for l in range(nl))
+    tot = sum(x["phase_a_flops"] + x["phase_c_flops"] for x in ranks)
+    for x in ranks:
+        del x["level_flops"]
+    print(json.dumps({"dry_run": True, "config": args.config, "n_gpus": args.gpus,
+                      "markers_match": len({x["markers"] for x in ranks}) == 1,
+                      "work_partition_exact": abs(tot - whole) <= 1e-9 * whole,
+                      "work_model_speedup": whole / crit, "single_gpu_arena_GB": arena1 / 1e9, "ranks": ranks}))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -216,10 +244,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: build every rank's host-only plan for --gpus N and print the schedule model")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.dry_run:
+        dry_run(args)
         return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(self_launch(args))

@@ -157,3 +157,18 @@ def test_fullsize_distribution_model(name):
         if name == "C4" and W == 8:
             assert whole / crit >= 6.0, whole / crit
         assert max(r_[7] for r_ in res) <= arena1 * (1.5 / W + 0.2)
+
+
+def test_bench_dry_run_two_ranks():
+    """`bench.py --dry-run --gpus N` (no GPU): every rank's host-only plan, the same marker count on all
+    ranks and an exact partition of the single-GPU work."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for n in (2, 4):
+        out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--dry-run", "--gpus", str(n),
+                              "--config", "S4"], capture_output=True, text=True, timeout=300, check=True).stdout
+        d = json.loads([ln for ln in out.splitlines() if ln.startswith("{")][-1])
+        assert d["n_gpus"] == n and len(d["ranks"]) == n
+        assert d["markers_match"] and d["work_partition_exact"]
