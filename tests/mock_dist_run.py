@@ -63,8 +63,9 @@ def main(name, world, nrounds=2, check_panels=True, full=False):
     """Factor + solve `nrounds` times on `world` rank threads; every rank holds only its own part of L
     (the sum of the ranks' panel exports is L), checked against the oracle."""
     prob = gen.make(name)
+    pr = int(os.environ.get("MOCK_PR", "0"))
     uid = sp.spchol_dist_nccl_unique_id()
-    hs = [sp.Solver.from_problem(prob, dist_world=world, dist_rank=r) for r in range(world)]
+    hs = [sp.Solver.from_problem(prob, dist_world=world, dist_rank=r, partition_refinement=pr) for r in range(world)]
     xs, b = gen.rhs(prob)
     out = [None] * world
     err = [None] * world
@@ -124,7 +125,7 @@ def main(name, world, nrounds=2, check_panels=True, full=False):
         rec["llt_err"], rec["llt_entries"] = llt_sample_error(prob, s_gpu, off, ld, pan, cols)
         del pan
     elif check_panels:
-        o = oracle.Oracle.from_problem(prob)
+        o = oracle.Oracle.from_problem(prob, pr=pr)
         assert o.factor() == -1
         Lp, Li, Lx = o.L_csc()
         s_gpu = hs[0].spchol_export_symbolic()

@@ -237,6 +237,14 @@ def test_distributed_nccl_path_mock(name, world, minflops, outer):
         assert r["ntop_dist"] > 0
 
 
+@pytest.mark.parametrize("name,world", [("S4", 3), ("S5", 2)])
+def test_distributed_partition_refinement_mock(name, world):
+    """The multi-GPU path on a partition-refined analysis (reading R14): same parity bar as above."""
+    r = run_mock(name, world, {"MOCK_PR": "1", "SPCHOL_DIST_MINFLOPS": "0"})
+    assert r["ok"], r
+    assert r["lerr"] <= TOL_L and r["berr"] <= TOL_BERR and r["ranks_agree"] and r["padding_nonzeros"] == 0, r
+
+
 @pytest.mark.parametrize("name,world", [("C4", 2), ("C4", 4), ("C4", 8), ("C5", 2), ("C5", 4)])
 def test_distributed_fullsize_mock(name, world):
     """The north_star's multi-GPU configs (C4 at 2/4/8 ranks, C5 at 2/4) through the real NCCL code
