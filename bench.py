@@ -356,7 +356,11 @@ def main():
                                "(profiles/fp64_peak.json; MEASURED_PEAKS.json has no FP64 entry)",
                 "per_kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in stats.items()},
                 "per_kernel_tflops": {k: (v["flops"] / (v["ms"] / 1e3) / 1e12 if v["ms"] > 0 and v["flops"] > 0 else None)
-                                      for k, v in stats.items()}}
+                                      for k, v in stats.items()},
+                # algorithmic bytes / time of each class (the HBM roofline of a1 init, the small
+                # kernels and the assembly; 6539 GB/s measured copy bandwidth, MEASURED_PEAKS.json)
+                "per_kernel_GBps": {k: (v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 and v["bytes"] > 0 else None)
+                                    for k, v in stats.items()}}
 
     # ---- end to end through the public API with host buffers (pinned): H2D of A's values and b,
     # factor, solve, D2H of x — every step.
