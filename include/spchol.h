@@ -278,7 +278,7 @@ int spchol_export_diagonal(spchol_handle* h, double* diag);
  * stream while enabled; disabled by default and incompatible with graph replay, which is
  * bypassed while enabled).  kind: 0 = fused small-supernode kernel, 1 = POTRF, 2 = TRSM,
  * 3 = in-panel update GEMM, 4 = SYRK/GEMM + relind scatter (U_J), 5 = panel init, 6 = RLB
- * block-pair updates.
+ * block-pair updates, 7 = fused outer-block cdiv (POTRF + TRSM + in-block updates in one launch).
  * Returns launches, summed milliseconds, algorithmic flops and bytes of that class since the last
  * reset.  spchol_kernel_stats synchronizes the stream. */
 int spchol_enable_kernel_timing(spchol_handle* h, int enable);

@@ -30,7 +30,7 @@ Q = dict(N=0, NNZ_A=1, NNZ_L=2, NFUND=3, NSUPER=4, ADDED=5, NLEVELS=6, ROWS_LEN=
          UPDATE_ENTRIES=15, NBLOCKS=16, NMARKERS=17, NTOP_DIST=18, DEVICE_BYTES=19, COMM_SEND_BYTES=20,
          COMM_RECV_BYTES=21, ARENA_BYTES=22, DIST_GRAPH=23, COMM_B_SEND_BYTES=24, COMM_B_RECV_BYTES=25, NBATCHES=26,
          HOST_BYTES=27)
-KERNEL_KINDS = dict(small=0, potrf=1, trsm=2, local_update=3, syrk_scatter=4, init=5, rlb_update=6)
+KERNEL_KINDS = dict(small=0, potrf=1, trsm=2, local_update=3, syrk_scatter=4, init=5, rlb_update=6, panel=7)
 
 # Every symbol include/spchol.h declares (checked by tests/test_capi_exports.py).
 EXPORTS = [

@@ -275,11 +275,23 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
     // multi-GPU: event after the trailing-stream reads (NEXT_b, REST) of outer block column C; the
     // broadcast into C's ring slot waits for the readers of the slot's previous block, C - ring_ns
     std::vector<int> rest_ev_of_C(maxblk / std::max(1, OUTER) + 2, -1);
+    // fused cdiv (panel_kernel): one launch per outer block step does POTRF, TRSM and the in-block
+    // updates of the whole outer block; NEXT is then one critical-stream launch (no NEXT_a / NEXT_b)
+    // (levels with at most panel_max_sn large supernodes: where the chain is critical; wide levels
+    // keep the batched launches, whose many CTAs per SM hide the short-K tiles' latency better)
+    int nlarge = 0;
+    for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x)
+      nlarge += !h->is_small[h->level_sns[x]] && (active(h->level_sns[x]) || dtop(h->level_sns[x]));
+    const bool panel = h->panel_mode && NB == NBMAX && nlarge <= h->panel_max_sn;
     const bool split_next = !h->no_lookahead && !h->no_next_split;
     for (int s = 0; s < maxblk; ++s) {
       long long p0 = (long long)h->ptasks.size(), t0 = (long long)h->gtasks.size();
       double fp = 0, ft = 0, fl = 0, bp = 0, bt = 0, bl = 0, fn = 0, bn = 0, fr = 0, br = 0, fnb = 0, bnb = 0;
       std::vector<GTask> local, left, nxt, nxtb, rest;
+      std::vector<std::vector<PanTask>> pan;   // per supernode: its outer block's tiles in order
+      double fpan = 0, bpan = 0;
+      int nd = 0;
+      bool pan_next = false;
       double flf = 0, blf = 0;
       std::vector<std::pair<int, int>> bcast;   // (J, column block) finished at this step
       for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x) {
@@ -293,7 +305,34 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         const int nb = std::min(NB, I.k - c0), c1 = c0 + nb;
         const int C0 = (c0 / W) * W, C1 = std::min(C0 + W, I.k);   // enclosing outer block
         auto own = [&](int col) { return !dj || blk_owner(h, J, col / W) == h->rank; };
-        if (own(C0)) {
+        // fused cdiv for the outer block starting at column C: in chain-critical levels, once the rows
+        // left (m - C) are few enough that the trailing update no longer hides the chain
+        auto pan_at = [&](int C) { return panel && I.m - C <= h->panel_max_rows; };
+        if (own(C0) && pan_at(C0)) {
+          if (c0 == C0) {   // the whole outer block [C0, C1) as one set of panel tiles
+            const int w = C1 - C0, nbk = (w + NB - 1) / NB;
+            const int ntile = (I.m - C0 + TILE - 1) / TILE;
+            std::vector<PanTask> v;
+            // the lookahead update by the previous outer block (NEXT) is folded into the tiles
+            // (not for a distributed top supernode: its NEXT runs on the next block's owner)
+            const int pw = C0 > 0 && !dj ? W : 0;   // NEXT(C0 - W) folded here (see the NEXT emission below)
+            // diagonal-region blocks (i, j <= i) in pair order, then the tiles below
+            for (int i = 0; i < nbk; ++i)
+              for (int j = 0; j <= i; ++j) v.push_back(PanTask{J, C0, w, i, j, slot, h->npanflags, pw});
+            for (int j = 0; j < nbk; ++j)
+              for (int i = nbk; i < ntile; ++i) v.push_back(PanTask{J, C0, w, i, j, slot, h->npanflags, pw});
+            h->npanflags += 16 + 4 * std::max(0, ntile - nbk);
+            pan.push_back(std::move(v));
+            pan_next = pan_next || pw > 0;
+            for (int c = C0; c < C1 && pw > 0; ++c) { fpan += 2.0 * pw * (double)(I.m - c); bpan += 16.0 * (double)(I.m - c); }
+            for (int b = C0; b < C1; b += NB) {   // POTRF + TRSM + in-block update of inner block b
+              const int nbb = std::min(NB, C1 - b), b1 = b + nbb;
+              fpan += (double)nbb * nbb * nbb / 3.0 + (double)(I.m - b1) * nbb * nbb;
+              bpan += 16.0 * nbb * nbb + 16.0 * (double)(I.m - b1) * nbb;
+              for (int c = b1; c < C1; ++c) { fpan += 2.0 * nbb * (double)(I.m - c); bpan += 16.0 * (double)(I.m - c); }
+            }
+          }
+        } else if (own(C0)) {
           h->ptasks.push_back(PTask{J, c0, nb, slot});
           fp += (double)nb * nb * nb / 3.0;
           bp += 16.0 * nb * nb;
@@ -321,7 +360,7 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         // TILE there, so no tile straddles two blocks)
         if (c1 == C1 && C1 < I.k) {
           const int C2 = std::min(C1 + W, I.k);
-          if (own(C1)) {
+          if (own(C1) && (!pan_at(C1) || dj)) {   // (else folded into the next outer block's panel launch)
             const int Ca = split_next ? std::min(C1 + NB, C2) : C2;
             for_tiles(C1, I.m, C1, Ca, [&](int r0, int s0) { nxt.push_back(GTask{J, r0, s0, C0, C1 - C0, Ca}); });
             for (int c = C1; c < Ca; ++c) { fn += 2.0 * (C1 - C0) * (double)(I.m - c); bn += 16.0 * (double)(I.m - c); }
@@ -342,6 +381,28 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
         long long f0 = (long long)h->gtasks.size();
         h->gtasks.insert(h->gtasks.end(), left.begin(), left.end());
         push(K_LOCAL, f0, (long long)h->gtasks.size(), flf, blf);
+      }
+      if (!pan.empty()) {   // task x of every outer block after the tasks < x of all of them (the
+                            // diagonal-region pairs, then the tiles below, each in dependency order)
+        const long long q0 = (long long)h->pantasks.size();
+        size_t mx = 0;
+        for (const auto& v : pan) mx = std::max(mx, v.size());
+        for (int below = 0; below < 2; ++below)
+          for (size_t i = 0; i < mx; ++i)
+            for (const auto& v : pan) {
+              if (i >= v.size()) continue;
+              const bool isb = v[i].tile >= (v[i].w + NB - 1) / NB;
+              if (isb == (below == 1)) h->pantasks.push_back(v[i]);
+              if (!below && !isb) ++nd;
+            }
+        // the folded NEXT(S-1) touches the entries REST(S-2) updated: wait for it (REST(S-1) is disjoint)
+        const int Cn = s / OUTER;
+        if (pan_next && Cn >= 2 && rest_ev_of_C[Cn - 2] >= 0)
+          h->plan.push_back(Launch{0, 0, 0, 0, 0, OP_WAIT, SB, rest_ev_of_C[Cn - 2]});
+        Launch P{K_PANEL, q0, (int)((long long)h->pantasks.size() - q0), fpan, bpan, OP_LAUNCH, SB, -1};
+        P.aux = h->npanlaunch++;   // sync3 index
+        P.aux2 = nd;               // diagonal tiles first
+        h->plan.push_back(P);
       }
       push(K_POTRF, p0, p1, fp, bp);
       push(K_TRSM, t0, t1, ft, bt);
@@ -904,6 +965,8 @@ static int setup_device(spchol_handle* h) {
   CK(upload(&h->d_gtasks, h->gtasks));
   CK(upload(&h->d_rtasks, h->rtasks));
   CK(upload(&h->d_ptasks, h->ptasks));
+  CK(upload(&h->d_pantasks, h->pantasks));
+  CK(dalloc(&h->d_pansync, (size_t)h->npanflags + 3 * (size_t)h->npanlaunch));
   if (h->world == 1) CK(dalloc(&h->d_linv, (size_t)std::max(1, h->nslots_total) * NBMAX * NBMAX));
   if (h->use_tma) {
     // TMA descriptors: panel J as a 2D tensor (m_J rows contiguous, k_J columns, row stride ld_J),
@@ -969,7 +1032,7 @@ static void free_device(spchol_handle* h) {
   if (h->d_ainit_dst) cudaFree(h->d_ainit_dst);
   void* ptrs[] = {h->d_ssolve, h->d_stasks, h->d_sflags, h->d_rtasks, h->d_tmaps, h->d_tmap_linv, h->d_small_sns, h->d_diag_idx, h->d_panels, h->d_avals, h->d_linv, h->d_y, h->d_y2, h->d_amap, h->d_ucol_base, h->d_ucol_map,
                   h->d_rows_ptr, h->d_posmap, h->d_sfirst, h->d_rows, h->d_perm, h->d_level_sns, h->d_sn,
-                  h->d_gtasks, h->d_ptasks, h->d_fail};
+                  h->d_gtasks, h->d_ptasks, h->d_pantasks, h->d_pansync, h->d_fail};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : h->plan_events) if (e) cudaEventDestroy(e);
@@ -1010,6 +1073,10 @@ static int finish_handle(spchol_handle* h) {
   if (const char* e = getenv("SPCHOL_OUTER")) h->outer = std::max(1, atoi(e));
   if (const char* e = getenv("SPCHOL_DIST_MINFLOPS")) h->dist_min_flops = atof(e);
   if (const char* e = getenv("SPCHOL_RING_NS")) h->ring_ns = std::max(2, atoi(e));   // diagnostics
+  if (const char* e = getenv("SPCHOL_PANEL")) h->panel_mode = atoi(e) != 0;
+  if (const char* e = getenv("SPCHOL_PANEL_GRID")) h->panel_grid = std::max(0, atoi(e));
+  if (const char* e = getenv("SPCHOL_PANEL_MAX_SN")) h->panel_max_sn = atoi(e);
+  if (const char* e = getenv("SPCHOL_PANEL_MAX_ROWS")) h->panel_max_rows = atoi(e);
   if (const char* e = getenv("SPCHOL_SMALL_WARP")) h->small_warp = atoi(e) != 0;
   if (const char* e = getenv("SPCHOL_SMALL_WARP_MAXM")) h->small_warp_maxm = std::max(0, std::min(128, atoi(e)));
   if (h->opt.device_mem_cap < 0 || (h->opt.device_mem_cap > 0 && h->world > 1))
@@ -1311,6 +1378,10 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
       case K_POTRF:
         launch_potrf(h->d_ptasks + L.off, L.n, h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, ls, prio);
         break;
+      case K_PANEL:
+        launch_panel(h->d_pantasks + L.off, L.aux2, L.n - L.aux2, h->d_pansync + h->npanflags + 3 * L.aux, h->d_pansync,
+                     h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, h->panel_grid, ls, prio);
+        break;
       case K_TRSM:
         if (h->use_tma)
           launch_gemm_tma(MODE_TRSM, h->d_gtasks + L.off, L.n, h->d_sn, h->d_panels, h->d_tmaps, h->d_tmap_linv, h->d_ucol_base, h->d_ucol_map, h->d_posmap, ls, prio);
@@ -1404,6 +1475,9 @@ static int enqueue_factor_capped(spchol_handle* h, cudaStream_t st) {
 }
 
 static int enqueue_factor(spchol_handle* h, cudaStream_t st) {
+  // panel_kernel ready flags and tickets start at 0 in every factor
+  if (h->npanflags + h->npanlaunch > 0)
+    CK(cudaMemsetAsync(h->d_pansync, 0, sizeof(int) * ((size_t)h->npanflags + 3 * (size_t)h->npanlaunch), st));
   if (h->capped) return enqueue_factor_capped(h, st);
   int rc = enqueue_init(h, st);
   if (rc) return rc;

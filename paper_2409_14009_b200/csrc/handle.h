@@ -24,7 +24,7 @@ int cuda_fail(cudaError_t e, const char* where);
     if (e_ != cudaSuccess) return ::spchol::cuda_fail(e_, #call);  \
   } while (0)
 
-enum LaunchKind { K_SMALL = 0, K_POTRF = 1, K_TRSM = 2, K_LOCAL = 3, K_SCATTER = 4, K_INIT = 5, K_RLB = 6, K_NKINDS = 7 };
+enum LaunchKind { K_SMALL = 0, K_POTRF = 1, K_TRSM = 2, K_LOCAL = 3, K_SCATTER = 4, K_INIT = 5, K_RLB = 6, K_PANEL = 7, K_NKINDS = 8 };
 
 // NCCL, loaded on demand (dlopen of libnccl.so.2, normally the copy torch already loaded): the
 // library has no link-time NCCL dependency and single-GPU use never touches it.
@@ -145,6 +145,12 @@ struct spchol_handle {
   std::vector<spchol::GTask> gtasks;
   std::vector<spchol::RTask> rtasks;    // RLB block-pair tiles (update_mode 1)
   std::vector<spchol::PTask> ptasks;
+  std::vector<spchol::PanTask> pantasks;   // fused outer-block cdiv tiles (K_PANEL launches; aux = ticket index)
+  int npanflags = 0, npanlaunch = 0;       // ready flags (16 per outer block) and K_PANEL launches
+  bool panel_mode = true;                  // SPCHOL_PANEL=0: the cdiv as separate POTRF / TRSM / update launches
+  int panel_grid = 0;                      // SPCHOL_PANEL_GRID: CTAs of a below launch (0 = min(tasks, 4 x 148))
+  int panel_max_sn = 2;                    // SPCHOL_PANEL_MAX_SN: fused cdiv in levels with <= this many large supernodes
+  int panel_max_rows = 1 << 30;            // SPCHOL_PANEL_MAX_ROWS: ... for outer blocks with m - c0 <= this many rows
   std::vector<int> level_sns, level_off;
   std::vector<int> small_sns;           // supernodes handled by the fused small kernel, by level
   std::vector<char> is_small;
@@ -252,6 +258,8 @@ struct spchol_handle {
   spchol::GTask* d_gtasks = nullptr;
   spchol::RTask* d_rtasks = nullptr;
   spchol::PTask* d_ptasks = nullptr;
+  spchol::PanTask* d_pantasks = nullptr;
+  int* d_pansync = nullptr;             // [npanflags] ready flags | 3 per K_PANEL launch (tickets, done count), zeroed per factor
   unsigned long long* d_fail = nullptr;
   bool values_set = false, factored = false;
   std::vector<cudaStream_t> pstreams;           // plan streams: even = cdiv chain (high priority),

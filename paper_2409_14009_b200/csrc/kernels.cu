@@ -858,25 +858,23 @@ __device__ __forceinline__ void p9_syrk_tile(double* Ls, int b, int r0, int c0) 
       if (r0 + i >= c0 + j) Ls[(c0 + j) * P9_LD + r0 + i] = acc[i][j];   // upper part of diagonal tiles unused
 }
 
-__global__ void __launch_bounds__(POTRF9_THREADS, 3) potrf9_kernel(const PTask* __restrict__ tasks,
-                                                                const SnInfo* __restrict__ sn,
-                                                                const int* __restrict__ sfirst, double* panels,
-                                                                double* linv, unsigned long long* fail) {
-  pdl_enter();
-  extern __shared__ __align__(16) double p9_smem[];
+// The whole block's factor + inverse by the CTA's 128 threads (POTRF9_SMEM bytes of shared memory at
+// p9_smem); used by potrf9_kernel and by the fused panel kernels.  LOAD = false: the caller has
+// already placed the (updated) block in Ls (column-major, stride P9_LD) and synchronised.
+template <bool LOAD = true>
+__device__ __forceinline__ void potrf9_block(const PTask& T, const SnInfo& S, const int* __restrict__ sfirst,
+                                             double* panels, double* linv, unsigned long long* fail, double* p9_smem) {
   double* Ls = p9_smem;                        // A -> L (column-major, lower part used)
   double* Xs = Ls + NBMAX * P9_LD;             // Y = I -> X = L^{-1} (column-major)
   double* rl = Xs + NBMAX * P9_LD;             // 1 / L_jj
   double* Xd = rl + NBMAX;                     // X_pp of the current panel (8 x 8, column-major)
   P9_CLK(0);
-  const PTask T = tasks[blockIdx.x];
-  const SnInfo S = sn[T.sn];
   const int nb = T.nb, tid = threadIdx.x, warp = tid >> 5;
   double* P = panels + S.off + (long long)T.c0 * S.ld + T.c0;
   // A's block: 16-byte cp.async of row pairs (rows >= nb zero-filled), Y = I meanwhile
   for (int e = tid; e < NBMAX * NBMAX / 2; e += POTRF9_THREADS) {
     const int c = e >> 5, r = (e & 31) * 2;
-    if (c < nb && r < nb) {
+    if (LOAD && c < nb && r < nb) {
       const unsigned sa = (unsigned)__cvta_generic_to_shared(Ls + c * P9_LD + r);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(P + (long long)c * S.ld + r),
                    "r"(r + 1 < nb ? 16 : 8));
@@ -1026,6 +1024,196 @@ __global__ void __launch_bounds__(POTRF9_THREADS, 3) potrf9_kernel(const PTask* 
     }
   }
   P9_CLK(20);
+}
+
+// ----------------------------------------------------------------------------------------------
+// potrf10_block: the same contract as potrf9_block (factor + inverse of one <= 64-column diagonal
+// block, "DPOTRF"), restructured so that only the 8x8 pivot factors stay sequential.  Panels p
+// of 8 columns (b = 8p), three barrier phases each:
+//   1  thread 0: D_p (already updated) -> L_pp, 1/L_jj, X_pp = L_pp^{-1} in registers;
+//      warps 1-3 meanwhile, on DMMA: the lookahead update of panel p+1's columns by panels < p
+//      (left-looking, K = 8p) and X's row block p-1: X_{p-1,<} = -X_{p-1,p-1} L_{p-1,<} X_{<,<}
+//      (L X = I by row blocks)
+//   2  TRSM of panel p's rows below: L_{r,p} = A_{r,p} X_pp^T (one thread per row, depth 8)
+//   3  panel p+1's columns -= L_{.,p} L_{p+1,p}^T (DMMA, K = 8)
+// L in shared memory column-major, X row-major (both stride P10_LD = 72: conflict-free fragments).
+// ----------------------------------------------------------------------------------------------
+constexpr int P10_LD = 72;
+constexpr int POTRF10_SMEM = (2 * NBMAX * P10_LD + NBMAX + 2 * 64 + 8 * 64) * (int)sizeof(double);
+
+template <bool LOAD = true>
+__device__ __forceinline__ void potrf10_block(const PTask& T, const SnInfo& S, const int* __restrict__ sfirst,
+                                              double* panels, double* linv, unsigned long long* fail, double* smem) {
+  double* Ls = smem;                       // L[r][c] at Ls[c * P10_LD + r]
+  double* Xs = Ls + NBMAX * P10_LD;        // X[r][c] at Xs[r * P10_LD + c]
+  double* rl = Xs + NBMAX * P10_LD;        // 1 / L_jj
+  double* Xd = rl + NBMAX;                 // X_pp of panels p (even / odd), row-major 8 x 8 each
+  double* Tsc = Xd + 128;                  // 8 x 64 row-major scratch (X row block products)
+  const int nb = T.nb, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  constexpr int LD = P10_LD;
+  double* P = panels + S.off + (long long)T.c0 * S.ld + T.c0;
+  if (LOAD) {
+    for (int e = tid; e < NBMAX * NBMAX / 2; e += POTRF9_THREADS) {
+      const int c = e >> 5, r = (e & 31) * 2;
+      if (c < nb && r < nb && r + 1 >= c) cp_async16(Ls + c * LD + r, P + (long long)c * S.ld + r, r + 1 < nb ? 16 : 8);
+    }
+    cp_async_commit();
+  }
+  for (int e = tid; e < NBMAX * LD / 2; e += POTRF9_THREADS) reinterpret_cast<double2*>(Xs)[e] = make_double2(0.0, 0.0);
+  if (LOAD) cp_async_wait<0>();
+  if (nb < NBMAX) {   // padding: identity (pivots 1, no coupling)
+    __syncthreads();
+    for (int e = tid; e < NBMAX * NBMAX; e += POTRF9_THREADS) {
+      const int c = e >> 6, r = e & 63;
+      if (c >= nb || r >= nb) Ls[c * LD + r] = r == c ? 1.0 : 0.0;
+    }
+  }
+  __syncthreads();
+  int bad = -1;
+  // X row block pb (rows 8 pb ..): T = L_{pb,<} X_{<,<} on column tile j0, then X = -X_pb,pb T
+  auto x_block = [&](int pb, int j0) {
+    const int bb = 8 * pb;
+    double acc[2] = {0.0, 0.0};
+    for (int q = j0; q < bb; q += 4) dmma(acc, Ls[(q + t) * LD + bb + g], Xs[(q + t) * LD + j0 + g]);
+    Tsc[g * 64 + j0 + 2 * t] = acc[0];
+    Tsc[g * 64 + j0 + 2 * t + 1] = acc[1];
+    __syncwarp();
+    const double* Xp = Xd + (pb & 1) * 64;
+    double x2[2] = {0.0, 0.0};
+    dmma(x2, Xp[g * 8 + t], Tsc[t * 64 + j0 + g]);
+    dmma(x2, Xp[g * 8 + 4 + t], Tsc[(4 + t) * 64 + j0 + g]);
+    Xs[(bb + g) * LD + j0 + 2 * t] = -x2[0];
+    Xs[(bb + g) * LD + j0 + 2 * t + 1] = -x2[1];
+  };
+  // rows r0.. x columns c0..c0+7 of L's trailing part -= L[r0.., q0..q1) L[c0.., q0..q1)^T
+  auto upd_tile = [&](int r0, int c0, int q0, int q1) {
+    double acc[2] = {Ls[(c0 + 2 * t) * LD + r0 + g], Ls[(c0 + 2 * t + 1) * LD + r0 + g]};
+    for (int q = q0; q < q1; q += 4) dmma(acc, -Ls[(q + t) * LD + r0 + g], Ls[(q + t) * LD + c0 + g]);
+    Ls[(c0 + 2 * t) * LD + r0 + g] = acc[0];
+    Ls[(c0 + 2 * t + 1) * LD + r0 + g] = acc[1];
+  };
+  for (int p = 0; p < NBMAX / 8; ++p) {
+    const int b = 8 * p;
+    // ---- phase 1
+    if (warp == 0) {
+      if (tid == 0) {
+        double a[8][8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int i = j; i < 8; ++i) a[i][j] = Ls[(b + j) * LD + b + i];
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double d = a[j][j];
+          if (bad < 0 && b + j < nb && !(d > 0.0)) bad = b + j;
+          r[j] = rsqrt_nr(d);
+          a[j][j] = d * r[j];
+#pragma unroll
+          for (int i = j + 1; i < 8; ++i) a[i][j] *= r[j];
+#pragma unroll
+          for (int q = j + 1; q < 8; ++q)
+#pragma unroll
+            for (int i = q; i < 8; ++i) a[i][q] = fma(-a[i][j], a[q][j], a[i][q]);
+        }
+        double x[8][8];   // X_pp = L_pp^{-1}, column by column (columns independent)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          x[c][c] = r[c];
+#pragma unroll
+          for (int i = c + 1; i < 8; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = c; q < i; ++q) acc = fma(a[i][q], x[q][c], acc);
+            x[i][c] = -acc * r[i];
+          }
+        }
+        double* Xp = Xd + (p & 1) * 64;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          rl[b + j] = r[j];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (i >= j) {
+              Ls[(b + j) * LD + b + i] = a[i][j];
+              Xs[(b + i) * LD + b + j] = x[i][j];
+            }
+            Xp[i * 8 + j] = i >= j ? x[i][j] : 0.0;
+          }
+        }
+      }
+    } else {
+      const int nl = 7 - p;                 // lookahead tiles: rows b+8+8u, panel p+1's columns, K = b
+      const int nx = p >= 1 ? p - 1 : 0;    // X row block p-1: column tiles 0, 8, .. (p-2)*8
+      for (int job = warp - 1; job < nl + nx; job += 3) {
+        if (job < nl) upd_tile(b + 8 + 8 * job, b + 8, 0, b);
+        else x_block(p - 1, 8 * (job - nl));
+      }
+    }
+    __syncthreads();
+    if (p == NBMAX / 8 - 1) break;
+    // ---- phase 2: TRSM of panel p's rows below its diagonal block
+    if (tid < NBMAX - b - 8) {
+      const int r = b + 8 + tid;
+      const double* Xp = Xd + (p & 1) * 64;
+      double a[8], x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = Ls[(b + j) * LD + r];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q <= j; ++q) acc = fma(a[q], Xp[j * 8 + q], acc);
+        x[j] = acc;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) Ls[(b + j) * LD + r] = x[j];
+    }
+    __syncthreads();
+    // ---- phase 3: panel p+1's columns by panel p (K = 8)
+    for (int u = warp; u < 7 - p; u += 4) upd_tile(b + 8 + 8 * u, b + 8, b, b + 8);
+    __syncthreads();
+  }
+  // X row block 7
+  for (int job = warp; job < 7; job += 4) x_block(7, 8 * job);
+  if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[T.sn] + T.c0 + bad));
+  __syncthreads();
+  // L (lower, r >= c) into the panel; X (lower, zero elsewhere) column-major into the inverse slot
+  double* W = linv + (long long)T.slot * (NBMAX * NBMAX);
+  for (int e = tid; e < NBMAX * NBMAX / 2; e += POTRF9_THREADS) {
+    const int c = e >> 5, r = (e & 31) * 2;
+    const double2 l = *reinterpret_cast<const double2*>(Ls + c * LD + r);
+    const bool in0 = r >= c && r < nb && c < nb, in1 = r + 1 >= c && r + 1 < nb && c < nb;
+    *reinterpret_cast<double2*>(W + e * 2) = make_double2(in0 ? Xs[r * LD + c] : 0.0, in1 ? Xs[(r + 1) * LD + c] : 0.0);
+    double* d = P + (long long)c * S.ld + r;
+    if (in0 && in1) *reinterpret_cast<double2*>(d) = l;
+    else {
+      if (in0) d[0] = l.x;
+      if (in1) d[1] = l.y;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(POTRF9_THREADS, 2) potrf10_kernel(const PTask* __restrict__ tasks,
+                                                                 const SnInfo* __restrict__ sn,
+                                                                 const int* __restrict__ sfirst, double* panels,
+                                                                 double* linv, unsigned long long* fail) {
+  pdl_enter();
+  extern __shared__ __align__(16) double p10_smem[];
+  const PTask T = tasks[blockIdx.x];
+  const SnInfo S = sn[T.sn];
+  potrf10_block(T, S, sfirst, panels, linv, fail, p10_smem);
+}
+
+__global__ void __launch_bounds__(POTRF9_THREADS, 3) potrf9_kernel(const PTask* __restrict__ tasks,
+                                                                const SnInfo* __restrict__ sn,
+                                                                const int* __restrict__ sfirst, double* panels,
+                                                                double* linv, unsigned long long* fail) {
+  pdl_enter();
+  extern __shared__ __align__(16) double p9_smem[];
+  const PTask T = tasks[blockIdx.x];
+  const SnInfo S = sn[T.sn];
+  potrf9_block(T, S, sfirst, panels, linv, fail, p9_smem);
 }
 
 __global__ void init_scatter_kernel(const double* __restrict__ vals, const long long* __restrict__ amap,
@@ -1474,10 +1662,409 @@ __global__ void gather_kernel(const double* __restrict__ src, const long long* _
     out[i] = idx[i] >= 0 ? src[idx[i]] : 0.0;   // idx < 0: entry held by another rank (multi-GPU)
 }
 
+// ----------------------------------------------------------------------------------------------
+// Fused cdiv of one 256-column outer block [c0, c0 + w) of a large supernode ("DPOTRF" +
+// "DTRSM", with the right-looking updates inside the outer block and the lookahead update by the
+// previous outer block), as one launch pair instead of ~12 launches.  nbk = ceil(w / 64) inner
+// blocks; the rows [c0, m) are cut into 64-row tiles, tile i < nbk holding diagonal block i.
+//   panel_diag_kernel  the nbk (nbk + 1) / 2 blocks (i, j <= i) of the diagonal region, one task each:
+//     (i, i)  NEXT on the block, A_ii -= L_is L_is^T for s < i - 1, then the critical step fused in
+//             shared memory: L_{i,i-1} = A_{i,i-1} X_{i-1}^T, A_ii -= L_{i,i-1} L_{i,i-1}^T, POTRF(i)
+//             (factor + inverse X_i) without a round trip through memory
+//     (i, j<i) NEXT on the block, A_ij -= L_is L_js^T for s < j, then (j < i - 1) L_ij = A_ij X_j^T
+//   panel_below_kernel the blocks (i >= nbk, j < nbk) below it, one task each: NEXT, the updates by
+//             the blocks s < j, TRSM.
+// Ready flags per outer block, F[4 i + j] (diagonal region): (j < i) 1 = A_ij fully updated, 2 = L_ij
+// in memory; (j == i) 1 = L_ii and X_i in memory; F[16 + 4 (i - nbk) + j] (below): 2 = L_ij in memory.  Tasks are claimed through a ticket in an order in which
+// every wait is on an earlier task of the same outer block, so neither launch can deadlock whatever
+// the residency; the below launch is the programmatic dependent of the diagonal one (released once
+// every diagonal CTA is resident) and never waits for tasks it could block.  Operands are read with
+// cp.async.cg (L2); results are published with threadfence + st.release.gpu, observed with
+// ld.acquire.gpu (as in the level solve).
+// ----------------------------------------------------------------------------------------------
+#ifdef SPCHOL_PK_CLOCKS   // tools/panel_probe.cu: globaltimer stamps per task
+__device__ long long pk_clk[8192][8];
+#define PK_T(q, e) do { if (threadIdx.x == 0 && (q) < 8192) { long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); pk_clk[q][e] = t_; } } while (0)
+#else
+#define PK_T(q, e) do { } while (0)
+#endif
+
+// acc = A B^T over K columns: A, B = 64-row blocks of column-major matrices (rows past arows /
+// brows and columns past K read as zero); the gemm_kernel pipeline (BK-column chunks, cp.async).
+template <int BK = spchol::BK, int STAGES = spchol::STAGES>
+__device__ __forceinline__ void pk_mma(const double* A, long long lda, int arows, const double* B, long long ldb,
+                                       int brows, int K, double (&acc)[4][4][2], double* smem) {
+  double* sA = smem;
+  double* sB = smem + STAGES * BK * LDS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int nchunks = (K + BK - 1) / BK;
+  constexpr int NP = (BK * TILE / 2) / GEMM_THREADS;
+  const double* srcA[NP];
+  const double* srcB[NP];
+  int byA[NP], byB[NP], kkp[NP], dofs[NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    const int p = tid + i * GEMM_THREADS;
+    const int kk = p >> 5, rp = (p & 31) * 2;
+    const int ra = max(0, min(2, arows - rp)), rb = max(0, min(2, brows - rp));
+    byA[i] = ra * 8;
+    byB[i] = rb * 8;
+    srcA[i] = ra ? A + kk * lda + rp : A;
+    srcB[i] = rb ? B + kk * ldb + rp : B;
+    kkp[i] = kk;
+    dofs[i] = kk * LDS + rp;
+  }
+  auto load_chunk = [&](int chunk, int stage) {
+    double* dA = sA + stage * BK * LDS;
+    double* dB = sB + stage * BK * LDS;
+    const int kc = chunk * BK;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const bool kval = kc + kkp[i] < K;
+      cp_async16(dA + dofs[i], kval && byA[i] ? srcA[i] + kc * lda : A, kval ? byA[i] : 0);
+      cp_async16(dB + dofs[i], kval && byB[i] ? srcB[i] + kc * ldb : B, kval ? byB[i] : 0);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nchunks) load_chunk(s, s);
+    cp_async_commit();
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nc = c + STAGES - 1;
+    if (nc < nchunks) load_chunk(nc, nc % STAGES);
+    cp_async_commit();
+    const double* cA = sA + (c % STAGES) * BK * LDS + wm * 32 + g;
+    const double* cB = sB + (c % STAGES) * BK * LDS + wn * 32 + g;
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = cA[(ks * 4 + t) * LDS + i * 8];
+        b[i] = cB[(ks * 4 + t) * LDS + i * 8];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+// dst (column-major, leading dimension ld, 16-byte aligned row pairs) := C (sub = false) or -= C
+// (sub = true) on rows rlo <= r < nrows, columns c < ncols, and r >= c if lower.  The tile is staged
+// through shared memory; each warp streams whole columns (16-byte accesses, loads before stores).
+__device__ __forceinline__ void pk_store(const double (&acc)[4][4][2], double* smem, double* dst, long long ld, int rlo,
+                                         int nrows, int ncols, bool sub, bool lower) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+  constexpr int LDC = TILE + 4;
+  double* sC = smem;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) sC[(wn * 32 + j * 8 + 2 * t + v) * LDC + wm * 32 + i * 8 + g] = acc[i][j][v];
+  __syncthreads();
+  const int pr = 2 * lane;
+  constexpr int NIT = TILE / (GEMM_THREADS / 32);
+  double2 dv[NIT];
+  if (sub) {
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int col = warp + 4 * it;
+      const bool ok = col < ncols && pr + 1 >= rlo && pr < nrows && (!lower || pr + 1 >= col);
+      dv[it] = ok ? *reinterpret_cast<const double2*>(dst + col * ld + pr) : make_double2(0.0, 0.0);
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int col = warp + 4 * it;
+    const bool v0 = col < ncols && pr >= rlo && pr < nrows && (!lower || pr >= col);
+    const bool v1 = col < ncols && pr + 1 >= rlo && pr + 1 < nrows && (!lower || pr + 1 >= col);
+    if (!v0 && !v1) continue;
+    double2 c2 = *reinterpret_cast<const double2*>(sC + col * LDC + pr);
+    if (sub) c2 = make_double2(dv[it].x - c2.x, dv[it].y - c2.y);
+    double* d = dst + col * ld + pr;
+    if (v0 && v1) *reinterpret_cast<double2*>(d) = c2;
+    else if (v0) d[0] = c2.x;
+    else d[1] = c2.y;
+  }
+  __threadfence();
+  __syncthreads();
+}
+
+__device__ __forceinline__ void pk_wait(const int* f, int v) {
+  if (threadIdx.x == 0)
+    while (ld_acquire(f) < v) __nanosleep(20);
+  __syncthreads();
+}
+__device__ __forceinline__ void pk_publish(int* f, int v) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(f, v);
+}
+
+// Geometry of one panel task: tile i's rows, block j's columns.
+struct PkGeo {
+  int i, nbk, r0, nrows, nr64;
+  double* Pc;   // column c0 of the panel
+};
+__device__ __forceinline__ PkGeo pk_geo(const PanTask& T, const SnInfo& S, double* panels) {
+  PkGeo G;
+  G.i = T.tile;
+  G.nbk = (T.w + NBMAX - 1) / NBMAX;
+  G.r0 = T.c0 + NBMAX * G.i;
+  G.nrows = S.m - G.r0;
+  G.nr64 = min(G.nrows, TILE);
+  G.Pc = panels + S.off + (long long)T.c0 * S.ld;
+  return G;
+}
+// A_{i,j} -= L_{i,q} L_{j,q}^T over the columns [c0 + off, c0 + off + K) (off < 0: the previous outer
+// block, NEXT); lower if j == i.
+__device__ __forceinline__ void pk_update(const PanTask& T, const SnInfo& S, const PkGeo& G, int j, int off, int K,
+                                          double* smem) {
+  double acc[4][4][2];
+  const double* Pq = G.Pc + (long long)off * S.ld;
+  const int cj = NBMAX * j;
+  pk_mma(Pq + G.r0, S.ld, G.nrows, Pq + T.c0 + cj, S.ld, S.m - (T.c0 + cj), K, acc, smem);
+  pk_store(acc, smem, G.Pc + (long long)cj * S.ld + G.r0, S.ld, 0, G.nr64, min(NBMAX, T.w - cj), true, j == G.i);
+}
+// L_{i,s} = A_{i,s} X_s^T on rows >= rlo of the tile
+__device__ __forceinline__ void pk_trsm(const PanTask& T, const SnInfo& S, const PkGeo& G, int s, int rlo,
+                                        const double* linv, double* smem) {
+  double acc[4][4][2];
+  const int nbs = min(NBMAX, T.w - NBMAX * s);
+  double* Ps = G.Pc + (long long)NBMAX * s * S.ld;
+  pk_mma(Ps + G.r0, S.ld, G.nrows, linv + (long long)(T.slot + s) * (NBMAX * NBMAX), NBMAX, nbs, nbs, acc, smem);
+  pk_store(acc, smem, Ps + G.r0, S.ld, rlo, G.nr64, nbs, false, false);
+}
+
+// 64 x 64 column-major block (rows contiguous, leading dimension ld) -> shared memory (stride LDS),
+// 16-byte cp.async.
+__device__ __forceinline__ void pk_stage64(double* dst, const double* src, long long ld) {
+  for (int e = threadIdx.x; e < TILE * TILE / 2; e += GEMM_THREADS) {
+    const int c = e >> 5, r = (e & 31) * 2;
+    cp_async16(dst + c * LDS + r, src + c * ld + r, 16);
+  }
+}
+// acc (zeroed here) = sA sB^T over K = 64, both operands in shared memory (stride LDS); with
+// skip_upper the warp of the strictly upper quadrant (wm < wn) does nothing.
+__device__ __forceinline__ void pk_mma_smem(const double* sA, const double* sB, double (&acc)[4][4][2], bool skip_upper) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (skip_upper && wm < wn) return;
+  const double* cA = sA + wm * 32 + g;
+  const double* cB = sB + wn * 32 + g;
+#pragma unroll 4
+  for (int k = 0; k < TILE; k += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a[i] = cA[(k + t) * LDS + i * 8];
+      b[i] = cB[(k + t) * LDS + i * 8];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+  }
+}
+
+constexpr int PANEL_DIAG_SMEM = POTRF10_SMEM + 2 * TILE * LDS * (int)sizeof(double);
+static_assert(2 * TILE * LDS >= 2 * STAGES * BK * LDS && 2 * TILE * LDS >= TILE * (TILE + 4), "pk_mma / pk_store staging");
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1) panel_diag_kernel(const PanTask* __restrict__ tasks, int ntasks,
+                                                                    int* sync3, int* flags, const SnInfo* __restrict__ sn,
+                                                                    const int* __restrict__ sfirst, double* panels,
+                                                                    double* linv, unsigned long long* fail, int trigger) {
+  pdl_enter();
+  if (trigger) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  extern __shared__ __align__(16) double smem[];
+  double* gsm = smem + POTRF10_SMEM / (int)sizeof(double);   // GEMM staging: sA | sB
+  double* sA = gsm;
+  double* sB = gsm + TILE * LDS;
+  double* Ls = smem;
+  __shared__ int s_task;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_task = atomicAdd(sync3, 1);
+    __syncthreads();
+    const int q = s_task;
+    if (q >= ntasks) break;
+    PK_T(q, 0);
+    const PanTask T = tasks[q];
+    const SnInfo S = sn[T.sn];
+    const PkGeo G = pk_geo(T, S, panels);
+    const int i = G.i, j = T.blk;
+    int* F = flags + T.flag;
+    if (T.pw > 0) pk_update(T, S, G, j, -T.pw, T.pw, gsm);   // NEXT
+    PK_T(q, 1);
+    if (j < i) {   // ---- off-diagonal block of the diagonal region
+      for (int s = 0; s < j; ++s) {
+        pk_wait(F + 4 * i + s, 2);
+        pk_wait(F + 4 * j + s, 2);
+        pk_update(T, S, G, j, NBMAX * s, min(NBMAX, T.w - NBMAX * s), gsm);
+      }
+      if (j == i - 1) {
+        pk_publish(F + 4 * i + j, 1);   // the diagonal task i does its TRSM (fused)
+      } else {
+        pk_wait(F + 5 * j, 1);
+        pk_trsm(T, S, G, j, 0, linv, gsm);
+        pk_publish(F + 4 * i + j, 2);
+      }
+      PK_T(q, 7);
+      continue;
+    }
+    // ---- diagonal block i
+    for (int s = 0; s + 1 < i; ++s) {   // A_ii -= L_is L_is^T
+      pk_wait(F + 4 * i + s, 2);
+      pk_update(T, S, G, i, NBMAX * s, NBMAX, gsm);
+    }
+    PK_T(q, 2);
+    const int ci = NBMAX * i, nbi = min(NBMAX, T.w - ci);
+    const PTask P{T.sn, T.c0 + ci, nbi, T.slot + i};
+    if (i >= 1 && nbi == NBMAX && G.nrows >= TILE) {
+      const int s = i - 1;
+      double* Ps = G.Pc + (long long)NBMAX * s * S.ld;
+      pk_wait(F + 4 * i + s, 1);
+      pk_wait(F + 5 * s, 1);
+      PK_T(q, 3);
+      pk_stage64(sA, Ps + G.r0, S.ld);
+      pk_stage64(sB, linv + (long long)(T.slot + s) * (NBMAX * NBMAX), NBMAX);
+      {   // A_ii -> Ls (stride P10_LD), lower row pairs
+        const double* Aii = G.Pc + (long long)ci * S.ld + G.r0;
+        for (int e = threadIdx.x; e < NBMAX * NBMAX / 2; e += GEMM_THREADS) {
+          const int c = e >> 5, r = (e & 31) * 2;
+          if (r + 1 >= c) cp_async16(Ls + c * P10_LD + r, Aii + c * S.ld + r, 16);
+        }
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      double acc[4][4][2];
+      pk_mma_smem(sA, sB, acc, false);   // L_{i,s} = A_{i,s} X_s^T
+      __syncthreads();
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) sA[(wn * 32 + b * 8 + 2 * t + v) * LDS + wm * 32 + a * 8 + g] = acc[a][b][v];
+      __syncthreads();
+      for (int c = warp; c < NBMAX; c += GEMM_THREADS / 32)   // L_{i,s} -> panel, then publish
+        *reinterpret_cast<double2*>(Ps + (long long)c * S.ld + G.r0 + 2 * lane) =
+            *reinterpret_cast<const double2*>(sA + c * LDS + 2 * lane);
+      pk_publish(F + 4 * i + s, 2);
+      PK_T(q, 4);
+      pk_mma_smem(sA, sA, acc, true);    // A_ii -= L_{i,s} L_{i,s}^T (lower quadrants)
+      if (wm >= wn) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int r = wm * 32 + a * 8 + g, c = wn * 32 + b * 8 + 2 * t + v;
+              if (r >= c) Ls[c * P10_LD + r] -= acc[a][b][v];
+            }
+      }
+      __syncthreads();
+      PK_T(q, 5);
+      potrf10_block<false>(P, S, sfirst, panels, linv, fail, smem);
+    } else {
+      if (i >= 1) {   // the critical step through memory (partial block or short tile)
+        const int s = i - 1;
+        pk_wait(F + 4 * i + s, 1);
+        pk_wait(F + 5 * s, 1);
+        pk_trsm(T, S, G, s, 0, linv, gsm);
+        pk_publish(F + 4 * i + s, 2);
+        pk_update(T, S, G, i, NBMAX * s, NBMAX, gsm);
+      }
+      potrf10_block<true>(P, S, sfirst, panels, linv, fail, smem);
+      if (nbi < NBMAX && G.nrows > nbi) {   // block narrower than the tile: TRSM of the rows below it
+        __threadfence();
+        __syncthreads();
+        pk_trsm(T, S, G, i, nbi, linv, gsm);
+      }
+    }
+    pk_publish(F + 5 * i, 1);
+    PK_T(q, 6);
+  }
+  // this CTA's work is in memory: count it (panel_below_kernel does not finish before all of them)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(sync3 + 2, 1);
+  }
+}
+
+// Blocks (i, j) below the diagonal region (tile i >= nbk, j < nbk), one task each: NEXT on the
+// block (independent of the chain), A_ij -= L_is L_js^T for s < j (after (i, s) and the diagonal
+// region's (j, s) are published), then L_ij = A_ij X_j^T after POTRF(j); flag F[16 + 4 (i - nbk) + j].
+// Launched as the programmatic dependent of panel_diag_kernel WITHOUT griddepcontrol.wait (it
+// synchronises through the flags, and only waits for diagonal-kernel tasks or its own earlier
+// tasks); it finishes only after every diagonal CTA has counted itself out, so the launch after it
+// (whose griddepcontrol.wait covers only this grid) sees all of the outer block's results.
+__global__ void __launch_bounds__(GEMM_THREADS, 4) panel_below_kernel(const PanTask* __restrict__ tasks, int ntasks,
+                                                                     int* sync3, int ndiag_ctas, int* flags,
+                                                                     const SnInfo* __restrict__ sn, double* panels,
+                                                                     const double* __restrict__ linv) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_task;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_task = atomicAdd(sync3 + 1, 1);
+    __syncthreads();
+    const int q = s_task;
+    if (q >= ntasks) break;
+    PK_T(4096 + q, 0);
+    const PanTask T = tasks[q];
+    const SnInfo S = sn[T.sn];
+    const PkGeo G = pk_geo(T, S, panels);
+    const int j = T.blk;
+    int* F = flags + T.flag;
+    int* Fi = F + 16 + 4 * (G.i - G.nbk);
+    if (T.pw > 0) pk_update(T, S, G, j, -T.pw, T.pw, smem);
+    PK_T(4096 + q, 1);
+    for (int s = 0; s < j; ++s) {
+      pk_wait(Fi + s, 2);
+      pk_wait(F + 4 * j + s, 2);
+      pk_update(T, S, G, j, NBMAX * s, NBMAX, smem);
+    }
+    pk_wait(F + 5 * j, 1);
+    pk_trsm(T, S, G, j, 0, linv, smem);
+    if (j + 1 < G.nbk) pk_publish(Fi + j, 2);
+    PK_T(4096 + q, 2);
+  }
+  if (threadIdx.x == 0)
+    while (ld_acquire(sync3 + 2) < ndiag_ctas) __nanosleep(64);
+}
+
 // ---------------------------------------------------------------------------------------------- launchers
 cudaError_t kernels_init_attributes() {
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(potrf9_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF9_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(potrf10_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF10_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(panel_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PANEL_DIAG_SMEM))) return e;
+  if ((e = cudaFuncSetAttribute(panel_below_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 1 + 4) * SMALL_MAXK + 8 * 32 * 1) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 2 + 4) * SMALL_MAXK + 8 * 32 * 2) * 8))) return e;
   if ((e = cudaFuncSetAttribute(small_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, ((32 * 4 + 4) * SMALL_MAXK + 8 * 32 * 4) * 8))) return e;
@@ -1578,9 +2165,23 @@ void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels, double* linv,
                   unsigned long long* fail, cudaStream_t st, int prio) {
   if (ntasks <= 0) return;
-  launch_prio(potrf9_kernel, ntasks, POTRF9_THREADS, POTRF9_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
+  static const bool p9 = getenv("SPCHOL_POTRF9") && atoi(getenv("SPCHOL_POTRF9")) != 0;
+  if (p9) launch_prio(potrf9_kernel, ntasks, POTRF9_THREADS, POTRF9_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
+  else launch_prio(potrf10_kernel, ntasks, POTRF9_THREADS, POTRF10_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
 }
 
+void launch_panel(const PanTask* tasks, int ndiag, int nbelow, int* sync3, int* flags, const SnInfo* sn,
+                  const int* sfirst, double* panels, double* linv, unsigned long long* fail, int grid_cap,
+                  cudaStream_t st, int prio) {
+  if (ndiag <= 0) return;
+  const int gd = std::min(ndiag, 148);
+  launch_prio(panel_diag_kernel, gd, GEMM_THREADS, PANEL_DIAG_SMEM, st, prio, tasks, ndiag, sync3, flags, sn, sfirst,
+              panels, linv, fail, nbelow > 0 ? 1 : 0);
+  if (nbelow <= 0) return;
+  const int gb = std::min(nbelow, grid_cap > 0 ? grid_cap : 4 * 148);
+  launch_prio(panel_below_kernel, gb, GEMM_THREADS, GEMM_SMEM, st, prio, tasks + ndiag, nbelow, sync3, gd, flags, sn,
+              panels, (const double*)linv);
+}
 
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,
                   const long long* ucol_base, const long long* ucol_map, const int* posmap, unsigned long long* fail,

@@ -8,6 +8,10 @@
 //     MODE_LOCAL        right-looking update of the supernode's own trailing columns
 //     MODE_SCATTER      a5+a6: U_J = L_{R,J} L_{R,J}^T ("DSYRK") with the relind assembly
 //                        fused into the epilogue: FP64 RED into ancestors
+//   panel_diag_kernel / panel_below_kernel
+//                       a3+a4 fused: the cdiv of one 256-column outer block (its lookahead update by
+//                       the previous outer block, POTRF, TRSM and the in-block updates of every 64-row
+//                       tile) in one launch pair, flag-synchronised
 //   init_scatter        a1: A's entries into the zeroed panel arena
 //   solve kernels       forward / backward supernodal triangular solves
 #pragma once
@@ -104,6 +108,22 @@ void launch_gemm_tma(int mode, const GTask* tasks, int ntasks, const SnInfo* sn,
 void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels, cudaStream_t st, int prio = 0);
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels,
                   double* linv, unsigned long long* fail, cudaStream_t st, int prio = 0);
+// Fused cdiv of one outer block (columns [c0, c0 + w), w <= 4 * NBMAX) of supernode sn, rows [c0, m)
+// cut into 64-row tiles (tile i: rows c0 + 64 i ...; tiles < nbk = ceil(w / 64) hold the diagonal
+// blocks).  A task is block (tile, blk), blk < nbk, blk <= tile.  flag = first of the outer block's
+// 16 + 4 (ntile - nbk) ready flags (see panel_diag_kernel); slot = inverse slot of inner block 0;
+// pw > 0: the task first applies the
+// lookahead update by the previous outer block [c0 - pw, c0) (NEXT, K = pw).
+struct PanTask {
+  int sn, c0, w, tile, blk, slot, flag, pw;
+};
+// One launch = the panel tasks of one outer step over a level's supernodes: the ndiag diagonal-region
+// tasks (pair-major: (0,0), (1,0), (1,1), (2,0) ... each pair over all outer blocks), then the
+// nbelow blocks below them (column-major: (nbk, 0), (nbk+1, 0), ..., (nbk, 1), ...).  sync3 = {diagonal ticket, below ticket, diagonal CTAs
+// done}, zeroed per factor.
+void launch_panel(const PanTask* tasks, int ndiag, int nbelow, int* sync3, int* flags, const SnInfo* sn,
+                  const int* sfirst, double* panels, double* linv, unsigned long long* fail, int grid_cap,
+                  cudaStream_t st, int prio = 0);
 constexpr int SMALL_THREADS = 256;
 constexpr int SMALL_MAXK = 64;
 constexpr int SMALL_MAXM = SMALL_THREADS;

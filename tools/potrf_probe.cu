@@ -5,6 +5,8 @@
 #include "../paper_2409_14009_b200/csrc/kernels.cu"
 #include <cstdio>
 #include <vector>
+#include <cmath>
+#include <algorithm>
 using namespace spchol;
 int main() {
   const int n = 64, ld = 64;
@@ -32,12 +34,14 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int variant = 9; variant <= 9; ++variant) {
+  std::vector<double> L9(n * ld), W9(NBMAX * NBMAX), L10(n * ld), W10(NBMAX * NBMAX);
+  for (int variant = 9; variant <= 10; ++variant) {
     float best = 1e9;
     for (int rep = 0; rep < 50; ++rep) {
       cudaMemcpy(dA, A.data(), sizeof(double) * n * ld, cudaMemcpyHostToDevice);
       cudaEventRecord(e0);
-      potrf9_kernel<<<1, POTRF9_THREADS, POTRF9_SMEM>>>(dT, dS, dF, dA, dW, dfail);
+      if (variant == 9) potrf9_kernel<<<1, POTRF9_THREADS, POTRF9_SMEM>>>(dT, dS, dF, dA, dW, dfail);
+      else potrf10_kernel<<<1, POTRF9_THREADS, POTRF10_SMEM>>>(dT, dS, dF, dA, dW, dfail);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -45,17 +49,43 @@ int main() {
       if (ms < best) best = ms;
     }
     printf("potrf%d: best %.2f us (event, one CTA)\n", variant, best * 1e3);
+    cudaMemcpy(variant == 9 ? L9.data() : L10.data(), dA, sizeof(double) * n * ld, cudaMemcpyDeviceToHost);
+    cudaMemcpy(variant == 9 ? W9.data() : W10.data(), dW, sizeof(double) * NBMAX * NBMAX, cudaMemcpyDeviceToHost);
 #ifdef SPCHOL_P9_CLOCKS
     if (variant == 9) {
       long long c[64];
       cudaMemcpyFromSymbol(c, p9_clocks, sizeof(c));
       for (int i = 1; i < 21 && c[i]; ++i) printf("  phase %2d: %lld cycles (cum %lld)\n", i, c[i] - c[i - 1], c[i] - c[0]);
-      for (int p = 0; p < 7; ++p)
-        printf("  panel %d phase-2 start %lld: t0 tile done +%lld, t0 diag done +%lld, t64 X_p done +%lld, t32 syrk done +%lld, t64 syrk done +%lld, barrier +%lld\n",
-               p, c[3 + 2 * p] - c[0], c[21 + p] - c[3 + 2 * p], c[29 + p] - c[3 + 2 * p], c[37 + p] - c[3 + 2 * p],
-               c[45 + p] - c[3 + 2 * p], c[53 + p] - c[3 + 2 * p], c[4 + 2 * p] - c[3 + 2 * p]);
     }
 #endif
+  }
+  double dl = 0, dw = 0, ml = 0, mw = 0;
+  for (int j = 0; j < n; ++j)
+    for (int i = j; i < n; ++i) {
+      dl = std::max(dl, std::fabs(L9[j * ld + i] - L10[j * ld + i]));
+      ml = std::max(ml, std::fabs(L9[j * ld + i]));
+    }
+  for (int e = 0; e < NBMAX * NBMAX; ++e) {
+    dw = std::max(dw, std::fabs(W9[e] - W10[e]));
+    mw = std::max(mw, std::fabs(W9[e]));
+  }
+  printf("potrf10 vs potrf9: max|dL|/max|L| = %.3e, max|dX|/max|X| = %.3e\n", dl / ml, dw / mw);
+  // partial block (nb = 40): padding path
+  {
+    PTask T2{0, 0, 40, 0};
+    cudaMemcpy(dT, &T2, sizeof(T2), cudaMemcpyHostToDevice);
+    for (int variant = 9; variant <= 10; ++variant) {
+      cudaMemcpy(dA, A.data(), sizeof(double) * n * ld, cudaMemcpyHostToDevice);
+      if (variant == 9) potrf9_kernel<<<1, POTRF9_THREADS, POTRF9_SMEM>>>(dT, dS, dF, dA, dW, dfail);
+      else potrf10_kernel<<<1, POTRF9_THREADS, POTRF10_SMEM>>>(dT, dS, dF, dA, dW, dfail);
+      cudaDeviceSynchronize();
+      cudaMemcpy(variant == 9 ? L9.data() : L10.data(), dA, sizeof(double) * n * ld, cudaMemcpyDeviceToHost);
+      cudaMemcpy(variant == 9 ? W9.data() : W10.data(), dW, sizeof(double) * NBMAX * NBMAX, cudaMemcpyDeviceToHost);
+    }
+    double d1 = 0, d2 = 0;
+    for (int e = 0; e < n * ld; ++e) d1 = std::max(d1, std::fabs(L9[e] - L10[e]));
+    for (int e = 0; e < NBMAX * NBMAX; ++e) d2 = std::max(d2, std::fabs(W9[e] - W10[e]));
+    printf("nb=40: max|dL| = %.3e, max|dX| = %.3e\n", d1, d2);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
