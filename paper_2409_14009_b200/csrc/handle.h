@@ -150,7 +150,7 @@ struct spchol_handle {
   bool panel_mode = true;                  // SPCHOL_PANEL=0: the cdiv as separate POTRF / TRSM / update launches
   int panel_grid = 0;                      // SPCHOL_PANEL_GRID: CTAs of a below launch (0 = min(tasks, 4 x 148))
   int panel_max_sn = 2;                    // SPCHOL_PANEL_MAX_SN: fused cdiv in levels with <= this many large supernodes
-  int panel_max_rows = 1 << 30;            // SPCHOL_PANEL_MAX_ROWS: ... for outer blocks with m - c0 <= this many rows
+  int panel_max_rows = 6144;               // SPCHOL_PANEL_MAX_ROWS: ... for outer blocks with m - c0 <= this many rows
   std::vector<int> level_sns, level_off;
   std::vector<int> small_sns;           // supernodes handled by the fused small kernel, by level
   std::vector<char> is_small;

@@ -378,3 +378,82 @@ def test_parity_partition_refinement(name, mode):
     bit-exact symbolic arrays against the oracle's O7b, the factor of the refined order within the
     parity bar, padding exactly 0, solve within the backward-error bound."""
     run_parity(gen.make(name), partition_refinement=1, update_mode=mode)
+
+
+FUSED_ALL = {"SPCHOL_PANEL_MAX_SN": "1000000", "SPCHOL_PANEL_MAX_ROWS": "1000000000"}
+
+
+def _dense_spd(n, seed, extra_rows=0):
+    """Dense SPD block of n columns (one supernode) plus, with extra_rows, a second dense block
+    coupled to it, so the first supernode has rows below its diagonal block (m > k)."""
+    rng = np.random.default_rng(seed)
+    N = n + extra_rows
+    D = np.tril(-rng.uniform(0.0, 1.0, (N, N)) / N, -1)
+    np.fill_diagonal(D, 2.0 + rng.uniform(0.0, 0.1, N))
+    return gen.from_dense_lower(D)
+
+
+@pytest.mark.parametrize("env", [{}, {"SPCHOL_PDL": "0"}, {"SPCHOL_PANEL_GRID": "3"}])
+@pytest.mark.parametrize("name", ["C1", "T3", "S3", "S4", "S5"])
+def test_parity_fused_panel_all_levels(name, env, monkeypatch):
+    """The fused outer-block cdiv (panel_diag_kernel + panel_below_kernel, lookahead update folded in)
+    forced on every level and outer block: same factor, same solve; also without programmatic
+    dependent launch (the below launch then runs after the diagonal one) and with a 3-CTA below
+    launch (every CTA works through many tasks in ticket order)."""
+    for k, v in {**FUSED_ALL, **env}.items():
+        monkeypatch.setenv(k, v)
+    run_parity(gen.make(name), small_max_k=-1)
+    run_parity(gen.make(name))
+
+
+@pytest.mark.parametrize("n,extra", [(64, 0), (200, 0), (256, 0), (300, 0), (700, 0), (520, 130), (1000, 333)])
+def test_parity_fused_panel_dense(n, extra, monkeypatch):
+    """Dense blocks held as one or two supernodes: outer blocks of 1-4 inner blocks, a partial last
+    block (k mod 64 != 0), rows below the diagonal region and tiles cut by m; fused path vs oracle."""
+    for k, v in FUSED_ALL.items():
+        monkeypatch.setenv(k, v)
+    run_parity(_dense_spd(n, n + extra, extra), small_max_k=-1)
+
+
+def test_parity_fused_panel_kernel_timing(monkeypatch):
+    """Kernel timing serializes every launch on one stream (no PDL): the fused path still completes
+    and the per-kind statistics account for its launches."""
+    for k, v in FUSED_ALL.items():
+        monkeypatch.setenv(k, v)
+    p = gen.make("S5")
+    o = oracle.Oracle.from_problem(p)
+    assert o.factor() == -1
+    Lp, Li, Lx = o.L_csc()
+    with sp.Solver.from_problem(p, small_max_k=-1) as h:
+        h.spchol_enable_kernel_timing(True)
+        assert h.spchol_factor() == (-1, -1)
+        st = h.spchol_kernel_stats("panel")
+        assert st["launches"] > 0 and st["flops"] > 0
+        h.spchol_enable_kernel_timing(False)
+        cLp, cLi, cLx, _ = h.spchol_export_factor_csc()
+        assert np.abs(cLx - Lx).max() <= TOL_L * np.abs(Lx).max()
+
+
+@pytest.mark.parametrize("name", ["T3", "S4"])
+def test_not_spd_fused_panel(name, monkeypatch):
+    """A failing pivot inside the fused path is reported as the sequential first failing column."""
+    for k, v in FUSED_ALL.items():
+        monkeypatch.setenv(k, v)
+    test_not_spd_first_failing_column(name)
+
+
+@pytest.mark.parametrize("name,world,minflops,outer", [("S4", 2, None, None), ("S5", 3, "0", None), ("S4", 4, "0", "1"),
+                                                       ("T3", 2, "0", "2")])
+def test_distributed_fused_panel_mock(name, world, minflops, outer):
+    """The fused outer-block cdiv on every level of the multi-GPU path (own subtrees, undistributed
+    top supernodes with the lookahead folded in, distributed top supernodes with their NEXT on the
+    next block column's owner), through the real NCCL code path over the single-process stand-in."""
+    env = dict(FUSED_ALL)
+    if minflops is not None:
+        env["SPCHOL_DIST_MINFLOPS"] = minflops
+    if outer is not None:
+        env["SPCHOL_OUTER"] = outer
+    r = run_mock(name, world, env)
+    assert r["ok"], r
+    assert r["lerr"] <= TOL_L and r["berr"] <= TOL_BERR and r["ranks_agree"], r
+    assert r["padding_nonzeros"] == 0, r

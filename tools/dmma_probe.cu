@@ -53,6 +53,15 @@ __global__ void glob_mma(long long* out, double* M, int ld, int K, int reps) {
   }
   if (threadIdx.x == 0) { out[0] = tm / (reps - 1); out[1] = ts / (reps - 1); }
 }
+__global__ void dmma_lat(long long* out, double* sink, int n) {
+  double acc[2] = {1e-3 * threadIdx.x, 0.0};
+  const double a = 1.0000001, b = 0.9999999;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) dmma(acc, a, b);
+  long long t1 = clock64();
+  sink[threadIdx.x] = acc[0] + acc[1];
+  if (threadIdx.x == 0) out[0] = (t1 - t0) / n;
+}
 int main() {
   long long* d; double* sink; double* M;
   cudaMalloc(&d, 64); cudaMalloc(&sink, 8192); cudaMalloc(&M, sizeof(double) * 256 * 600);
@@ -63,6 +72,8 @@ int main() {
   cudaFuncSetAttribute(glob_mma<16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
   cudaFuncSetAttribute(glob_mma<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
   cudaFuncSetAttribute(glob_mma<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
+  dmma_lat<<<1, 32>>>(d, sink, 1000);
+  { long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost); printf("dependent DMMA chain: %lld cycles per DMMA\n", h); }
   for (int warps : {4, 8, 16}) {
     smem_mma<<<1, 32 * warps, 2 * TILE * LDS * 8>>>(d, sink, 20);
     long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
