@@ -316,12 +316,16 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
             // the lookahead update by the previous outer block (NEXT) is folded into the tiles
             // (not for a distributed top supernode: its NEXT runs on the next block's owner)
             const int pw = C0 > 0 && !dj ? W : 0;   // NEXT(C0 - W) folded here (see the NEXT emission below)
-            // diagonal-region blocks (i, j <= i) in pair order, then the tiles below
+            // the diagonal region's NEXT in K = 64 quarters, its blocks (i, j <= i) in pair order, then
+            // the blocks below
+            for (int q = 0; pw > 0 && q < (pw + NB - 1) / NB; ++q)
+              for (int i = 0; i < nbk; ++i)
+                for (int j = 0; j <= i; ++j) v.push_back(PanTask{J, C0, w, i, j, slot, h->npanflags, pw, q});
             for (int i = 0; i < nbk; ++i)
-              for (int j = 0; j <= i; ++j) v.push_back(PanTask{J, C0, w, i, j, slot, h->npanflags, pw});
+              for (int j = 0; j <= i; ++j) v.push_back(PanTask{J, C0, w, i, j, slot, h->npanflags, pw, -1});
             for (int j = 0; j < nbk; ++j)
-              for (int i = nbk; i < ntile; ++i) v.push_back(PanTask{J, C0, w, i, j, slot, h->npanflags, pw});
-            h->npanflags += 16 + 4 * std::max(0, ntile - nbk);
+              for (int i = nbk; i < ntile; ++i) v.push_back(PanTask{J, C0, w, i, j, slot, h->npanflags, pw, -1});
+            h->npanflags += 32 + 4 * std::max(0, ntile - nbk);
             pan.push_back(std::move(v));
             pan_next = pan_next || pw > 0;
             for (int c = C0; c < C1 && pw > 0; ++c) { fpan += 2.0 * pw * (double)(I.m - c); bpan += 16.0 * (double)(I.m - c); }

@@ -1675,7 +1675,10 @@ __global__ void gather_kernel(const double* __restrict__ src, const long long* _
 //   panel_below_kernel the blocks (i >= nbk, j < nbk) below it, one task each: NEXT, the updates by
 //             the blocks s < j, TRSM.
 // Ready flags per outer block, F[4 i + j] (diagonal region): (j < i) 1 = A_ij fully updated, 2 = L_ij
-// in memory; (j == i) 1 = L_ii and X_i in memory; F[16 + 4 (i - nbk) + j] (below): 2 = L_ij in memory.  Tasks are claimed through a ticket in an order in which
+// in memory; (j == i) 1 = L_ii and X_i in memory; F[16 + 4 i + j]: quarters of block (i, j)'s NEXT done
+// (the diagonal region's lookahead update runs as four K = 64 tasks per block, RED-accumulated, so
+// it costs the chain one short product instead of a K = 256 one); F[32 + 4 (i - nbk) + j] (below):
+// 2 = L_ij in memory.  Tasks are claimed through a ticket in an order in which
 // every wait is on an earlier task of the same outer block, so neither launch can deadlock whatever
 // the residency; the below launch is the programmatic dependent of the diagonal one (released once
 // every diagonal CTA is resident) and never waits for tasks it could block.  Operands are read with
@@ -1765,7 +1768,7 @@ __device__ __forceinline__ void pk_mma(const double* A, long long lda, int arows
 // (sub = true) on rows rlo <= r < nrows, columns c < ncols, and r >= c if lower.  The tile is staged
 // through shared memory; each warp streams whole columns (16-byte accesses, loads before stores).
 __device__ __forceinline__ void pk_store(const double (&acc)[4][4][2], double* smem, double* dst, long long ld, int rlo,
-                                         int nrows, int ncols, bool sub, bool lower) {
+                                         int nrows, int ncols, bool sub, bool lower, bool red = false) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
   constexpr int LDC = TILE + 4;
@@ -1780,7 +1783,7 @@ __device__ __forceinline__ void pk_store(const double (&acc)[4][4][2], double* s
   const int pr = 2 * lane;
   constexpr int NIT = TILE / (GEMM_THREADS / 32);
   double2 dv[NIT];
-  if (sub) {
+  if (sub && !red) {
 #pragma unroll
     for (int it = 0; it < NIT; ++it) {
       const int col = warp + 4 * it;
@@ -1795,8 +1798,13 @@ __device__ __forceinline__ void pk_store(const double (&acc)[4][4][2], double* s
     const bool v1 = col < ncols && pr + 1 >= rlo && pr + 1 < nrows && (!lower || pr + 1 >= col);
     if (!v0 && !v1) continue;
     double2 c2 = *reinterpret_cast<const double2*>(sC + col * LDC + pr);
-    if (sub) c2 = make_double2(dv[it].x - c2.x, dv[it].y - c2.y);
     double* d = dst + col * ld + pr;
+    if (red) {   // dst -= C by FP64 RED (several tasks accumulate into one block)
+      if (v0) atomicAdd(d, -c2.x);
+      if (v1) atomicAdd(d + 1, -c2.y);
+      continue;
+    }
+    if (sub) c2 = make_double2(dv[it].x - c2.x, dv[it].y - c2.y);
     if (v0 && v1) *reinterpret_cast<double2*>(d) = c2;
     else if (v0) d[0] = c2.x;
     else d[1] = c2.y;
@@ -1834,12 +1842,12 @@ __device__ __forceinline__ PkGeo pk_geo(const PanTask& T, const SnInfo& S, doubl
 // A_{i,j} -= L_{i,q} L_{j,q}^T over the columns [c0 + off, c0 + off + K) (off < 0: the previous outer
 // block, NEXT); lower if j == i.
 __device__ __forceinline__ void pk_update(const PanTask& T, const SnInfo& S, const PkGeo& G, int j, int off, int K,
-                                          double* smem) {
+                                          double* smem, bool red = false) {
   double acc[4][4][2];
   const double* Pq = G.Pc + (long long)off * S.ld;
   const int cj = NBMAX * j;
   pk_mma(Pq + G.r0, S.ld, G.nrows, Pq + T.c0 + cj, S.ld, S.m - (T.c0 + cj), K, acc, smem);
-  pk_store(acc, smem, G.Pc + (long long)cj * S.ld + G.r0, S.ld, 0, G.nr64, min(NBMAX, T.w - cj), true, j == G.i);
+  pk_store(acc, smem, G.Pc + (long long)cj * S.ld + G.r0, S.ld, 0, G.nr64, min(NBMAX, T.w - cj), true, j == G.i, red);
 }
 // L_{i,s} = A_{i,s} X_s^T on rows >= rlo of the tile
 __device__ __forceinline__ void pk_trsm(const PanTask& T, const SnInfo& S, const PkGeo& G, int s, int rlo,
@@ -1913,7 +1921,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) panel_diag_kernel(const PanTa
     const PkGeo G = pk_geo(T, S, panels);
     const int i = G.i, j = T.blk;
     int* F = flags + T.flag;
-    if (T.pw > 0) pk_update(T, S, G, j, -T.pw, T.pw, gsm);   // NEXT
+    if (T.q >= 0) {   // ---- a quarter (K = 64) of block (i, j)'s NEXT, RED-accumulated, then counted
+      pk_update(T, S, G, j, -T.pw + NBMAX * T.q, min(NBMAX, T.pw - NBMAX * T.q), gsm, true);
+      if (threadIdx.x == 0) atomicAdd(F + 16 + 4 * i + j, 1);
+      continue;
+    }
+    if (T.pw > 0) pk_wait(F + 16 + 4 * i + j, (T.pw + NBMAX - 1) / NBMAX);   // NEXT done by its quarter tasks
     PK_T(q, 1);
     if (j < i) {   // ---- off-diagonal block of the diagonal region
       for (int s = 0; s < j; ++s) {
@@ -2018,7 +2031,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) panel_diag_kernel(const PanTa
 
 // Blocks (i, j) below the diagonal region (tile i >= nbk, j < nbk), one task each: NEXT on the
 // block (independent of the chain), A_ij -= L_is L_js^T for s < j (after (i, s) and the diagonal
-// region's (j, s) are published), then L_ij = A_ij X_j^T after POTRF(j); flag F[16 + 4 (i - nbk) + j].
+// region's (j, s) are published), then L_ij = A_ij X_j^T after POTRF(j); flag F[32 + 4 (i - nbk) + j].
 // Launched as the programmatic dependent of panel_diag_kernel WITHOUT griddepcontrol.wait (it
 // synchronises through the flags, and only waits for diagonal-kernel tasks or its own earlier
 // tasks); it finishes only after every diagonal CTA has counted itself out, so the launch after it
@@ -2041,7 +2054,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 4) panel_below_kernel(const PanT
     const PkGeo G = pk_geo(T, S, panels);
     const int j = T.blk;
     int* F = flags + T.flag;
-    int* Fi = F + 16 + 4 * (G.i - G.nbk);
+    int* Fi = F + 32 + 4 * (G.i - G.nbk);
     if (T.pw > 0) pk_update(T, S, G, j, -T.pw, T.pw, smem);
     PK_T(4096 + q, 1);
     for (int s = 0; s < j; ++s) {

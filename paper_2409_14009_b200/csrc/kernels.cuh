@@ -111,11 +111,11 @@ void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* s
 // Fused cdiv of one outer block (columns [c0, c0 + w), w <= 4 * NBMAX) of supernode sn, rows [c0, m)
 // cut into 64-row tiles (tile i: rows c0 + 64 i ...; tiles < nbk = ceil(w / 64) hold the diagonal
 // blocks).  A task is block (tile, blk), blk < nbk, blk <= tile.  flag = first of the outer block's
-// 16 + 4 (ntile - nbk) ready flags (see panel_diag_kernel); slot = inverse slot of inner block 0;
+// 32 + 4 (ntile - nbk) ready flags (see panel_diag_kernel); slot = inverse slot of inner block 0;
 // pw > 0: the task first applies the
 // lookahead update by the previous outer block [c0 - pw, c0) (NEXT, K = pw).
 struct PanTask {
-  int sn, c0, w, tile, blk, slot, flag, pw;
+  int sn, c0, w, tile, blk, slot, flag, pw, q;   // q >= 0: quarter q of the block's NEXT (diagonal region)
 };
 // One launch = the panel tasks of one outer step over a level's supernodes: the ndiag diagonal-region
 // tasks (pair-major: (0,0), (1,0), (1,1), (2,0) ... each pair over all outer blocks), then the

@@ -32,11 +32,14 @@ int main(int argc, char** argv) {
   for (int C = 0; C < 2; ++C) {
     const int c0 = C * W, w = W, nbk = 4, ntile = (n - c0 + 63) / 64, pw = C ? W : 0;
     std::vector<PanTask> t;
+    for (int q = 0; pw > 0 && q < 4; ++q)
+      for (int i = 0; i < nbk; ++i)
+        for (int j = 0; j <= i; ++j) t.push_back(PanTask{0, c0, w, i, j, C * 4, 0, pw, q});
     for (int i = 0; i < nbk; ++i)
-      for (int j = 0; j <= i; ++j) t.push_back(PanTask{0, c0, w, i, j, C * 4, 0, pw});
+      for (int j = 0; j <= i; ++j) t.push_back(PanTask{0, c0, w, i, j, C * 4, 0, pw, -1});
     const int nd = (int)t.size();
     for (int j = 0; j < nbk; ++j)
-      for (int i = nbk; i < ntile; ++i) t.push_back(PanTask{0, c0, w, i, j, C * 4, 0, pw});
+      for (int i = nbk; i < ntile; ++i) t.push_back(PanTask{0, c0, w, i, j, C * 4, 0, pw, -1});
     cudaMemcpy(dT, t.data(), sizeof(PanTask) * t.size(), cudaMemcpyHostToDevice);
     float best = 1e9;
     for (int rep = 0; rep < 20; ++rep) {
@@ -60,6 +63,7 @@ int main(int argc, char** argv) {
     for (int q = 0; q < nd; ++q) t0 = std::min(t0, c[q][0]);
     printf("outer block %d (pw %d): best %.1f us; diag-region tasks (ns from first claim):\n", C, pw, best * 1e3);
     for (int q = 0; q < nd; ++q) {
+      if (t[q].q >= 0) continue;
       printf("  (%d,%d) claim %6lld next %6lld", t[q].tile, t[q].blk, c[q][0] - t0, c[q][1] - t0);
       if (t[q].blk == t[q].tile)
         printf(" steps %6lld waited %6lld L-pub %6lld syrk %6lld potrf-done %6lld", c[q][2] - t0, c[q][3] - t0,
