@@ -1041,6 +1041,9 @@ __device__ __forceinline__ void potrf9_block(const PTask& T, const SnInfo& S, co
 constexpr int P10_LD = 72;
 constexpr int POTRF10_SMEM = (2 * NBMAX * P10_LD + NBMAX + 2 * 64 + 8 * 64) * (int)sizeof(double);
 
+__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// (potrf10_block synchronises its 128 threads on named barrier 1, so a caller with more threads runs it
+// on threads 0-127 only)
 template <bool LOAD = true>
 __device__ __forceinline__ void potrf10_block(const PTask& T, const SnInfo& S, const int* __restrict__ sfirst,
                                               double* panels, double* linv, unsigned long long* fail, double* smem) {
@@ -1062,13 +1065,13 @@ __device__ __forceinline__ void potrf10_block(const PTask& T, const SnInfo& S, c
   for (int e = tid; e < NBMAX * LD / 2; e += POTRF9_THREADS) reinterpret_cast<double2*>(Xs)[e] = make_double2(0.0, 0.0);
   if (LOAD) cp_async_wait<0>();
   if (nb < NBMAX) {   // padding: identity (pivots 1, no coupling)
-    __syncthreads();
+    bar_sync_n(1, POTRF9_THREADS);
     for (int e = tid; e < NBMAX * NBMAX; e += POTRF9_THREADS) {
       const int c = e >> 6, r = e & 63;
       if (c >= nb || r >= nb) Ls[c * LD + r] = r == c ? 1.0 : 0.0;
     }
   }
-  __syncthreads();
+  bar_sync_n(1, POTRF9_THREADS);
   int bad = -1;
   // X row block pb (rows 8 pb ..): T = L_{pb,<} X_{<,<} on column tile j0, then X = -X_pb,pb T
   auto x_block = [&](int pb, int j0) {
@@ -1150,7 +1153,7 @@ __device__ __forceinline__ void potrf10_block(const PTask& T, const SnInfo& S, c
         else x_block(p - 1, 8 * (job - nl));
       }
     }
-    __syncthreads();
+    bar_sync_n(1, POTRF9_THREADS);
     if (p == NBMAX / 8 - 1) break;
     // ---- phase 2: TRSM of panel p's rows below its diagonal block
     if (tid < NBMAX - b - 8) {
@@ -1169,15 +1172,15 @@ __device__ __forceinline__ void potrf10_block(const PTask& T, const SnInfo& S, c
 #pragma unroll
       for (int j = 0; j < 8; ++j) Ls[(b + j) * LD + r] = x[j];
     }
-    __syncthreads();
+    bar_sync_n(1, POTRF9_THREADS);
     // ---- phase 3: panel p+1's columns by panel p (K = 8)
     for (int u = warp; u < 7 - p; u += 4) upd_tile(b + 8 + 8 * u, b + 8, b, b + 8);
-    __syncthreads();
+    bar_sync_n(1, POTRF9_THREADS);
   }
   // X row block 7
   for (int job = warp; job < 7; job += 4) x_block(7, 8 * job);
   if (tid == 0 && bad >= 0) atomicMin(fail, (unsigned long long)(sfirst[T.sn] + T.c0 + bad));
-  __syncthreads();
+  bar_sync_n(1, POTRF9_THREADS);
   // L (lower, r >= c) into the panel; X (lower, zero elsewhere) column-major into the inverse slot
   double* W = linv + (long long)T.slot * (NBMAX * NBMAX);
   for (int e = tid; e < NBMAX * NBMAX / 2; e += POTRF9_THREADS) {
@@ -1694,25 +1697,52 @@ __device__ long long pk_clk[8192][8];
 
 // acc = A B^T over K columns: A, B = 64-row blocks of column-major matrices (rows past arows /
 // brows and columns past K read as zero); the gemm_kernel pipeline (BK-column chunks, cp.async).
-template <int BK = spchol::BK, int STAGES = spchol::STAGES>
+// 128 threads: 4 warps in a 2 x 2 grid of 32 x 32 warp tiles.  256 threads (NT): warps 4-7 form a
+// second 2 x 2 grid that takes the odd k-steps of every chunk (two warps per SM sub-partition issue
+// DMMA, as a lone CTA on the chain needs), reduced into warps 0-3 through shared memory at the end.
+template <int NT = GEMM_THREADS>
+__device__ __forceinline__ void pk_reduce(double (&acc)[4][4][2], double* red) {
+  if (NT == GEMM_THREADS) return;
+  const int tid = threadIdx.x;
+  if (tid >= GEMM_THREADS) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) red[(i * 8 + j * 2 + v) * GEMM_THREADS + tid - GEMM_THREADS] = acc[i][j][v];
+  }
+  __syncthreads();
+  if (tid < GEMM_THREADS) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) acc[i][j][v] += red[(i * 8 + j * 2 + v) * GEMM_THREADS + tid];
+  }
+  __syncthreads();
+}
+
+template <int NT = GEMM_THREADS, int BK = spchol::BK, int STAGES = spchol::STAGES>
 __device__ __forceinline__ void pk_mma(const double* A, long long lda, int arows, const double* B, long long ldb,
                                        int brows, int K, double (&acc)[4][4][2], double* smem) {
   double* sA = smem;
   double* sB = smem + STAGES * BK * LDS;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, grp = warp >> 2;
+  const int wm = (warp >> 1) & 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const int nchunks = (K + BK - 1) / BK;
-  constexpr int NP = (BK * TILE / 2) / GEMM_THREADS;
+  constexpr int NP = (BK * TILE / 2) / NT;
   const double* srcA[NP];
   const double* srcB[NP];
   int byA[NP], byB[NP], kkp[NP], dofs[NP];
 #pragma unroll
   for (int i = 0; i < NP; ++i) {
-    const int p = tid + i * GEMM_THREADS;
+    const int p = tid + i * NT;
     const int kk = p >> 5, rp = (p & 31) * 2;
     const int ra = max(0, min(2, arows - rp)), rb = max(0, min(2, brows - rp));
     byA[i] = ra * 8;
@@ -1748,6 +1778,7 @@ __device__ __forceinline__ void pk_mma(const double* A, long long lda, int arows
     const double* cB = sB + (c % STAGES) * BK * LDS + wn * 32 + g;
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
+      if (NT > GEMM_THREADS && (ks & 1) != grp) continue;
       double a[4], b[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -1762,38 +1793,44 @@ __device__ __forceinline__ void pk_mma(const double* A, long long lda, int arows
   }
   cp_async_wait<0>();
   __syncthreads();
+  pk_reduce<NT>(acc, smem);
 }
 
 // dst (column-major, leading dimension ld, 16-byte aligned row pairs) := C (sub = false) or -= C
 // (sub = true) on rows rlo <= r < nrows, columns c < ncols, and r >= c if lower.  The tile is staged
 // through shared memory; each warp streams whole columns (16-byte accesses, loads before stores).
+// (NT = 256: the tile is in warps 0-3's accumulators; all eight warps stream it out.)
+template <int NT = GEMM_THREADS>
 __device__ __forceinline__ void pk_store(const double (&acc)[4][4][2], double* smem, double* dst, long long ld, int rlo,
                                          int nrows, int ncols, bool sub, bool lower, bool red = false) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) & 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
   constexpr int LDC = TILE + 4;
+  constexpr int NW = NT / 32;
   double* sC = smem;
+  if (tid < GEMM_THREADS) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int v = 0; v < 2; ++v) sC[(wn * 32 + j * 8 + 2 * t + v) * LDC + wm * 32 + i * 8 + g] = acc[i][j][v];
+        for (int v = 0; v < 2; ++v) sC[(wn * 32 + j * 8 + 2 * t + v) * LDC + wm * 32 + i * 8 + g] = acc[i][j][v];
+  }
   __syncthreads();
   const int pr = 2 * lane;
-  constexpr int NIT = TILE / (GEMM_THREADS / 32);
+  constexpr int NIT = TILE / NW;
   double2 dv[NIT];
   if (sub && !red) {
 #pragma unroll
     for (int it = 0; it < NIT; ++it) {
-      const int col = warp + 4 * it;
+      const int col = warp + NW * it;
       const bool ok = col < ncols && pr + 1 >= rlo && pr < nrows && (!lower || pr + 1 >= col);
       dv[it] = ok ? *reinterpret_cast<const double2*>(dst + col * ld + pr) : make_double2(0.0, 0.0);
     }
   }
 #pragma unroll
   for (int it = 0; it < NIT; ++it) {
-    const int col = warp + 4 * it;
+    const int col = warp + NW * it;
     const bool v0 = col < ncols && pr >= rlo && pr < nrows && (!lower || pr >= col);
     const bool v1 = col < ncols && pr + 1 >= rlo && pr + 1 < nrows && (!lower || pr + 1 >= col);
     if (!v0 && !v1) continue;
@@ -1841,46 +1878,53 @@ __device__ __forceinline__ PkGeo pk_geo(const PanTask& T, const SnInfo& S, doubl
 }
 // A_{i,j} -= L_{i,q} L_{j,q}^T over the columns [c0 + off, c0 + off + K) (off < 0: the previous outer
 // block, NEXT); lower if j == i.
+template <int NT = GEMM_THREADS>
 __device__ __forceinline__ void pk_update(const PanTask& T, const SnInfo& S, const PkGeo& G, int j, int off, int K,
                                           double* smem, bool red = false) {
   double acc[4][4][2];
   const double* Pq = G.Pc + (long long)off * S.ld;
   const int cj = NBMAX * j;
-  pk_mma(Pq + G.r0, S.ld, G.nrows, Pq + T.c0 + cj, S.ld, S.m - (T.c0 + cj), K, acc, smem);
-  pk_store(acc, smem, G.Pc + (long long)cj * S.ld + G.r0, S.ld, 0, G.nr64, min(NBMAX, T.w - cj), true, j == G.i, red);
+  pk_mma<NT>(Pq + G.r0, S.ld, G.nrows, Pq + T.c0 + cj, S.ld, S.m - (T.c0 + cj), K, acc, smem);
+  pk_store<NT>(acc, smem, G.Pc + (long long)cj * S.ld + G.r0, S.ld, 0, G.nr64, min(NBMAX, T.w - cj), true, j == G.i, red);
 }
 // L_{i,s} = A_{i,s} X_s^T on rows >= rlo of the tile
+template <int NT = GEMM_THREADS>
 __device__ __forceinline__ void pk_trsm(const PanTask& T, const SnInfo& S, const PkGeo& G, int s, int rlo,
                                         const double* linv, double* smem) {
   double acc[4][4][2];
   const int nbs = min(NBMAX, T.w - NBMAX * s);
   double* Ps = G.Pc + (long long)NBMAX * s * S.ld;
-  pk_mma(Ps + G.r0, S.ld, G.nrows, linv + (long long)(T.slot + s) * (NBMAX * NBMAX), NBMAX, nbs, nbs, acc, smem);
-  pk_store(acc, smem, Ps + G.r0, S.ld, rlo, G.nr64, nbs, false, false);
+  pk_mma<NT>(Ps + G.r0, S.ld, G.nrows, linv + (long long)(T.slot + s) * (NBMAX * NBMAX), NBMAX, nbs, nbs, acc, smem);
+  pk_store<NT>(acc, smem, Ps + G.r0, S.ld, rlo, G.nr64, nbs, false, false);
 }
 
 // 64 x 64 column-major block (rows contiguous, leading dimension ld) -> shared memory (stride LDS),
 // 16-byte cp.async.
+template <int NT = GEMM_THREADS>
 __device__ __forceinline__ void pk_stage64(double* dst, const double* src, long long ld) {
-  for (int e = threadIdx.x; e < TILE * TILE / 2; e += GEMM_THREADS) {
+  for (int e = threadIdx.x; e < TILE * TILE / 2; e += NT) {
     const int c = e >> 5, r = (e & 31) * 2;
     cp_async16(dst + c * LDS + r, src + c * ld + r, 16);
   }
 }
 // acc (zeroed here) = sA sB^T over K = 64, both operands in shared memory (stride LDS); with
 // skip_upper the warp of the strictly upper quadrant (wm < wn) does nothing.
-__device__ __forceinline__ void pk_mma_smem(const double* sA, const double* sB, double (&acc)[4][4][2], bool skip_upper) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+// (NT = 256: warps 4-7 take k in [32, 64), reduced into warps 0-3 through red, 32 KB of scratch.)
+template <int NT = GEMM_THREADS>
+__device__ __forceinline__ void pk_mma_smem(const double* sA, const double* sB, double (&acc)[4][4][2], bool skip_upper,
+                                            double* red = nullptr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, grp = warp >> 2;
+  const int wm = (warp >> 1) & 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  if (skip_upper && wm < wn) return;
   const double* cA = sA + wm * 32 + g;
   const double* cB = sB + wn * 32 + g;
+  const int k0 = NT > GEMM_THREADS ? grp * (TILE / 2) : 0, k1 = NT > GEMM_THREADS ? k0 + TILE / 2 : TILE;
 #pragma unroll 4
-  for (int k = 0; k < TILE; k += 4) {
+  for (int k = k0; k < k1; k += 4) {
+    if (skip_upper && wm < wn) break;
     double a[4], b[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -1892,12 +1936,14 @@ __device__ __forceinline__ void pk_mma_smem(const double* sA, const double* sB, 
 #pragma unroll
       for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
   }
+  pk_reduce<NT>(acc, red);
 }
 
 constexpr int PANEL_DIAG_SMEM = POTRF10_SMEM + 2 * TILE * LDS * (int)sizeof(double);
 static_assert(2 * TILE * LDS >= 2 * STAGES * BK * LDS && 2 * TILE * LDS >= TILE * (TILE + 4), "pk_mma / pk_store staging");
 
-__global__ void __launch_bounds__(GEMM_THREADS, 1) panel_diag_kernel(const PanTask* __restrict__ tasks, int ntasks,
+constexpr int PANEL_DIAG_THREADS = 2 * GEMM_THREADS;   // two 2 x 2 warp grids (K split, see pk_mma)
+__global__ void __launch_bounds__(PANEL_DIAG_THREADS, 1) panel_diag_kernel(const PanTask* __restrict__ tasks, int ntasks,
                                                                     int* sync3, int* flags, const SnInfo* __restrict__ sn,
                                                                     const int* __restrict__ sfirst, double* panels,
                                                                     double* linv, unsigned long long* fail, int trigger) {
@@ -1922,7 +1968,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) panel_diag_kernel(const PanTa
     const int i = G.i, j = T.blk;
     int* F = flags + T.flag;
     if (T.q >= 0) {   // ---- a quarter (K = 64) of block (i, j)'s NEXT, RED-accumulated, then counted
-      pk_update(T, S, G, j, -T.pw + NBMAX * T.q, min(NBMAX, T.pw - NBMAX * T.q), gsm, true);
+      pk_update<PANEL_DIAG_THREADS>(T, S, G, j, -T.pw + NBMAX * T.q, min(NBMAX, T.pw - NBMAX * T.q), gsm, true);
       if (threadIdx.x == 0) atomicAdd(F + 16 + 4 * i + j, 1);
       continue;
     }
@@ -1932,13 +1978,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) panel_diag_kernel(const PanTa
       for (int s = 0; s < j; ++s) {
         pk_wait(F + 4 * i + s, 2);
         pk_wait(F + 4 * j + s, 2);
-        pk_update(T, S, G, j, NBMAX * s, min(NBMAX, T.w - NBMAX * s), gsm);
+        pk_update<PANEL_DIAG_THREADS>(T, S, G, j, NBMAX * s, min(NBMAX, T.w - NBMAX * s), gsm);
       }
       if (j == i - 1) {
         pk_publish(F + 4 * i + j, 1);   // the diagonal task i does its TRSM (fused)
       } else {
         pk_wait(F + 5 * j, 1);
-        pk_trsm(T, S, G, j, 0, linv, gsm);
+        pk_trsm<PANEL_DIAG_THREADS>(T, S, G, j, 0, linv, gsm);
         pk_publish(F + 4 * i + j, 2);
       }
       PK_T(q, 7);
@@ -1947,7 +1993,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) panel_diag_kernel(const PanTa
     // ---- diagonal block i
     for (int s = 0; s + 1 < i; ++s) {   // A_ii -= L_is L_is^T
       pk_wait(F + 4 * i + s, 2);
-      pk_update(T, S, G, i, NBMAX * s, NBMAX, gsm);
+      pk_update<PANEL_DIAG_THREADS>(T, S, G, i, NBMAX * s, NBMAX, gsm);
     }
     PK_T(q, 2);
     const int ci = NBMAX * i, nbi = min(NBMAX, T.w - ci);
@@ -1955,40 +2001,44 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) panel_diag_kernel(const PanTa
     if (i >= 1 && nbi == NBMAX && G.nrows >= TILE) {
       const int s = i - 1;
       double* Ps = G.Pc + (long long)NBMAX * s * S.ld;
-      pk_wait(F + 4 * i + s, 1);
-      pk_wait(F + 5 * s, 1);
-      PK_T(q, 3);
-      pk_stage64(sA, Ps + G.r0, S.ld);
-      pk_stage64(sB, linv + (long long)(T.slot + s) * (NBMAX * NBMAX), NBMAX);
+      pk_wait(F + 4 * i + s, 1);          // A_{i,s} (and A_ii, this task's own) fully updated: prefetch them
+      pk_stage64<PANEL_DIAG_THREADS>(sA, Ps + G.r0, S.ld);
       {   // A_ii -> Ls (stride P10_LD), lower row pairs
         const double* Aii = G.Pc + (long long)ci * S.ld + G.r0;
-        for (int e = threadIdx.x; e < NBMAX * NBMAX / 2; e += GEMM_THREADS) {
+        for (int e = threadIdx.x; e < NBMAX * NBMAX / 2; e += PANEL_DIAG_THREADS) {
           const int c = e >> 5, r = (e & 31) * 2;
           if (r + 1 >= c) cp_async16(Ls + c * P10_LD + r, Aii + c * S.ld + r, 16);
         }
       }
       cp_async_commit();
+      pk_wait(F + 5 * s, 1);              // POTRF(s): X_s
+      PK_T(q, 3);
+      pk_stage64<PANEL_DIAG_THREADS>(sB, linv + (long long)(T.slot + s) * (NBMAX * NBMAX), NBMAX);
+      cp_async_commit();
       cp_async_wait<0>();
       __syncthreads();
       double acc[4][4][2];
-      pk_mma_smem(sA, sB, acc, false);   // L_{i,s} = A_{i,s} X_s^T
-      __syncthreads();
+      double* red = Ls + NBMAX * P10_LD;   // (the POTRF's X area: free until potrf10_block starts)
+      pk_mma_smem<PANEL_DIAG_THREADS>(sA, sB, acc, false, red);   // L_{i,s} = A_{i,s} X_s^T (in warps 0-3)
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+      const int wm = (warp >> 1) & 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+      if (warp < 4) {
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+          for (int b = 0; b < 4; ++b)
 #pragma unroll
-          for (int v = 0; v < 2; ++v) sA[(wn * 32 + b * 8 + 2 * t + v) * LDS + wm * 32 + a * 8 + g] = acc[a][b][v];
+            for (int v = 0; v < 2; ++v) sA[(wn * 32 + b * 8 + 2 * t + v) * LDS + wm * 32 + a * 8 + g] = acc[a][b][v];
+      }
       __syncthreads();
-      for (int c = warp; c < NBMAX; c += GEMM_THREADS / 32)   // L_{i,s} -> panel, then publish
+      for (int c = warp; c < NBMAX; c += PANEL_DIAG_THREADS / 32)   // L_{i,s} -> panel (published below)
         *reinterpret_cast<double2*>(Ps + (long long)c * S.ld + G.r0 + 2 * lane) =
             *reinterpret_cast<const double2*>(sA + c * LDS + 2 * lane);
-      pk_publish(F + 4 * i + s, 2);
       PK_T(q, 4);
-      pk_mma_smem(sA, sA, acc, true);    // A_ii -= L_{i,s} L_{i,s}^T (lower quadrants)
-      if (wm >= wn) {
+      // A_ii -= L_{i,s} L_{i,s}^T (lower quadrants) while the stores drain; L_{i,s}'s consumers (the
+      // blocks below, off the critical path) see it after the SYRK
+      pk_mma_smem<PANEL_DIAG_THREADS>(sA, sA, acc, true, red);
+      if (warp < 4 && wm >= wn) {
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -1999,23 +2049,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) panel_diag_kernel(const PanTa
               if (r >= c) Ls[c * P10_LD + r] -= acc[a][b][v];
             }
       }
-      __syncthreads();
+      pk_publish(F + 4 * i + s, 2);
       PK_T(q, 5);
-      potrf10_block<false>(P, S, sfirst, panels, linv, fail, smem);
+      if (threadIdx.x < POTRF9_THREADS) potrf10_block<false>(P, S, sfirst, panels, linv, fail, smem);
     } else {
       if (i >= 1) {   // the critical step through memory (partial block or short tile)
         const int s = i - 1;
         pk_wait(F + 4 * i + s, 1);
         pk_wait(F + 5 * s, 1);
-        pk_trsm(T, S, G, s, 0, linv, gsm);
+        pk_trsm<PANEL_DIAG_THREADS>(T, S, G, s, 0, linv, gsm);
         pk_publish(F + 4 * i + s, 2);
-        pk_update(T, S, G, i, NBMAX * s, NBMAX, gsm);
+        pk_update<PANEL_DIAG_THREADS>(T, S, G, i, NBMAX * s, NBMAX, gsm);
       }
-      potrf10_block<true>(P, S, sfirst, panels, linv, fail, smem);
+      if (threadIdx.x < POTRF9_THREADS) potrf10_block<true>(P, S, sfirst, panels, linv, fail, smem);
       if (nbi < NBMAX && G.nrows > nbi) {   // block narrower than the tile: TRSM of the rows below it
         __threadfence();
         __syncthreads();
-        pk_trsm(T, S, G, i, nbi, linv, gsm);
+        pk_trsm<PANEL_DIAG_THREADS>(T, S, G, i, nbi, linv, gsm);
       }
     }
     pk_publish(F + 5 * i, 1);
@@ -2188,7 +2238,7 @@ void launch_panel(const PanTask* tasks, int ndiag, int nbelow, int* sync3, int* 
                   cudaStream_t st, int prio) {
   if (ndiag <= 0) return;
   const int gd = std::min(ndiag, 148);
-  launch_prio(panel_diag_kernel, gd, GEMM_THREADS, PANEL_DIAG_SMEM, st, prio, tasks, ndiag, sync3, flags, sn, sfirst,
+  launch_prio(panel_diag_kernel, gd, PANEL_DIAG_THREADS, PANEL_DIAG_SMEM, st, prio, tasks, ndiag, sync3, flags, sn, sfirst,
               panels, linv, fail, nbelow > 0 ? 1 : 0);
   if (nbelow <= 0) return;
   const int gb = std::min(nbelow, grid_cap > 0 ? grid_cap : 4 * 148);
