@@ -282,7 +282,8 @@ static void append_levels(spchol_handle* h, Active active, bool record_solve, in
     int nlarge = 0;
     for (int x = h->level_off[l]; x < h->level_off[l + 1]; ++x)
       nlarge += !h->is_small[h->level_sns[x]] && (active(h->level_sns[x]) || dtop(h->level_sns[x]));
-    const bool panel = h->panel_mode && NB == NBMAX && OUTER <= 4 && nlarge <= h->panel_max_sn;
+    // (not in deterministic mode: the lookahead quarters accumulate by FP64 RED in arrival order)
+    const bool panel = h->panel_mode && NB == NBMAX && OUTER <= 4 && nlarge <= h->panel_max_sn && !h->opt.deterministic;
     const bool split_next = !h->no_lookahead && !h->no_next_split;
     for (int s = 0; s < maxblk; ++s) {
       long long p0 = (long long)h->ptasks.size(), t0 = (long long)h->gtasks.size();

@@ -2228,7 +2228,7 @@ void launch_rlb(const RTask* tasks, int ntasks, const SnInfo* sn, double* panels
 void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* sfirst, double* panels, double* linv,
                   unsigned long long* fail, cudaStream_t st, int prio) {
   if (ntasks <= 0) return;
-  static const bool p9 = getenv("SPCHOL_POTRF9") && atoi(getenv("SPCHOL_POTRF9")) != 0;
+  const bool p9 = getenv("SPCHOL_POTRF9") && atoi(getenv("SPCHOL_POTRF9")) != 0;   // read per launch (tests)
   if (p9) launch_prio(potrf9_kernel, ntasks, POTRF9_THREADS, POTRF9_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
   else launch_prio(potrf10_kernel, ntasks, POTRF9_THREADS, POTRF10_SMEM, st, prio, tasks, sn, sfirst, panels, linv, fail);
 }

@@ -263,11 +263,11 @@ def test_distributed_fullsize_mock(name, world):
 
 @pytest.mark.parametrize("name", ["S3", "S4", "S5"])
 @pytest.mark.parametrize("env", [{"SPCHOL_LEFT_INNER": "1"}, {"SPCHOL_NO_NEXT_SPLIT": "1"}, {"SPCHOL_REST_SMEM": "60000"},
-                                 {"SPCHOL_PDL": "0"}])
+                                 {"SPCHOL_PDL": "0"}, {"SPCHOL_POTRF9": "1", "SPCHOL_PANEL": "0"}, {"SPCHOL_PANEL": "0"}])
 def test_parity_schedule_options(name, env, monkeypatch):
     """Scheduling variants of the large-supernode cdiv (left-looking in-block updates, NEXT as one
-    launch, capped trailing-stream residency, no programmatic dependent launch): same factor, same
-    solve."""
+    launch, capped trailing-stream residency, no programmatic dependent launch, the right-looking
+    potrf9 reference kernel, no fused outer-block path): same factor, same solve."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     run_parity(gen.make(name), small_max_k=-1)
