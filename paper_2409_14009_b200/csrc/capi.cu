@@ -1385,7 +1385,8 @@ static int enqueue_ops(spchol_handle* h, cudaStream_t st, size_t begin, size_t e
         break;
       case K_PANEL:
         launch_panel(h->d_pantasks + L.off, L.aux2, L.n - L.aux2, h->d_pansync + h->npanflags + 3 * L.aux, h->d_pansync,
-                     h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, h->panel_grid, ls, prio);
+                     h->d_sn, h->d_sfirst, h->d_panels, h->d_linv, h->d_fail, h->panel_grid, ls, prio, h->npanflags,
+                     h->world > 1 ? INT_MAX : h->nslots_total);
         break;
       case K_TRSM:
         if (h->use_tma)

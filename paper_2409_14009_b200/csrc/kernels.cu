@@ -1695,6 +1695,31 @@ __device__ long long pk_clk[8192][8];
 #define PK_T(q, e) do { } while (0)
 #endif
 
+// SPCHOL_PK_CHECK (the bounds-checked test build, `make spchol_check`): every panel task's column
+// range, rows, inverse slots and flag indices are checked against the launch's bounds; a violation
+// prints the task and traps (the sanitizer substitute on this pool).
+#ifdef SPCHOL_PK_CHECK
+#define PK_CHECK(cond, T)                                                                                  \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("PK_CHECK failed: %s (sn %d c0 %d w %d tile %d blk %d slot %d flag %d pw %d q %d)\n", #cond, \
+             (T).sn, (T).c0, (T).w, (T).tile, (T).blk, (T).slot, (T).flag, (T).pw, (T).q);                \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define PK_CHECK(cond, T) do { } while (0)
+#endif
+__device__ __forceinline__ void pk_check_task(const PanTask& T, const SnInfo& S, int nflags, int nslots) {
+  const int nbk = (T.w + NBMAX - 1) / NBMAX, ntile = (S.m - T.c0 + TILE - 1) / TILE;
+  PK_CHECK(T.c0 >= 0 && T.w >= 1 && T.w <= 4 * NBMAX && T.c0 + T.w <= S.k && T.c0 % NBMAX == 0, T);
+  PK_CHECK(T.tile >= 0 && T.tile < ntile && T.blk >= 0 && T.blk < nbk && (T.tile >= nbk || T.blk <= T.tile), T);
+  PK_CHECK(T.slot >= 0 && T.slot + nbk <= nslots, T);
+  PK_CHECK(T.flag >= 0 && T.flag + 32 + 4 * max(0, ntile - nbk) <= nflags, T);
+  PK_CHECK(T.pw >= 0 && T.c0 - T.pw >= 0 && T.q >= -1 && (T.q < 0 || (T.tile < nbk && NBMAX * T.q < T.pw)), T);
+  (void)nbk; (void)ntile; (void)nflags; (void)nslots;
+}
+
 // acc = A B^T over K columns: A, B = 64-row blocks of column-major matrices (rows past arows /
 // brows and columns past K read as zero); the gemm_kernel pipeline (BK-column chunks, cp.async).
 // 128 threads: 4 warps in a 2 x 2 grid of 32 x 32 warp tiles.  256 threads (NT): warps 4-7 form a
@@ -1884,6 +1909,7 @@ __device__ __forceinline__ void pk_update(const PanTask& T, const SnInfo& S, con
   double acc[4][4][2];
   const double* Pq = G.Pc + (long long)off * S.ld;
   const int cj = NBMAX * j;
+  PK_CHECK(T.c0 + off >= 0 && K >= 1 && T.c0 + off + K <= S.k && cj < T.w && G.r0 < S.m && T.c0 + cj < S.m, T);
   pk_mma<NT>(Pq + G.r0, S.ld, G.nrows, Pq + T.c0 + cj, S.ld, S.m - (T.c0 + cj), K, acc, smem);
   pk_store<NT>(acc, smem, G.Pc + (long long)cj * S.ld + G.r0, S.ld, 0, G.nr64, min(NBMAX, T.w - cj), true, j == G.i, red);
 }
@@ -1894,6 +1920,7 @@ __device__ __forceinline__ void pk_trsm(const PanTask& T, const SnInfo& S, const
   double acc[4][4][2];
   const int nbs = min(NBMAX, T.w - NBMAX * s);
   double* Ps = G.Pc + (long long)NBMAX * s * S.ld;
+  PK_CHECK(s >= 0 && nbs >= 1 && T.c0 + NBMAX * s + nbs <= S.k && G.r0 < S.m && rlo >= 0, T);
   pk_mma<NT>(Ps + G.r0, S.ld, G.nrows, linv + (long long)(T.slot + s) * (NBMAX * NBMAX), NBMAX, nbs, nbs, acc, smem);
   pk_store<NT>(acc, smem, Ps + G.r0, S.ld, rlo, G.nr64, nbs, false, false);
 }
@@ -1946,7 +1973,8 @@ constexpr int PANEL_DIAG_THREADS = 2 * GEMM_THREADS;   // two 2 x 2 warp grids (
 __global__ void __launch_bounds__(PANEL_DIAG_THREADS, 1) panel_diag_kernel(const PanTask* __restrict__ tasks, int ntasks,
                                                                     int* sync3, int* flags, const SnInfo* __restrict__ sn,
                                                                     const int* __restrict__ sfirst, double* panels,
-                                                                    double* linv, unsigned long long* fail, int trigger) {
+                                                                    double* linv, unsigned long long* fail, int trigger,
+                                                                    int nflags, int nslots) {
   pdl_enter();
   if (trigger) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   extern __shared__ __align__(16) double smem[];
@@ -1964,6 +1992,8 @@ __global__ void __launch_bounds__(PANEL_DIAG_THREADS, 1) panel_diag_kernel(const
     PK_T(q, 0);
     const PanTask T = tasks[q];
     const SnInfo S = sn[T.sn];
+    pk_check_task(T, S, nflags, nslots);
+    PK_CHECK(T.tile < (T.w + NBMAX - 1) / NBMAX, T);
     const PkGeo G = pk_geo(T, S, panels);
     const int i = G.i, j = T.blk;
     int* F = flags + T.flag;
@@ -2089,7 +2119,7 @@ __global__ void __launch_bounds__(PANEL_DIAG_THREADS, 1) panel_diag_kernel(const
 __global__ void __launch_bounds__(GEMM_THREADS, 4) panel_below_kernel(const PanTask* __restrict__ tasks, int ntasks,
                                                                      int* sync3, int ndiag_ctas, int* flags,
                                                                      const SnInfo* __restrict__ sn, double* panels,
-                                                                     const double* __restrict__ linv) {
+                                                                     const double* __restrict__ linv, int nflags, int nslots) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int s_task;
   for (;;) {
@@ -2101,6 +2131,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 4) panel_below_kernel(const PanT
     PK_T(4096 + q, 0);
     const PanTask T = tasks[q];
     const SnInfo S = sn[T.sn];
+    pk_check_task(T, S, nflags, nslots);
+    PK_CHECK(T.tile >= (T.w + NBMAX - 1) / NBMAX && T.q < 0, T);
     const PkGeo G = pk_geo(T, S, panels);
     const int j = T.blk;
     int* F = flags + T.flag;
@@ -2235,15 +2267,15 @@ void launch_potrf(const PTask* tasks, int ntasks, const SnInfo* sn, const int* s
 
 void launch_panel(const PanTask* tasks, int ndiag, int nbelow, int* sync3, int* flags, const SnInfo* sn,
                   const int* sfirst, double* panels, double* linv, unsigned long long* fail, int grid_cap,
-                  cudaStream_t st, int prio) {
+                  cudaStream_t st, int prio, int nflags, int nslots) {
   if (ndiag <= 0) return;
   const int gd = std::min(ndiag, 148);
   launch_prio(panel_diag_kernel, gd, PANEL_DIAG_THREADS, PANEL_DIAG_SMEM, st, prio, tasks, ndiag, sync3, flags, sn, sfirst,
-              panels, linv, fail, nbelow > 0 ? 1 : 0);
+              panels, linv, fail, nbelow > 0 ? 1 : 0, nflags, nslots);
   if (nbelow <= 0) return;
   const int gb = std::min(nbelow, grid_cap > 0 ? grid_cap : 4 * 148);
   launch_prio(panel_below_kernel, gb, GEMM_THREADS, GEMM_SMEM, st, prio, tasks + ndiag, nbelow, sync3, gd, flags, sn,
-              panels, (const double*)linv);
+              panels, (const double*)linv, nflags, nslots);
 }
 
 void launch_small(const int* sns, int count, const SnInfo* sn, const int* sfirst, double* panels,

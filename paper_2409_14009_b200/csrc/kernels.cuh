@@ -121,9 +121,10 @@ struct PanTask {
 // tasks (pair-major: (0,0), (1,0), (1,1), (2,0) ... each pair over all outer blocks), then the
 // nbelow blocks below them (column-major: (nbk, 0), (nbk+1, 0), ..., (nbk, 1), ...).  sync3 = {diagonal ticket, below ticket, diagonal CTAs
 // done}, zeroed per factor.
+// nflags / nslots: sizes of the flag array and of the inverse slots (bounds of the checked build).
 void launch_panel(const PanTask* tasks, int ndiag, int nbelow, int* sync3, int* flags, const SnInfo* sn,
                   const int* sfirst, double* panels, double* linv, unsigned long long* fail, int grid_cap,
-                  cudaStream_t st, int prio = 0);
+                  cudaStream_t st, int prio, int nflags, int nslots);
 constexpr int SMALL_THREADS = 256;
 constexpr int SMALL_MAXK = 64;
 constexpr int SMALL_MAXM = SMALL_THREADS;

@@ -50,7 +50,7 @@ int main(int argc, char** argv) {
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaEventRecord(e0, st);
-      launch_panel(dT, nd, (int)t.size() - nd, dsync + 4000, dsync, dS, dsf, dA, dX, dfail, 0, st, -1);
+      launch_panel(dT, nd, (int)t.size() - nd, dsync + 4000, dsync, dS, dsf, dA, dX, dfail, 0, st, -1, 4000, n / 64 + 1);
       cudaEventRecord(e1, st);
       cudaEventSynchronize(e1);
       float ms;
