@@ -859,9 +859,7 @@ __device__ __forceinline__ void p9_syrk_tile(double* Ls, int b, int r0, int c0) 
 }
 
 // The whole block's factor + inverse by the CTA's 128 threads (POTRF9_SMEM bytes of shared memory at
-// p9_smem); used by potrf9_kernel and by the fused panel kernels.  LOAD = false: the caller has
-// already placed the (updated) block in Ls (column-major, stride P9_LD) and synchronised.
-template <bool LOAD = true>
+// p9_smem); potrf9_kernel is the right-looking reference for potrf10 (SPCHOL_POTRF9=1, probe).
 __device__ __forceinline__ void potrf9_block(const PTask& T, const SnInfo& S, const int* __restrict__ sfirst,
                                              double* panels, double* linv, unsigned long long* fail, double* p9_smem) {
   double* Ls = p9_smem;                        // A -> L (column-major, lower part used)
@@ -874,7 +872,7 @@ __device__ __forceinline__ void potrf9_block(const PTask& T, const SnInfo& S, co
   // A's block: 16-byte cp.async of row pairs (rows >= nb zero-filled), Y = I meanwhile
   for (int e = tid; e < NBMAX * NBMAX / 2; e += POTRF9_THREADS) {
     const int c = e >> 5, r = (e & 31) * 2;
-    if (LOAD && c < nb && r < nb) {
+    if (c < nb && r < nb) {
       const unsigned sa = (unsigned)__cvta_generic_to_shared(Ls + c * P9_LD + r);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(P + (long long)c * S.ld + r),
                    "r"(r + 1 < nb ? 16 : 8));

@@ -1,9 +1,10 @@
 // sm_100a device kernels of the numeric RL factorization (arXiv 2409.14009, §II.A "RL").
 // P:n = PAPER.md line n.  All arithmetic is FP64 ("D" BLAS).
 //
-//   potrf9_kernel       a3: cdiv POTRF of one <=64-column diagonal block in shared memory, plus its
-//                       triangular inverse (used by TRSM-as-GEMM)               ("DPOTRF")
-//   gemm_kernel<MODE>   FP64 DMMA (mma.sync m8n8k4) 64x64 tile, cp.async 3-stage smem pipeline
+//   potrf10_kernel      a3: cdiv POTRF of one <=64-column diagonal block in shared memory, plus its
+//                       triangular inverse (used by TRSM-as-GEMM and the solve)  ("DPOTRF");
+//                       potrf9_kernel: the right-looking reference (SPCHOL_POTRF9=1)
+//   gemm_kernel<MODE>   FP64 DMMA (mma.sync m8n8k4) 64x64 tile, cp.async 4-stage smem pipeline
 //     MODE_TRSM         a4: L_{R,b} = A_{R,b} L_bb^{-T}                          ("DTRSM")
 //     MODE_LOCAL        right-looking update of the supernode's own trailing columns
 //     MODE_SCATTER      a5+a6: U_J = L_{R,J} L_{R,J}^T ("DSYRK") with the relind assembly
