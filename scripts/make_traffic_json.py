@@ -42,8 +42,8 @@ kern = open(os.path.join(ROOT, "paper_2409_14009_b200", "csrc", "kernels.cu"), "
 out = {"config": "C4", "kernel": "syrk_scatter", "launches": n, "traffic_bytes_per_launch": traffic,
        "algorithmic_bytes_per_launch": alg, "traffic_over_algorithmic": traffic / alg, "ncu_total_ms": ms,
        "kernels_cu_sha256": hashlib.sha256(kern).hexdigest(),
-       "source": "profiles/r02_scatter_dram_C4.csv: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
+       "source": "profiles/" + os.path.basename(src) + ": ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
                  "gpu__time_duration.sum,sm__pipe_fp64_cycles_active... on every SYRK+scatter launch (gemm_kernel<2>) "
-                 "of one C4 factor (scripts/ncu_scatter_only.sh, round 2)"}
+                 "of one C4 factor (scripts/stamp_r02b.sh)"}
 json.dump(out, open(os.path.join(ROOT, "profiles", "roofline_traffic.json"), "w"), indent=1)
 print(json.dumps(out, indent=1))
