@@ -1747,7 +1747,8 @@ extern "C" int spchol_query(const spchol_handle* h, int key, int64_t* value) {
       int64_t nl = 1;
       const size_t b = h->world == 1 ? h->plan_factor_begin : h->plan_all_end;
       const size_t e = h->world == 1 ? h->plan_all_end : h->plan.size();
-      for (size_t i = b; i < e; ++i) nl += h->plan[i].op == OP_LAUNCH;
+      for (size_t i = b; i < e; ++i)   // a fused cdiv step launches the diagonal and (if any) the below kernel
+        nl += h->plan[i].op == OP_LAUNCH ? (h->plan[i].kind == K_PANEL && h->plan[i].n > h->plan[i].aux2 ? 2 : 1) : 0;
       *value = nl;
       break;
     }
