@@ -945,6 +945,11 @@ static int setup_device(spchol_handle* h) {
     }
     CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    if (h->world == 1 && !h->capped) {
+      CK(cudaStreamCreateWithFlags(&h->zstream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&h->ev_zs, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_zd, cudaEventDisableTiming));
+    }
   }
   h->plan_events.resize(h->nevents);
   for (auto& e : h->plan_events) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1030,6 +1035,11 @@ static void free_device(spchol_handle* h) {
   }
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->graph) cudaGraphDestroy(h->graph);
+  if (h->gexec_nz) cudaGraphExecDestroy(h->gexec_nz);
+  if (h->graph_nz) cudaGraphDestroy(h->graph_nz);
+  if (h->zstream) cudaStreamDestroy(h->zstream);
+  if (h->ev_zs) cudaEventDestroy(h->ev_zs);
+  if (h->ev_zd) cudaEventDestroy(h->ev_zd);
   if (h->world > 1) dist_free_device(h);   // the VMM arenas (d_panels, d_linv)
   if (h->h_panels) cudaFreeHost(h->h_panels);
   h->h_panels = nullptr;
@@ -1288,10 +1298,19 @@ extern "C" int spchol_set_values(spchol_handle* h, const double* values) {
   if (!h || !values) return fail(SPCHOL_ERR_VALIDATION, "NULL handle or values");
   if (host_only(h)) return fail(SPCHOL_ERR_STATE, "host-only handle (device < 0)");
   CK(cudaSetDevice(h->opt.device));
+  const bool zero = h->world == 1 && !h->capped && h->zstream;
+  if (zero) {   // zero the arena on the side stream during the upload (after the handle's earlier work)
+    CK(cudaEventRecord(h->ev_zs, h->stream));
+    CK(cudaStreamWaitEvent(h->zstream, h->ev_zs, 0));
+    CK(cudaMemsetAsync(h->d_panels, 0, sizeof(double) * (size_t)std::max(1LL, h->panel_doubles), h->zstream));
+    CK(cudaEventRecord(h->ev_zd, h->zstream));
+  }
   CK(cudaMemcpyAsync(h->d_avals, values, sizeof(double) * (size_t)h->S.nnzA, cudaMemcpyHostToDevice, h->stream));
+  if (zero) CK(cudaStreamWaitEvent(h->stream, h->ev_zd, 0));
   CK(cudaStreamSynchronize(h->stream));
   h->values_set = true;
   h->factored = false;
+  h->prezeroed = zero;
   return SPCHOL_OK;
 }
 
@@ -1448,7 +1467,8 @@ static int enqueue_init(spchol_handle* h, cudaStream_t st) {
     if (rc) return rc;
   } else {
     CK(cudaMemsetAsync(h->d_fail, 0xFF, sizeof(unsigned long long), st));
-    CK(cudaMemsetAsync(h->d_panels, 0, sizeof(double) * (size_t)std::max(1LL, h->panel_doubles), st));
+    if (!h->skip_zero)   // (else zeroed by spchol_set_values alongside the upload)
+      CK(cudaMemsetAsync(h->d_panels, 0, sizeof(double) * (size_t)std::max(1LL, h->panel_doubles), st));
     launch_init(h->d_avals, h->d_amap, h->S.nnzA, h->d_panels, st);
   }
   if (h->timing) cudaEventRecord(h->ev_pool[ti + 1], st);
@@ -1512,6 +1532,34 @@ extern "C" int spchol_factor_async(spchol_handle* h) {
   // captured.
   const bool dist_graph = h->world > 1 && g_nccl.capturable && !h->dist_capture_failed && h->dist_eager_done &&
                           !(getenv("SPCHOL_DIST_GRAPH") && atoi(getenv("SPCHOL_DIST_GRAPH")) == 0);
+  // the arena was zeroed by spchol_set_values: this factor skips its memset (variant graph)
+  h->skip_zero = h->prezeroed && h->world == 1 && !h->capped;
+  h->prezeroed = false;
+  if (h->skip_zero && h->opt.use_graph && !h->timing) {
+    int rc = SPCHOL_OK;
+    if (!h->gexec_nz) {
+      cudaStream_t cs = h->own_stream;
+      CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      rc = enqueue_factor(h, cs);
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(cs, &g);
+      if (rc != SPCHOL_OK || e != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        h->skip_zero = false;
+        return rc != SPCHOL_OK ? rc : cuda_fail(e, "cudaStreamEndCapture");
+      }
+      h->graph_nz = g;
+      CK(cudaGraphInstantiateWithFlags(&h->gexec_nz, g, cudaGraphInstantiateFlagUseNodePriority));
+    }
+    h->skip_zero = false;
+    CK(cudaGraphLaunch(h->gexec_nz, h->stream));
+    return SPCHOL_OK;
+  }
+  if (h->skip_zero) {   // eager (no graph / kernel timing)
+    const int rc = enqueue_factor(h, h->stream);
+    h->skip_zero = false;
+    return rc;
+  }
   if (h->opt.use_graph && !h->timing && (h->world == 1 || dist_graph)) {
     if (!h->gexec) {
       cudaStream_t cs = h->own_stream;

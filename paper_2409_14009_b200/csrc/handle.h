@@ -271,6 +271,13 @@ struct spchol_handle {
   // graph
   cudaGraph_t graph = nullptr, solve_graph[3] = {nullptr, nullptr, nullptr};   // solve: per nr = 1, 2, 4
   cudaGraphExec_t gexec = nullptr, solve_gexec[3] = {nullptr, nullptr, nullptr};
+  // spchol_set_values zeroes the arena on zstream while A's values travel (single GPU, resident): the
+  // next factor then replays the variant graph without the memset
+  bool prezeroed = false, skip_zero = false;
+  cudaGraph_t graph_nz = nullptr;
+  cudaGraphExec_t gexec_nz = nullptr;
+  cudaStream_t zstream = nullptr;
+  cudaEvent_t ev_zs = nullptr, ev_zd = nullptr;
   // timing
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;

@@ -457,3 +457,32 @@ def test_distributed_fused_panel_mock(name, world, minflops, outer):
     assert r["ok"], r
     assert r["lerr"] <= TOL_L and r["berr"] <= TOL_BERR and r["ranks_agree"], r
     assert r["padding_nonzeros"] == 0, r
+
+
+@pytest.mark.parametrize("use_graph", [1, 0])
+def test_set_values_prezeroed_arena(use_graph):
+    """spchol_set_values zeroes the panel arena on a side stream during the upload, and the next factor
+    skips its memset (variant graph): factor after set_values, factor again without it (full graph),
+    and a refactor with new values all give the oracle's factor; a pending solve is not disturbed by
+    the next set_values' zeroing (it waits for the handle's earlier work)."""
+    p = gen.make("S4")
+    o = oracle.Oracle.from_problem(p)
+    assert o.factor() == -1
+    _, _, Lx = o.L_csc()
+    q = gen.Problem(p.name, p.n, p.colptr, p.rowidx, 4.0 * p.values, p.perm)   # L(4A) = 2 L(A)
+    with sp.Solver.from_problem(p, use_graph=use_graph) as h:
+        for _ in range(2):
+            assert h.spchol_factor() == (-1, -1)
+            _, _, cLx, _ = h.spchol_export_factor_csc()
+            assert np.abs(cLx - Lx).max() <= TOL_L * np.abs(Lx).max()
+        xs, b = gen.rhs(p)
+        x = h.spchol_solve(b)
+        assert backward_error(p, x, b) <= TOL_BERR
+        h.spchol_set_values(q.values)
+        assert h.spchol_factor() == (-1, -1)
+        _, _, cLx, _ = h.spchol_export_factor_csc()
+        assert np.abs(cLx - 2.0 * Lx).max() <= 2.0 * TOL_L * np.abs(Lx).max()
+        h.spchol_set_values(p.values)
+        assert h.spchol_factor() == (-1, -1)
+        _, _, cLx, _ = h.spchol_export_factor_csc()
+        assert np.abs(cLx - Lx).max() <= TOL_L * np.abs(Lx).max()
