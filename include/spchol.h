@@ -134,7 +134,9 @@ int spchol_save_analysis(const spchol_handle* h, const char* path);
 int spchol_load_analysis(const char* path, const spchol_options* opt, spchol_handle** out);
 
 /* Replace A's values (same pattern as analyze; host array of colptr[n] doubles, copied to the
- * device on the handle's stream, synchronously w.r.t. the host buffer). */
+ * device on the handle's stream, synchronously w.r.t. the host buffer).  Single GPU, resident
+ * arena: the panel arena is zeroed on a side stream during the upload (after the handle's earlier
+ * work), so the next factor skips its own zeroing (a1); the previous factor's panels are gone. */
 int spchol_set_values(spchol_handle* h, const double* values);
 
 /* Same, from a device array (d_values, colptr[n] doubles), enqueued on the handle's stream. */
